@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Training events/sec of the DistTGL training step on B200 (BASELINE.json metric).
+
+One "step" = one barrier of the i x j x k schedule: every rank runs one
+sub-iteration over its 600-event slice (sample -> plan -> memory read -> GRU
+freshen -> attention -> decoder/BCE -> backward -> root writes -> gradient
+all-reduce -> Adam). N=1 runs BASELINE configs[1] (Reddit shape, TGN + static
+memory); N>1 runs the same workload with memory parallelism k=N, one GPU per
+trainer, weak scaling (epochs=N so every memory copy sweeps a full epoch).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training events/sec (device-timed, max over ranks)"
+CONFIGS = {
+    # BASELINE.json configs[1]: Reddit shape, TGN + static node memory
+    "c2": dict(workload="synthetic Reddit-shape CTDG (C2): 10,984 nodes, 672,447 events, "
+                        "172-d edge feats, TGN + static memory, 10 recent nbrs, mem 100, batch 600",
+               nodes=10984, events=672447, d_e=172, d_static=100),
+    "c1": dict(workload="synthetic Wikipedia-shape CTDG (C1): 9,227 nodes, 157,474 events, "
+                        "172-d edge feats, TGN, 10 recent nbrs, mem 100, batch 600",
+               nodes=9227, events=157474, d_e=172, d_static=0),
+    "c5p": dict(workload="synthetic GDELT-shape CTDG (C5, 5M-event prefix): 16,682 nodes, "
+                         "186-d edge feats, TGN + static memory, batch 600",
+                nodes=16682, events=5_000_000, d_e=186, d_static=100),
+}
+LOCAL_BATCH = 600
+TRAIN_FRAC = 0.70
+
+
+def model_dims(cfg):
+    return dict(d_mem=100, d_time=100, d_static=cfg["d_static"], d_attn=100, d_hidden=100,
+                n_neighbors=10)
+
+
+# ----------------------------------------------------------------- roofline bookkeeping
+def attn_proj_flops(sz, cfg):
+    """Algorithmic FLOPs of the attention projection launch (Q for R roots,
+    K and V for P pairs): 2 * (R * q_in * d_attn + 2 * P * kv_in * d_attn)."""
+    d, ds, de, dt, da = 100, cfg["d_static"], cfg["d_e"], 100, 100
+    q_in, kv_in = d + ds + dt, d + ds + de + dt
+    return 2.0 * (sz["R"] * q_in * da + 2 * sz["P"] * kv_in * da)
+
+
+def step_model_flops(sz, cfg):
+    """SURVEY.md 8(d) model FLOPs of one sub-iteration (forward + dW + dX ~ 3x
+    forward MACs x 2): KV, Q, GRU and decoder contractions."""
+    d, ds, de, dt, da, dh = 100, cfg["d_static"], cfg["d_e"], 100, 100, 100
+    q_in, kv_in, gin = d + ds + dt, d + ds + de + dt, 3 * d + dt + de
+    macs = (2 * sz["P"] * kv_in * da + sz["R"] * q_in * da + sz["U"] * (3 * d * gin)
+            + 2 * sz["B"] * 2 * da * dh)
+    return 6.0 * macs
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = list(self.rows)
+        if not rows:  # region too short for the sampler: take one reading now
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits", "-i", str(self.device)],
+                                     capture_output=True, text=True, timeout=10).stdout
+                rows = [[p.strip() for p in out.strip().split(",")]]
+            except Exception:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- reference (CPU) arm
+def reference_time(cfg, n_groups, barriers, warmup, log=print):
+    """Times the unmodified reference (oracle/_ref, compiled from
+    /root/reference/proj/include by oracle/Makefile) on this host's cores:
+    run_sequential at (1,1,1), run_training (threaded) at (1,1,k). Returns
+    (events/s, seconds, events, threads)."""
+    from oracle import ref
+    from oracle import tgnn_oracle as O
+
+    t0 = time.time()
+    g = ref.RefGraph.synthetic(cfg["nodes"], cfg["events"], d_e=cfg["d_e"], seed=1)
+    _, _, t, _ = g.export(feats=False)
+    log(f"[ref] graph ready in {time.time() - t0:.1f}s")
+    mc = O.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(t[-1]), **model_dims(cfg))
+    gb = LOCAL_BATCH
+    mid = int(cfg["events"] * TRAIN_FRAC) // 2
+    out = None
+    for phase, nbar in (("warmup", warmup), ("timed", barriers)):
+        if nbar <= 0:
+            continue
+        lo = mid
+        hi = lo + nbar * gb * n_groups
+        tc = ref.train_cfg(k=n_groups, local_batch=gb, seed=1, epochs=1, lr_base=1e-3)
+        r = g.run(mc, tc, lo, hi, want_params=False)
+        assert r["barriers"] == nbar
+        if phase == "timed":
+            ev = nbar * gb * n_groups
+            out = (ev / r["elapsed_s"], r["elapsed_s"], ev, 2 * n_groups if n_groups > 1 else 1)
+        mid = hi
+    return out
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    # bound the sample: each reference barrier is several seconds of CPU work
+    steps = min(args.steps, args.ref_max_steps)
+    warm = min(args.warmup, 1)
+    value, secs, ev, threads = reference_time(cfg, world, steps, warm, log=lambda *a: print(*a, file=sys.stderr))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s",
+        "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * secs / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference gen_synthetic, seed 1)",
+        "config": {"workload": cfg["workload"], "parallelism": f"(i,j,k)=(1,1,{world}) host threads",
+                   "global_batch": LOCAL_BATCH * world},
+        "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
+                         "sample": f"{steps} barriers x {world} x 600 events mid-stream, "
+                                   f"run_{'training' if world > 1 else 'sequential'} (oracle/_ref)"},
+        "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------- B200 arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--profile-steps", type=int, default=5)
+    ap.add_argument("--cpu-baseline-steps", type=int, default=3)
+    ap.add_argument("--ref-max-steps", type=int, default=12)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world == 1 and args.gpus != 1:
+        print(f"warning: --gpus {args.gpus} without torchrun; running 1 rank", file=sys.stderr)
+
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2307_07649_b200 as T
+
+    def log(*a):
+        if rank == 0:
+            print(*a, file=sys.stderr, flush=True)
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    cfg = CONFIGS[args.config]
+    t0 = time.time()
+    s = T.gen_synthetic(T.SynthParams(nodes=cfg["nodes"], events=cfg["events"], d_e=cfg["d_e"], seed=1))
+    log(f"stream generated in {time.time() - t0:.1f}s")
+    ctx = T.Context(local_rank)
+    g = T.TemporalGraph.from_stream(ctx, s)
+    mc = T.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(s.t[-1]), **model_dims(cfg))
+    train_end = int(round(cfg["events"] * TRAIN_FRAC))
+    tc = T.TrainConfig(i=1, j=1, k=world, local_batch=LOCAL_BATCH, lr_base=1e-3, seed=1, epochs=world)
+    run = T.Run(ctx, g, mc, tc, 0, train_end, rank=rank, nranks=world)
+    need = args.warmup + args.steps + args.profile_steps + args.e2e_steps + 1
+    if run.barriers < need:
+        raise SystemExit(f"schedule has {run.barriers} barriers, need {need}")
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(T.comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        run.comm_init(bytes(uid.cpu().numpy().tobytes()))
+    log(f"setup {time.time() - t0:.1f}s; {run.barriers} barriers, {run.nparam} params")
+
+    launches = run.launches_per_barrier() if world == 1 else None
+    run.step(args.warmup)
+    ctx.synchronize()
+
+    # ---- timed region: K barriers, CUDA events on the context stream
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    first = run.next
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        run.step(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    ctx.synchronize()
+    losses = run.losses(first, args.steps)  # also checks the non-finite flag
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    events = run.traversed(first, args.steps)
+    value = events / (ms_max / 1e3)
+    log(f"timed {args.steps} barriers: {ms_max:.2f} ms, {events} events, {value:,.0f} events/s, "
+        f"loss {losses[0]:.4f} -> {losses[-1]:.4f}")
+
+    # ---- phase profile (dominant kernel for the roofline)
+    prof = []
+    for _ in range(args.profile_steps):
+        ph, sz = run.profile_barrier()
+        prof.append((ph, sz))
+    ph_mean = {k: float(np.mean([p[0][k] for p in prof])) for k in prof[0][0]}
+    sz_mean = {k: float(np.mean([p[1][k] for p in prof])) for k in prof[0][1]}
+    proj_ms = ph_mean["attn_proj"]
+    flops = attn_proj_flops(sz_mean, cfg)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+    achieved_tf = flops / (proj_ms / 1e3) / 1e12
+    roofline = {"kernel": "attention projection GEMM group (Q + K + V, fp32 SIMT)", "bound": "tensor",
+                "achieved": achieved_tf, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved_tf / peaks["bf16_tflops"], "traffic": None,
+                "flops_per_launch": flops, "launch_ms": proj_ms,
+                "share_of_step": proj_ms / max(sum(ph_mean.values()), 1e-9)}
+    log("phases (ms): " + ", ".join(f"{k}={v:.3f}" for k, v in ph_mean.items()))
+    log(f"plan sizes: {sz_mean}")
+
+    # ---- end-to-end through the public API: per step H2D of the step's events
+    # (src/dst/t/edge features from pinned host memory) + barrier + D2H loss read
+    nb, sched = T.schedule_query(tc, 0, train_end, rank, run.next, args.e2e_steps)
+    d_e = cfg["d_e"]
+    maxb = LOCAL_BATCH
+    p_src = T.pinned_empty((maxb,), np.int32)
+    p_dst = T.pinned_empty((maxb,), np.int32)
+    p_t = T.pinned_empty((maxb,), np.float64)
+    p_f = T.pinned_empty((maxb, d_e), np.float32)
+    h2d = 0
+    if world > 1:
+        dist.barrier()
+    ctx.synchronize()
+    tw0 = time.perf_counter()
+    first_e2e = run.next
+    for x in range(args.e2e_steps):
+        b0, b1 = int(sched["slice_begin"][x]), int(sched["slice_end"][x])
+        n = b1 - b0
+        if sched["active"][x] and n > 0:
+            p_src[:n] = s.src[b0:b1]
+            p_dst[:n] = s.dst[b0:b1]
+            p_t[:n] = s.t[b0:b1]
+            p_f[:n] = s.efeat[b0:b1]
+            g.ingest(b0, p_src[:n], p_dst[:n], p_t[:n], p_f[:n])
+            h2d += n * (4 + 4 + 8 + 4 * d_e)
+        run.step(1)
+        run.losses(run.next - 1, 1)  # D2H read of the step's loss (synchronises)
+    e2e_s = time.perf_counter() - tw0
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_events = run.traversed(first_e2e, args.e2e_steps)
+    e2e_value = e2e_events / float(e2e_t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            v, secs, ev, thr = reference_time(cfg, 1, args.cpu_baseline_steps, 0, log=log)
+            cpu = {"value": v, "unit": "events/s", "cores": thr, "kind": "reference",
+                   "sample": f"{args.cpu_baseline_steps} barriers x 600 events mid-stream, "
+                             f"run_sequential of the unmodified reference (oracle/_ref), {secs:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (bit-identical gen_synthetic, seed 1)",
+            "config": {"workload": cfg["workload"],
+                       "parallelism": f"(i,j,k)=(1,1,{world}), one trainer per GPU",
+                       "global_batch": LOCAL_BATCH * world, "local_batch": LOCAL_BATCH,
+                       "l2": "inputs larger than L2 (edge features "
+                             f"{cfg['events'] * cfg['d_e'] * 4 / 1e6:.0f} MB; each step reads a new "
+                             "event window); no explicit flush"},
+            "e2e": {"value": e2e_value, "unit": "events/s",
+                    "h2d_bytes_per_step": int(h2d / max(args.e2e_steps, 1)),
+                    "d2h_bytes_per_step": 8},
+            "gpu_launches": (launches * args.steps) if launches is not None else None,
+            "gpu_launches_per_step": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "phases_ms": ph_mean,
+            "plan_sizes": sz_mean,
+            "model_tflops": step_model_flops(sz_mean, cfg) * world / (ms_max / args.steps / 1e3) / 1e12,
+            "loss_first_last": [float(losses[0]), float(losses[-1])],
+        }
+        print(json.dumps(line))
+    run.close()
+    g.close()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,213 @@
+/*
+ * tgnn_b200.h -- C ABI of the B200-native DistTGL training step.
+ *
+ * Drop-in boundary for the reference's hot path (/root/reference/proj/include/tgnn,
+ * "ref" below). Every entry point names the reference interface it replaces.
+ * POD arguments only, opaque handles, int status + thread-local message:
+ *   0 ok, 1 config_error, 2 parse_error, 3 numeric_error, 4 protocol_error,
+ *   5 shape_error, 6 CUDA error, 7 NCCL error      (ref common.hpp:16-34, tensor.hpp:16)
+ * Threading: one context per host thread and device; all calls on a context
+ * are ordered on its CUDA stream; collectives are enqueued on the same stream.
+ * Ownership: handles own device memory; host inputs are copied during the
+ * call; outputs go to caller-provided buffers.
+ */
+#ifndef TGNN_B200_H
+#define TGNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tgnn_ctx tgnn_ctx;
+typedef struct tgnn_graph tgnn_graph;
+typedef struct tgnn_memstore tgnn_memstore;
+typedef struct tgnn_trainer tgnn_trainer;
+typedef struct tgnn_run tgnn_run;
+
+/* ModelConfig, ref model.hpp:19-35 (d_hidden 0 => d_mem). */
+typedef struct tgnn_model_config {
+  int64_t d_mem, d_time, d_static, d_attn, d_hidden, d_e, n_neighbors, num_nodes;
+  double max_t;
+} tgnn_model_config;
+
+/* TrainConfig, ref parallel.hpp:15-26. */
+typedef struct tgnn_train_config {
+  int32_t i, j, k, p, q;
+  int32_t epochs;
+  int64_t local_batch;
+  double lr_base;
+  uint64_t seed;
+  int64_t local_batch_ref;
+  int64_t neg_groups;
+} tgnn_train_config;
+
+/* SynthParams, ref synthetic.hpp:14-25. */
+typedef struct tgnn_synth_params {
+  int64_t nodes, events;
+  double burst_prob, pref_prob;
+  int32_t prefs_per_src;
+  double src_frac;
+  int32_t bipartite;
+  int64_t d_e;
+  double zipf_s;
+  uint64_t seed;
+} tgnn_synth_params;
+
+/* ------------------------------------------------------------------ basics */
+const char* tgnn_last_error(void);
+int tgnn_version(void);
+int tgnn_device_count(int* out);
+int tgnn_ctx_create(int device, tgnn_ctx** out);
+int tgnn_ctx_destroy(tgnn_ctx* ctx);
+int tgnn_ctx_synchronize(tgnn_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for event timing by callers. */
+int tgnn_ctx_stream(tgnn_ctx* ctx, void** stream_out);
+
+/* ------------------------------------------------------------------ input
+ * gen_synthetic (ref synthetic.hpp:54-112), bit-identical host generator.
+ * Events come out finalized (time-sorted); efeat is [events x d_e] float32
+ * (the reference's f64 values rounded to f32) and may be NULL. */
+int tgnn_gen_synthetic(const tgnn_synth_params* p, int64_t* src, int64_t* dst, double* t,
+                       float* efeat, int64_t* bipartite_boundary);
+
+/* ------------------------------------------------------------------ graph
+ * TemporalGraph + finalize (ref temporal_graph.hpp:33-95): stable sort by t,
+ * validate (config_error), build the device T-CSR. efeat float32 [E x d_e]. */
+int tgnn_graph_create(tgnn_ctx* ctx, int64_t num_nodes, int64_t bipartite_boundary,
+                      int64_t num_events, const int64_t* src, const int64_t* dst,
+                      const double* t, const float* efeat, int64_t d_e, tgnn_graph** out);
+/* Same, with float64 features (converted on upload). */
+int tgnn_graph_create_f64(tgnn_ctx* ctx, int64_t num_nodes, int64_t bipartite_boundary,
+                          int64_t num_events, const int64_t* src, const int64_t* dst,
+                          const double* t, const double* efeat, int64_t d_e, tgnn_graph** out);
+int tgnn_graph_destroy(tgnn_graph* g);
+int tgnn_graph_info(tgnn_graph* g, int64_t* num_nodes, int64_t* boundary, int64_t* num_events,
+                    int64_t* d_e);
+/* Finalized events back to host (parity checks). */
+int tgnn_graph_events(tgnn_graph* g, int64_t* src, int64_t* dst, double* t);
+
+/* sample_recent_neighbors (ref temporal_graph.hpp:296-318), batched over
+ * (node, time) queries. Outputs [count x n], most recent first; counts[count]. */
+int tgnn_sample_recent_neighbors(tgnn_graph* g, const int64_t* nodes, const double* times,
+                                 int64_t count, int64_t n, int64_t* nbr_node,
+                                 int64_t* nbr_event, double* nbr_dt, int64_t* nbr_count);
+/* sample_negatives (ref temporal_graph.hpp:355-370). */
+int tgnn_sample_negatives(tgnn_graph* g, int64_t batch_index, int64_t group, int64_t count,
+                          uint64_t seed, int64_t* out);
+/* plan_sub_batch (ref trainer.hpp:76-106). Roots event-major (src, dst, neg);
+ * neighbour arrays [3B x n]; supports (ascending) needs 3B(n+1) slots. */
+int tgnn_plan_sub_batch(tgnn_graph* g, int64_t begin, int64_t end, const int64_t* negatives,
+                        int64_t n, int64_t* root_node, double* root_t, int64_t* nbr_count,
+                        int64_t* nbr_node, int64_t* nbr_event, double* nbr_dt,
+                        int64_t* supports, int64_t* num_supports);
+
+/* ------------------------------------------------------------------ memory store
+ * NodeMemoryState (ref memory_store.hpp:16-50) resident in HBM, with the
+ * MemoryClient read/write semantics (ref shared_buffers.hpp:124-165). Mail
+ * rows are packed {mem2 (2 d_mem) | t | dt | event} (ref memory_store.hpp:52-80). */
+int tgnn_memstore_create(tgnn_ctx* ctx, int64_t num_nodes, int64_t d_mem, tgnn_memstore** out);
+int tgnn_memstore_destroy(tgnn_memstore* m);
+int tgnn_memstore_reset(tgnn_memstore* m);                        /* reset_state */
+int tgnn_memstore_read(tgnn_memstore* m, const int64_t* nodes, int64_t count, double* mem_rows,
+                       double* mail_rows);                         /* MemoryClient::read */
+int tgnn_memstore_write(tgnn_memstore* m, const int64_t* nodes, int64_t count,
+                        const double* mem_rows, const double* mail_rows); /* ::write */
+/* Full state export: memory [N x d], last_update [N], mail_mem [N x 2d],
+ * mail_t [N], mail_dt [N], mail_event [N] (any pointer may be NULL). */
+int tgnn_memstore_export(tgnn_memstore* m, double* memory, double* last_update, double* mail_mem,
+                         double* mail_t, double* mail_dt, int64_t* mail_event);
+int tgnn_memstore_import(tgnn_memstore* m, const double* memory, const double* last_update,
+                         const double* mail_mem, const double* mail_t, const double* mail_dt,
+                         const int64_t* mail_event);
+
+/* ------------------------------------------------------------------ trainer core
+ * TrainerCore (ref trainer.hpp:490-562): parameter replica, gradients and
+ * Adam state in HBM, plus the step workspace. max_local_batch bounds the
+ * slice length. */
+int tgnn_param_count(const tgnn_model_config* m, int64_t* out);   /* param_count */
+/* init_params (ref model.hpp:122-141), bit-identical, canonical flat order. */
+int tgnn_init_params(const tgnn_model_config* m, uint64_t seed, double* flat);
+int tgnn_trainer_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_model_config* m,
+                        int64_t max_local_batch, uint64_t seed, tgnn_trainer** out);
+int tgnn_trainer_destroy(tgnn_trainer* tr);
+int tgnn_trainer_set_params(tgnn_trainer* tr, const double* flat);
+int tgnn_trainer_get_params(tgnn_trainer* tr, double* flat);
+int tgnn_trainer_get_grads(tgnn_trainer* tr, double* flat);
+/* sub_step (ref trainer.hpp:170-272) on an injected read view aligned with
+ * plan_sub_batch(begin, end, negatives).supports. Gradients are zeroed, then
+ * filled; s_hat_out [U x d_mem] may be NULL. */
+int tgnn_trainer_sub_step(tgnn_trainer* tr, int64_t begin, int64_t end,
+                          const int64_t* negatives, const double* view_mem,
+                          const double* view_mail, double* loss_out, double* s_hat_out);
+/* build_root_writes (ref trainer.hpp:284-330) for the last sub_step; rows in
+ * ascending node order; arrays sized 2B. */
+int tgnn_trainer_root_writes(tgnn_trainer* tr, int64_t* nodes, double* mem_rows,
+                             double* mail_rows, int64_t* num_writes);
+/* Adam::step (ref optimizer.hpp:40-56) with the trainer's current gradients. */
+int tgnn_trainer_adam_step(tgnn_trainer* tr, double lr);
+/* One full (1,1,1) barrier against a memory store: plan (device negatives),
+ * read, sub_step, root writes, Adam -- TrainerCore::iterate + apply. */
+int tgnn_trainer_iterate(tgnn_trainer* tr, tgnn_memstore* m, int64_t batch_index,
+                         int64_t group, int64_t batch_begin, int64_t begin, int64_t end,
+                         double lr, double* loss_out);
+
+/* ------------------------------------------------------------------ runs
+ * run_training / run_sequential (ref trainer.hpp:630-867) for one rank of an
+ * i x j x k job. With nranks == 1 the whole job runs here; otherwise call
+ * tgnn_run_comm_init first (one process per GPU). */
+typedef struct tgnn_run_options {
+  tgnn_model_config model;
+  tgnn_train_config train;
+  int64_t train_begin, train_end;
+  int32_t rank, nranks;
+  int32_t use_graphs; /* capture barrier steps as CUDA graphs */
+} tgnn_run_options;
+
+/* build_assignment + Assignment::task (ref parallel.hpp:150-331), host only.
+ * For barriers [first, first+count) of `rank`, out[count x 12] holds:
+ * active, sub, subs, batch, batch_begin, batch_end, slice_begin, slice_end,
+ * neg_group(sub), reset_before(stint read), active_trainers(b), traversed_after(b). */
+int tgnn_schedule_query(const tgnn_train_config* tc, int64_t train_begin, int64_t train_end,
+                        int32_t rank, int64_t first, int64_t count, int64_t* out,
+                        int64_t* barriers_out);
+
+int tgnn_comm_unique_id(char* out128);
+int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, tgnn_run** out);
+int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128);
+int tgnn_run_destroy(tgnn_run* r);
+int tgnn_run_info(tgnn_run* r, int64_t* barriers, int64_t* param_count);
+/* Enqueue barriers [first, first + count) on the context stream (no host sync). */
+int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count);
+/* Sync, check numeric flag, copy barrier losses [first, first+count) (mean
+ * over active trainers, ref trainer.hpp:713-722; valid on every rank). */
+int tgnn_run_losses(tgnn_run* r, int64_t first, int64_t count, double* out);
+int tgnn_run_params(tgnn_run* r, double* flat);
+/* Events traversed by ALL ranks in barriers [first, first+count) (ref parallel.hpp:302-314). */
+int tgnn_run_traversed(tgnn_run* r, int64_t first, int64_t count, int64_t* out);
+/* Kernel launches issued per barrier by this rank (counted by capturing the
+ * next barrier's enqueue sequence into a CUDA graph; nothing is executed). */
+int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out);
+/* Runs the next barrier with CUDA-event phase markers and returns per-phase
+ * device milliseconds [TGNN_PHASES] (plan, gru_fwd, attn_assemble, attn_proj,
+ * attn_softmax, decoder, decoder_bwd, attn_bwd, attn_bwd_gemm, gru_bwd,
+ * writes, allreduce, adam) and the plan sizes [8] (B, R, P, U, -, items, 2B, -). */
+#define TGNN_PHASES 13
+int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes);
+
+/* ------------------------------------------------------------------ host I/O
+ * Streaming ingestion: (re)writes events [first, first+count) of a device
+ * graph from host buffers (src/dst/t must match the finalized order; edge
+ * features float32 [count x d_e]). Used to stream feature windows and by the
+ * end-to-end measurement. Pinned buffers make the copies asynchronous. */
+int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t* src,
+                      const int32_t* dst, const double* t, const float* efeat);
+int tgnn_pinned_alloc(int64_t bytes, void** out);
+int tgnn_pinned_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TGNN_B200_H */

@@ -1,0 +1,1421 @@
+// C ABI (include/tgnn_b200.h): host runtime of the B200 DistTGL training step.
+//
+// Host C++ owns contexts, the device T-CSR, node-memory replicas, the trainer
+// core (parameters, gradients, Adam state, workspaces) and the i x j x k
+// schedule; every compute step is a CUDA kernel on the context stream and
+// every exchange is an NCCL collective on the same stream (NVLink/NVSwitch).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/tgnn_b200.h"
+#include "common.cuh"
+#include "device_types.cuh"
+#include "host/schedule.hpp"
+#include "host/synth.hpp"
+#include "plan.cuh"
+#include "step.cuh"
+
+using namespace tgb;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define NCCL_CHECK(x)                                                                 \
+  do {                                                                                \
+    ncclResult_t r__ = (x);                                                           \
+    if (r__ != ncclSuccess)                                                           \
+      throw ::tgb::Error(::tgb::kNccl, std::string(#x) + ": " + ncclGetErrorString(r__)); \
+  } while (0)
+
+#define API_BEGIN try {
+#define API_END                                  \
+  }                                              \
+  catch (const tgb::Error& e) {                  \
+    g_err = e.what();                            \
+    return e.code;                               \
+  }                                              \
+  catch (const std::bad_alloc& e) {              \
+    g_err = std::string("host allocation: ") + e.what(); \
+    return kCuda;                                \
+  }                                              \
+  catch (const std::exception& e) {              \
+    g_err = e.what();                            \
+    return 8;                                    \
+  }                                              \
+  return 0;
+
+template <typename T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  TGB_CUDA(cudaMalloc(&p, (n > 0 ? n : 1) * sizeof(T)));
+  return p;
+}
+
+template <typename T>
+void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) TGB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <typename T>
+void d2h(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) TGB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+ModelDims dims_of(const tgnn_model_config* c) {
+  ModelDims m;
+  m.d_mem = c->d_mem;
+  m.d_time = c->d_time;
+  m.d_static = c->d_static;
+  m.d_attn = c->d_attn;
+  m.d_hidden = c->d_hidden;
+  m.d_e = c->d_e;
+  m.n_neighbors = c->n_neighbors;
+  m.num_nodes = c->num_nodes;
+  m.max_t = c->max_t;
+  return m;
+}
+
+host::TrainCfg train_of(const tgnn_train_config* c) {
+  host::TrainCfg t;
+  t.i = c->i;
+  t.j = c->j;
+  t.k = c->k;
+  t.p = c->p;
+  t.q = c->q;
+  t.epochs = c->epochs;
+  t.local_batch = c->local_batch;
+  t.lr_base = c->lr_base;
+  t.seed = c->seed;
+  t.local_batch_ref = c->local_batch_ref;
+  t.neg_groups = c->neg_groups;
+  return t;
+}
+
+void validate_dims(const ModelDims& m) {
+  TGB_REQUIRE(m.d_mem >= 1 && m.d_attn >= 1 && m.d_time >= 0 && m.d_static >= 0 && m.d_e >= 0,
+              kConfig, "model: dimensions must be positive");
+  TGB_REQUIRE(m.d_attn <= 256, kConfig, "model: d_attn above 256 is not supported on device");
+  TGB_REQUIRE(m.n_neighbors >= 0 && m.n_neighbors <= 32, kConfig,
+              "model: n_neighbors must lie in [0, 32] on device");
+  TGB_REQUIRE(m.num_nodes > 0, kConfig, "model: num_nodes must be positive");
+}
+
+// init_params (ref model.hpp:122-141): U(+-1/sqrt(cols)) for every rank-2
+// tensor except omega and the static table, streams keyed by the 1-based
+// tensor slot; omega log-spaced over [1e-5, 1] / max_t.
+std::vector<double> host_init_params(const ModelDims& m, uint64_t seed) {
+  const ParamLayout L = ParamLayout::make(m);
+  std::vector<double> flat(static_cast<size_t>(L.total), 0.0);
+  for (int x = 0; x < tNumTensors; ++x) {
+    const bool rank2 = !(x == tOmega || x == tBz || x == tBr || x == tBh || x == tBq || x == tBk ||
+                         x == tBv || x == tB1 || x == tB2);
+    if (!rank2 || x == tStatic) continue;
+    host::Stream st(host::hash64_3(seed, 0x696e6974ull, static_cast<uint64_t>(x + 1)));
+    const double bound = 1.0 / std::sqrt(static_cast<double>(L.cols[x]));
+    double* p = flat.data() + L.off[x];
+    const int64_t n = L.rows[x] * L.cols[x];
+    for (int64_t q = 0; q < n; ++q) p[q] = -bound + (bound - (-bound)) * st.unit();
+  }
+  const int64_t dt = m.d_time;
+  for (int64_t i = 0; i < dt; ++i) {
+    const double frac = dt == 1 ? 1.0 : static_cast<double>(i) / static_cast<double>(dt - 1);
+    flat[static_cast<size_t>(L.off[tOmega] + i)] =
+        std::pow(10.0, -5.0 * (1.0 - frac)) / std::max(m.max_t, 1e-12);
+  }
+  return flat;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- handles
+struct tgnn_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int* d_flag = nullptr;
+
+  void check_numeric() {
+    int f = 0;
+    TGB_CUDA(cudaMemcpyAsync(&f, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    TGB_CUDA(cudaStreamSynchronize(stream));
+    if (f) {
+      TGB_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
+      throw Error(kNumeric, "non-finite value in the training step");
+    }
+  }
+  void use() const { TGB_CUDA(cudaSetDevice(device)); }
+};
+
+struct tgnn_graph {
+  tgnn_ctx* ctx = nullptr;
+  DGraph d;
+  std::vector<int32_t> h_src, h_dst;
+  std::vector<double> h_t;
+  ~tgnn_graph() {
+    void* ptrs[] = {d.src, d.dst, d.t, d.inc_ptr, d.inc_t, d.inc_eid, d.inc_nbr, d.efeat};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+struct tgnn_memstore {
+  tgnn_ctx* ctx = nullptr;
+  DMem d;
+  int32_t* win = nullptr;
+  ~tgnn_memstore() {
+    void* ptrs[] = {d.memory, d.mail_mem, d.last_update, d.mail_t, d.mail_dt, d.mail_ev, win};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+
+void plan_alloc(DPlan& pl, int cap_B, int n, int cap_U, int64_t N) {
+  pl.cap_B = cap_B;
+  pl.n = n;
+  pl.cap_R = 3 * cap_B;
+  pl.cap_P = pl.cap_R * (n > 0 ? n : 1);
+  pl.cap_U = cap_U;
+  pl.args = dalloc<PlanArgs>(1);
+  pl.sizes = dalloc<int32_t>(kSzCount);
+  TGB_CUDA(cudaMemset(pl.sizes, 0, sizeof(int32_t) * kSzCount));
+  pl.negs = dalloc<int32_t>(cap_B);
+  pl.root_node = dalloc<int32_t>(pl.cap_R);
+  pl.root_t = dalloc<double>(pl.cap_R);
+  pl.nbr_cnt = dalloc<int32_t>(pl.cap_R);
+  const size_t slots = static_cast<size_t>(pl.cap_R) * (n > 0 ? n : 1);
+  pl.slot_node = dalloc<int32_t>(slots);
+  pl.slot_event = dalloc<int32_t>(slots);
+  pl.slot_dt = dalloc<double>(slots);
+  pl.pair_ptr = dalloc<int32_t>(pl.cap_R + 1);
+  pl.pair_node = dalloc<int32_t>(pl.cap_P);
+  pl.pair_event = dalloc<int32_t>(pl.cap_P);
+  pl.pair_root = dalloc<int32_t>(pl.cap_P);
+  pl.pair_sup = dalloc<int32_t>(pl.cap_P);
+  pl.pair_dt = dalloc<double>(pl.cap_P);
+  pl.root_sup = dalloc<int32_t>(pl.cap_R);
+  pl.supports = dalloc<int32_t>(cap_U);
+  pl.sup_row = dalloc<int32_t>(static_cast<size_t>(N));
+  const int items = pl.cap_R + pl.cap_P;
+  pl.item_key = dalloc<int32_t>(items);
+  pl.item_val = dalloc<int32_t>(items);
+  pl.item_key_s = dalloc<int32_t>(items);
+  pl.item_val_s = dalloc<int32_t>(items);
+  pl.sup_item_ptr = dalloc<int32_t>(cap_U + 1);
+  int bits = 1;
+  while ((1ll << bits) <= cap_U) ++bits;
+  pl.sort_bits = bits;
+  pl.sort_tmp_bytes = plan_sort_tmp_bytes(items, bits);
+  TGB_CUDA(cudaMalloc(&pl.sort_tmp, pl.sort_tmp_bytes > 0 ? pl.sort_tmp_bytes : 1));
+  pl.bitmap = dalloc<uint32_t>(static_cast<size_t>((N + 31) / 32));
+  TGB_CUDA(cudaMemset(pl.bitmap, 0, sizeof(uint32_t) * ((N + 31) / 32)));
+}
+
+void plan_free(DPlan& pl) {
+  void* ptrs[] = {pl.args, pl.sizes, pl.negs, pl.root_node, pl.root_t, pl.nbr_cnt, pl.slot_node,
+                  pl.slot_event, pl.slot_dt, pl.pair_ptr, pl.pair_node, pl.pair_event, pl.pair_root,
+                  pl.pair_sup, pl.pair_dt, pl.root_sup, pl.supports, pl.sup_row, pl.item_key,
+                  pl.item_val, pl.item_key_s, pl.item_val_s, pl.sup_item_ptr, pl.sort_tmp,
+                  pl.bitmap};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  pl = DPlan{};
+}
+
+void view_alloc(DView& v, int cap_U, int64_t d) {
+  v.cap_U = cap_U;
+  v.mem = dalloc<float>(static_cast<size_t>(cap_U) * d);
+  v.mail_mem = dalloc<float>(static_cast<size_t>(cap_U) * 2 * d);
+  v.mail_t = dalloc<double>(cap_U);
+  v.mail_dt = dalloc<double>(cap_U);
+  v.mail_ev = dalloc<int32_t>(cap_U);
+}
+
+void view_free(DView& v) {
+  void* ptrs[] = {v.mem, v.mail_mem, v.mail_t, v.mail_dt, v.mail_ev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  v = DView{};
+}
+
+int cap_U_for(int64_t N, int cap_B, int64_t n) {
+  const int64_t c = std::min<int64_t>(N, 3ll * cap_B * (n + 1));
+  return static_cast<int>(std::max<int64_t>(c, 1));
+}
+
+}  // namespace
+
+struct tgnn_trainer {
+  tgnn_ctx* ctx = nullptr;
+  tgnn_graph* g = nullptr;
+  ModelDims m;
+  ParamLayout L;
+  uint64_t seed = 1;
+  float *params = nullptr, *grads = nullptr, *am = nullptr, *av = nullptr;
+  int64_t adam_t = 0;
+  StepWork w;
+  std::vector<DPlan> plans;
+  std::vector<DView> views;
+  double* d_loss = nullptr;
+  int cap_B = 0, cap_U = 0;
+  int last_U = -1;
+
+  StepCtx sc() {
+    StepCtx c;
+    c.m = m;
+    c.L = L;
+    c.g = &g->d;
+    c.params = params;
+    c.grads = grads;
+    c.w = &w;
+    c.d_numeric_flag = ctx->d_flag;
+    return c;
+  }
+
+  void init(tgnn_ctx* cx, tgnn_graph* gr, const ModelDims& md, int64_t max_local_batch, uint64_t sd,
+            int subs) {
+    ctx = cx;
+    g = gr;
+    m = md;
+    if (m.num_nodes <= 0) m.num_nodes = gr->d.N;
+    TGB_REQUIRE(m.num_nodes == gr->d.N, kConfig, "model num_nodes does not match the dataset");
+    TGB_REQUIRE(m.d_e == gr->d.d_e, kConfig, "model edge feature width does not match the dataset");
+    validate_dims(m);
+    TGB_REQUIRE(max_local_batch >= 1 && max_local_batch <= (1 << 24), kConfig,
+                "trainer: local batch out of range");
+    L = ParamLayout::make(m);
+    seed = sd;
+    cap_B = static_cast<int>(max_local_batch);
+    cap_U = cap_U_for(m.num_nodes, cap_B, m.n_neighbors);
+    params = dalloc<float>(L.total);
+    grads = dalloc<float>(L.total);
+    am = dalloc<float>(L.total);
+    av = dalloc<float>(L.total);
+    TGB_CUDA(cudaMemset(grads, 0, sizeof(float) * L.total));
+    TGB_CUDA(cudaMemset(am, 0, sizeof(float) * L.total));
+    TGB_CUDA(cudaMemset(av, 0, sizeof(float) * L.total));
+    set_params(host_init_params(m, seed).data());
+    step_alloc(w, m, cap_B, cap_U, m.num_nodes);
+    plans.resize(static_cast<size_t>(subs));
+    views.resize(static_cast<size_t>(subs));
+    for (int s = 0; s < subs; ++s) {
+      plan_alloc(plans[static_cast<size_t>(s)], cap_B, static_cast<int>(m.n_neighbors), cap_U, m.num_nodes);
+      view_alloc(views[static_cast<size_t>(s)], cap_U, m.d_mem);
+    }
+    d_loss = dalloc<double>(1);
+  }
+
+  void set_params(const double* flat) {
+    std::vector<float> f(static_cast<size_t>(L.total));
+    for (int64_t x = 0; x < L.total; ++x) f[static_cast<size_t>(x)] = static_cast<float>(flat[x]);
+    TGB_CUDA(cudaMemcpy(params, f.data(), sizeof(float) * f.size(), cudaMemcpyHostToDevice));
+  }
+  void get_flat(const float* src, double* out) {
+    std::vector<float> f(static_cast<size_t>(L.total));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    TGB_CUDA(cudaMemcpy(f.data(), src, sizeof(float) * f.size(), cudaMemcpyDeviceToHost));
+    for (int64_t x = 0; x < L.total; ++x) out[x] = f[static_cast<size_t>(x)];
+  }
+
+  void adam(double lr, float grad_scale) {
+    ++adam_t;
+    const double c1 = 1.0 - std::pow(0.9, static_cast<double>(adam_t));
+    const double c2 = 1.0 - std::pow(0.999, static_cast<double>(adam_t));
+    adam_launch(params, grads, am, av, L.total, static_cast<float>(lr), static_cast<float>(c1),
+                static_cast<float>(c2), grad_scale, ctx->stream);
+  }
+
+  ~tgnn_trainer() {
+    step_free(w);
+    for (auto& p : plans) plan_free(p);
+    for (auto& v : views) view_free(v);
+    void* ptrs[] = {params, grads, am, av, d_loss};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+struct tgnn_run {
+  tgnn_ctx* ctx = nullptr;
+  tgnn_graph* g = nullptr;
+  std::unique_ptr<tgnn_trainer> tr;
+  std::unique_ptr<tgnn_memstore> mem;
+  host::Schedule sched;
+  host::TrainCfg tc;
+  int rank = 0, nranks = 1;
+  int group = 0, team = 0, member = 0, group_size = 1;
+  ncclComm_t comm = nullptr, gcomm = nullptr;
+  bool comm_ready = false;
+  double* d_losses = nullptr;
+  void* gathered = nullptr;  // [i, wpack_bytes]
+  int64_t next_barrier = 0;
+  int64_t launches = -1;
+  PhaseMarks marks;
+  bool marks_ready = false;
+
+  ~tgnn_run() {
+    if (gcomm) ncclCommDestroy(gcomm);
+    if (comm) ncclCommDestroy(comm);
+    if (d_losses) cudaFree(d_losses);
+    if (gathered) cudaFree(gathered);
+  }
+};
+
+// ----------------------------------------------------------------- runtime pieces
+namespace {
+
+tgnn_memstore* memstore_new(tgnn_ctx* ctx, int64_t N, int64_t d) {
+  TGB_REQUIRE(N > 0 && d > 0, kConfig, "memstore: invalid shape");
+  auto* m = new tgnn_memstore();
+  m->ctx = ctx;
+  m->d.N = N;
+  m->d.d = d;
+  m->d.memory = dalloc<float>(static_cast<size_t>(N * d));
+  m->d.mail_mem = dalloc<float>(static_cast<size_t>(N * 2 * d));
+  m->d.last_update = dalloc<double>(N);
+  m->d.mail_t = dalloc<double>(N);
+  m->d.mail_dt = dalloc<double>(N);
+  m->d.mail_ev = dalloc<int32_t>(N);
+  m->win = dalloc<int32_t>(N);
+  TGB_CUDA(cudaMemset(m->win, 0, sizeof(int32_t) * N));
+  reset_state_launch(m->d, ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return m;
+}
+
+void upload_view(tgnn_trainer* tr, DView& v, int U, const double* view_mem, const double* view_mail) {
+  const int64_t d = tr->m.d_mem, mw = 2 * d + 3;
+  std::vector<float> mem(static_cast<size_t>(U * d)), mail(static_cast<size_t>(U * 2 * d));
+  std::vector<double> mt(U), mdt(U);
+  std::vector<int32_t> mev(U);
+  for (int64_t u = 0; u < U; ++u) {
+    for (int64_t x = 0; x < d; ++x) mem[u * d + x] = static_cast<float>(view_mem[u * d + x]);
+    for (int64_t x = 0; x < 2 * d; ++x) mail[u * 2 * d + x] = static_cast<float>(view_mail[u * mw + x]);
+    mt[u] = view_mail[u * mw + 2 * d];
+    mdt[u] = view_mail[u * mw + 2 * d + 1];
+    mev[u] = static_cast<int32_t>(view_mail[u * mw + 2 * d + 2]);
+  }
+  TGB_CUDA(cudaMemcpy(v.mem, mem.data(), sizeof(float) * mem.size(), cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(v.mail_mem, mail.data(), sizeof(float) * mail.size(), cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(v.mail_t, mt.data(), sizeof(double) * U, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(v.mail_dt, mdt.data(), sizeof(double) * U, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(v.mail_ev, mev.data(), sizeof(int32_t) * U, cudaMemcpyHostToDevice));
+}
+
+int plan_size(tgnn_ctx* ctx, const DPlan& pl, SizeIdx which) {
+  int32_t sz[kSzCount];
+  TGB_CUDA(cudaMemcpyAsync(sz, pl.sizes, sizeof(sz), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return sz[which];
+}
+
+// Plan with explicit negatives (parity path) on plans[slot].
+void plan_explicit(tgnn_trainer* tr, int slot, int64_t begin, int64_t end, const int64_t* negatives) {
+  tgnn_ctx* ctx = tr->ctx;
+  const DGraph& g = tr->g->d;
+  TGB_REQUIRE(begin >= 0 && end <= g.E && begin <= end, kConfig,
+              "plan_sub_batch: event range out of bounds");
+  TGB_REQUIRE(end - begin <= tr->cap_B, kConfig, "plan_sub_batch: slice exceeds the trainer capacity");
+  DPlan& pl = tr->plans[static_cast<size_t>(slot)];
+  const int64_t B = end - begin;
+  std::vector<int32_t> negs(static_cast<size_t>(B));
+  for (int64_t x = 0; x < B; ++x) {
+    TGB_REQUIRE(negatives[x] >= 0 && negatives[x] < g.N, kConfig, "plan_sub_batch: negative out of range");
+    negs[static_cast<size_t>(x)] = static_cast<int32_t>(negatives[x]);
+  }
+  TGB_CUDA(cudaMemcpyAsync(pl.negs, negs.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, ctx->stream));
+  PlanArgs a;
+  a.begin = begin;
+  a.end = end;
+  a.batch_begin = begin;
+  a.seed = tr->seed;
+  a.neg_mode = 0;
+  a.valid = 1;
+  set_plan_args_launch(pl.args, a, ctx->stream);
+  plan_launch(g, pl, ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// One barrier of a run on this rank (TrainerCore::iterate + the daemon's
+// read/write brackets + average_active_grads + Adam::step).
+void run_barrier(tgnn_run* r, int64_t b) {
+  tgnn_ctx* ctx = r->ctx;
+  tgnn_trainer* tr = r->tr.get();
+  cudaStream_t s = ctx->stream;
+  const host::TrainCfg& c = r->tc;
+  const host::Task t = r->sched.task(r->rank, b);
+  StepCtx sc = tr->sc();
+  sc.marks = r->marks.on ? &r->marks : nullptr;
+  sc.mark(phPlan, s);
+  double* loss_slot = r->d_losses + b;
+  const int i = c.i, j = c.j;
+  if (b % j == 0) {
+    // Stint start: the group's teams read and write in pair order (the
+    // daemon plan's R/W brackets, parallel.hpp:278-291). A team publishes its
+    // root writes right after its GRU freshen; the rows are identical to the
+    // reference's post-step writes (they depend only on the read view and s_hat).
+    for (int tt = 0; tt < j; ++tt) {
+      const int probe = r->group * i * j + tt * i;  // member 0 of team tt
+      const host::Task tk = r->sched.task(probe, b);
+      if (!tk.active) continue;
+      if (tk.reset_before) reset_state_launch(r->mem->d, s);
+      if (tt == r->team) {
+        for (int sub = 0; sub < t.subs; ++sub) {
+          PlanArgs a;
+          a.begin = t.slice_begin;
+          a.end = t.slice_end;
+          a.batch_begin = t.batch_begin;
+          a.batch_index = t.batch;
+          a.group = t.neg_group[static_cast<size_t>(sub)];
+          a.seed = c.seed;
+          a.neg_mode = 1;
+          a.valid = 1;
+          DPlan& pl = tr->plans[static_cast<size_t>(sub)];
+          set_plan_args_launch(pl.args, a, s);
+          plan_launch(r->g->d, pl, s);
+          gather_view_launch(pl, r->mem->d, tr->views[static_cast<size_t>(sub)], s);
+        }
+        substep_gru_launch(sc, tr->plans[0], tr->views[0], s);
+        sc.mark(phWrites, s);
+        root_writes_launch(sc, tr->plans[0], tr->views[0], s);
+      }
+      const size_t pb = tr->w.wpack_bytes;
+      const int cap = 2 * tr->cap_B;
+      if (r->group_size > 1) {
+        NCCL_CHECK(ncclGroupStart());
+        for (int mm = 0; mm < i; ++mm) {
+          const int root = tt * i + mm;
+          char* dst = static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb;
+          NCCL_CHECK(ncclBroadcast(tr->w.wpack, dst, pb, ncclChar, root, r->gcomm, s));
+        }
+        NCCL_CHECK(ncclGroupEnd());
+        std::vector<WriteSet> sets;
+        for (int mm = 0; mm < i; ++mm)
+          sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap,
+                                   tr->m.d_mem));
+        apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+      } else {
+        apply_writes_launch({pack_view(tr->w.wpack, cap, tr->m.d_mem)}, r->mem->d, r->mem->win, s);
+      }
+    }
+    if (t.active) {
+      substep_rest_launch(sc, tr->plans[0], tr->views[0], loss_slot, s);
+    } else {
+      TGB_CUDA(cudaMemsetAsync(tr->grads, 0, sizeof(float) * tr->L.total, s));
+      TGB_CUDA(cudaMemsetAsync(loss_slot, 0, sizeof(double), s));
+    }
+  } else {
+    if (t.active) {
+      substep_launch(sc, tr->plans[static_cast<size_t>(t.sub)], tr->views[static_cast<size_t>(t.sub)],
+                     loss_slot, s);
+    } else {
+      TGB_CUDA(cudaMemsetAsync(tr->grads, 0, sizeof(float) * tr->L.total, s));
+      TGB_CUDA(cudaMemsetAsync(loss_slot, 0, sizeof(double), s));
+    }
+  }
+  // average_active_grads (trainer.hpp:473-483): idle ranks contribute zeros.
+  sc.mark(phAllreduce, s);
+  if (r->nranks > 1)
+    NCCL_CHECK(ncclAllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
+                             r->comm, s));
+  const int64_t active = r->sched.active_trainers[static_cast<size_t>(b)];
+  sc.mark(phAdam, s);
+  tr->adam(c.lr_eff(), 1.0f / static_cast<float>(active > 0 ? active : 1));
+  sc.mark(phCount, s);
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- C ABI
+extern "C" {
+
+const char* tgnn_last_error(void) { return g_err.c_str(); }
+int tgnn_version(void) { return 1; }
+
+int tgnn_device_count(int* out) {
+  API_BEGIN
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *out = n;
+  API_END
+}
+
+int tgnn_ctx_create(int device, tgnn_ctx** out) {
+  API_BEGIN
+  TGB_CUDA(cudaSetDevice(device));
+  auto* c = new tgnn_ctx();
+  c->device = device;
+  TGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->d_flag = dalloc<int>(1);
+  TGB_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
+  *out = c;
+  API_END
+}
+
+int tgnn_ctx_destroy(tgnn_ctx* ctx) {
+  API_BEGIN
+  if (!ctx) return 0;
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_flag);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  API_END
+}
+
+int tgnn_ctx_synchronize(tgnn_ctx* ctx) {
+  API_BEGIN
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int tgnn_ctx_stream(tgnn_ctx* ctx, void** stream_out) {
+  API_BEGIN
+  *stream_out = reinterpret_cast<void*>(ctx->stream);
+  API_END
+}
+
+int tgnn_gen_synthetic(const tgnn_synth_params* p, int64_t* src, int64_t* dst, double* t,
+                       float* efeat, int64_t* bipartite_boundary) {
+  API_BEGIN
+  host::SynthConfig c;
+  c.nodes = p->nodes;
+  c.events = p->events;
+  c.burst_prob = p->burst_prob;
+  c.pref_prob = p->pref_prob;
+  c.prefs_per_src = p->prefs_per_src;
+  c.src_frac = p->src_frac;
+  c.bipartite = p->bipartite != 0;
+  c.d_e = p->d_e;
+  c.zipf_s = p->zipf_s;
+  c.seed = p->seed;
+  *bipartite_boundary = host::synthesize(c, src, dst, t, efeat);
+  API_END
+}
+
+namespace {
+
+int graph_create_impl(tgnn_ctx* ctx, int64_t num_nodes, int64_t boundary, int64_t E,
+                      const int64_t* src, const int64_t* dst, const double* t, const float* ef32,
+                      const double* ef64, int64_t d_e, tgnn_graph** out) {
+  API_BEGIN
+  ctx->use();
+  // TemporalGraph::finalize (temporal_graph.hpp:55-91)
+  TGB_REQUIRE(num_nodes > 0, kConfig, "graph: num_nodes must be positive");
+  TGB_REQUIRE(num_nodes < (1ll << 31) && E < (1ll << 31), kConfig, "graph: too large for int32 ids");
+  if (boundary >= 0)
+    TGB_REQUIRE(boundary > 0 && boundary < num_nodes, kConfig,
+                "graph: bipartite boundary leaves an empty partition");
+  TGB_REQUIRE(E >= 0 && d_e >= 0, kConfig, "graph: invalid sizes");
+  std::vector<int64_t> order(static_cast<size_t>(E));
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return t[a] < t[b]; });
+  auto g = std::make_unique<tgnn_graph>();
+  g->ctx = ctx;
+  g->h_src.resize(static_cast<size_t>(E));
+  g->h_dst.resize(static_cast<size_t>(E));
+  g->h_t.resize(static_cast<size_t>(E));
+  std::vector<int64_t> deg(static_cast<size_t>(num_nodes) + 1, 0);
+  for (int64_t e = 0; e < E; ++e) {
+    const int64_t o = order[static_cast<size_t>(e)];
+    const int64_t s = src[o], d = dst[o];
+    if (s < 0 || s >= num_nodes || d < 0 || d >= num_nodes)
+      throw Error(kConfig, "graph: node id out of range at event " + std::to_string(e));
+    if (boundary >= 0 && !(s < boundary && d >= boundary))
+      throw Error(kConfig, "graph: event " + std::to_string(e) + " does not cross the bipartite boundary");
+    g->h_src[static_cast<size_t>(e)] = static_cast<int32_t>(s);
+    g->h_dst[static_cast<size_t>(e)] = static_cast<int32_t>(d);
+    g->h_t[static_cast<size_t>(e)] = t[o];
+    ++deg[static_cast<size_t>(s) + 1];
+    ++deg[static_cast<size_t>(d) + 1];
+  }
+  for (int64_t v = 0; v < num_nodes; ++v) deg[static_cast<size_t>(v) + 1] += deg[static_cast<size_t>(v)];
+  // T-CSR: per-node ascending (t, event id) incidence; each event is listed
+  // under src then dst (a self-loop twice), temporal_graph.hpp:78-90.
+  const int64_t M = 2 * E;
+  std::vector<int32_t> inc_eid(static_cast<size_t>(M)), inc_nbr(static_cast<size_t>(M));
+  std::vector<double> inc_t(static_cast<size_t>(M));
+  std::vector<int64_t> cur(deg.begin(), deg.end() - 1);
+  for (int64_t e = 0; e < E; ++e) {
+    const int32_t s = g->h_src[static_cast<size_t>(e)], d = g->h_dst[static_cast<size_t>(e)];
+    for (int side = 0; side < 2; ++side) {
+      const int32_t v = side == 0 ? s : d;
+      const int64_t at = cur[static_cast<size_t>(v)]++;
+      inc_eid[static_cast<size_t>(at)] = static_cast<int32_t>(e);
+      inc_nbr[static_cast<size_t>(at)] = s == v ? d : s;
+      inc_t[static_cast<size_t>(at)] = g->h_t[static_cast<size_t>(e)];
+    }
+  }
+  DGraph& D = g->d;
+  D.N = num_nodes;
+  D.boundary = boundary;
+  D.E = E;
+  D.d_e = d_e;
+  D.d_e_pad = (d_e + 3) / 4 * 4;
+  D.src = dalloc<int32_t>(E);
+  D.dst = dalloc<int32_t>(E);
+  D.t = dalloc<double>(E);
+  D.inc_ptr = dalloc<int64_t>(num_nodes + 1);
+  D.inc_t = dalloc<double>(M);
+  D.inc_eid = dalloc<int32_t>(M);
+  D.inc_nbr = dalloc<int32_t>(M);
+  D.efeat = dalloc<float>(static_cast<size_t>(E * std::max<int64_t>(D.d_e_pad, 1)));
+  TGB_CUDA(cudaMemcpy(D.src, g->h_src.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(D.dst, g->h_dst.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(D.t, g->h_t.data(), sizeof(double) * E, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(D.inc_ptr, deg.data(), sizeof(int64_t) * (num_nodes + 1), cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(D.inc_t, inc_t.data(), sizeof(double) * M, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(D.inc_eid, inc_eid.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(D.inc_nbr, inc_nbr.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice));
+  if (d_e > 0) {
+    // padded fp32 rows, uploaded in chunks to bound host staging
+    const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / (4 * D.d_e_pad));
+    std::vector<float> buf(static_cast<size_t>(std::min(chunk, E) * D.d_e_pad), 0.0f);
+    for (int64_t e0 = 0; e0 < E; e0 += chunk) {
+      const int64_t e1 = std::min(E, e0 + chunk);
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t o = order[static_cast<size_t>(e)];
+        float* row = buf.data() + (e - e0) * D.d_e_pad;
+        for (int64_t f = 0; f < d_e; ++f)
+          row[f] = ef32 ? ef32[o * d_e + f] : static_cast<float>(ef64[o * d_e + f]);
+      }
+      TGB_CUDA(cudaMemcpy(D.efeat + e0 * D.d_e_pad, buf.data(), sizeof(float) * (e1 - e0) * D.d_e_pad,
+                          cudaMemcpyHostToDevice));
+    }
+  }
+  *out = g.release();
+  API_END
+}
+
+}  // namespace
+
+int tgnn_graph_create(tgnn_ctx* ctx, int64_t num_nodes, int64_t bipartite_boundary, int64_t num_events,
+                      const int64_t* src, const int64_t* dst, const double* t, const float* efeat,
+                      int64_t d_e, tgnn_graph** out) {
+  return graph_create_impl(ctx, num_nodes, bipartite_boundary, num_events, src, dst, t, efeat, nullptr,
+                           d_e, out);
+}
+
+int tgnn_graph_create_f64(tgnn_ctx* ctx, int64_t num_nodes, int64_t bipartite_boundary,
+                          int64_t num_events, const int64_t* src, const int64_t* dst, const double* t,
+                          const double* efeat, int64_t d_e, tgnn_graph** out) {
+  return graph_create_impl(ctx, num_nodes, bipartite_boundary, num_events, src, dst, t, nullptr, efeat,
+                           d_e, out);
+}
+
+int tgnn_graph_destroy(tgnn_graph* g) {
+  API_BEGIN
+  delete g;
+  API_END
+}
+
+int tgnn_graph_info(tgnn_graph* g, int64_t* num_nodes, int64_t* boundary, int64_t* num_events,
+                    int64_t* d_e) {
+  API_BEGIN
+  *num_nodes = g->d.N;
+  *boundary = g->d.boundary;
+  *num_events = g->d.E;
+  *d_e = g->d.d_e;
+  API_END
+}
+
+int tgnn_graph_events(tgnn_graph* g, int64_t* src, int64_t* dst, double* t) {
+  API_BEGIN
+  for (int64_t e = 0; e < g->d.E; ++e) {
+    src[e] = g->h_src[static_cast<size_t>(e)];
+    dst[e] = g->h_dst[static_cast<size_t>(e)];
+    t[e] = g->h_t[static_cast<size_t>(e)];
+  }
+  API_END
+}
+
+int tgnn_sample_recent_neighbors(tgnn_graph* g, const int64_t* nodes, const double* times, int64_t count,
+                                 int64_t n, int64_t* nbr_node, int64_t* nbr_event, double* nbr_dt,
+                                 int64_t* nbr_count) {
+  API_BEGIN
+  tgnn_ctx* ctx = g->ctx;
+  ctx->use();
+  TGB_REQUIRE(n >= 0 && n <= 32, kConfig, "sample_recent_neighbors: n must lie in [0, 32]");
+  if (count == 0) return 0;
+  std::vector<int32_t> qn(static_cast<size_t>(count));
+  for (int64_t q = 0; q < count; ++q) {
+    TGB_REQUIRE(nodes[q] >= 0 && nodes[q] < g->d.N, kConfig, "sample_recent_neighbors: node out of range");
+    qn[static_cast<size_t>(q)] = static_cast<int32_t>(nodes[q]);
+  }
+  const int64_t nn = std::max<int64_t>(n, 1);
+  int32_t* d_nodes = dalloc<int32_t>(count);
+  double* d_times = dalloc<double>(count);
+  int32_t* d_nn = dalloc<int32_t>(count * nn);
+  int32_t* d_ne = dalloc<int32_t>(count * nn);
+  double* d_nd = dalloc<double>(count * nn);
+  int32_t* d_c = dalloc<int32_t>(count);
+  h2d(d_nodes, qn.data(), count, ctx->stream);
+  h2d(d_times, times, count, ctx->stream);
+  sample_queries_launch(g->d, d_nodes, d_times, static_cast<int>(count), static_cast<int>(n), d_nn, d_ne,
+                        d_nd, d_c, ctx->stream);
+  std::vector<int32_t> hn(static_cast<size_t>(count * nn)), he(static_cast<size_t>(count * nn)),
+      hc(static_cast<size_t>(count));
+  std::vector<double> hd(static_cast<size_t>(count * nn));
+  d2h(hn.data(), d_nn, count * nn, ctx->stream);
+  d2h(he.data(), d_ne, count * nn, ctx->stream);
+  d2h(hd.data(), d_nd, count * nn, ctx->stream);
+  d2h(hc.data(), d_c, count, ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (void* p : {static_cast<void*>(d_nodes), static_cast<void*>(d_times), static_cast<void*>(d_nn),
+                  static_cast<void*>(d_ne), static_cast<void*>(d_nd), static_cast<void*>(d_c)})
+    cudaFree(p);
+  for (int64_t q = 0; q < count; ++q) {
+    nbr_count[q] = hc[static_cast<size_t>(q)];
+    for (int64_t m = 0; m < n; ++m) {
+      const bool ok = m < hc[static_cast<size_t>(q)];
+      nbr_node[q * n + m] = ok ? hn[static_cast<size_t>(q * n + m)] : -1;
+      nbr_event[q * n + m] = ok ? he[static_cast<size_t>(q * n + m)] : -1;
+      nbr_dt[q * n + m] = ok ? hd[static_cast<size_t>(q * n + m)] : 0.0;
+    }
+  }
+  API_END
+}
+
+int tgnn_sample_negatives(tgnn_graph* g, int64_t batch_index, int64_t group, int64_t count, uint64_t seed,
+                          int64_t* out) {
+  API_BEGIN
+  tgnn_ctx* ctx = g->ctx;
+  ctx->use();
+  const int64_t lo = g->d.boundary >= 0 ? g->d.boundary : 0;
+  TGB_REQUIRE(g->d.N - lo > 0, kConfig, "negative sampling: empty destination partition");
+  if (count <= 0) return 0;
+  DPlan pl;  // only args + negs are used
+  pl.args = dalloc<PlanArgs>(1);
+  int32_t* negs = dalloc<int32_t>(count);
+  PlanArgs a;
+  a.begin = 0;
+  a.end = count;
+  a.batch_begin = 0;
+  a.batch_index = batch_index;
+  a.group = group;
+  a.seed = seed;
+  a.neg_mode = 1;
+  a.valid = 1;
+  set_plan_args_launch(pl.args, a, ctx->stream);
+  pl.negs = negs;
+  pl.cap_B = static_cast<int>(count);
+  negatives_only_launch(g->d, pl.args, static_cast<int>(count), negs, ctx->stream);
+  std::vector<int32_t> h(static_cast<size_t>(count));
+  d2h(h.data(), negs, count, ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(pl.args);
+  cudaFree(negs);
+  for (int64_t x = 0; x < count; ++x) out[x] = h[static_cast<size_t>(x)];
+  API_END
+}
+
+int tgnn_plan_sub_batch(tgnn_graph* g, int64_t begin, int64_t end, const int64_t* negatives, int64_t n,
+                        int64_t* root_node, double* root_t, int64_t* nbr_count, int64_t* nbr_node,
+                        int64_t* nbr_event, double* nbr_dt, int64_t* supports, int64_t* num_supports) {
+  API_BEGIN
+  tgnn_ctx* ctx = g->ctx;
+  ctx->use();
+  TGB_REQUIRE(n >= 0 && n <= 32, kConfig, "plan_sub_batch: n must lie in [0, 32]");
+  TGB_REQUIRE(begin >= 0 && end <= g->d.E && begin <= end, kConfig,
+              "plan_sub_batch: event range out of bounds");
+  const int64_t B = end - begin;
+  if (B == 0) {
+    *num_supports = 0;
+    return 0;
+  }
+  tgnn_trainer tmp;  // plan-only harness: one plan, no model
+  tmp.ctx = ctx;
+  tmp.g = g;
+  tmp.cap_B = static_cast<int>(B);
+  tmp.seed = 0;
+  tmp.plans.resize(1);
+  const int capU = cap_U_for(g->d.N, static_cast<int>(B), n);
+  plan_alloc(tmp.plans[0], static_cast<int>(B), static_cast<int>(n), capU, g->d.N);
+  plan_explicit(&tmp, 0, begin, end, negatives);
+  DPlan& pl = tmp.plans[0];
+  const int R = static_cast<int>(3 * B);
+  const int nn = static_cast<int>(std::max<int64_t>(n, 1));
+  std::vector<int32_t> rn(R), cnt(R), sn(static_cast<size_t>(R) * nn), se(static_cast<size_t>(R) * nn),
+      sup(static_cast<size_t>(capU));
+  std::vector<double> rt(R), sd(static_cast<size_t>(R) * nn);
+  int32_t sz[kSzCount];
+  d2h(sz, pl.sizes, kSzCount, ctx->stream);
+  d2h(rn.data(), pl.root_node, R, ctx->stream);
+  d2h(rt.data(), pl.root_t, R, ctx->stream);
+  d2h(cnt.data(), pl.nbr_cnt, R, ctx->stream);
+  if (n > 0) {
+    d2h(sn.data(), pl.slot_node, static_cast<size_t>(R) * n, ctx->stream);
+    d2h(se.data(), pl.slot_event, static_cast<size_t>(R) * n, ctx->stream);
+    d2h(sd.data(), pl.slot_dt, static_cast<size_t>(R) * n, ctx->stream);
+  }
+  d2h(sup.data(), pl.supports, capU, ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int r = 0; r < R; ++r) {
+    root_node[r] = rn[r];
+    root_t[r] = rt[r];
+    nbr_count[r] = cnt[r];
+    for (int64_t m = 0; m < n; ++m) {
+      const bool ok = m < cnt[r];
+      nbr_node[r * n + m] = ok ? sn[r * n + m] : -1;
+      nbr_event[r * n + m] = ok ? se[r * n + m] : -1;
+      nbr_dt[r * n + m] = ok ? sd[r * n + m] : 0.0;
+    }
+  }
+  *num_supports = sz[kSzU];
+  for (int u = 0; u < sz[kSzU]; ++u) supports[u] = sup[static_cast<size_t>(u)];
+  plan_free(tmp.plans[0]);
+  tmp.plans.clear();
+  API_END
+}
+
+// ----------------------------------------------------------------- memstore
+int tgnn_memstore_create(tgnn_ctx* ctx, int64_t num_nodes, int64_t d_mem, tgnn_memstore** out) {
+  API_BEGIN
+  ctx->use();
+  *out = memstore_new(ctx, num_nodes, d_mem);
+  API_END
+}
+
+int tgnn_memstore_destroy(tgnn_memstore* m) {
+  API_BEGIN
+  delete m;
+  API_END
+}
+
+int tgnn_memstore_reset(tgnn_memstore* m) {
+  API_BEGIN
+  m->ctx->use();
+  reset_state_launch(m->d, m->ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  API_END
+}
+
+int tgnn_memstore_export(tgnn_memstore* m, double* memory, double* last_update, double* mail_mem,
+                         double* mail_t, double* mail_dt, int64_t* mail_event) {
+  API_BEGIN
+  m->ctx->use();
+  const int64_t N = m->d.N, d = m->d.d;
+  cudaStream_t s = m->ctx->stream;
+  std::vector<float> mem(static_cast<size_t>(N * d)), mail(static_cast<size_t>(N * 2 * d));
+  std::vector<double> lu(N), mt(N), mdt(N);
+  std::vector<int32_t> ev(N);
+  d2h(mem.data(), m->d.memory, mem.size(), s);
+  d2h(mail.data(), m->d.mail_mem, mail.size(), s);
+  d2h(lu.data(), m->d.last_update, N, s);
+  d2h(mt.data(), m->d.mail_t, N, s);
+  d2h(mdt.data(), m->d.mail_dt, N, s);
+  d2h(ev.data(), m->d.mail_ev, N, s);
+  TGB_CUDA(cudaStreamSynchronize(s));
+  if (memory) for (size_t x = 0; x < mem.size(); ++x) memory[x] = mem[x];
+  if (mail_mem) for (size_t x = 0; x < mail.size(); ++x) mail_mem[x] = mail[x];
+  for (int64_t v = 0; v < N; ++v) {
+    if (last_update) last_update[v] = lu[v];
+    if (mail_t) mail_t[v] = mt[v];
+    if (mail_dt) mail_dt[v] = mdt[v];
+    if (mail_event) mail_event[v] = ev[v];
+  }
+  API_END
+}
+
+int tgnn_memstore_import(tgnn_memstore* m, const double* memory, const double* last_update,
+                         const double* mail_mem, const double* mail_t, const double* mail_dt,
+                         const int64_t* mail_event) {
+  API_BEGIN
+  m->ctx->use();
+  const int64_t N = m->d.N, d = m->d.d;
+  std::vector<float> mem(static_cast<size_t>(N * d)), mail(static_cast<size_t>(N * 2 * d));
+  std::vector<int32_t> ev(N);
+  for (size_t x = 0; x < mem.size(); ++x) mem[x] = static_cast<float>(memory[x]);
+  for (size_t x = 0; x < mail.size(); ++x) mail[x] = static_cast<float>(mail_mem[x]);
+  for (int64_t v = 0; v < N; ++v) ev[v] = static_cast<int32_t>(mail_event[v]);
+  TGB_CUDA(cudaMemcpy(m->d.memory, mem.data(), sizeof(float) * mem.size(), cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(m->d.mail_mem, mail.data(), sizeof(float) * mail.size(), cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(m->d.last_update, last_update, sizeof(double) * N, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(m->d.mail_t, mail_t, sizeof(double) * N, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(m->d.mail_dt, mail_dt, sizeof(double) * N, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(m->d.mail_ev, ev.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+  API_END
+}
+
+int tgnn_memstore_read(tgnn_memstore* m, const int64_t* nodes, int64_t count, double* mem_rows,
+                       double* mail_rows) {
+  API_BEGIN
+  m->ctx->use();
+  const int64_t N = m->d.N, d = m->d.d;
+  for (int64_t x = 0; x < count; ++x)
+    TGB_REQUIRE(nodes[x] >= 0 && nodes[x] < N, kProtocol, "read: index out of range");
+  std::vector<double> mem(static_cast<size_t>(N * d)), mail(static_cast<size_t>(N * 2 * d)), mt(N), mdt(N),
+      lu(N);
+  std::vector<int64_t> ev(N);
+  int rc = tgnn_memstore_export(m, mem.data(), lu.data(), mail.data(), mt.data(), mdt.data(), ev.data());
+  if (rc) return rc;
+  const int64_t mw = 2 * d + 3;
+  for (int64_t x = 0; x < count; ++x) {
+    const int64_t v = nodes[x];
+    for (int64_t q = 0; q < d; ++q) mem_rows[x * d + q] = mem[v * d + q];
+    for (int64_t q = 0; q < 2 * d; ++q) mail_rows[x * mw + q] = mail[v * 2 * d + q];
+    mail_rows[x * mw + 2 * d] = mt[v];
+    mail_rows[x * mw + 2 * d + 1] = mdt[v];
+    mail_rows[x * mw + 2 * d + 2] = static_cast<double>(ev[v]);
+  }
+  API_END
+}
+
+int tgnn_memstore_write(tgnn_memstore* m, const int64_t* nodes, int64_t count, const double* mem_rows,
+                        const double* mail_rows) {
+  API_BEGIN
+  m->ctx->use();
+  const int64_t N = m->d.N, d = m->d.d, mw = 2 * d + 3;
+  if (count == 0) return 0;
+  // later rows win (apply_root_write in row order): keep the last row per node
+  std::vector<int64_t> keep;
+  {
+    std::vector<int64_t> last(static_cast<size_t>(N), -1);
+    for (int64_t x = 0; x < count; ++x) {
+      TGB_REQUIRE(nodes[x] >= 0 && nodes[x] < N, kProtocol, "write: index out of range");
+      last[static_cast<size_t>(nodes[x])] = x;
+    }
+    for (int64_t x = 0; x < count; ++x)
+      if (last[static_cast<size_t>(nodes[x])] == x) keep.push_back(x);
+  }
+  const int K = static_cast<int>(keep.size());
+  const size_t bytes = pack_bytes(K, d);
+  std::vector<char> host(bytes, 0);
+  WriteSet v = pack_view(host.data(), K, d);
+  *const_cast<int32_t*>(v.count) = K;
+  for (int q = 0; q < K; ++q) {
+    const int64_t x = keep[static_cast<size_t>(q)];
+    const_cast<int32_t*>(v.node)[q] = static_cast<int32_t>(nodes[x]);
+    const_cast<int32_t*>(v.event)[q] = static_cast<int32_t>(mail_rows[x * mw + 2 * d + 2]);
+    const_cast<double*>(v.t)[q] = mail_rows[x * mw + 2 * d];
+    const_cast<double*>(v.dt)[q] = mail_rows[x * mw + 2 * d + 1];
+    for (int64_t i = 0; i < d; ++i) const_cast<float*>(v.mem)[q * d + i] = static_cast<float>(mem_rows[x * d + i]);
+    for (int64_t i = 0; i < 2 * d; ++i)
+      const_cast<float*>(v.mail)[q * 2 * d + i] = static_cast<float>(mail_rows[x * mw + i]);
+  }
+  void* dev = nullptr;
+  TGB_CUDA(cudaMalloc(&dev, bytes));
+  TGB_CUDA(cudaMemcpy(dev, host.data(), bytes, cudaMemcpyHostToDevice));
+  apply_writes_launch({pack_view(dev, K, d)}, m->d, m->win, m->ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  cudaFree(dev);
+  API_END
+}
+
+// ----------------------------------------------------------------- trainer
+int tgnn_param_count(const tgnn_model_config* m, int64_t* out) {
+  API_BEGIN
+  *out = ParamLayout::make(dims_of(m)).total;
+  API_END
+}
+
+int tgnn_init_params(const tgnn_model_config* m, uint64_t seed, double* flat) {
+  API_BEGIN
+  auto v = host_init_params(dims_of(m), seed);
+  std::memcpy(flat, v.data(), sizeof(double) * v.size());
+  API_END
+}
+
+int tgnn_trainer_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_model_config* m, int64_t max_local_batch,
+                        uint64_t seed, tgnn_trainer** out) {
+  API_BEGIN
+  ctx->use();
+  auto tr = std::make_unique<tgnn_trainer>();
+  tr->init(ctx, g, dims_of(m), max_local_batch, seed, 1);
+  *out = tr.release();
+  API_END
+}
+
+int tgnn_trainer_destroy(tgnn_trainer* tr) {
+  API_BEGIN
+  delete tr;
+  API_END
+}
+
+int tgnn_trainer_set_params(tgnn_trainer* tr, const double* flat) {
+  API_BEGIN
+  tr->ctx->use();
+  TGB_CUDA(cudaStreamSynchronize(tr->ctx->stream));
+  tr->set_params(flat);
+  API_END
+}
+
+int tgnn_trainer_get_params(tgnn_trainer* tr, double* flat) {
+  API_BEGIN
+  tr->ctx->use();
+  tr->get_flat(tr->params, flat);
+  API_END
+}
+
+int tgnn_trainer_get_grads(tgnn_trainer* tr, double* flat) {
+  API_BEGIN
+  tr->ctx->use();
+  tr->get_flat(tr->grads, flat);
+  API_END
+}
+
+int tgnn_trainer_sub_step(tgnn_trainer* tr, int64_t begin, int64_t end, const int64_t* negatives,
+                          const double* view_mem, const double* view_mail, double* loss_out,
+                          double* s_hat_out) {
+  API_BEGIN
+  tgnn_ctx* ctx = tr->ctx;
+  ctx->use();
+  plan_explicit(tr, 0, begin, end, negatives);
+  const int U = plan_size(ctx, tr->plans[0], kSzU);
+  upload_view(tr, tr->views[0], U, view_mem, view_mail);
+  substep_launch(tr->sc(), tr->plans[0], tr->views[0], tr->d_loss, ctx->stream);
+  double loss = 0;
+  d2h(&loss, tr->d_loss, 1, ctx->stream);
+  ctx->check_numeric();
+  *loss_out = loss;
+  tr->last_U = U;
+  if (s_hat_out) {
+    const int64_t d = tr->m.d_mem;
+    std::vector<float> sh(static_cast<size_t>(U * d));
+    d2h(sh.data(), tr->w.s_hat, sh.size(), ctx->stream);
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (size_t x = 0; x < sh.size(); ++x) s_hat_out[x] = sh[x];
+  }
+  API_END
+}
+
+int tgnn_trainer_root_writes(tgnn_trainer* tr, int64_t* nodes, double* mem_rows, double* mail_rows,
+                             int64_t* num_writes) {
+  API_BEGIN
+  tgnn_ctx* ctx = tr->ctx;
+  ctx->use();
+  TGB_REQUIRE(tr->last_U >= 0, kProtocol, "root_writes: no sub_step has run");
+  root_writes_launch(tr->sc(), tr->plans[0], tr->views[0], ctx->stream);
+  const int64_t d = tr->m.d_mem;
+  const int cap = 2 * tr->cap_B;
+  std::vector<char> host(tr->w.wpack_bytes);
+  d2h(host.data(), static_cast<char*>(tr->w.wpack), host.size(), ctx->stream);
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  WriteSet v = pack_view(host.data(), cap, d);
+  const int W = *v.count;
+  std::vector<int> order(W);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return v.node[a] < v.node[b]; });
+  const int64_t mw = 2 * d + 3;
+  for (int q = 0; q < W; ++q) {
+    const int x = order[q];
+    nodes[q] = v.node[x];
+    for (int64_t i = 0; i < d; ++i) mem_rows[q * d + i] = v.mem[x * d + i];
+    for (int64_t i = 0; i < 2 * d; ++i) mail_rows[q * mw + i] = v.mail[x * 2 * d + i];
+    mail_rows[q * mw + 2 * d] = v.t[x];
+    mail_rows[q * mw + 2 * d + 1] = v.dt[x];
+    mail_rows[q * mw + 2 * d + 2] = static_cast<double>(v.event[x]);
+  }
+  *num_writes = W;
+  API_END
+}
+
+int tgnn_trainer_adam_step(tgnn_trainer* tr, double lr) {
+  API_BEGIN
+  tr->ctx->use();
+  tr->adam(lr, 1.0f);
+  TGB_CUDA(cudaStreamSynchronize(tr->ctx->stream));
+  API_END
+}
+
+int tgnn_trainer_iterate(tgnn_trainer* tr, tgnn_memstore* m, int64_t batch_index, int64_t group,
+                         int64_t batch_begin, int64_t begin, int64_t end, double lr, double* loss_out) {
+  API_BEGIN
+  tgnn_ctx* ctx = tr->ctx;
+  ctx->use();
+  cudaStream_t s = ctx->stream;
+  TGB_REQUIRE(begin >= 0 && end <= tr->g->d.E && begin < end && end - begin <= tr->cap_B, kConfig,
+              "iterate: slice out of range");
+  PlanArgs a;
+  a.begin = begin;
+  a.end = end;
+  a.batch_begin = batch_begin;
+  a.batch_index = batch_index;
+  a.group = group;
+  a.seed = tr->seed;
+  a.neg_mode = 1;
+  a.valid = 1;
+  DPlan& pl = tr->plans[0];
+  set_plan_args_launch(pl.args, a, s);
+  plan_launch(tr->g->d, pl, s);
+  gather_view_launch(pl, m->d, tr->views[0], s);
+  StepCtx sc = tr->sc();
+  substep_launch(sc, pl, tr->views[0], tr->d_loss, s);
+  root_writes_launch(sc, pl, tr->views[0], s);
+  apply_writes_launch({pack_view(tr->w.wpack, 2 * tr->cap_B, tr->m.d_mem)}, m->d, m->win, s);
+  tr->adam(lr, 1.0f);
+  double loss = 0;
+  d2h(&loss, tr->d_loss, 1, s);
+  ctx->check_numeric();
+  *loss_out = loss;
+  tr->last_U = -1;
+  API_END
+}
+
+// ----------------------------------------------------------------- runs
+int tgnn_schedule_query(const tgnn_train_config* tc, int64_t train_begin, int64_t train_end, int32_t rank,
+                        int64_t first, int64_t count, int64_t* out, int64_t* barriers_out) {
+  API_BEGIN
+  const host::TrainCfg c = train_of(tc);
+  const host::Schedule sc = host::Schedule::build(c, train_begin, train_end);
+  TGB_REQUIRE(rank >= 0 && rank < c.trainers(), kConfig, "schedule: rank out of range");
+  *barriers_out = sc.barriers;
+  for (int64_t x = 0; x < count; ++x) {
+    const int64_t b = first + x;
+    int64_t* o = out + x * 12;
+    for (int q = 0; q < 12; ++q) o[q] = 0;
+    if (b < 0 || b >= sc.barriers) continue;
+    const host::Task t = sc.task(rank, b);
+    o[0] = t.active;
+    o[1] = t.sub;
+    o[2] = t.subs;
+    o[3] = t.batch;
+    o[4] = t.batch_begin;
+    o[5] = t.batch_end;
+    o[6] = t.slice_begin;
+    o[7] = t.slice_end;
+    o[8] = t.active ? t.neg_group[static_cast<size_t>(t.sub)] : -1;
+    o[9] = t.active && t.sub == 0 && t.reset_before;
+    o[10] = sc.active_trainers[static_cast<size_t>(b)];
+    o[11] = sc.traversed_after[static_cast<size_t>(b)];
+  }
+  API_END
+}
+
+int tgnn_comm_unique_id(char* out128) {
+  API_BEGIN
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  NCCL_CHECK(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, 128);
+  API_END
+}
+
+int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, tgnn_run** out) {
+  API_BEGIN
+  ctx->use();
+  auto r = std::make_unique<tgnn_run>();
+  r->ctx = ctx;
+  r->g = g;
+  r->tc = train_of(&opt->train);
+  r->tc.validate();
+  r->rank = opt->rank;
+  r->nranks = opt->nranks;
+  const int T = r->tc.trainers();
+  TGB_REQUIRE(r->nranks == T, kConfig, "run: one rank per trainer is required (nranks == i*j*k)");
+  TGB_REQUIRE(r->rank >= 0 && r->rank < T, kConfig, "run: rank out of range");
+  r->sched = host::Schedule::build(r->tc, opt->train_begin, opt->train_end);
+  r->group = r->sched.group_of(r->rank);
+  r->team = r->sched.team_of(r->rank);
+  r->member = r->sched.member_of(r->rank);
+  r->group_size = r->tc.i * r->tc.j;
+  ModelDims m = dims_of(&opt->model);
+  r->tr = std::make_unique<tgnn_trainer>();
+  r->tr->init(ctx, g, m, r->tc.local_batch, r->tc.seed, r->tc.j);
+  r->mem.reset(memstore_new(ctx, g->d.N, m.d_mem));
+  r->d_losses = dalloc<double>(static_cast<size_t>(std::max<int64_t>(r->sched.barriers, 1)));
+  TGB_CUDA(cudaMemset(r->d_losses, 0, sizeof(double) * std::max<int64_t>(r->sched.barriers, 1)));
+  if (r->group_size > 1) {
+    TGB_CUDA(cudaMalloc(&r->gathered, r->tr->w.wpack_bytes * static_cast<size_t>(r->tc.i)));
+  }
+  *out = r.release();
+  API_END
+}
+
+int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128) {
+  API_BEGIN
+  r->ctx->use();
+  if (r->nranks == 1) return 0;
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id128, 128);
+  NCCL_CHECK(ncclCommInitRank(&r->comm, r->nranks, id, r->rank));
+  if (r->group_size > 1) {
+    NCCL_CHECK(ncclCommSplit(r->comm, r->group, r->rank, &r->gcomm, nullptr));
+  }
+  r->comm_ready = true;
+  API_END
+}
+
+int tgnn_run_destroy(tgnn_run* r) {
+  API_BEGIN
+  if (r) {
+    cudaSetDevice(r->ctx->device);
+    cudaStreamSynchronize(r->ctx->stream);
+  }
+  delete r;
+  API_END
+}
+
+int tgnn_run_info(tgnn_run* r, int64_t* barriers, int64_t* param_count) {
+  API_BEGIN
+  *barriers = r->sched.barriers;
+  *param_count = r->tr->L.total;
+  API_END
+}
+
+int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(first == r->next_barrier, kProtocol, "run: barriers must be issued in order");
+  TGB_REQUIRE(first + count <= r->sched.barriers, kConfig, "run: barrier range past the schedule");
+  TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
+  for (int64_t b = first; b < first + count; ++b) run_barrier(r, b);
+  r->next_barrier = first + count;
+  API_END
+}
+
+int tgnn_run_losses(tgnn_run* r, int64_t first, int64_t count, double* out) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(first >= 0 && first + count <= r->next_barrier, kConfig, "run: loss range not yet run");
+  cudaStream_t s = r->ctx->stream;
+  double* tmp = dalloc<double>(static_cast<size_t>(std::max<int64_t>(count, 1)));
+  TGB_CUDA(cudaMemcpyAsync(tmp, r->d_losses + first, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+  if (r->nranks > 1)
+    NCCL_CHECK(ncclAllReduce(tmp, tmp, static_cast<size_t>(count), ncclDouble, ncclSum, r->comm, s));
+  d2h(out, tmp, static_cast<size_t>(count), s);
+  r->ctx->check_numeric();
+  cudaFree(tmp);
+  for (int64_t b = 0; b < count; ++b) {
+    const int64_t a = r->sched.active_trainers[static_cast<size_t>(first + b)];
+    out[b] = a > 0 ? out[b] / static_cast<double>(a) : 0.0;
+  }
+  API_END
+}
+
+int tgnn_run_params(tgnn_run* r, double* flat) {
+  API_BEGIN
+  r->ctx->use();
+  r->tr->get_flat(r->tr->params, flat);
+  API_END
+}
+
+int tgnn_run_traversed(tgnn_run* r, int64_t first, int64_t count, int64_t* out) {
+  API_BEGIN
+  const auto& ta = r->sched.traversed_after;
+  TGB_REQUIRE(first >= 0 && first + count <= r->sched.barriers, kConfig, "run: range out of bounds");
+  const int64_t hi = count > 0 ? ta[static_cast<size_t>(first + count - 1)] : 0;
+  const int64_t lo = first > 0 ? ta[static_cast<size_t>(first - 1)] : 0;
+  *out = count > 0 ? hi - lo : 0;
+  API_END
+}
+
+int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(r->next_barrier < r->sched.barriers, kConfig, "run: no barrier left to inspect");
+  TGB_REQUIRE(r->nranks == 1, kConfig, "run: launch counting is done on single-rank runs");
+  cudaStream_t s = r->ctx->stream;
+  TGB_CUDA(cudaStreamSynchronize(s));
+  const int64_t saved_t = r->tr->adam_t;
+  cudaGraph_t graph = nullptr;
+  TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    run_barrier(r, r->next_barrier);
+  } catch (...) {
+    cudaStreamEndCapture(s, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    r->tr->adam_t = saved_t;
+    throw;
+  }
+  TGB_CUDA(cudaStreamEndCapture(s, &graph));
+  r->tr->adam_t = saved_t;
+  size_t n = 0;
+  TGB_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  TGB_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n));
+  int64_t kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    TGB_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  cudaGraphDestroy(graph);
+  r->launches = kernels;
+  *out = kernels;
+  API_END
+}
+
+int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(r->next_barrier < r->sched.barriers, kConfig, "run: no barrier left to profile");
+  TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
+  if (!r->marks_ready) {
+    for (auto& e : r->marks.ev) TGB_CUDA(cudaEventCreate(&e));
+    r->marks_ready = true;
+  }
+  for (auto& h : r->marks.hit) h = false;
+  r->marks.on = true;
+  try {
+    run_barrier(r, r->next_barrier);
+  } catch (...) {
+    r->marks.on = false;
+    throw;
+  }
+  r->marks.on = false;
+  ++r->next_barrier;
+  TGB_CUDA(cudaStreamSynchronize(r->ctx->stream));
+  r->ctx->check_numeric();
+  // order the recorded markers by time; each interval belongs to its opening marker
+  std::vector<std::pair<float, int>> at;
+  for (int x = 0; x <= phCount; ++x) {
+    if (!r->marks.hit[x]) continue;
+    float ms = 0;
+    TGB_CUDA(cudaEventElapsedTime(&ms, r->marks.ev[phPlan], r->marks.ev[x]));
+    at.push_back({ms, x});
+  }
+  std::stable_sort(at.begin(), at.end());
+  for (int x = 0; x < phCount; ++x) phase_ms[x] = 0.0;
+  for (size_t q = 0; q + 1 < at.size(); ++q)
+    if (at[q].second < phCount) phase_ms[at[q].second] += at[q + 1].first - at[q].first;
+  int32_t sz[kSzCount];
+  TGB_CUDA(cudaMemcpy(sz, r->tr->plans[0].sizes, sizeof(sz), cudaMemcpyDeviceToHost));
+  for (int x = 0; x < kSzCount; ++x) sizes[x] = sz[x];
+  API_END
+}
+
+int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t* src, const int32_t* dst,
+                      const double* t, const float* efeat) {
+  API_BEGIN
+  tgnn_ctx* ctx = g->ctx;
+  ctx->use();
+  TGB_REQUIRE(first >= 0 && count >= 0 && first + count <= g->d.E, kConfig, "ingest: range out of bounds");
+  cudaStream_t s = ctx->stream;
+  h2d(g->d.src + first, src, static_cast<size_t>(count), s);
+  h2d(g->d.dst + first, dst, static_cast<size_t>(count), s);
+  h2d(g->d.t + first, t, static_cast<size_t>(count), s);
+  if (g->d.d_e > 0 && efeat) {
+    if (g->d.d_e == g->d.d_e_pad) {
+      h2d(g->d.efeat + first * g->d.d_e_pad, efeat, static_cast<size_t>(count * g->d.d_e), s);
+    } else {
+      TGB_CUDA(cudaMemcpy2DAsync(g->d.efeat + first * g->d.d_e_pad, sizeof(float) * g->d.d_e_pad, efeat,
+                                 sizeof(float) * g->d.d_e, sizeof(float) * g->d.d_e, static_cast<size_t>(count),
+                                 cudaMemcpyHostToDevice, s));
+    }
+  }
+  API_END
+}
+
+int tgnn_pinned_alloc(int64_t bytes, void** out) {
+  API_BEGIN
+  TGB_CUDA(cudaMallocHost(out, static_cast<size_t>(bytes > 0 ? bytes : 1)));
+  API_END
+}
+
+int tgnn_pinned_free(void* p) {
+  API_BEGIN
+  if (p) TGB_CUDA(cudaFreeHost(p));
+  API_END
+}
+
+}  // extern "C"

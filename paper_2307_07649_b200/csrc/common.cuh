@@ -1,0 +1,94 @@
+// Shared device/host helpers for the B200 DistTGL training step.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace tgb {
+
+// Status codes of the C ABI (include/tgnn_b200.h); they map 1:1 onto the
+// reference exception taxonomy (common.hpp:16-34, tensor.hpp:16).
+enum Status : int {
+  kOk = 0,
+  kConfig = 1,
+  kParse = 2,
+  kNumeric = 3,
+  kProtocol = 4,
+  kShape = 5,
+  kCuda = 6,
+  kNccl = 7,
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define TGB_CUDA(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e__ = (x);                                                              \
+    if (e__ != cudaSuccess)                                                             \
+      throw ::tgb::Error(::tgb::kCuda, std::string(#x) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define TGB_REQUIRE(cond, code, msg)                     \
+  do {                                                   \
+    if (!(cond)) throw ::tgb::Error((code), (msg));      \
+  } while (0)
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+
+// rng.hpp:12-17
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += kGamma;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// One fold step of rng.hpp:21-24: hash64(a, b, rest...) = hash64(fold(a, b), rest...).
+__host__ __device__ __forceinline__ uint64_t hash_fold(uint64_t a, uint64_t b) {
+  return splitmix64(a ^ (b + kGamma + (a << 6) + (a >> 2)));
+}
+
+__host__ __device__ __forceinline__ uint64_t hash64_5(uint64_t a, uint64_t b, uint64_t c,
+                                                       uint64_t d, uint64_t e) {
+  return splitmix64(hash_fold(hash_fold(hash_fold(hash_fold(a, b), c), d), e));
+}
+
+// First draw of Rng(seed) (rng.hpp:30-35).
+__host__ __device__ __forceinline__ uint64_t rng_first_u64(uint64_t seed) {
+  return splitmix64(splitmix64(seed ^ 0xa02bdbf7bb3c0a7ull));
+}
+
+constexpr uint64_t kTagNegatives = 0x6e656761ull;  // "nega", temporal_graph.hpp:365
+constexpr uint64_t kTagEval = 0x6576616cull;       // "eval", trainer.hpp:417
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+constexpr int kSMs = 148;
+
+}  // namespace tgb

@@ -1,0 +1,1090 @@
+// TGN sub-step on device: GRU freshen, temporal attention, link decoder, BCE,
+// and the analytic backward of all of them (trainer.hpp:170-272), plus root
+// writes / COMB (trainer.hpp:284-330, memory_store.hpp:121-136), memory reset
+// (memory_store.hpp:43-50) and dense Adam (optimizer.hpp:40-56).
+//
+// fp32 throughout (times and Delta-t stay f64). Every reduction has a fixed
+// order, so a step is bitwise reproducible run to run:
+//  * GEMMs: in-order FMA chains, weight gradients via fixed split-K + in-order
+//    partial reduction (gemm_simt.cu);
+//  * per-support gradient routing: items sorted by support (stable radix sort)
+//    and summed in fixed chunks with an in-order carry fix-up;
+//  * loss and omega gradient: fixed-shape tree / chunk reductions.
+// Algebraic restructuring (summation order only, within the 1e-4 bound):
+//  * decoder: W1 {h_u | h_v} = W1a h_u + W1b h_v, computed once per root;
+//  * attention input gradient: the s_hat/static slices of dkv are linear in
+//    (dq, dK, dV), so dK/dV/dq are first summed per support and multiplied by
+//    the weights once per support (U rows) instead of once per pair (P rows);
+//  * omega gradient of the pair time encodings: sum_p (W^T dKV_p)_i g_p,i =
+//    sum_j W_j,i (dKV^T G)_j,i.
+#include <cmath>
+
+#include "step.cuh"
+
+namespace tgb {
+
+ParamLayout ParamLayout::make(const ModelDims& m) {
+  ParamLayout L;
+  const int64_t d = m.d_mem, gin = m.gin(), da = m.d_attn, dh = m.dh();
+  const int64_t shapes[tNumTensors][2] = {
+      {m.d_time, 1}, {d, gin}, {d, gin}, {d, gin}, {d, 1}, {d, 1}, {d, 1},
+      {da, m.q_in()}, {da, 1}, {da, m.kv_in()}, {da, 1}, {da, m.kv_in()}, {da, 1},
+      {m.num_nodes, m.d_static}, {dh, 2 * da}, {dh, 1}, {1, dh}, {1, 1}};
+  int64_t at = 0;
+  for (int x = 0; x < tNumTensors; ++x) {
+    L.off[x] = at;
+    L.rows[x] = shapes[x][0];
+    L.cols[x] = shapes[x][1];
+    at += shapes[x][0] * shapes[x][1];
+  }
+  L.off[tNumTensors] = at;
+  L.total = at;
+  return L;
+}
+
+namespace {
+
+constexpr int kWarps = 8;  // warps per block for row kernels
+constexpr int kChunk = 32; // routing chunk (items)
+constexpr int kOmegaRows = 256;
+
+inline int row_blocks(int64_t rows) {
+  int64_t b = ceil_div(rows, kWarps);
+  if (b > 16 * kSMs) b = 16 * kSMs;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
+__device__ __forceinline__ int64_t gwarp() {
+  return (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+}
+__device__ __forceinline__ int64_t nwarp() {
+  return (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+}
+
+__device__ __forceinline__ void flag_if_nonfinite(float v, int* flag) {
+  if (!isfinite(v)) atomicExch(flag, 1);
+}
+
+struct Dims {  // flattened for kernels
+  int d, dt, ds, de, de_pad, da, dh, md, gin, q_in, kv_in;
+};
+
+Dims make_dims(const ModelDims& m, const DGraph& g) {
+  Dims D;
+  D.d = static_cast<int>(m.d_mem);
+  D.dt = static_cast<int>(m.d_time);
+  D.ds = static_cast<int>(m.d_static);
+  D.de = static_cast<int>(m.d_e);
+  D.de_pad = static_cast<int>(g.d_e_pad);
+  D.da = static_cast<int>(m.d_attn);
+  D.dh = static_cast<int>(m.dh());
+  D.md = static_cast<int>(m.mail_dim());
+  D.gin = static_cast<int>(m.gin());
+  D.q_in = static_cast<int>(m.q_in());
+  D.kv_in = static_cast<int>(m.kv_in());
+  return D;
+}
+
+// ---------------------------------------------------------------- forward
+// GRU input rows {mail_mem | cos(dt w) | e(mail event) | s} (make_mail,
+// model.hpp:153-166) and GU = -dt sin(dt w) (time_encode_backward factor).
+__global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const float* __restrict__ omega,
+                                    float* __restrict__ Xg, int64_t ldx, float* __restrict__ GU) {
+  const int U = pl.sizes[kSzU];
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = gwarp(); u < U; u += nwarp()) {
+    const int32_t ev = vw.mail_ev[u];
+    const bool has = ev >= 0;
+    const double dt = vw.mail_dt[u];
+    float* row = Xg + u * ldx;
+    for (int x = lane; x < 2 * D.d; x += 32) row[x] = vw.mail_mem[u * 2 * D.d + x];
+    for (int i = lane; i < D.dt; i += 32) {
+      const double arg = dt * static_cast<double>(omega[i]);
+      row[2 * D.d + i] = static_cast<float>(cos(arg));
+      GU[u * D.dt + i] = has ? static_cast<float>(-dt * sin(arg)) : 0.0f;
+    }
+    const float* ef = has ? g.efeat + static_cast<int64_t>(ev) * D.de_pad : nullptr;
+    for (int x = lane; x < D.de; x += 32) row[2 * D.d + D.dt + x] = has ? ef[x] : 0.0f;
+    for (int x = lane; x < D.d; x += 32) row[D.md + x] = vw.mem[u * D.d + x];
+  }
+}
+
+// z, r = sigmoid(gates + b) (bias already added by the GEMM); RS = r * s.
+__global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
+                               float* __restrict__ RS) {
+  const int U = pl.sizes[kSzU];
+  const int64_t total = static_cast<int64_t>(U) * D.d;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int64_t u = x / D.d, i = x % D.d;
+    float* gr = Gates + u * 3 * D.d;
+    const float z = sigmoidf_(gr[i]);
+    const float r = sigmoidf_(gr[D.d + i]);
+    gr[i] = z;
+    gr[D.d + i] = r;
+    RS[x] = r * vw.mem[x];
+  }
+}
+
+// h = tanh(.), s_hat = (1 - z) s + z h for rows with a mail, else s
+// (freshen_memory, trainer.hpp:111-124; gru_update, gru.hpp:59-85).
+__global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
+                               float* __restrict__ s_hat, int* flag) {
+  const int U = pl.sizes[kSzU];
+  const int64_t total = static_cast<int64_t>(U) * D.d;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int64_t u = x / D.d, i = x % D.d;
+    float* gr = Gates + u * 3 * D.d;
+    const float h = tanhf(gr[2 * D.d + i]);
+    gr[2 * D.d + i] = h;
+    const float s = vw.mem[x];
+    float out = s;
+    if (vw.mail_ev[u] >= 0) {
+      const float z = gr[i];
+      out = (1.0f - z) * s + z * h;
+      flag_if_nonfinite(out, flag);
+    }
+    s_hat[x] = out;
+  }
+}
+
+// Attention inputs: Qin = {s_hat | static | cos(0 w) = 1} per root, KVin =
+// {s_hat | static | e | cos(dt w)} per pair (embed_root, trainer.hpp:128-159),
+// Gt = -dt sin(dt w) per pair.
+__global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __restrict__ omega,
+                                     const float* __restrict__ stat, const float* __restrict__ s_hat,
+                                     float* __restrict__ Qin, int64_t ldq, float* __restrict__ KVin,
+                                     int64_t ldkv, float* __restrict__ Gt) {
+  const int R = pl.sizes[kSzR], P = pl.sizes[kSzP];
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = gwarp(); w < R + P; w += nwarp()) {
+    if (w < R) {
+      const int64_t su = pl.root_sup[w];
+      const int64_t node = pl.root_node[w];
+      float* row = Qin + w * ldq;
+      for (int x = lane; x < D.d; x += 32) row[x] = s_hat[su * D.d + x];
+      for (int x = lane; x < D.ds; x += 32) row[D.d + x] = stat[node * D.ds + x];
+      for (int x = lane; x < D.dt; x += 32) row[D.d + D.ds + x] = 1.0f;
+    } else {
+      const int64_t p = w - R;
+      const int64_t su = pl.pair_sup[p];
+      const int64_t node = pl.pair_node[p];
+      const int64_t ev = pl.pair_event[p];
+      const double dt = pl.pair_dt[p];
+      float* row = KVin + p * ldkv;
+      for (int x = lane; x < D.d; x += 32) row[x] = s_hat[su * D.d + x];
+      for (int x = lane; x < D.ds; x += 32) row[D.d + x] = stat[node * D.ds + x];
+      const float* ef = g.efeat + ev * D.de_pad;
+      for (int x = lane; x < D.de; x += 32) row[D.d + D.ds + x] = ef[x];
+      for (int i = lane; i < D.dt; i += 32) {
+        const double arg = dt * static_cast<double>(omega[i]);
+        row[D.d + D.ds + D.de + i] = static_cast<float>(cos(arg));
+        Gt[p * D.dt + i] = static_cast<float>(-dt * sin(arg));
+      }
+    }
+  }
+}
+
+constexpr int kMaxDaLanes = 8;  // d_attn <= 256
+
+// attention_forward (attention.hpp:36-91): scores q.K / sqrt(n), stable
+// softmax, h = sum a V; n = 0 gives h = 0. One warp per root.
+__global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
+                                const float* __restrict__ KV, float* __restrict__ attn_a,
+                                float* __restrict__ H, int* flag) {
+  const int R = pl.sizes[kSzR];
+  const int lane = threadIdx.x & 31;
+  const int da = D.da;
+  for (int64_t r = gwarp(); r < R; r += nwarp()) {
+    const int n = pl.nbr_cnt[r];
+    float* h = H + r * da;
+    if (n == 0) {
+      for (int i = lane; i < da; i += 32) h[i] = 0.0f;
+      continue;
+    }
+    const int p0 = pl.pair_ptr[r];
+    float q[kMaxDaLanes];
+#pragma unroll
+    for (int c = 0; c < kMaxDaLanes; ++c) {
+      const int i = lane + 32 * c;
+      q[c] = i < da ? Q[r * da + i] : 0.0f;
+    }
+    const float scale = 1.0f / sqrtf(static_cast<float>(n));
+    float my_score = -INFINITY;
+    for (int m = 0; m < n; ++m) {
+      const float* K = KV + static_cast<int64_t>(p0 + m) * 2 * da;
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kMaxDaLanes; ++c) {
+        const int i = lane + 32 * c;
+        if (i < da) acc = fmaf(q[c], K[i], acc);
+      }
+      acc = warp_sum(acc) * scale;
+      if (lane == m) my_score = acc;
+    }
+    const float mx = warp_max(my_score);
+    const float ex = lane < n ? expf(my_score - mx) : 0.0f;
+    const float denom = warp_sum(ex);
+    const float a = ex / denom;
+    if (lane < n) attn_a[p0 + lane] = a;
+    float hv[kMaxDaLanes];
+#pragma unroll
+    for (int c = 0; c < kMaxDaLanes; ++c) hv[c] = 0.0f;
+    for (int m = 0; m < n; ++m) {
+      const float am = __shfl_sync(0xffffffffu, a, m);
+      const float* V = KV + static_cast<int64_t>(p0 + m) * 2 * da + da;
+#pragma unroll
+      for (int c = 0; c < kMaxDaLanes; ++c) {
+        const int i = lane + 32 * c;
+        if (i < da) hv[c] = fmaf(am, V[i], hv[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxDaLanes; ++c) {
+      const int i = lane + 32 * c;
+      if (i < da) {
+        h[i] = hv[c];
+        flag_if_nonfinite(hv[c], flag);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double softplus_d(double x) {
+  return fmax(x, 0.0) + log1p(exp(-fabs(x)));
+}
+
+// decode_link x2 per event (decoder.hpp:30-53), per-event BCE terms
+// (decoder.hpp:85-98), bce_backward (decoder.hpp:101-109) and the decoder
+// hidden-layer gradient. One warp per event; rows 0..B-1 positive, B..2B-1 negative.
+__global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
+                               const float* __restrict__ AB, const float* __restrict__ b1,
+                               const float* __restrict__ W2, const float* __restrict__ b2,
+                               float* __restrict__ HID, float* __restrict__ Dhid,
+                               float* __restrict__ Hin, float* __restrict__ dlogit,
+                               float* __restrict__ logits, double* __restrict__ loss_terms,
+                               int* flag) {
+  const int B = pl.sizes[kSzB];
+  const int lane = threadIdx.x & 31;
+  const int dh = D.dh, da = D.da;
+  for (int64_t e = gwarp(); e < B; e += nwarp()) {
+    const float* As = AB + (3 * e) * 2 * dh;
+    const float* Bd = AB + (3 * e + 1) * 2 * dh + dh;
+    const float* Bn = AB + (3 * e + 2) * 2 * dh + dh;
+    float sp = 0.0f, sn = 0.0f;
+    for (int j = lane; j < dh; j += 32) {
+      const float hp = fmaxf(As[j] + Bd[j] + b1[j], 0.0f);
+      const float hn = fmaxf(As[j] + Bn[j] + b1[j], 0.0f);
+      HID[e * dh + j] = hp;
+      HID[(B + e) * dh + j] = hn;
+      sp = fmaf(W2[j], hp, sp);
+      sn = fmaf(W2[j], hn, sn);
+    }
+    const float pos = warp_sum(sp) + b2[0];
+    const float neg = warp_sum(sn) + b2[0];
+    const double invB = 1.0 / static_cast<double>(B);
+    const float dpos = static_cast<float>(-(1.0 / (1.0 + exp(static_cast<double>(pos)))) * invB);
+    const float dneg = static_cast<float>((1.0 / (1.0 + exp(-static_cast<double>(neg)))) * invB);
+    for (int j = lane; j < dh; j += 32) {
+      const float hp = HID[e * dh + j];
+      const float hn = HID[(B + e) * dh + j];
+      Dhid[e * dh + j] = hp > 0.0f ? dpos * W2[j] : 0.0f;
+      Dhid[(B + e) * dh + j] = hn > 0.0f ? dneg * W2[j] : 0.0f;
+    }
+    const float* hs = H + (3 * e) * da;
+    const float* hd = H + (3 * e + 1) * da;
+    const float* hn = H + (3 * e + 2) * da;
+    for (int i = lane; i < da; i += 32) {
+      Hin[e * 2 * da + i] = hs[i];
+      Hin[e * 2 * da + da + i] = hd[i];
+      Hin[(B + e) * 2 * da + i] = hs[i];
+      Hin[(B + e) * 2 * da + da + i] = hn[i];
+    }
+    if (lane == 0) {
+      dlogit[e] = dpos;
+      dlogit[B + e] = dneg;
+      logits[e] = pos;
+      logits[B + e] = neg;
+      loss_terms[2 * e] = softplus_d(-static_cast<double>(pos));
+      loss_terms[2 * e + 1] = softplus_d(static_cast<double>(neg));
+      flag_if_nonfinite(pos, flag);
+      flag_if_nonfinite(neg, flag);
+    }
+  }
+}
+
+// bce_loss: mean softplus(-pos) + mean softplus(neg), fixed-order f64 reduction.
+__global__ void __launch_bounds__(1024) loss_kernel(DPlan pl, const double* __restrict__ terms,
+                                                    double* loss_out, int* flag) {
+  __shared__ double sp[1024], sn[1024];
+  const int B = pl.sizes[kSzB];
+  double a = 0.0, b = 0.0;
+  for (int e = threadIdx.x; e < B; e += 1024) {
+    a += terms[2 * e];
+    b += terms[2 * e + 1];
+  }
+  sp[threadIdx.x] = a;
+  sn[threadIdx.x] = b;
+  __syncthreads();
+  for (int s = 512; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sp[threadIdx.x] += sp[threadIdx.x + s];
+      sn[threadIdx.x] += sn[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double loss = B > 0 ? sp[0] / B + sn[0] / B : 0.0;
+    *loss_out = loss;
+    if (!isfinite(loss)) atomicExch(flag, 1);
+  }
+}
+
+// attention_backward (attention.hpp:96-140), one warp per root. dh comes from
+// the decoder input gradient: the source root gets both pairs' halves.
+__global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
+                                const float* __restrict__ Q, const float* __restrict__ KV,
+                                const float* __restrict__ attn_a, float* __restrict__ dQ,
+                                float* __restrict__ dKV) {
+  const int R = pl.sizes[kSzR];
+  const int B = pl.sizes[kSzB];
+  const int lane = threadIdx.x & 31;
+  const int da = D.da;
+  for (int64_t r = gwarp(); r < R; r += nwarp()) {
+    const int64_t e = r / 3;
+    const int side = static_cast<int>(r % 3);
+    float dh[kMaxDaLanes];
+#pragma unroll
+    for (int c = 0; c < kMaxDaLanes; ++c) {
+      const int i = lane + 32 * c;
+      float v = 0.0f;
+      if (i < da) {
+        if (side == 0) v = (0.0f + dIn[e * 2 * da + i]) + dIn[(B + e) * 2 * da + i];
+        else if (side == 1) v = dIn[e * 2 * da + da + i];
+        else v = dIn[(B + e) * 2 * da + da + i];
+      }
+      dh[c] = v;
+    }
+    const int n = pl.nbr_cnt[r];
+    if (n == 0) {
+      for (int i = lane; i < da; i += 32) dQ[r * da + i] = 0.0f;
+      continue;
+    }
+    const int p0 = pl.pair_ptr[r];
+    const float scale = 1.0f / sqrtf(static_cast<float>(n));
+    const float a_l = lane < n ? attn_a[p0 + lane] : 0.0f;
+    float da_l = 0.0f;
+    for (int m = 0; m < n; ++m) {
+      const float* V = KV + static_cast<int64_t>(p0 + m) * 2 * da + da;
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kMaxDaLanes; ++c) {
+        const int i = lane + 32 * c;
+        if (i < da) acc = fmaf(dh[c], V[i], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == m) da_l = acc;
+    }
+    const float mixed = warp_sum(a_l * da_l);
+    const float g_l = a_l * (da_l - mixed) * scale;
+    float q[kMaxDaLanes], dq[kMaxDaLanes];
+#pragma unroll
+    for (int c = 0; c < kMaxDaLanes; ++c) {
+      const int i = lane + 32 * c;
+      q[c] = i < da ? Q[r * da + i] : 0.0f;
+      dq[c] = 0.0f;
+    }
+    for (int m = 0; m < n; ++m) {
+      const float am = __shfl_sync(0xffffffffu, a_l, m);
+      const float gm = __shfl_sync(0xffffffffu, g_l, m);
+      const int64_t p = p0 + m;
+      const float* K = KV + p * 2 * da;
+      float* out = dKV + p * 2 * da;
+#pragma unroll
+      for (int c = 0; c < kMaxDaLanes; ++c) {
+        const int i = lane + 32 * c;
+        if (i < da) {
+          dq[c] = fmaf(gm, K[i], dq[c]);
+          out[i] = gm * q[c];
+          out[da + i] = am * dh[c];
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxDaLanes; ++c) {
+      const int i = lane + 32 * c;
+      if (i < da) dQ[r * da + i] = dq[c];
+    }
+  }
+}
+
+// Routing pass 1: fixed chunks of kChunk sorted items; runs fully inside a
+// chunk are written directly, runs that cross a chunk edge leave partials.
+// Row layout of dNodeAcc: {sum dq | sum dK | sum dV} (3 d_attn).
+__global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__ dQ,
+                                     const float* __restrict__ dKV, float* __restrict__ dNodeAcc,
+                                     float* __restrict__ part_first, float* __restrict__ part_last) {
+  const int items = pl.sizes[kSzItems];
+  const int R = pl.sizes[kSzR];
+  const int nchunks = (items + kChunk - 1) / kChunk;
+  const int lane = threadIdx.x & 31;
+  const int da = D.da, w3 = 3 * D.da;
+  for (int64_t c = gwarp(); c < nchunks; c += nwarp()) {
+    const int i0 = static_cast<int>(c) * kChunk;
+    const int i1 = min(items, i0 + kChunk);
+    const bool cont_in = i0 > 0 && pl.item_key_s[i0 - 1] == pl.item_key_s[i0];
+    const bool cont_out = i1 < items && pl.item_key_s[i1] == pl.item_key_s[i1 - 1];
+    float acc[3 * kMaxDaLanes];
+#pragma unroll
+    for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] = 0.0f;
+    int run_start = i0;
+    for (int i = i0; i < i1; ++i) {
+      const int v = pl.item_val_s[i];
+      if (v < R) {
+#pragma unroll
+        for (int cc = 0; cc < kMaxDaLanes; ++cc) {
+          const int f = lane + 32 * cc;
+          if (f < da) acc[cc] += dQ[static_cast<int64_t>(v) * da + f];
+        }
+      } else {
+        const float* row = dKV + static_cast<int64_t>(v - R) * 2 * da;
+#pragma unroll
+        for (int cc = 0; cc < kMaxDaLanes; ++cc) {
+          const int f = lane + 32 * cc;
+          if (f < da) {
+            acc[kMaxDaLanes + cc] += row[f];
+            acc[2 * kMaxDaLanes + cc] += row[da + f];
+          }
+        }
+      }
+      const bool run_end = (i + 1 == i1) || pl.item_key_s[i + 1] != pl.item_key_s[i];
+      if (run_end) {
+        const int key = pl.item_key_s[i];
+        float* dst;
+        const bool first = run_start == i0 && cont_in;
+        const bool last = (i + 1 == i1) && cont_out;
+        if (first) dst = part_first + c * w3;
+        else if (last) dst = part_last + c * w3;
+        else dst = dNodeAcc + static_cast<int64_t>(key) * w3;
+#pragma unroll
+        for (int cc = 0; cc < kMaxDaLanes; ++cc) {
+          const int f = lane + 32 * cc;
+          if (f < da) {
+            dst[f] = acc[cc];
+            dst[da + f] = acc[kMaxDaLanes + cc];
+            dst[2 * da + f] = acc[2 * kMaxDaLanes + cc];
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] = 0.0f;
+        run_start = i + 1;
+      }
+    }
+  }
+}
+
+// Routing pass 2: supports whose item run spans chunks sum their partials in
+// chunk order.
+__global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNodeAcc,
+                                     const float* __restrict__ part_first,
+                                     const float* __restrict__ part_last) {
+  const int U = pl.sizes[kSzU];
+  const int lane = threadIdx.x & 31;
+  const int w3 = 3 * D.da;
+  for (int64_t u = gwarp(); u < U; u += nwarp()) {
+    const int b = pl.sup_item_ptr[u], e = pl.sup_item_ptr[u + 1];
+    const int c0 = b / kChunk, c1 = (e - 1) / kChunk;
+    if (c0 == c1) continue;
+    for (int f = lane; f < w3; f += 32) {
+      float s = part_last[static_cast<int64_t>(c0) * w3 + f];
+      for (int c = c0 + 1; c <= c1; ++c) s += part_first[static_cast<int64_t>(c) * w3 + f];
+      dNodeAcc[u * w3 + f] = s;
+    }
+  }
+}
+
+// GRU backward part 1 (gru.hpp:98-117) and static-table gradient scatter
+// (trainer.hpp:239-253; supports are unique nodes, so rows never collide).
+__global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ dNode,
+                                const float* __restrict__ Gates, float* __restrict__ Dg,
+                                float* __restrict__ g_static) {
+  const int U = pl.sizes[kSzU];
+  const int nd = D.d + D.ds;
+  const int64_t total = static_cast<int64_t>(U) * D.d;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int64_t u = x / D.d, i = x % D.d;
+    const bool has = vw.mail_ev[u] >= 0;
+    const float* gr = Gates + u * 3 * D.d;
+    const float ds = dNode[u * nd + i];
+    const float z = gr[i], h = gr[2 * D.d + i], s = vw.mem[x];
+    float* dg = Dg + u * 3 * D.d;
+    dg[i] = has ? ds * (h - s) * z * (1.0f - z) : 0.0f;
+    dg[D.d + i] = 0.0f;
+    dg[2 * D.d + i] = has ? ds * z * (1.0f - h * h) : 0.0f;
+  }
+  if (D.ds > 0) {
+    const int64_t tot2 = static_cast<int64_t>(U) * D.ds;
+    for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < tot2; x += gridDim.x * blockDim.x) {
+      const int64_t u = x / D.ds, j = x % D.ds;
+      g_static[static_cast<int64_t>(pl.supports[u]) * D.ds + j] = dNode[u * nd + D.d + j];
+    }
+  }
+}
+
+// da_r = (Wh^T da_h)[s part] * s * r (1 - r)  (gru.hpp:124-127).
+__global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ T1,
+                                const float* __restrict__ Gates, float* __restrict__ Dg) {
+  const int U = pl.sizes[kSzU];
+  const int64_t total = static_cast<int64_t>(U) * D.d;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int64_t u = x / D.d, i = x % D.d;
+    const bool has = vw.mail_ev[u] >= 0;
+    const float r = Gates[u * 3 * D.d + D.d + i];
+    Dg[u * 3 * D.d + D.d + i] = has ? T1[x] * vw.mem[x] * r * (1.0f - r) : 0.0f;
+  }
+}
+
+// Column dot partials: part[c][i] = sum_{rows in chunk c} X[m, i] * Y[m, i].
+__global__ void coldot_kernel(const int32_t* rows_dev, int ncol, const float* __restrict__ X,
+                              const float* __restrict__ Y, float* __restrict__ part, int nchunks) {
+  const int rows = *rows_dev;
+  for (int64_t w = blockIdx.x; w < nchunks; w += gridDim.x) {
+    const int m0 = static_cast<int>(w) * kOmegaRows;
+    const int m1 = min(rows, m0 + kOmegaRows);
+    for (int i = threadIdx.x; i < ncol; i += blockDim.x) {
+      float s = 0.0f;
+      for (int m = m0; m < m1; ++m) s = fmaf(X[static_cast<int64_t>(m) * ncol + i], Y[static_cast<int64_t>(m) * ncol + i], s);
+      part[w * ncol + i] = s;
+    }
+  }
+}
+
+// omega gradient = pair time encodings (via Mom = dKV^T G) + GRU mail time
+// encodings (chunk partials), trainer.hpp:254-268.
+__global__ void omega_final_kernel(Dims D, const float* __restrict__ params, int64_t offWk,
+                                   int64_t offWv, const float* __restrict__ Mom,
+                                   const float* __restrict__ part, int nchunks,
+                                   float* __restrict__ g_omega) {
+  const int t0 = D.d + D.ds + D.de;
+  for (int i = threadIdx.x; i < D.dt; i += blockDim.x) {
+    float s = 0.0f;
+    for (int j = 0; j < D.da; ++j) {
+      s = fmaf(params[offWk + static_cast<int64_t>(j) * D.kv_in + t0 + i], Mom[j * D.dt + i], s);
+      s = fmaf(params[offWv + static_cast<int64_t>(j) * D.kv_in + t0 + i], Mom[(D.da + j) * D.dt + i], s);
+    }
+    for (int c = 0; c < nchunks; ++c) s += part[c * D.dt + i];
+    g_omega[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------- writes
+// build_root_writes (trainer.hpp:284-330) + comb (memory_store.hpp:121-136):
+// events are sorted by (t, id), so the kept mail of a node is the one of its
+// largest event index.
+__global__ void rw_mark_kernel(DPlan pl, DGraph g, int32_t* __restrict__ win, int32_t* count) {
+  const PlanArgs a = *pl.args;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = 0;
+  if (!a.valid) return;
+  const int64_t B = a.end - a.begin;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * B; x += gridDim.x * blockDim.x) {
+    const int64_t e = a.begin + x / 2;
+    const int side = static_cast<int>(x % 2);
+    const int32_t self = side == 0 ? g.src[e] : g.dst[e];
+    atomicMax(&win[self], static_cast<int32_t>(e + 1));
+  }
+}
+
+__global__ void rw_emit_kernel(Dims D, DPlan pl, DGraph g, DView vw, const float* __restrict__ s_hat,
+                               int32_t* __restrict__ win, StepWork w) {
+  const PlanArgs a = *pl.args;
+  if (!a.valid) return;
+  const int64_t B = a.end - a.begin;
+  const int lane = threadIdx.x & 31;
+  for (int64_t x = gwarp(); x < 2 * B; x += nwarp()) {
+    const int64_t e = a.begin + x / 2;
+    const int side = static_cast<int>(x % 2);
+    const int32_t self = side == 0 ? g.src[e] : g.dst[e];
+    const int32_t other = side == 0 ? g.dst[e] : g.src[e];
+    if (side == 1 && self == other) continue;  // self-loop: one mail suffices
+    int slot = -1;
+    if (lane == 0) {
+      if (win[self] == static_cast<int32_t>(e + 1)) {
+        slot = atomicAdd(w.w_count, 1);
+        win[self] = 0;
+      }
+    }
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (slot < 0) continue;
+    const int64_t u = pl.sup_row[self], o = pl.sup_row[other];
+    const double t = g.t[e];
+    for (int i = lane; i < D.d; i += 32) {
+      w.w_mem[static_cast<int64_t>(slot) * D.d + i] = s_hat[u * D.d + i];
+      w.w_mail[static_cast<int64_t>(slot) * 2 * D.d + i] = vw.mem[u * D.d + i];
+      w.w_mail[static_cast<int64_t>(slot) * 2 * D.d + D.d + i] = vw.mem[o * D.d + i];
+    }
+    if (lane == 0) {
+      const double t_minus = vw.mail_ev[u] >= 0 ? vw.mail_t[u] : 0.0;
+      w.w_node[slot] = self;
+      w.w_event[slot] = static_cast<int32_t>(e);
+      w.w_t[slot] = t;
+      w.w_dt[slot] = t - t_minus;
+    }
+  }
+}
+
+__global__ void apply_mark_kernel(WriteSet ws, int32_t* __restrict__ win) {
+  const int n = *ws.count;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+    atomicMax(&win[ws.node[x]], ws.event[x] + 1);
+}
+
+// apply_root_write (memory_store.hpp:168-181). With several row sets, a row
+// is applied only if it carries the node's largest event (== later rank wins).
+__global__ void apply_rows_kernel(WriteSet ws, DMem st, int32_t* __restrict__ win, int use_win) {
+  const int n = *ws.count;
+  const int lane = threadIdx.x & 31;
+  const int64_t d = st.d;
+  for (int64_t x = gwarp(); x < n; x += nwarp()) {
+    const int64_t v = ws.node[x];
+    if (use_win) {
+      int ok = 0;
+      if (lane == 0) ok = win[v] == ws.event[x] + 1;
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (!ok) continue;
+    }
+    for (int64_t i = lane; i < d; i += 32) st.memory[v * d + i] = ws.mem[x * d + i];
+    for (int64_t i = lane; i < 2 * d; i += 32) st.mail_mem[v * 2 * d + i] = ws.mail[x * 2 * d + i];
+    if (lane == 0) {
+      st.mail_t[v] = ws.t[x];
+      st.mail_dt[v] = ws.dt[x];
+      st.mail_ev[v] = ws.event[x];
+      st.last_update[v] = ws.t[x];
+    }
+  }
+}
+
+__global__ void apply_clear_kernel(WriteSet ws, int32_t* __restrict__ win) {
+  const int n = *ws.count;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+    win[ws.node[x]] = 0;
+}
+
+__global__ void fill_kernel(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) p[x] = v;
+}
+
+// Dense Adam, optimizer.hpp:40-56 (fp32 state).
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, int64_t n, float lr, float c1, float c2,
+                            float scale) {
+  const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    const float gr = g[x] * scale;
+    const float mm = b1 * m[x] + (1.0f - b1) * gr;
+    const float vv = b2 * v[x] + (1.0f - b2) * gr * gr;
+    m[x] = mm;
+    v[x] = vv;
+    p[x] -= lr * (mm / c1) / (sqrtf(vv / c2) + eps);
+  }
+}
+
+template <typename T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  TGB_CUDA(cudaMalloc(&p, (n > 0 ? n : 1) * sizeof(T)));
+  return p;
+}
+
+int choose_splits(int M, int N, int64_t Kcap) {
+  const int tiles = static_cast<int>(ceil_div(M, 64) * ceil_div(N, 64));
+  int s = static_cast<int>(ceil_div(2 * kSMs, tiles));
+  const int max_by_k = static_cast<int>(ceil_div(Kcap, 128));
+  if (s > max_by_k) s = max_by_k;
+  if (s < 1) s = 1;
+  if (s > 64) s = 64;
+  return s;
+}
+
+struct WsCarver {
+  float* base;
+  size_t used = 0, cap;
+  float* take(size_t n) {
+    if (used + n > cap) throw Error(kConfig, "split-K workspace exhausted");
+    float* p = base + used;
+    used += n;
+    return p;
+  }
+};
+
+void add_tn(GemmGroup& gg, WsCarver& wc, int M, int N, int Kcap, const int* K_dev, Operand a,
+            Operand b, float* C, int64_t ldc) {
+  GemmProblem& P = gg.p[gg.count++];
+  P.M = M;
+  P.N = N;
+  P.K = Kcap;
+  P.K_dev = K_dev;
+  P.a = a;
+  P.b = b;
+  P.C = C;
+  P.ldc = ldc;
+  P.splits = choose_splits(M, N, Kcap);
+  if (P.splits > 1) P.ws = wc.take(static_cast<size_t>(P.splits) * M * N);
+}
+
+void add_nn(GemmGroup& gg, int Mcap, const int* M_dev, int N, int K, Operand a, Operand b, float* C,
+            int64_t ldc, const float* bias = nullptr, float beta = 0.0f) {
+  GemmProblem& P = gg.p[gg.count++];
+  P.M = Mcap;
+  P.M_dev = M_dev;
+  P.N = N;
+  P.K = K;
+  P.a = a;
+  P.b = b;
+  P.C = C;
+  P.ldc = ldc;
+  P.bias = bias;
+  P.beta = beta;
+}
+
+Operand ones_op(const float* ones, int K) { return op_dense(ones, 0, 0, K); }
+
+}  // namespace
+
+void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes) {
+  const int n = static_cast<int>(m.n_neighbors);
+  w.cap_B = cap_B;
+  w.cap_R = 3 * cap_B;
+  w.cap_P = w.cap_R * (n > 0 ? n : 1);
+  w.cap_U = cap_U;
+  const int64_t d = m.d_mem, dt = m.d_time, da = m.d_attn, dh = m.dh();
+  auto r4 = [](int64_t x) { return (x + 3) / 4 * 4; };
+  w.ldx = r4(m.gin());
+  w.ldq = r4(m.q_in());
+  w.ldkv = r4(m.kv_in());
+  const int64_t U = cap_U, R = w.cap_R, P = w.cap_P, B2 = 2 * cap_B;
+  w.Xg = dalloc<float>(U * w.ldx);
+  w.GU = dalloc<float>(U * dt);
+  w.Gates = dalloc<float>(U * 3 * d);
+  w.RS = dalloc<float>(U * d);
+  w.s_hat = dalloc<float>(U * d);
+  w.Qin = dalloc<float>(R * w.ldq);
+  w.KVin = dalloc<float>(P * w.ldkv);
+  w.Gt = dalloc<float>(P * dt);
+  w.Q = dalloc<float>(R * da);
+  w.KV = dalloc<float>(P * 2 * da);
+  w.attn_a = dalloc<float>(P);
+  w.H = dalloc<float>(R * da);
+  w.AB = dalloc<float>(R * 2 * dh);
+  w.HID = dalloc<float>(B2 * dh);
+  w.Dhid = dalloc<float>(B2 * dh);
+  w.Hin = dalloc<float>(B2 * 2 * da);
+  w.dlogit = dalloc<float>(B2);
+  w.logits = dalloc<float>(B2);
+  w.dIn = dalloc<float>(B2 * 2 * da);
+  w.dQ = dalloc<float>(R * da);
+  w.dKV = dalloc<float>(P * 2 * da);
+  w.dNodeAcc = dalloc<float>(U * 3 * da);
+  w.dNode = dalloc<float>(U * (d + m.d_static));
+  w.Dg = dalloc<float>(U * 3 * d);
+  w.T1 = dalloc<float>(U * d);
+  w.DMT = dalloc<float>(U * dt);
+  w.Mom = dalloc<float>(2 * da * dt);
+  w.omega_chunks = static_cast<int>(ceil_div(U, kOmegaRows));
+  w.omega_part = dalloc<float>(static_cast<size_t>(w.omega_chunks) * dt);
+  const int64_t max_ones = std::max<int64_t>(std::max<int64_t>(P, U), B2);
+  w.ones = dalloc<float>(1);
+  const float one = 1.0f;
+  TGB_CUDA(cudaMemcpy(w.ones, &one, sizeof(float), cudaMemcpyHostToDevice));
+  (void)max_ones;
+  w.loss_terms = dalloc<double>(2 * cap_B);
+  // routing partials live in the split-K arena's tail; size generously
+  const int64_t gin = m.gin(), kv = m.kv_in(), q = m.q_in();
+  size_t ws = 0;
+  auto acc = [&](int M, int N, int64_t K) { ws += static_cast<size_t>(choose_splits(M, N, K)) * M * N; };
+  // decoder bwd
+  acc(static_cast<int>(dh), static_cast<int>(2 * da), B2);
+  acc(1, static_cast<int>(dh), B2);
+  acc(1, static_cast<int>(dh), B2);
+  acc(1, 1, B2);
+  // attention bwd
+  acc(static_cast<int>(da), static_cast<int>(q), R);
+  acc(1, static_cast<int>(da), R);
+  acc(static_cast<int>(da), static_cast<int>(kv), P);
+  acc(1, static_cast<int>(da), P);
+  acc(static_cast<int>(da), static_cast<int>(kv), P);
+  acc(1, static_cast<int>(da), P);
+  acc(static_cast<int>(2 * da), static_cast<int>(dt), P);
+  // gru bwd
+  acc(static_cast<int>(2 * d), static_cast<int>(gin), U);
+  acc(static_cast<int>(d), static_cast<int>(m.mail_dim()), U);
+  acc(static_cast<int>(d), static_cast<int>(d), U);
+  acc(1, static_cast<int>(3 * d), U);
+  const int64_t nchunks = ceil_div(R + P, kChunk) + 1;
+  ws += 2 * static_cast<size_t>(nchunks) * 3 * da;
+  w.splitk_ws_floats = ws;
+  w.splitk_ws = dalloc<float>(ws);
+  w.wpack_bytes = pack_bytes(static_cast<int>(B2), d);
+  TGB_CUDA(cudaMalloc(&w.wpack, w.wpack_bytes));
+  TGB_CUDA(cudaMemset(w.wpack, 0, w.wpack_bytes));
+  {
+    WriteSet v = pack_view(w.wpack, static_cast<int>(B2), d);
+    w.w_count = const_cast<int32_t*>(v.count);
+    w.w_node = const_cast<int32_t*>(v.node);
+    w.w_event = const_cast<int32_t*>(v.event);
+    w.w_t = const_cast<double*>(v.t);
+    w.w_dt = const_cast<double*>(v.dt);
+    w.w_mem = const_cast<float*>(v.mem);
+    w.w_mail = const_cast<float*>(v.mail);
+  }
+  w.win = dalloc<int32_t>(num_nodes);
+  TGB_CUDA(cudaMemset(w.win, 0, sizeof(int32_t) * num_nodes));
+  TGB_CUDA(cudaMemset(w.w_count, 0, sizeof(int32_t)));
+}
+
+void step_free(StepWork& w) {
+  void* ptrs[] = {w.Xg, w.GU, w.Gates, w.RS, w.s_hat, w.Qin, w.KVin, w.Gt, w.Q, w.KV, w.attn_a,
+                  w.H, w.AB, w.HID, w.Dhid, w.Hin, w.dlogit, w.logits, w.dIn, w.dQ, w.dKV,
+                  w.dNodeAcc, w.dNode, w.Dg, w.T1, w.DMT, w.Mom, w.omega_part, w.ones,
+                  w.loss_terms, w.splitk_ws, w.wpack, w.win};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  w = StepWork{};
+}
+
+size_t pack_bytes(int cap, int64_t d) {
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  return 16 + 2 * a16(4 * static_cast<size_t>(cap)) + 2 * a16(8 * static_cast<size_t>(cap)) +
+         a16(4 * static_cast<size_t>(cap) * d) + a16(8 * static_cast<size_t>(cap) * d);
+}
+
+WriteSet pack_view(void* base, int cap, int64_t d) {
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  char* p = static_cast<char*>(base);
+  WriteSet ws;
+  ws.cap = cap;
+  ws.count = reinterpret_cast<const int32_t*>(p);
+  p += 16;
+  ws.node = reinterpret_cast<const int32_t*>(p);
+  p += a16(4 * static_cast<size_t>(cap));
+  ws.event = reinterpret_cast<const int32_t*>(p);
+  p += a16(4 * static_cast<size_t>(cap));
+  ws.t = reinterpret_cast<const double*>(p);
+  p += a16(8 * static_cast<size_t>(cap));
+  ws.dt = reinterpret_cast<const double*>(p);
+  p += a16(8 * static_cast<size_t>(cap));
+  ws.mem = reinterpret_cast<const float*>(p);
+  p += a16(4 * static_cast<size_t>(cap) * d);
+  ws.mail = reinterpret_cast<const float*>(p);
+  return ws;
+}
+
+void substep_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
+                    cudaStream_t s) {
+  substep_gru_launch(c, pl, vw, s);
+  substep_rest_launch(c, pl, vw, loss_out, s);
+}
+
+void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s) {
+  const ModelDims& m = c.m;
+  const ParamLayout& L = c.L;
+  StepWork& w = *c.w;
+  const DGraph& g = *c.g;
+  const Dims D = make_dims(m, g);
+  const float* P = c.params;
+  const int d = D.d, md = D.md, gin = D.gin;
+  const int U = w.cap_U;
+  const int* szU = pl.sizes + kSzU;
+  // ---- GRU freshen (K5)
+  c.mark(phGruFwd, s);
+  assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, vw, g, P + L.off[tOmega], w.Xg,
+                                                             w.ldx, w.GU);
+  {
+    GemmGroup gg;
+    add_nn(gg, U, szU, 2 * d, gin, A_rows(w.Xg, w.ldx, gin), B_wT(P + L.off[tWz], gin, gin), w.Gates,
+           3 * d, P + L.off[tBz]);
+    add_nn(gg, U, szU, d, md, A_rows(w.Xg, w.ldx, md), B_wT(P + L.off[tWh], gin, md), w.Gates + 2 * d,
+           3 * d, P + L.off[tBh]);
+    gemm_group_launch(gg, s);
+  }
+  const int eblocks = 4 * kSMs;
+  gru_mid_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, w.RS);
+  {
+    GemmGroup gg;
+    add_nn(gg, U, szU, d, d, A_rows(w.RS, d, d), B_wT(P + L.off[tWh] + md, gin, d), w.Gates + 2 * d,
+           3 * d, nullptr, 1.0f);
+    gemm_group_launch(gg, s);
+  }
+  gru_out_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, w.s_hat, c.d_numeric_flag);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
+                         cudaStream_t s) {
+  const ModelDims& m = c.m;
+  const ParamLayout& L = c.L;
+  StepWork& w = *c.w;
+  const DGraph& g = *c.g;
+  const Dims D = make_dims(m, g);
+  const float* P = c.params;
+  float* G = c.grads;
+  const int d = D.d, dt = D.dt, da = D.da, dh = D.dh, md = D.md, gin = D.gin;
+  const int U = w.cap_U, R = w.cap_R, Pc = w.cap_P, B2 = 2 * w.cap_B;
+  const int* szU = pl.sizes + kSzU;
+  const int* szR = pl.sizes + kSzR;
+  const int* szP = pl.sizes + kSzP;
+  const int* sz2B = pl.sizes + kSz2B;
+
+  TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));
+  const int eblocks = 4 * kSMs;
+
+  // ---- attention forward (K6)
+  c.mark(phAttnAssemble, s);
+  assemble_attn_kernel<<<row_blocks(R + Pc), 32 * kWarps, 0, s>>>(
+      D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, w.Qin, w.ldq, w.KVin, w.ldkv, w.Gt);
+  c.mark(phAttnProj, s);
+  {
+    GemmGroup gg;
+    add_nn(gg, R, szR, da, D.q_in, A_rows(w.Qin, w.ldq, D.q_in), B_wT(P + L.off[tWq], D.q_in, D.q_in),
+           w.Q, da, P + L.off[tBq]);
+    add_nn(gg, Pc, szP, da, D.kv_in, A_rows(w.KVin, w.ldkv, D.kv_in),
+           B_wT(P + L.off[tWk], D.kv_in, D.kv_in), w.KV, 2 * da, P + L.off[tBk]);
+    add_nn(gg, Pc, szP, da, D.kv_in, A_rows(w.KVin, w.ldkv, D.kv_in),
+           B_wT(P + L.off[tWv], D.kv_in, D.kv_in), w.KV + da, 2 * da, P + L.off[tBv]);
+    gemm_group_launch(gg, s);
+  }
+  c.mark(phAttnSoftmax, s);
+  attn_fwd_kernel<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.Q, w.KV, w.attn_a, w.H,
+                                                         c.d_numeric_flag);
+
+  // ---- decoder + loss (K7)
+  c.mark(phDecoder, s);
+  {
+    GemmGroup gg;
+    add_nn(gg, R, szR, dh, da, A_rows(w.H, da, da), B_wT(P + L.off[tW1], 2 * da, da), w.AB, 2 * dh);
+    add_nn(gg, R, szR, dh, da, A_rows(w.H, da, da), B_wT(P + L.off[tW1] + da, 2 * da, da), w.AB + dh,
+           2 * dh);
+    gemm_group_launch(gg, s);
+  }
+  decoder_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(
+      D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, w.Dhid, w.Hin,
+      w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag);
+  loss_kernel<<<1, 1024, 0, s>>>(pl, w.loss_terms, loss_out, c.d_numeric_flag);
+
+  WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
+  c.mark(phDecoderBwd, s);
+  {
+    GemmGroup gg;
+    add_tn(gg, wc, dh, 2 * da, B2, sz2B, A_trans(w.Dhid, dh, B2), B_w(w.Hin, 2 * da, B2),
+           G + L.off[tW1], 2 * da);
+    add_tn(gg, wc, 1, dh, B2, sz2B, ones_op(w.ones, B2), B_w(w.Dhid, dh, B2), G + L.off[tB1], dh);
+    add_tn(gg, wc, 1, dh, B2, sz2B, op_dense(w.dlogit, 0, 1, B2), B_w(w.HID, dh, B2), G + L.off[tW2],
+           dh);
+    add_tn(gg, wc, 1, 1, B2, sz2B, ones_op(w.ones, B2), op_dense(w.dlogit, 1, 0, B2), G + L.off[tB2],
+           1);
+    add_nn(gg, B2, sz2B, 2 * da, dh, A_rows(w.Dhid, dh, dh), B_w(P + L.off[tW1], 2 * da, dh), w.dIn,
+           2 * da);
+    gemm_group_launch(gg, s);
+  }
+
+  // ---- attention backward (K8)
+  c.mark(phAttnBwd, s);
+  attn_bwd_kernel<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ,
+                                                         w.dKV);
+  const int64_t nchunks = ceil_div(R + Pc, kChunk) + 1;
+  float* part_first = wc.take(static_cast<size_t>(nchunks) * 3 * da);
+  float* part_last = wc.take(static_cast<size_t>(nchunks) * 3 * da);
+  routing_chunk_kernel<<<row_blocks(nchunks), 32 * kWarps, 0, s>>>(D, pl, w.dQ, w.dKV, w.dNodeAcc,
+                                                                    part_first, part_last);
+  routing_fixup_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, w.dNodeAcc, part_first,
+                                                             part_last);
+  c.mark(phAttnBwdGemm, s);
+  {
+    GemmGroup gg;
+    Operand bs;
+    op_append(bs, P + L.off[tWq], D.q_in, 1, da);
+    op_append(bs, P + L.off[tWk], D.kv_in, 1, da);
+    op_append(bs, P + L.off[tWv], D.kv_in, 1, da);
+    add_nn(gg, U, szU, d + D.ds, 3 * da, A_rows(w.dNodeAcc, 3 * da, 3 * da), bs, w.dNode, d + D.ds);
+    add_tn(gg, wc, da, D.q_in, R, szR, A_trans(w.dQ, da, R), B_w(w.Qin, w.ldq, R), G + L.off[tWq],
+           D.q_in);
+    add_tn(gg, wc, 1, da, R, szR, ones_op(w.ones, R), B_w(w.dQ, da, R), G + L.off[tBq], da);
+    add_tn(gg, wc, da, D.kv_in, Pc, szP, A_trans(w.dKV, 2 * da, Pc), B_w(w.KVin, w.ldkv, Pc),
+           G + L.off[tWk], D.kv_in);
+    add_tn(gg, wc, 1, da, Pc, szP, ones_op(w.ones, Pc), B_w(w.dKV, 2 * da, Pc), G + L.off[tBk], da);
+    add_tn(gg, wc, da, D.kv_in, Pc, szP, A_trans(w.dKV + da, 2 * da, Pc), B_w(w.KVin, w.ldkv, Pc),
+           G + L.off[tWv], D.kv_in);
+    add_tn(gg, wc, 1, da, Pc, szP, ones_op(w.ones, Pc), B_w(w.dKV + da, 2 * da, Pc), G + L.off[tBv],
+           da);
+    add_tn(gg, wc, 2 * da, dt, Pc, szP, A_trans(w.dKV, 2 * da, Pc), B_w(w.Gt, dt, Pc), w.Mom, dt);
+    gemm_group_launch(gg, s);
+  }
+
+  // ---- GRU backward (K9)
+  c.mark(phGruBwd, s);
+  gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, w.Dg, G + L.off[tStatic]);
+  {
+    GemmGroup gg;
+    add_nn(gg, U, szU, d, d, A_rows(w.Dg + 2 * d, 3 * d, d), B_w(P + L.off[tWh] + md, gin, d), w.T1, d);
+    gemm_group_launch(gg, s);
+  }
+  gru_bwd2_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.T1, w.Gates, w.Dg);
+  {
+    GemmGroup gg;
+    add_tn(gg, wc, 2 * d, gin, U, szU, A_trans(w.Dg, 3 * d, U), B_w(w.Xg, w.ldx, U), G + L.off[tWz], gin);
+    add_tn(gg, wc, d, md, U, szU, A_trans(w.Dg + 2 * d, 3 * d, U), B_w(w.Xg, w.ldx, U), G + L.off[tWh],
+           gin);
+    add_tn(gg, wc, d, d, U, szU, A_trans(w.Dg + 2 * d, 3 * d, U), B_w(w.RS, d, U),
+           G + L.off[tWh] + md, gin);
+    add_tn(gg, wc, 1, 3 * d, U, szU, ones_op(w.ones, U), B_w(w.Dg, 3 * d, U), G + L.off[tBz], 3 * d);
+    add_nn(gg, U, szU, dt, 3 * d, A_rows(w.Dg, 3 * d, 3 * d), B_w(P + L.off[tWz] + 2 * d, gin, 3 * d),
+           w.DMT, dt);
+    gemm_group_launch(gg, s);
+  }
+  coldot_kernel<<<w.omega_chunks, 128, 0, s>>>(szU, dt, w.DMT, w.GU, w.omega_part, w.omega_chunks);
+  omega_final_kernel<<<1, 128, 0, s>>>(D, P, L.off[tWk], L.off[tWv], w.Mom, w.omega_part,
+                                       w.omega_chunks, G + L.off[tOmega]);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s) {
+  StepWork& w = *c.w;
+  const Dims D = make_dims(c.m, *c.g);
+  const int B2 = 2 * w.cap_B;
+  rw_mark_kernel<<<static_cast<int>(ceil_div(B2, 256)), 256, 0, s>>>(pl, *c.g, w.win, w.w_count);
+  rw_emit_kernel<<<row_blocks(B2), 32 * kWarps, 0, s>>>(D, pl, *c.g, vw, w.s_hat, w.win, w);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void apply_writes_launch(const std::vector<WriteSet>& sets, DMem& st, int32_t* win, cudaStream_t s) {
+  const bool multi = sets.size() > 1;
+  if (multi) {
+    for (const WriteSet& ws : sets)
+      apply_mark_kernel<<<static_cast<int>(ceil_div(ws.cap, 256)), 256, 0, s>>>(ws, win);
+  }
+  for (const WriteSet& ws : sets)
+    apply_rows_kernel<<<row_blocks(ws.cap), 32 * kWarps, 0, s>>>(ws, st, win, multi ? 1 : 0);
+  if (multi) {
+    for (const WriteSet& ws : sets)
+      apply_clear_kernel<<<static_cast<int>(ceil_div(ws.cap, 256)), 256, 0, s>>>(ws, win);
+  }
+  TGB_CUDA(cudaGetLastError());
+}
+
+void reset_state_launch(DMem& st, cudaStream_t s) {
+  TGB_CUDA(cudaMemsetAsync(st.memory, 0, sizeof(float) * st.N * st.d, s));
+  TGB_CUDA(cudaMemsetAsync(st.mail_mem, 0, sizeof(float) * st.N * 2 * st.d, s));
+  TGB_CUDA(cudaMemsetAsync(st.last_update, 0, sizeof(double) * st.N, s));
+  TGB_CUDA(cudaMemsetAsync(st.mail_t, 0, sizeof(double) * st.N, s));
+  TGB_CUDA(cudaMemsetAsync(st.mail_dt, 0, sizeof(double) * st.N, s));
+  fill_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(st.N, 256), 4 * kSMs)), 256, 0, s>>>(
+      st.mail_ev, st.N, -1);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void adam_launch(float* params, const float* grads, float* m, float* v, int64_t n, float lr,
+                 float c1, float c2, float grad_scale, cudaStream_t s) {
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
+  adam_kernel<<<blocks, 256, 0, s>>>(params, grads, m, v, n, lr, c1, c2, grad_scale);
+  TGB_CUDA(cudaGetLastError());
+}
+
+}  // namespace tgb

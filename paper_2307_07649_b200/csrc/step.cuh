@@ -1,0 +1,139 @@
+// The TGN training sub-step on device (trainer.hpp:170-272) and the root
+// memory writes (trainer.hpp:284-330).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+#include "device_types.cuh"
+#include "gemm_simt.cuh"
+
+namespace tgb {
+
+// ModelConfig (model.hpp:19-35) and the canonical flat parameter layout
+// (for_each_tensor order, model.hpp:56-76).
+struct ModelDims {
+  int64_t d_mem = 100, d_time = 100, d_static = 100, d_attn = 100, d_hidden = 0, d_e = 0;
+  int64_t n_neighbors = 10, num_nodes = 0;
+  double max_t = 1.0;
+
+  int64_t mail_dim() const { return 2 * d_mem + d_time + d_e; }
+  int64_t gin() const { return mail_dim() + d_mem; }
+  int64_t node_dim() const { return d_mem + d_static; }
+  int64_t q_in() const { return node_dim() + d_time; }
+  int64_t kv_in() const { return node_dim() + d_e + d_time; }
+  int64_t dh() const { return d_hidden ? d_hidden : d_mem; }
+};
+
+enum TensorId {
+  tOmega = 0, tWz, tWr, tWh, tBz, tBr, tBh, tWq, tBq, tWk, tBk, tWv, tBv, tStatic, tW1, tB1, tW2,
+  tB2, tNumTensors
+};
+
+struct ParamLayout {
+  int64_t off[tNumTensors + 1] = {};
+  int64_t rows[tNumTensors] = {}, cols[tNumTensors] = {};
+  int64_t total = 0;
+  static ParamLayout make(const ModelDims& m);
+};
+
+// Per-trainer activation workspace (capacities fixed at creation).
+struct StepWork {
+  int cap_B = 0, cap_R = 0, cap_P = 0, cap_U = 0;
+  int64_t ldx = 0, ldq = 0, ldkv = 0;
+  float *Xg = nullptr, *GU = nullptr, *Gates = nullptr, *RS = nullptr, *s_hat = nullptr;
+  float *Qin = nullptr, *KVin = nullptr, *Gt = nullptr, *Q = nullptr, *KV = nullptr;
+  float *attn_a = nullptr, *H = nullptr, *AB = nullptr, *HID = nullptr, *Dhid = nullptr;
+  float *Hin = nullptr, *dlogit = nullptr, *logits = nullptr, *dIn = nullptr, *dQ = nullptr;
+  float *dKV = nullptr, *dNodeAcc = nullptr, *dNode = nullptr, *Dg = nullptr, *T1 = nullptr;
+  float *DMT = nullptr, *Mom = nullptr, *omega_part = nullptr, *ones = nullptr;
+  double* loss_terms = nullptr;
+  float* splitk_ws = nullptr;
+  size_t splitk_ws_floats = 0;
+  int omega_chunks = 0;
+  // root writes (compact rows) live in one packed buffer so they can be
+  // exchanged with a single collective: see pack_layout().
+  void* wpack = nullptr;
+  size_t wpack_bytes = 0;
+  int32_t* w_count = nullptr;   // [1]
+  int32_t* w_node = nullptr;    // [2 cap_B]
+  int32_t* w_event = nullptr;
+  double* w_t = nullptr;
+  double* w_dt = nullptr;
+  float* w_mem = nullptr;       // [2 cap_B, d]
+  float* w_mail = nullptr;      // [2 cap_B, 2d]
+  int32_t* win = nullptr;       // [N] COMB scratch (0 = empty, else event + 1)
+};
+
+// Optional CUDA-event phase markers (bench.py reads per-phase device time).
+enum Phase {
+  phPlan = 0, phGruFwd, phAttnAssemble, phAttnProj, phAttnSoftmax, phDecoder, phDecoderBwd,
+  phAttnBwd, phAttnBwdGemm, phGruBwd, phWrites, phAllreduce, phAdam, phCount
+};
+struct PhaseMarks {
+  bool on = false;
+  cudaEvent_t ev[phCount + 1] = {};
+  bool hit[phCount + 1] = {};
+  void mark(int slot, cudaStream_t s) {
+    if (on) {
+      cudaEventRecord(ev[slot], s);
+      hit[slot] = true;
+    }
+  }
+};
+
+struct StepCtx {
+  ModelDims m;
+  ParamLayout L;
+  const DGraph* g = nullptr;
+  float* params = nullptr;
+  float* grads = nullptr;
+  StepWork* w = nullptr;
+  int* d_numeric_flag = nullptr;  // set when a non-finite value escapes a kernel
+  PhaseMarks* marks = nullptr;
+  void mark(int slot, cudaStream_t s) const {
+    if (marks) marks->mark(slot, s);
+  }
+};
+
+void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes);
+void step_free(StepWork& w);
+
+// Forward + backward of one sub-iteration on (plan, view). Writes the loss to
+// *loss_out (device double) and the flat gradient (grads zeroed first).
+void substep_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
+                    cudaStream_t s);
+// The same split in two: the GRU freshen (s_hat, all the root writes need)
+// and everything after it. substep_launch == gru + rest.
+void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s);
+void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
+                         cudaStream_t s);
+// build_root_writes + COMB for the plan's slice into w.w_* (compact rows).
+void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s);
+// Applies compact write rows (one or more row sets, later sets win on equal
+// nodes -- ascending-rank application, memory_daemon.hpp:35-38) to the state.
+struct WriteSet {
+  const int32_t* count;
+  const int32_t* node;
+  const int32_t* event;
+  const double* t;
+  const double* dt;
+  const float* mem;
+  const float* mail;
+  int cap;
+};
+void apply_writes_launch(const std::vector<WriteSet>& sets, DMem& st, int32_t* win,
+                         cudaStream_t s);
+
+// Packed write-row buffer: {count | node[cap] | event[cap] | t[cap] | dt[cap] |
+// mem[cap, d] | mail[cap, 2d]}, every segment 16-byte aligned.
+size_t pack_bytes(int cap, int64_t d);
+WriteSet pack_view(void* base, int cap, int64_t d);
+void reset_state_launch(DMem& st, cudaStream_t s);
+
+// Dense Adam over the flat parameters (optimizer.hpp:40-56). Gradients are
+// scaled by grad_scale first (1 / active trainers after an all-reduce sum).
+void adam_launch(float* params, const float* grads, float* m, float* v, int64_t n, float lr,
+                 float c1, float c2, float grad_scale, cudaStream_t s);
+
+}  // namespace tgb

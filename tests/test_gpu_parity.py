@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+Checkers: the unmodified reference compiled in-process (oracle/_ref) and the
+numpy restatement (oracle/tgnn_oracle.py). Integer/index outputs must be
+bit-exact; fp32 values within 1e-4 relative of the f64 reference
+(tolerance REL_TOL in tests/helpers.py).
+"""
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+import pytest
+
+import paper_2307_07649_b200 as T
+from oracle import ref
+from oracle import tgnn_oracle as O
+from tests.helpers import REL_TOL, random_state, rel_close, tensor_slices
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(nodes=60, events=800, d_e=4, seed=3)
+SMALL_MODEL = dict(d_mem=6, d_time=4, d_static=3, d_attn=5, d_hidden=4, n_neighbors=5)
+# Wikipedia shape (BASELINE C1): 9,227 nodes, 157,474 events, 172-d features, TGN (no static)
+WIKI = dict(nodes=9227, events=157474, d_e=172, seed=1)
+WIKI_MODEL = dict(d_mem=100, d_time=100, d_static=0, d_attn=100, d_hidden=100, n_neighbors=10)
+# Reddit-shape dims (BASELINE C2: static memory, 172-d features), 120k-event prefix
+REDDIT = dict(nodes=10984, events=120000, d_e=172, seed=1)
+REDDIT_MODEL = dict(d_mem=100, d_time=100, d_static=100, d_attn=100, d_hidden=100, n_neighbors=10)
+
+
+@functools.lru_cache(maxsize=None)
+def _streams(key):
+    p = dict(key)
+    s = T.gen_synthetic(T.SynthParams(**p))
+    rg = ref.RefGraph.synthetic(p["nodes"], p["events"], d_e=p["d_e"], seed=p["seed"])
+    return s, rg
+
+
+@functools.lru_cache(maxsize=None)
+def _graph(key, ctxh):
+    s, _ = _streams(key)
+    return T.TemporalGraph.from_stream(_CTX[0], s)
+
+
+_CTX = []
+
+
+@pytest.fixture(scope="module")
+def env(ctx):
+    _CTX[:] = [ctx]
+    return ctx
+
+
+def setup(key, env):
+    s, rg = _streams(tuple(sorted(key.items())))
+    g = _graph(tuple(sorted(key.items())), id(env))
+    return s, rg, g
+
+
+def model_for(s, mdims):
+    return T.ModelConfig(d_e=s.d_e, num_nodes=s.num_nodes, max_t=float(s.t[-1]), **mdims)
+
+
+# ---------------------------------------------------------------- sampler (K1/K2/K3)
+@pytest.mark.parametrize("cfg", [SMALL, WIKI])
+def test_sampler_bit_exact(env, cfg):
+    s, rg, g = setup(cfg, env)
+    rng = np.random.default_rng(0)
+    q = 3000
+    nodes = rng.integers(0, s.num_nodes, q)
+    times = s.t[rng.integers(0, s.num_events, q)]
+    times[:50] = s.t[0]  # nothing strictly before the first event
+    for n in (10, 1):
+        nn, ne, nd, cnt = g.sample_recent_neighbors_batch(nodes, times, n)
+        for x in range(q):
+            a = rg.sample_recent_neighbors(int(nodes[x]), float(times[x]), n)
+            c = int(cnt[x])
+            assert c == len(a[0])
+            assert np.array_equal(nn[x, :c], a[0]) and np.array_equal(ne[x, :c], a[1])
+            assert np.array_equal(nd[x, :c], a[2])  # f64 subtraction: bit-exact
+
+
+def test_sampler_known_answer(env):
+    """ref/tests/test_temporal_graph.cpp:40-57 toy graph."""
+    g = T.TemporalGraph(env, 5, 3, [0, 1, 0, 2, 0], [3, 3, 4, 3, 3], [1.0, 2.0, 3.0, 3.0, 5.0])
+    nn, ne, nd = g.sample_recent_neighbors(0, 5.0, 10)
+    assert list(nn) == [4, 3] and list(nd) == [2.0, 4.0]
+    nn, _, _ = g.sample_recent_neighbors(0, 5.0, 1)
+    assert list(nn) == [4]
+    assert len(g.sample_recent_neighbors(0, 1.0, 10)[0]) == 0
+    negs = g.sample_negatives(0, 0, 200, 7)
+    assert negs.min() >= 3 and negs.max() < 5
+    assert np.array_equal(g.sample_negatives(0, 0, 200, 7), negs)
+    assert not np.array_equal(g.sample_negatives(0, 1, 200, 7), negs)
+
+
+@pytest.mark.parametrize("cfg", [SMALL, WIKI])
+def test_negatives_bit_exact(env, cfg):
+    s, rg, g = setup(cfg, env)
+    for batch, group, count, seed in [(0, 0, 600, 1), (17, 5, 1200, 3), (3, 123456, 7, 99)]:
+        assert np.array_equal(g.sample_negatives(batch, group, count, seed),
+                              rg.sample_negatives(batch, group, count, seed))
+
+
+@pytest.mark.parametrize("cfg,begin,B", [(SMALL, 300, 50), (WIKI, 60000, 600), (WIKI, 0, 600)])
+def test_plan_bit_exact(env, cfg, begin, B):
+    s, rg, g = setup(cfg, env)
+    negs = rg.sample_negatives(begin // B, 7, B, 1)
+    a = g.plan_sub_batch(begin, begin + B, negs, 10)
+    b = rg.plan_sub_batch(begin, begin + B, negs, 10)
+    for k in ("root_node", "root_t", "nbr_count", "nbr_node", "nbr_event", "nbr_dt", "supports"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+# ---------------------------------------------------------------- memory store
+def test_memstore_semantics(env):
+    m = T.NodeMemoryStore(env, 4, 2)
+    mem2 = np.array([[0.1, 0.2, 0.3, 0.4, 5.0, 4.5, 17.0]])
+    m.write([1], [[9.0, 8.0]], mem2)
+    st = m.export()
+    assert st["memory"][1].tolist() == [9.0, 8.0]
+    assert np.allclose(st["mail_mem"][1], [0.1, 0.2, 0.3, 0.4], atol=1e-7)
+    assert st["mail_t"][1] == 5.0 and st["mail_dt"][1] == 4.5 and st["mail_event"][1] == 17
+    assert st["last_update"][1] == st["mail_t"][1]
+    assert st["mail_event"][0] == -1 and st["memory"][0].tolist() == [0.0, 0.0]
+    # later rows win within one write (apply_root_write in order)
+    m.write([2, 2], [[1.0, 1.0], [2.0, 2.0]], np.zeros((2, 7)) + [[0, 0, 0, 0, 1, 1, 3]])
+    v = m.read([[2, 1]])[0]
+    assert v.mem[0].tolist() == [2.0, 2.0] and v.mail[1, 6] == 17.0
+    m.reset()
+    st = m.export()
+    assert st["memory"].sum() == 0 and (st["mail_event"] == -1).all() and st["last_update"].sum() == 0
+
+
+# ---------------------------------------------------------------- model step (K4-K13)
+def _substep_case(env, cfg, mdims, begin, B, seed=0):
+    s, rg, g = setup(cfg, env)
+    mc = model_for(s, mdims)
+    params = O.init_params(mc, 5) if mc.d_mem < 20 else ref.init_params(mc, 5)
+    rng = np.random.default_rng(seed)
+    params = params + rng.normal(scale=0.02, size=params.shape) * (params != 0)
+    negs = rg.sample_negatives(begin // B, 3, B, 1)
+    plan = rg.plan_sub_batch(begin, begin + B, negs, mc.n_neighbors)
+    st = random_state(s.num_nodes, mc.d_mem, s.t, begin, seed=seed)
+    vm, vl = st.read(plan["supports"])
+    return s, rg, g, mc, params, negs, plan, vm, vl
+
+
+@pytest.mark.parametrize("case", ["small", "wiki", "reddit"])
+def test_sub_step_parity(env, case):
+    cfg, mdims, begin, B = {"small": (SMALL, SMALL_MODEL, 300, 50),
+                            "wiki": (WIKI, WIKI_MODEL, 60000, 600),
+                            "reddit": (REDDIT, REDDIT_MODEL, 90000, 600)}[case]
+    s, rg, g, mc, params, negs, plan, vm, vl = _substep_case(env, cfg, mdims, begin, B)
+    loss_r, grads_r, shat_r = rg.sub_step(mc, params, begin, begin + B, negs, vm, vl)
+    tr = T.TrainerCore(env, g, mc, B, 1)
+    tr.set_params(params)
+    loss, shat = tr.sub_step(begin, begin + B, negs, vm, vl)
+    grads = tr.grads()
+    assert abs(loss - loss_r) <= REL_TOL * abs(loss_r), (loss, loss_r)
+    ok, err, sc = rel_close(shat, shat_r)
+    assert ok, ("s_hat", err, sc)
+    for name, sl in tensor_slices(mc).items():
+        ok, err, sc = rel_close(grads[sl], grads_r[sl], floor=1e-7)
+        assert ok, (name, err, sc)
+        # untouched parameters (static rows, zero-gradient entries) stay exactly zero
+        assert np.all(grads[sl][grads_r[sl] == 0] == 0), name
+    # determinism: a second identical step is bitwise identical
+    loss2, shat2 = tr.sub_step(begin, begin + B, negs, vm, vl)
+    assert loss2 == loss and np.array_equal(shat2, shat) and np.array_equal(tr.grads(), grads)
+    tr.close()
+
+
+@pytest.mark.parametrize("case", ["small", "wiki"])
+def test_root_writes_parity(env, case):
+    cfg, mdims, begin, B = {"small": (SMALL, SMALL_MODEL, 300, 50),
+                            "wiki": (WIKI, WIKI_MODEL, 60000, 600)}[case]
+    s, rg, g, mc, params, negs, plan, vm, vl = _substep_case(env, cfg, mdims, begin, B)
+    _, _, shat_r = rg.sub_step(mc, params, begin, begin + B, negs, vm, vl)
+    nodes_r, mem_r, mail_r = rg.build_root_writes(mc.d_mem, mc.n_neighbors, begin, begin + B,
+                                                  negs, vm, vl, shat_r)
+    tr = T.TrainerCore(env, g, mc, B, 1)
+    tr.set_params(params)
+    tr.sub_step(begin, begin + B, negs, vm, vl)
+    nodes, mem, mail = tr.root_writes()
+    d = mc.d_mem
+    assert np.array_equal(nodes, nodes_r)
+    assert np.array_equal(mail[:, 2 * d:], mail_r[:, 2 * d:])  # t, dt (f64) and event: exact
+    assert rel_close(mail[:, :2 * d], mail_r[:, :2 * d], tol=1e-6)[0]  # stale view rows (f32 copy)
+    assert rel_close(mem, mem_r)[0]
+    tr.close()
+
+
+def test_adam_parity(env):
+    s, rg, g = setup(SMALL, env)
+    mc = model_for(s, SMALL_MODEL)
+    p0 = O.init_params(mc, 2)
+    tr = T.TrainerCore(env, g, mc, 50, 1)
+    tr.set_params(p0)
+    negs = rg.sample_negatives(0, 0, 50, 1)
+    plan = rg.plan_sub_batch(300, 350, negs, mc.n_neighbors)
+    st = random_state(s.num_nodes, mc.d_mem, s.t, 300)
+    vm, vl = st.read(plan["supports"])
+    tr.sub_step(300, 350, negs, vm, vl)
+    grads = tr.grads()
+    adam = ref.RefAdam(len(p0))
+    pr = p0.copy()
+    for _ in range(3):
+        adam.step(mc, pr, grads, 1e-2)
+        tr.adam_step(1e-2)
+    assert rel_close(tr.params(), pr, tol=1e-5, floor=1e-6)[0]
+
+
+# ---------------------------------------------------------------- trainer loop
+@pytest.mark.parametrize("case", ["small", "wiki"])
+def test_run_sequential_parity(env, case):
+    cfg, mdims, B, nb = {"small": (SMALL, SMALL_MODEL, 50, 12), "wiki": (WIKI, WIKI_MODEL, 600, 3)}[case]
+    s, rg, g = setup(cfg, env)
+    mc = model_for(s, mdims)
+    end = B * nb
+    tc = T.TrainConfig(local_batch=B, seed=3, epochs=2 if case == "small" else 1)
+    r = rg.run(mc, ref.train_cfg(local_batch=B, seed=3, epochs=tc.epochs), 0, end)
+    res = T.run_sequential(env, g, mc, tc, 0, end)
+    assert res.barriers == r["barriers"]
+    ok, err, sc = rel_close(res.barrier_loss, r["barrier_loss"], tol=1e-3)
+    assert ok, (res.barrier_loss, r["barrier_loss"])
+    ok, err, sc = rel_close(res.params, r["params"], tol=2e-3, floor=1e-4)
+    assert ok, (err, sc)
