@@ -13,14 +13,27 @@ struct GroupParams {
   int count;
 };
 
-__device__ __forceinline__ float op_at(const Operand& o, int64_t r, int k) {
+__device__ __forceinline__ int seg_of(const Operand& o, int k) {
   // Segment lookup along K (<= 4 segments).
   int s = 0;
 #pragma unroll
   for (int x = 1; x < 4; ++x)
     if (x < o.nseg && k >= o.kb[x]) s = x;
+  return s;
+}
+
+// A(m, k) = seg.p[m * rs + (k - kb) * cs]
+__device__ __forceinline__ float a_at(const Operand& o, int64_t m, int k) {
+  const int s = seg_of(o, k);
   const Seg& sg = o.seg[s];
-  return sg.p[r * sg.rs + static_cast<int64_t>(k - o.kb[s]) * sg.cs];
+  return sg.p[m * sg.rs + static_cast<int64_t>(k - o.kb[s]) * sg.cs];
+}
+
+// B(k, n) = seg.p[(k - kb) * rs + n * cs]
+__device__ __forceinline__ float b_at(const Operand& o, int k, int64_t n) {
+  const int s = seg_of(o, k);
+  const Seg& sg = o.seg[s];
+  return sg.p[static_cast<int64_t>(k - o.kb[s]) * sg.rs + n * sg.cs];
 }
 
 // A tile [BM x BK] -> As[k][m];  B tile [BK x BN] -> Bs[k][n].
@@ -40,7 +53,7 @@ __device__ __forceinline__ void load_a(const Operand& o, int m0, int k0, int M, 
       mm = idx % BM;
     }
     const int m = m0 + mm, k = k0 + kk;
-    reg[i] = (m < M && k < K) ? op_at(o, m, k) : 0.0f;
+    reg[i] = (m < M && k < K) ? a_at(o, m, k) : 0.0f;
   }
   (void)As;
 }
@@ -76,7 +89,7 @@ __device__ __forceinline__ void load_b(const Operand& o, int n0, int k0, int N, 
       kk = idx % BK;
     }
     const int n = n0 + nn, k = k0 + kk;
-    reg[i] = (n < N && k < K) ? op_at(o, k, n) : 0.0f;
+    reg[i] = (n < N && k < K) ? b_at(o, k, n) : 0.0f;
   }
 }
 

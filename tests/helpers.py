@@ -33,9 +33,13 @@ def rel_close(a, b, tol=REL_TOL, floor=1e-6):
     return err <= tol * scale + floor, err, scale
 
 
+def ocfg(mc):
+    return mc if isinstance(mc, O.ModelConfig) else O.ModelConfig(**mc.__dict__)
+
+
 def tensor_slices(mc):
     out, at = {}, 0
-    for name, shape in O.tensor_shapes(mc):
+    for name, shape in O.tensor_shapes(ocfg(mc)):
         k = int(np.prod(shape))
         out[name] = slice(at, at + k)
         at += k
