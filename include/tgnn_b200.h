@@ -196,6 +196,20 @@ int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out);
 #define TGNN_PHASES 13
 int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes);
 
+/* ------------------------------------------------------------------ GEMM engine
+ * Process-wide choice for the step's dense contractions:
+ *   1 (default) tcgen05 tensor cores, bf16x3 split (hi*hi + hi*lo + lo*hi,
+ *     fp32 accumulate in TMEM) -- fp32-class accuracy;
+ *   0 fp32 FMA on CUDA cores -- the exact fp32 path. */
+int tgnn_set_gemm_impl(int impl);
+int tgnn_get_gemm_impl(int* impl);
+/* Test hook: C[M x N] = A . B on device with the chosen engine. A is [M x K]
+ * (a_trans = 0) or stored [K x M] (a_trans = 1); B is [K x N] (b_trans = 0) or
+ * stored [N x K] (b_trans = 1); all row-major float32 host buffers. splits > 1
+ * exercises the split-K path. */
+int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, int a_trans,
+                    const float* B, int b_trans, float* C, int splits);
+
 /* ------------------------------------------------------------------ host I/O
  * Streaming ingestion: (re)writes events [first, first+count) of a device
  * graph from host buffers (src/dst/t must match the finalized order; edge

@@ -464,6 +464,33 @@ def schedule_query(train: TrainConfig, train_begin: int, train_end: int, rank: i
     return nb.value, {k: out[:count, x].copy() for x, k in enumerate(SCHEDULE_FIELDS)}
 
 
+GEMM_SIMT, GEMM_TENSOR = 0, 1
+
+
+def set_gemm_impl(impl: int):
+    """0: exact fp32 CUDA-core GEMMs; 1 (default): tcgen05 bf16x3 tensor-core GEMMs."""
+    check(lib().tgnn_set_gemm_impl(impl))
+
+
+def get_gemm_impl() -> int:
+    v = C.c_int()
+    check(lib().tgnn_get_gemm_impl(C.byref(v)))
+    return v.value
+
+
+def debug_gemm(A, B, impl=GEMM_TENSOR, a_trans=False, b_trans=False, splits=1):
+    """C = op(A) op(B) on device (test hook for the GEMM engines)."""
+    A = np.ascontiguousarray(A, np.float32)
+    B = np.ascontiguousarray(B, np.float32)
+    M = A.shape[1] if a_trans else A.shape[0]
+    K = A.shape[0] if a_trans else A.shape[1]
+    N = B.shape[0] if b_trans else B.shape[1]
+    out = np.empty((M, N), np.float32)
+    check(lib().tgnn_debug_gemm(impl, M, N, K, _p(A, f32p), int(a_trans), _p(B, f32p), int(b_trans),
+                                _p(out, f32p), splits))
+    return out
+
+
 def comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().tgnn_comm_unique_id(buf))

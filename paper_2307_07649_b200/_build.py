@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", CSRC, "-I", os.path.join(HERE, "..", "include")]
-SOURCES = ["plan.cu", "gemm_simt.cu", "step.cu", "api.cu"]
+SOURCES = ["plan.cu", "gemm_simt.cu", "gemm_tc.cu", "step.cu", "api.cu"]
 
 
 def _deps_hash(src: str) -> str:
@@ -54,7 +54,7 @@ def build(verbose: bool = False) -> str:
     stamp_file = OUT + ".stamp"
     if os.path.exists(OUT) and os.path.exists(stamp_file) and open(stamp_file).read() == stamp:
         return OUT
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-lnccl", "-cudart", "static",
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-ldl", "-cudart", "static",
            "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -4,7 +4,6 @@
 // core (parameters, gradients, Adam state, workspaces) and the i x j x k
 // schedule; every compute step is a CUDA kernel on the context stream and
 // every exchange is an NCCL collective on the same stream (NVLink/NVSwitch).
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -19,6 +18,7 @@
 #include "device_types.cuh"
 #include "host/schedule.hpp"
 #include "host/synth.hpp"
+#include "nccl_dyn.hpp"
 #include "plan.cuh"
 #include "step.cuh"
 
@@ -32,7 +32,7 @@ thread_local std::string g_err;
   do {                                                                                \
     ncclResult_t r__ = (x);                                                           \
     if (r__ != ncclSuccess)                                                           \
-      throw ::tgb::Error(::tgb::kNccl, std::string(#x) + ": " + ncclGetErrorString(r__)); \
+      throw ::tgb::Error(::tgb::kNccl, std::string(#x) + ": " + nccl::api().GetErrorString(r__)); \
   } while (0)
 
 #define API_BEGIN try {
@@ -361,8 +361,8 @@ struct tgnn_run {
   bool marks_ready = false;
 
   ~tgnn_run() {
-    if (gcomm) ncclCommDestroy(gcomm);
-    if (comm) ncclCommDestroy(comm);
+    if (gcomm) nccl::api().CommDestroy(gcomm);
+    if (comm) nccl::api().CommDestroy(comm);
     if (d_losses) cudaFree(d_losses);
     if (gathered) cudaFree(gathered);
   }
@@ -489,13 +489,13 @@ void run_barrier(tgnn_run* r, int64_t b) {
       const size_t pb = tr->w.wpack_bytes;
       const int cap = 2 * tr->cap_B;
       if (r->group_size > 1) {
-        NCCL_CHECK(ncclGroupStart());
+        NCCL_CHECK(nccl::api().GroupStart());
         for (int mm = 0; mm < i; ++mm) {
           const int root = tt * i + mm;
           char* dst = static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb;
-          NCCL_CHECK(ncclBroadcast(tr->w.wpack, dst, pb, ncclChar, root, r->gcomm, s));
+          NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, dst, pb, ncclChar, root, r->gcomm, s));
         }
-        NCCL_CHECK(ncclGroupEnd());
+        NCCL_CHECK(nccl::api().GroupEnd());
         std::vector<WriteSet> sets;
         for (int mm = 0; mm < i; ++mm)
           sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap,
@@ -523,7 +523,7 @@ void run_barrier(tgnn_run* r, int64_t b) {
   // average_active_grads (trainer.hpp:473-483): idle ranks contribute zeros.
   sc.mark(phAllreduce, s);
   if (r->nranks > 1)
-    NCCL_CHECK(ncclAllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
+    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
                              r->comm, s));
   const int64_t active = r->sched.active_trainers[static_cast<size_t>(b)];
   sc.mark(phAdam, s);
@@ -1195,7 +1195,7 @@ int tgnn_comm_unique_id(char* out128) {
   API_BEGIN
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   ncclUniqueId id;
-  NCCL_CHECK(ncclGetUniqueId(&id));
+  NCCL_CHECK(nccl::api().GetUniqueId(&id));
   std::memcpy(out128, &id, 128);
   API_END
 }
@@ -1237,9 +1237,9 @@ int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128) {
   if (r->nranks == 1) return 0;
   ncclUniqueId id;
   std::memcpy(&id, unique_id128, 128);
-  NCCL_CHECK(ncclCommInitRank(&r->comm, r->nranks, id, r->rank));
+  NCCL_CHECK(nccl::api().CommInitRank(&r->comm, r->nranks, id, r->rank));
   if (r->group_size > 1) {
-    NCCL_CHECK(ncclCommSplit(r->comm, r->group, r->rank, &r->gcomm, nullptr));
+    NCCL_CHECK(nccl::api().CommSplit(r->comm, r->group, r->rank, &r->gcomm, nullptr));
   }
   r->comm_ready = true;
   API_END
@@ -1281,7 +1281,7 @@ int tgnn_run_losses(tgnn_run* r, int64_t first, int64_t count, double* out) {
   double* tmp = dalloc<double>(static_cast<size_t>(std::max<int64_t>(count, 1)));
   TGB_CUDA(cudaMemcpyAsync(tmp, r->d_losses + first, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
   if (r->nranks > 1)
-    NCCL_CHECK(ncclAllReduce(tmp, tmp, static_cast<size_t>(count), ncclDouble, ncclSum, r->comm, s));
+    NCCL_CHECK(nccl::api().AllReduce(tmp, tmp, static_cast<size_t>(count), ncclDouble, ncclSum, r->comm, s));
   d2h(out, tmp, static_cast<size_t>(count), s);
   r->ctx->check_numeric();
   cudaFree(tmp);
@@ -1403,6 +1403,51 @@ int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t
                                  cudaMemcpyHostToDevice, s));
     }
   }
+  API_END
+}
+
+int tgnn_set_gemm_impl(int impl) {
+  API_BEGIN
+  TGB_REQUIRE(impl == kGemmSimt || impl == kGemmTensor, kConfig, "gemm impl must be 0 or 1");
+  set_gemm_impl(impl);
+  API_END
+}
+
+int tgnn_get_gemm_impl(int* impl) {
+  API_BEGIN
+  *impl = gemm_impl();
+  API_END
+}
+
+int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, int a_trans, const float* B,
+                    int b_trans, float* C, int splits) {
+  API_BEGIN
+  TGB_REQUIRE(M > 0 && N > 0 && K > 0 && splits >= 1, kConfig, "debug_gemm: bad sizes");
+  float *dA = dalloc<float>(M * K), *dB = dalloc<float>(K * N), *dC = dalloc<float>(M * N);
+  float* ws = splits > 1 ? dalloc<float>(static_cast<size_t>(splits) * M * N) : nullptr;
+  TGB_CUDA(cudaMemcpy(dA, A, sizeof(float) * M * K, cudaMemcpyHostToDevice));
+  TGB_CUDA(cudaMemcpy(dB, B, sizeof(float) * K * N, cudaMemcpyHostToDevice));
+  GemmGroup gg;
+  GemmProblem& P = gg.p[gg.count++];
+  P.M = static_cast<int>(M);
+  P.N = static_cast<int>(N);
+  P.K = static_cast<int>(K);
+  P.a = a_trans ? A_trans(dA, M, static_cast<int>(K)) : A_rows(dA, K, static_cast<int>(K));
+  P.b = b_trans ? B_wT(dB, K, static_cast<int>(K)) : B_w(dB, N, static_cast<int>(K));
+  P.C = dC;
+  P.ldc = N;
+  P.splits = splits;
+  P.ws = ws;
+  if (impl == kGemmTensor)
+    gemm_group_launch_tc(gg, nullptr);
+  else
+    gemm_group_launch_simt(gg, nullptr);
+  TGB_CUDA(cudaDeviceSynchronize());
+  TGB_CUDA(cudaMemcpy(C, dC, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dC);
+  if (ws) cudaFree(ws);
   API_END
 }
 

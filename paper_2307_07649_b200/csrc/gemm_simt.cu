@@ -228,7 +228,32 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GroupParams gp) {
 
 }  // namespace
 
+namespace {
+int g_impl = kGemmTensor;
+}
+
+void set_gemm_impl(int impl) { g_impl = impl; }
+int gemm_impl() { return g_impl; }
+
+void splitk_reduce_launch(const GemmGroup& g, cudaStream_t s) {
+  GroupParams gp{};
+  gp.count = g.count;
+  for (int i = 0; i < g.count; ++i) gp.p[i] = g.p[i];
+  splitk_reduce_kernel<<<dim3(64, g.count), 256, 0, s>>>(gp);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void gemm_group_launch_tc(const GemmGroup& g, cudaStream_t s);
+
 void gemm_group_launch(const GemmGroup& g, cudaStream_t s) {
+  if (g_impl == kGemmTensor) {
+    gemm_group_launch_tc(g, s);
+    return;
+  }
+  gemm_group_launch_simt(g, s);
+}
+
+void gemm_group_launch_simt(const GemmGroup& g, cudaStream_t s) {
   if (g.count == 0) return;
   GroupParams gp{};
   gp.count = g.count;
@@ -245,10 +270,7 @@ void gemm_group_launch(const GemmGroup& g, cudaStream_t s) {
   if (max_tiles == 0) return;
   gemm_group_kernel<<<dim3(max_tiles, g.count), NT, 0, s>>>(gp);
   TGB_CUDA(cudaGetLastError());
-  if (any_split) {
-    splitk_reduce_kernel<<<dim3(64, g.count), 256, 0, s>>>(gp);
-    TGB_CUDA(cudaGetLastError());
-  }
+  if (any_split) splitk_reduce_launch(g, s);
 }
 
 }  // namespace tgb

@@ -72,6 +72,15 @@ inline Operand B_wT(const float* p, int64_t ldw, int K) { return op_dense(p, 1, 
 // B = W where W is row-major [K x N] (ldw).
 inline Operand B_w(const float* p, int64_t ldw, int K) { return op_dense(p, ldw, 1, K); }
 
+// Dispatch on the process-wide GEMM implementation:
+//  kGemmTensor: tcgen05 bf16x3 (gemm_tc.cu, default) -- fp32-class accuracy;
+//  kGemmSimt:   fp32 FMA on CUDA cores (gemm_simt.cu) -- exact fp32 reference path.
+enum GemmImpl { kGemmSimt = 0, kGemmTensor = 1 };
+void set_gemm_impl(int impl);
+int gemm_impl();
 void gemm_group_launch(const GemmGroup& g, cudaStream_t s);
+void gemm_group_launch_simt(const GemmGroup& g, cudaStream_t s);
+void gemm_group_launch_tc(const GemmGroup& g, cudaStream_t s);
+void splitk_reduce_launch(const GemmGroup& g, cudaStream_t s);
 
 }  // namespace tgb

@@ -543,37 +543,37 @@ __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restr
   }
 }
 
-// Column dot partials: part[c][i] = sum_{rows in chunk c} X[m, i] * Y[m, i].
-__global__ void coldot_kernel(const int32_t* rows_dev, int ncol, const float* __restrict__ X,
-                              const float* __restrict__ Y, float* __restrict__ part, int nchunks) {
-  const int rows = *rows_dev;
-  for (int64_t w = blockIdx.x; w < nchunks; w += gridDim.x) {
-    const int m0 = static_cast<int>(w) * kOmegaRows;
-    const int m1 = min(rows, m0 + kOmegaRows);
-    for (int i = threadIdx.x; i < ncol; i += blockDim.x) {
-      float s = 0.0f;
-      for (int m = m0; m < m1; ++m) s = fmaf(X[static_cast<int64_t>(m) * ncol + i], Y[static_cast<int64_t>(m) * ncol + i], s);
-      part[w * ncol + i] = s;
-    }
-  }
-}
-
-// omega gradient = pair time encodings (via Mom = dKV^T G) + GRU mail time
-// encodings (chunk partials), trainer.hpp:254-268.
-__global__ void omega_final_kernel(Dims D, const float* __restrict__ params, int64_t offWk,
-                                   int64_t offWv, const float* __restrict__ Mom,
-                                   const float* __restrict__ part, int nchunks,
-                                   float* __restrict__ g_omega) {
+// omega gradient (trainer.hpp:254-268): the pair time encodings contribute
+// sum_j W{k,v}[j, t0+i] Mom[j, i] (Mom = dKV^T G), the GRU mail encodings
+// sum_j Wall[j, 2d+i] M2[j, i] (M2 = Dg^T GU). One block per omega entry,
+// fixed-order tree reduction.
+__global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* __restrict__ params,
+                                                          int64_t offWk, int64_t offWv, int64_t offWz,
+                                                          const float* __restrict__ Mom,
+                                                          const float* __restrict__ M2,
+                                                          float* __restrict__ g_omega) {
+  __shared__ float red[256];
+  const int i = blockIdx.x;
   const int t0 = D.d + D.ds + D.de;
-  for (int i = threadIdx.x; i < D.dt; i += blockDim.x) {
-    float s = 0.0f;
-    for (int j = 0; j < D.da; ++j) {
+  const int n1 = 2 * D.da, n2 = 3 * D.d;
+  float s = 0.0f;
+  for (int j = threadIdx.x; j < n1 + n2; j += blockDim.x) {
+    if (j < D.da) {
       s = fmaf(params[offWk + static_cast<int64_t>(j) * D.kv_in + t0 + i], Mom[j * D.dt + i], s);
-      s = fmaf(params[offWv + static_cast<int64_t>(j) * D.kv_in + t0 + i], Mom[(D.da + j) * D.dt + i], s);
+    } else if (j < n1) {
+      s = fmaf(params[offWv + static_cast<int64_t>(j - D.da) * D.kv_in + t0 + i], Mom[j * D.dt + i], s);
+    } else {
+      const int jj = j - n1;
+      s = fmaf(params[offWz + static_cast<int64_t>(jj) * D.gin + 2 * D.d + i], M2[jj * D.dt + i], s);
     }
-    for (int c = 0; c < nchunks; ++c) s += part[c * D.dt + i];
-    g_omega[i] = s;
   }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) g_omega[i] = red[0];
 }
 
 // ---------------------------------------------------------------- writes
@@ -786,7 +786,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   w.dNode = dalloc<float>(U * (d + m.d_static));
   w.Dg = dalloc<float>(U * 3 * d);
   w.T1 = dalloc<float>(U * d);
-  w.DMT = dalloc<float>(U * dt);
+  w.DMT = dalloc<float>(3 * d * dt);  // M2 = Dg^T GU
   w.Mom = dalloc<float>(2 * da * dt);
   w.omega_chunks = static_cast<int>(ceil_div(U, kOmegaRows));
   w.omega_part = dalloc<float>(static_cast<size_t>(w.omega_chunks) * dt);
@@ -818,6 +818,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   acc(static_cast<int>(d), static_cast<int>(m.mail_dim()), U);
   acc(static_cast<int>(d), static_cast<int>(d), U);
   acc(1, static_cast<int>(3 * d), U);
+  acc(static_cast<int>(3 * d), static_cast<int>(dt), U);
   const int64_t nchunks = ceil_div(R + P, kChunk) + 1;
   ws += 2 * static_cast<size_t>(nchunks) * 3 * da;
   w.splitk_ws_floats = ws;
@@ -1035,13 +1036,12 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     add_tn(gg, wc, d, d, U, szU, A_trans(w.Dg + 2 * d, 3 * d, U), B_w(w.RS, d, U),
            G + L.off[tWh] + md, gin);
     add_tn(gg, wc, 1, 3 * d, U, szU, ones_op(w.ones, U), B_w(w.Dg, 3 * d, U), G + L.off[tBz], 3 * d);
-    add_nn(gg, U, szU, dt, 3 * d, A_rows(w.Dg, 3 * d, 3 * d), B_w(P + L.off[tWz] + 2 * d, gin, 3 * d),
-           w.DMT, dt);
+    add_tn(gg, wc, 3 * d, dt, U, szU, A_trans(w.Dg, 3 * d, U), B_w(w.GU, dt, U), w.DMT, dt);
     gemm_group_launch(gg, s);
   }
-  coldot_kernel<<<w.omega_chunks, 128, 0, s>>>(szU, dt, w.DMT, w.GU, w.omega_part, w.omega_chunks);
-  omega_final_kernel<<<1, 128, 0, s>>>(D, P, L.off[tWk], L.off[tWv], w.Mom, w.omega_part,
-                                       w.omega_chunks, G + L.off[tOmega]);
+  if (dt > 0)
+    omega_final_kernel<<<dt, 256, 0, s>>>(D, P, L.off[tWk], L.off[tWv], L.off[tWz], w.Mom, w.DMT,
+                                          G + L.off[tOmega]);
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -1,0 +1,55 @@
+"""Multi-GPU (one rank per trainer over NCCL): i x j x k runs against the
+reference's threaded run_training on the same stream and seeds. Needs >= 2
+GPUs (gpurun --gpus 2/4); skipped otherwise."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import ref
+from oracle import tgnn_oracle as O
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+SHAPES = [(1, 1, 2, 2), (2, 1, 1, 2), (1, 2, 1, 2), (2, 1, 2, 2), (1, 2, 2, 3), (1, 1, 4, 4)]
+
+
+@pytest.mark.parametrize("i,j,k,epochs", SHAPES)
+def test_parallel_run_matches_reference(i, j, k, epochs, tmp_path):
+    T_ = i * j * k
+    if ngpus() < T_:
+        pytest.skip(f"needs {T_} GPUs")
+    out = tmp_path / "r.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={T_}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + 7 * i + 3 * j + k),
+           os.path.join(ROOT, "tests", "mp_worker.py"), "--i", str(i), "--j", str(j), "--k", str(k),
+           "--epochs", str(epochs), "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = np.load(out)
+    assert bool(res["replicas_identical"])  # every rank holds bitwise-identical weights
+    rg = ref.RefGraph.synthetic(20, 120, d_e=2, seed=21)
+    _, _, t, _ = rg.export(feats=False)
+    mc = O.ModelConfig(d_mem=3, d_time=2, d_static=2, d_attn=3, d_hidden=2, d_e=2, n_neighbors=2,
+                       num_nodes=20, max_t=float(t[-1]))
+    tc = ref.train_cfg(i=i, j=j, k=k, local_batch=15, epochs=epochs, seed=3, lr_base=1e-3)
+    rr = rg.run(mc, tc, 0, 90, sequential=False)
+    assert int(res["barriers"]) == rr["barriers"]
+    assert np.abs(res["losses"] - rr["barrier_loss"]).max() <= 1e-3 * np.abs(rr["barrier_loss"]).max()
+    lr = 1e-3 * T_
+    assert np.abs(res["params"] - rr["params"]).max() <= 2.5 * lr * rr["barriers"]
+    assert np.median(np.abs(res["params"] - rr["params"])) <= 1e-5
