@@ -3,7 +3,7 @@
 // Same problem interface as gemm_simt.cu (GemmProblem: strided, K-segmented
 // fp32 operands, device-side row counts, split-K). Each CTA computes a
 // 128 x N_tile (N_tile <= 256) output tile:
-//   * all 4 warps gather the fp32 A / B tiles from global (coalesced along the
+//   * all 8 warps gather the fp32 A / B tiles from global (coalesced along the
 //     operand's unit-stride direction), split every value into a bf16 pair
 //     hi = bf16(x), lo = bf16(x - hi), and store them into shared memory in the
 //     canonical K-major SWIZZLE_128B layout (8-row x 128 B swizzle atoms);
@@ -12,7 +12,7 @@
 //     relative per product, i.e. fp32-class accuracy for the 1e-4 parity bound);
 //   * two shared-memory stages: the MMAs of stage s run while the warps fill
 //     stage s^1; tcgen05.commit -> mbarrier releases a stage;
-//   * epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes 32w..32w+31 = rows),
+//   * epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32(w%4).. = rows),
 //     alpha/beta/bias, or a split-K partial for the in-order reduction.
 #include <cuda_bf16.h>
 
@@ -25,7 +25,8 @@ namespace {
 constexpr int TBM = 128;         // UMMA_M (cta_group::1)
 constexpr int TBK = 64;          // k per stage = one 128 B swizzle row of bf16
 constexpr int TBN_MAX = 256;     // UMMA_N max
-constexpr int TNT = 128;         // threads per CTA
+constexpr int TNT = 128;         // epilogue threads (4 warps x 32 TMEM lanes)
+constexpr int TNT2 = 256;        // threads per CTA (all produce; warps w, w+4 share lanes)
 constexpr int kStages = 2;
 constexpr int kATile = TBM * TBK * 2;         // 16 KB per bf16 tile
 constexpr int kBTile = TBN_MAX * TBK * 2;     // 32 KB per bf16 tile
@@ -84,45 +85,77 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-// Fills one operand's [rows x 64] hi/lo tiles. `is_a` selects the accessor.
-// k_fast: the operand is contiguous along k -> each thread builds whole
-// 16-byte chunks from 8 consecutive k; else contiguous along rows -> lanes
-// take consecutive rows and loop over k.
-template <bool IS_A>
+// Fills one operand's [rows_tile x 64] hi/lo tiles. Work unit = (row, 8-k
+// chunk) -> one 16-byte swizzled store per tile. All loads of a thread's units
+// are issued before any conversion (memory-level parallelism).
+//  k_fast (unit stride along k): 8 consecutive lanes cover one row's 64 k
+//    (two 128-bit loads per unit when the operand is aligned, single-segment);
+//  row-fast (unit stride along rows): consecutive lanes take consecutive rows.
+template <bool IS_A, int MAXU>
 __device__ __forceinline__ void fill_tile(const Operand& o, int r0, int rows_valid, int rows_tile,
                                           int k0, int K, uint8_t* hi_tile, uint8_t* lo_tile) {
-  const bool k_fast = IS_A ? (o.seg[0].cs == 1) : (o.seg[0].rs == 1);
+  const Seg& s0 = o.seg[0];
+  const int64_t kstride = IS_A ? s0.cs : s0.rs;
+  const int64_t rstride = IS_A ? s0.rs : s0.cs;
+  const bool k_fast = kstride == 1;
+  const int units = rows_tile * 8;
+  float v[MAXU][8];
   if (k_fast) {
-    const int units = rows_tile * 8;
-    for (int u = threadIdx.x; u < units; u += TNT) {
-      const int r = u >> 3, c = u & 7;
-      float v[8];
-      const int kb = k0 + c * 8;
+    const bool vec = o.nseg == 1 && (rstride & 3) == 0 && ((reinterpret_cast<uintptr_t>(s0.p) & 15) == 0);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int k = kb + q;
-        v[q] = (r < rows_valid && k < K) ? (IS_A ? ld_a(o, r0 + r, k) : ld_b(o, k, r0 + r)) : 0.0f;
-      }
-      uint4 h, l;
-      split8(v, h, l);
-      const uint32_t off = sw128_off(r, c);
-      *reinterpret_cast<uint4*>(hi_tile + off) = h;
-      *reinterpret_cast<uint4*>(lo_tile + off) = l;
-    }
-  } else {
-    for (int r = threadIdx.x; r < rows_tile; r += TNT) {
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        float v[8];
-        const int kb = k0 + c * 8;
+    for (int i = 0; i < MAXU; ++i) {
+      const int u = threadIdx.x + i * TNT2;
+      const int r = u >> 3, c = u & 7;
+      const int kb = k0 + c * 8;
+      const bool rok = u < units && r < rows_valid;
+      if (vec && rok && kb + 8 <= K) {
+        const float4* src = reinterpret_cast<const float4*>(s0.p + static_cast<int64_t>(r0 + r) * rstride + kb);
+        const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
+        v[i][0] = x0.x; v[i][1] = x0.y; v[i][2] = x0.z; v[i][3] = x0.w;
+        v[i][4] = x1.x; v[i][5] = x1.y; v[i][6] = x1.z; v[i][7] = x1.w;
+      } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int k = kb + q;
-          v[q] = (r < rows_valid && k < K) ? (IS_A ? ld_a(o, r0 + r, k) : ld_b(o, k, r0 + r)) : 0.0f;
+          v[i][q] = (rok && k < K) ? (IS_A ? ld_a(o, r0 + r, k) : ld_b(o, k, r0 + r)) : 0.0f;
         }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MAXU; ++i) {
+      const int u = threadIdx.x + i * TNT2;
+      if (u < units) {
         uint4 h, l;
-        split8(v, h, l);
-        const uint32_t off = sw128_off(r, c);
+        split8(v[i], h, l);
+        const uint32_t off = sw128_off(u >> 3, u & 7);
+        *reinterpret_cast<uint4*>(hi_tile + off) = h;
+        *reinterpret_cast<uint4*>(lo_tile + off) = l;
+      }
+    }
+  } else {
+    const bool single = o.nseg == 1;
+#pragma unroll
+    for (int i = 0; i < MAXU; ++i) {
+      const int u = threadIdx.x + i * TNT2;
+      const int r = u % rows_tile, c = u / rows_tile;
+      const int kb = k0 + c * 8;
+      const bool rok = u < units && r < rows_valid;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = kb + q;
+        if (single)
+          v[i][q] = (rok && k < K) ? s0.p[static_cast<int64_t>(r0 + r) * rstride + static_cast<int64_t>(k) * kstride] : 0.0f;
+        else
+          v[i][q] = (rok && k < K) ? (IS_A ? ld_a(o, r0 + r, k) : ld_b(o, k, r0 + r)) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MAXU; ++i) {
+      const int u = threadIdx.x + i * TNT2;
+      if (u < units) {
+        uint4 h, l;
+        split8(v[i], h, l);
+        const uint32_t off = sw128_off(u % rows_tile, u / rows_tile);
         *reinterpret_cast<uint4*>(hi_tile + off) = h;
         *reinterpret_cast<uint4*>(lo_tile + off) = l;
       }
@@ -179,7 +212,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(TNT, 1) gemm_tc_kernel(const __grid_constant__ TcParams gp) {
+__global__ void __launch_bounds__(TNT2, 1) gemm_tc_kernel(const __grid_constant__ TcParams gp) {
   const int pi = blockIdx.y;
   if (pi >= gp.count) return;
   const GemmProblem& P = gp.p[pi];
@@ -235,8 +268,8 @@ __global__ void __launch_bounds__(TNT, 1) gemm_tc_kernel(const __grid_constant__
     uint8_t* b_hi = st + 2 * kATile;
     uint8_t* b_lo = st + 2 * kATile + kBTile;
     const int k0 = kbeg + kc * TBK;
-    fill_tile<true>(P.a, m0, mvalid, TBM, k0, kend, a_hi, a_lo);
-    fill_tile<false>(P.b, n0, nvalid, ntile, k0, kend, b_hi, b_lo);
+    fill_tile<true, TBM * 8 / TNT2>(P.a, m0, mvalid, TBM, k0, kend, a_hi, a_lo);
+    fill_tile<false, TBN_MAX * 8 / TNT2>(P.b, n0, nvalid, ntile, k0, kend, b_hi, b_lo);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -257,13 +290,15 @@ __global__ void __launch_bounds__(TNT, 1) gemm_tc_kernel(const __grid_constant__
   if (nk > 0) mbar_wait(bars + ((nk - 1) & 1), ((nk - 1) >> 1) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // Epilogue: warp w reads TMEM lanes [32w, 32w + 32) = tile rows.
-  const int row = warp * 32 + lane;
+  // Epilogue: warp w reads TMEM lanes [32 (w % 4), +32) = tile rows; warps w
+  // and w + 4 take alternating 16-column chunks.
+  const int quarter = warp & 3;
+  const int row = quarter * 32 + lane;
   const int m = m0 + row;
-  for (int c0 = 0; c0 < ntile; c0 += 16) {
+  for (int c0 = (warp >> 2) * 16; c0 < ntile; c0 += 32) {
     uint32_t v[16];
     if (nk > 0) {
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c0);
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c0);
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
           : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
@@ -329,7 +364,7 @@ void gemm_group_launch_tc(const GemmGroup& g, cudaStream_t s) {
     any_split |= g.p[i].splits > 1;
   }
   if (max_tiles == 0) return;
-  gemm_tc_kernel<<<dim3(max_tiles, g.count), TNT, kSmemBytes, s>>>(gp);
+  gemm_tc_kernel<<<dim3(max_tiles, g.count), TNT2, kSmemBytes, s>>>(gp);
   TGB_CUDA(cudaGetLastError());
   if (any_split) splitk_reduce_launch(g, s);
 }

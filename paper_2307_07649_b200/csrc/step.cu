@@ -695,6 +695,13 @@ T* dalloc(size_t n) {
 }
 
 int choose_splits(int M, int N, int64_t Kcap) {
+  if (gemm_impl() == kGemmTensor) {
+    // tensor tiles are 128 x 256; keep >= ~1024 reduction rows per CTA so the
+    // split-K partial traffic stays small next to the MMA work
+    const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
+    int s = static_cast<int>(std::min<int64_t>(ceil_div(Kcap, 1024), ceil_div(2 * kSMs, tiles)));
+    return std::max(1, std::min(s, 64));
+  }
   const int tiles = static_cast<int>(ceil_div(M, 64) * ceil_div(N, 64));
   int s = static_cast<int>(ceil_div(2 * kSMs, tiles));
   const int max_by_k = static_cast<int>(ceil_div(Kcap, 128));

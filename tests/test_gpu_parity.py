@@ -147,8 +147,16 @@ def _substep_case(env, cfg, mdims, begin, B, seed=0):
     return s, rg, g, mc, params, negs, plan, vm, vl
 
 
+@pytest.fixture(params=[T.GEMM_TENSOR, T.GEMM_SIMT], ids=["tcgen05", "simt"])
+def engine(request):
+    prev = T.get_gemm_impl()
+    T.set_gemm_impl(request.param)
+    yield request.param
+    T.set_gemm_impl(prev)
+
+
 @pytest.mark.parametrize("case", ["small", "wiki", "reddit"])
-def test_sub_step_parity(env, case):
+def test_sub_step_parity(env, case, engine):
     cfg, mdims, begin, B = {"small": (SMALL, SMALL_MODEL, 300, 50),
                             "wiki": (WIKI, WIKI_MODEL, 60000, 600),
                             "reddit": (REDDIT, REDDIT_MODEL, 90000, 600)}[case]
@@ -221,7 +229,7 @@ def test_adam_parity(env):
 
 # ---------------------------------------------------------------- trainer loop
 @pytest.mark.parametrize("case", ["small", "wiki"])
-def test_run_sequential_parity(env, case):
+def test_run_sequential_parity(env, case, engine):
     cfg, mdims, B, nb = {"small": (SMALL, SMALL_MODEL, 50, 12), "wiki": (WIKI, WIKI_MODEL, 600, 3)}[case]
     s, rg, g = setup(cfg, env)
     mc = model_for(s, mdims)
