@@ -199,8 +199,10 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes);
 /* ------------------------------------------------------------------ GEMM engine
  * Process-wide choice for the step's dense contractions:
  *   1 (default) tcgen05 tensor cores, bf16x3 split (hi*hi + hi*lo + lo*hi,
- *     fp32 accumulate in TMEM) -- fp32-class accuracy;
- *   0 fp32 FMA on CUDA cores -- the exact fp32 path. */
+ *     fp32 accumulate in TMEM), operands pre-split by their producers and
+ *     loaded by TMA -- fp32-class accuracy;
+ *   0 fp32 FMA on CUDA cores -- the exact fp32 path;
+ *   2 tcgen05 bf16x3 that gathers and splits fp32 operands inside the GEMM. */
 int tgnn_set_gemm_impl(int impl);
 int tgnn_get_gemm_impl(int* impl);
 /* Test hook: C[M x N] = A . B on device with the chosen engine. A is [M x K]

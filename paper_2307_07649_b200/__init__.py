@@ -464,11 +464,13 @@ def schedule_query(train: TrainConfig, train_begin: int, train_end: int, rank: i
     return nb.value, {k: out[:count, x].copy() for x, k in enumerate(SCHEDULE_FIELDS)}
 
 
-GEMM_SIMT, GEMM_TENSOR = 0, 1
+GEMM_SIMT, GEMM_TMA, GEMM_GATHER = 0, 1, 2
+GEMM_TENSOR = GEMM_TMA
 
 
 def set_gemm_impl(impl: int):
-    """0: exact fp32 CUDA-core GEMMs; 1 (default): tcgen05 bf16x3 tensor-core GEMMs."""
+    """0: exact fp32 CUDA-core GEMMs; 1 (default): TMA-fed tcgen05 bf16x3 GEMMs over
+    pre-split operands; 2: tcgen05 bf16x3 gathering fp32 operands in the GEMM."""
     check(lib().tgnn_set_gemm_impl(impl))
 
 
@@ -478,7 +480,7 @@ def get_gemm_impl() -> int:
     return v.value
 
 
-def debug_gemm(A, B, impl=GEMM_TENSOR, a_trans=False, b_trans=False, splits=1):
+def debug_gemm(A, B, impl=GEMM_TMA, a_trans=False, b_trans=False, splits=1):
     """C = op(A) op(B) on device (test hook for the GEMM engines)."""
     A = np.ascontiguousarray(A, np.float32)
     B = np.ascontiguousarray(B, np.float32)

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", CSRC, "-I", os.path.join(HERE, "..", "include")]
-SOURCES = ["plan.cu", "gemm_simt.cu", "gemm_tc.cu", "step.cu", "api.cu"]
+SOURCES = ["plan.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_tma.cu", "step.cu", "api.cu"]
 
 
 def _deps_hash(src: str) -> str:

@@ -21,6 +21,7 @@
 #include "nccl_dyn.hpp"
 #include "plan.cuh"
 #include "step.cuh"
+#include "gemm_tma.cuh"
 
 using namespace tgb;
 
@@ -1408,7 +1409,8 @@ int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t
 
 int tgnn_set_gemm_impl(int impl) {
   API_BEGIN
-  TGB_REQUIRE(impl == kGemmSimt || impl == kGemmTensor, kConfig, "gemm impl must be 0 or 1");
+  TGB_REQUIRE(impl == kGemmSimt || impl == kGemmTma || impl == kGemmGather, kConfig,
+              "gemm impl must be 0 (fp32 SIMT), 1 (TMA tcgen05) or 2 (gather tcgen05)");
   set_gemm_impl(impl);
   API_END
 }
@@ -1438,10 +1440,34 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
   P.ldc = N;
   P.splits = splits;
   P.ws = ws;
-  if (impl == kGemmTensor)
+  if (impl == kGemmTma) {
+    // TMA engine over bf16 hi/lo operands (the step's production path)
+    const int64_t ar = a_trans ? K : M, ac = a_trans ? M : K;
+    const int64_t br = b_trans ? N : K, bc = b_trans ? K : N;
+    BfMat ba = bf_alloc(ar, ac), bb = bf_alloc(br, bc);
+    bf_from_f32(ba, dA, ar, ac, ac, nullptr);
+    bf_from_f32(bb, dB, br, bc, bc, nullptr);
+    TcGroup tg;
+    TcProblem& T = tg.p[tg.count++];
+    T.M = static_cast<int>(M);
+    T.N = static_cast<int>(N);
+    T.K = static_cast<int>(K);
+    T.ntile = tc_ntile(static_cast<int>(N));
+    T.a = tma_view(ba, 0, ac, ar, !a_trans, 128);
+    T.b = tma_view(bb, 0, bc, br, b_trans, T.ntile);
+    T.C = dC;
+    T.ldc = N;
+    T.splits = splits;
+    T.ws = ws;
+    tc_group_launch(tg, nullptr);
+    TGB_CUDA(cudaDeviceSynchronize());
+    bf_free(ba);
+    bf_free(bb);
+  } else if (impl == kGemmGather) {
     gemm_group_launch_tc(gg, nullptr);
-  else
+  } else {
     gemm_group_launch_simt(gg, nullptr);
+  }
   TGB_CUDA(cudaDeviceSynchronize());
   TGB_CUDA(cudaMemcpy(C, dC, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
   cudaFree(dA);

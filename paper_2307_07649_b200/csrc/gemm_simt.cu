@@ -229,7 +229,7 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GroupParams gp) {
 }  // namespace
 
 namespace {
-int g_impl = kGemmTensor;
+int g_impl = kGemmTma;
 }
 
 void set_gemm_impl(int impl) { g_impl = impl; }
@@ -246,7 +246,7 @@ void splitk_reduce_launch(const GemmGroup& g, cudaStream_t s) {
 void gemm_group_launch_tc(const GemmGroup& g, cudaStream_t s);
 
 void gemm_group_launch(const GemmGroup& g, cudaStream_t s) {
-  if (g_impl == kGemmTensor) {
+  if (g_impl == kGemmGather) {
     gemm_group_launch_tc(g, s);
     return;
   }

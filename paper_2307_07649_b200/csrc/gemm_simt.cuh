@@ -72,10 +72,14 @@ inline Operand B_wT(const float* p, int64_t ldw, int K) { return op_dense(p, 1, 
 // B = W where W is row-major [K x N] (ldw).
 inline Operand B_w(const float* p, int64_t ldw, int K) { return op_dense(p, ldw, 1, K); }
 
-// Dispatch on the process-wide GEMM implementation:
-//  kGemmTensor: tcgen05 bf16x3 (gemm_tc.cu, default) -- fp32-class accuracy;
-//  kGemmSimt:   fp32 FMA on CUDA cores (gemm_simt.cu) -- exact fp32 reference path.
-enum GemmImpl { kGemmSimt = 0, kGemmTensor = 1 };
+// Process-wide GEMM engine for the training step:
+//  kGemmTma (default): tcgen05 bf16x3 fed by TMA from pre-split bf16 operands
+//                      (gemm_tma.cu) -- fp32-class accuracy;
+//  kGemmSimt:          fp32 FMA on CUDA cores (gemm_simt.cu) -- exact fp32 path;
+//  kGemmGather:        tcgen05 bf16x3 that gathers + splits fp32 operands inside
+//                      the GEMM (gemm_tc.cu) -- no pre-split operands needed.
+enum GemmImpl { kGemmSimt = 0, kGemmTma = 1, kGemmGather = 2 };
+constexpr int kGemmTensor = kGemmGather;  // debug-hook name of the gather engine
 void set_gemm_impl(int impl);
 int gemm_impl();
 void gemm_group_launch(const GemmGroup& g, cudaStream_t s);

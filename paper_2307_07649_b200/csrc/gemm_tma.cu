@@ -1,0 +1,402 @@
+// TMA-fed, warp-specialized tcgen05 GEMM (see gemm_tma.cuh).
+//
+// CTA = 6 warps: warp 0 issues TMA loads (one elected lane), warp 1 owns the
+// TMEM allocation and issues tcgen05.mma (one elected lane), warps 2-5 run the
+// epilogue (warp w reads TMEM lanes 32 (w % 4) .. +32). Two shared-memory
+// stages of {A_hi, A_lo, B_hi, B_lo} (128 B swizzled, K-major or MN-major per
+// operand) form a full/empty mbarrier ring; a final commit releases the
+// accumulator to the epilogue.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+
+#include "gemm_tma.cuh"
+
+namespace tgb {
+
+namespace {
+
+constexpr int kBM = 128, kBK = 64, kThreads = 192, kSt = 2;
+constexpr int kATileB = kBM * kBK * 2;   // 16 KB (one of hi / lo)
+constexpr int kBTileB = 256 * kBK * 2;   // 32 KB
+constexpr int kStageB = 2 * kATileB + 2 * kBTileB;
+constexpr int kSmem = kSt * kStageB + 1024 + 256;
+
+struct TcParams {
+  TcProblem p[kMaxTc];
+  int tiles_m[kMaxTc], tiles_n[kMaxTc];
+  int count;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra W_%=;\n\t}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100).
+//  K-major : LBO 16 B (unused), SBO 1024 B (8-row group stride);
+//  MN-major: LBO 8192 B (64-element MN block stride = one 64 x 64 TMA box),
+//            SBO 1024 B (8-k-row group stride).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, bool kmajor) {
+  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>(kmajor ? 1 : (8192 >> 4)) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ uint32_t idesc(int n, bool a_k, bool b_k) {
+  uint32_t d = (1u << 4) | (1u << 7) | (1u << 10);
+  d |= (a_k ? 0u : 1u) << 15;
+  d |= (b_k ? 0u : 1u) << 16;
+  d |= static_cast<uint32_t>(n >> 3) << 17;
+  d |= static_cast<uint32_t>(kBM >> 4) << 24;
+  return d;
+}
+
+__device__ __forceinline__ void umma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcParams gp) {
+  const int pi = blockIdx.y;
+  if (pi >= gp.count) return;
+  const TcProblem& P = gp.p[pi];
+  const int tm = gp.tiles_m[pi], tn = gp.tiles_n[pi];
+  const int tile = blockIdx.x;
+  if (tile >= tm * tn * P.splits) return;
+  const int split = tile / (tm * tn);
+  const int t2 = tile % (tm * tn);
+  const int m0 = (t2 / tn) * kBM;
+  const int n0 = (t2 % tn) * 256;
+  const int M = P.M_dev ? min(P.M, *P.M_dev) : P.M;
+  if (m0 >= M && P.splits == 1) return;
+  const int N = P.N;
+  const int Kcap = P.K;
+  const int K = P.K_dev ? min(Kcap, *P.K_dev) : Kcap;
+  const int kper = ((Kcap + P.splits - 1) / P.splits + kBK - 1) / kBK * kBK;
+  const int kbeg = split * kper;
+  const int kend = min(K, kbeg + kper);
+  const int nk = (kend > kbeg && m0 < M) ? (kend - kbeg + kBK - 1) / kBK : 0;
+  const int ntile = P.ntile;
+  const bool a_k = P.a.kmajor != 0, b_k = P.b.kmajor != 0;
+  const int a_boxes = a_k ? 1 : 2;
+  const int b_boxes = b_k ? 1 : (ntile + 63) / 64;
+  const uint32_t a_bytes = a_k ? static_cast<uint32_t>(P.a.box_rows) * 128u : 8192u * 2u;
+  const uint32_t b_bytes = b_k ? static_cast<uint32_t>(P.b.box_rows) * 128u : 8192u * static_cast<uint32_t>(b_boxes);
+  const uint32_t stage_tx = 2u * (a_bytes + b_bytes);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageB);
+  uint64_t* empty = full + kSt;
+  uint64_t* accf = empty + kSt;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accf + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSt; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % kSt;
+        if (kc >= kSt) mbar_wait(empty + s, ((kc / kSt) - 1) & 1);
+        uint8_t* st = smem + s * kStageB;
+        mbar_expect_tx(full + s, stage_tx);
+        const int k0 = kbeg + kc * kBK;
+        for (int h = 0; h < 2; ++h) {
+          const CUtensorMap* am = h ? &P.a.lo : &P.a.hi;
+          const CUtensorMap* bm = h ? &P.b.lo : &P.b.hi;
+          uint8_t* ad = st + h * kATileB;
+          uint8_t* bd = st + 2 * kATileB + h * kBTileB;
+          if (a_k) {
+            tma_2d(ad, am, k0, m0, full + s);
+          } else {
+            for (int j = 0; j < a_boxes; ++j) tma_2d(ad + j * 8192, am, m0 + 64 * j, k0, full + s);
+          }
+          if (b_k) {
+            tma_2d(bd, bm, k0, n0, full + s);
+          } else {
+            for (int j = 0; j < b_boxes; ++j) tma_2d(bd + j * 8192, bm, n0 + 64 * j, k0, full + s);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id = idesc(ntile, a_k, b_k);
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % kSt;
+        mbar_wait(full + s, (kc / kSt) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint8_t* st = smem + s * kStageB;
+        const uint32_t ahi = su32(st), alo = su32(st + kATileB);
+        const uint32_t bhi = su32(st + 2 * kATileB), blo = su32(st + 2 * kATileB + kBTileB);
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks) {
+          const uint32_t aoff = a_k ? ks * 32u : ks * 2048u;
+          const uint32_t boff = b_k ? ks * 32u : ks * 2048u;
+          const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+          umma(tmem, sdesc(ahi + aoff, a_k), sdesc(bhi + boff, b_k), id, acc);
+          umma(tmem, sdesc(ahi + aoff, a_k), sdesc(blo + boff, b_k), id, 1u);
+          umma(tmem, sdesc(alo + aoff, a_k), sdesc(bhi + boff, b_k), id, 1u);
+        }
+        umma_commit(empty + s);
+      }
+      if (nk > 0)
+        umma_commit(accf);
+      else
+        mbar_arrive(accf);
+    }
+  } else {
+    // epilogue warps 2..5
+    mbar_wait(accf, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int m = m0 + row;
+    const int nvalid = min(256, N - n0);
+    for (int c0 = 0; c0 < ntile; c0 += 16) {
+      uint32_t v[16];
+      if (nk > 0) {
+        const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15])
+            : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = 0u;
+      }
+      if (P.splits > 1) {
+        if (m < P.M) {
+          float* w = P.ws + static_cast<int64_t>(split) * P.M * N + static_cast<int64_t>(m) * N;
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c0 + q < nvalid) w[n0 + c0 + q] = m < M ? __uint_as_float(v[q]) : 0.0f;
+        }
+      } else if (m < M) {
+        float* crow = P.C + static_cast<int64_t>(m) * P.ldc;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int n = n0 + c0 + q;
+          if (c0 + q >= nvalid) continue;
+          const float x = P.alpha * __uint_as_float(v[q]);
+          if (P.C2 && n == N - 1) {
+            P.C2[m] = P.beta != 0.0f ? x + P.beta * P.C2[m] : x;
+          } else {
+            crow[n] = P.beta != 0.0f ? x + P.beta * crow[n] : x;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+__global__ void tc_splitk_reduce_kernel(const __grid_constant__ TcParams gp) {
+  const TcProblem& P = gp.p[blockIdx.y];
+  if (P.splits <= 1) return;
+  const int64_t total = static_cast<int64_t>(P.M) * P.N;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = 0.0f;
+    for (int sp = 0; sp < P.splits; ++sp) s += P.ws[sp * total + x];
+    const int64_t m = x / P.N, n = x % P.N;
+    const float v = P.alpha * s;
+    if (P.C2 && n == P.N - 1) {
+      P.C2[m] = P.beta != 0.0f ? v + P.beta * P.C2[m] : v;
+    } else {
+      float* c = P.C + m * P.ldc + n;
+      *c = P.beta != 0.0f ? v + P.beta * *c : v;
+    }
+  }
+}
+
+__global__ void bf_from_f32_kernel(BfMat m, const float* __restrict__ src, int64_t rows, int64_t cols,
+                                   int64_t ld_src) {
+  const int64_t total = rows * cols;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bf_put(m, x / cols, x % cols, src[(x / cols) * ld_src + x % cols]);
+}
+
+// ---------------------------------------------------------------- host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw Error(kCuda, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap encode(void* base, int64_t inner, int64_t outer, int64_t ld_bytes, int box_inner, int box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_bytes)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+using MapKey = std::tuple<const void*, const void*, int64_t, int64_t, int64_t, int, int>;
+
+struct KeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(std::get<0>(k)) ^ (std::hash<const void*>()(std::get<1>(k)) << 1);
+    h ^= std::hash<int64_t>()(std::get<2>(k)) * 0x9e3779b97f4a7c15ull;
+    h ^= std::hash<int64_t>()(std::get<3>(k)) * 0xbf58476d1ce4e5b9ull;
+    h ^= std::hash<int64_t>()(std::get<4>(k)) * 0x94d049bb133111ebull;
+    h ^= static_cast<size_t>(std::get<5>(k) * 131 + std::get<6>(k));
+    return h;
+  }
+};
+
+}  // namespace
+
+BfMat bf_alloc(int64_t rows, int64_t cols) {
+  BfMat m;
+  m.rows = rows;
+  m.ld = (cols + 7) / 8 * 8;
+  const size_t bytes = static_cast<size_t>(std::max<int64_t>(rows, 1)) * m.ld * sizeof(__nv_bfloat16);
+  TGB_CUDA(cudaMalloc(&m.hi, bytes));
+  TGB_CUDA(cudaMalloc(&m.lo, bytes));
+  TGB_CUDA(cudaMemset(m.hi, 0, bytes));
+  TGB_CUDA(cudaMemset(m.lo, 0, bytes));
+  return m;
+}
+
+void bf_from_f32(const BfMat& m, const float* src, int64_t rows, int64_t cols, int64_t ld_src, cudaStream_t s) {
+  if (rows * cols == 0) return;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(rows * cols, 256), 4 * kSMs));
+  bf_from_f32_kernel<<<blocks, 256, 0, s>>>(m, src, rows, cols, ld_src);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void bf_free(BfMat& m) {
+  if (m.hi) cudaFree(m.hi);
+  if (m.lo) cudaFree(m.lo);
+  m = BfMat{};
+}
+
+TmaOp tma_view(const BfMat& m, int64_t col0, int64_t cols, int64_t rows, bool kmajor, int box_rows) {
+  TGB_REQUIRE(col0 % 8 == 0, kConfig, "tma_view: column offset must be a multiple of 8");
+  TGB_REQUIRE(col0 + cols <= m.ld && rows <= m.rows && cols > 0 && rows > 0, kConfig, "tma_view: out of range");
+  static std::mutex mu;
+  static std::unordered_map<MapKey, TmaOp, KeyHash> cache;
+  const int box_outer = kmajor ? box_rows : 64;
+  const MapKey key = std::make_tuple(static_cast<const void*>(m.hi + col0), static_cast<const void*>(m.lo + col0),
+                                     cols, rows, m.ld, box_outer, kmajor ? 1 : 0);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  TmaOp op;
+  op.kmajor = kmajor ? 1 : 0;
+  op.box_rows = box_outer;
+  op.hi = encode(m.hi + col0, cols, rows, m.ld * 2, 64, box_outer);
+  op.lo = encode(m.lo + col0, cols, rows, m.ld * 2, 64, box_outer);
+  cache.emplace(key, op);
+  return op;
+}
+
+void tc_group_launch(const TcGroup& g, cudaStream_t s) {
+  if (g.count == 0) return;
+  static bool attr = false;
+  if (!attr) {
+    TGB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  TcParams gp;
+  std::memset(&gp, 0, sizeof(gp));
+  gp.count = g.count;
+  int max_tiles = 0;
+  bool any_split = false;
+  for (int i = 0; i < g.count; ++i) {
+    gp.p[i] = g.p[i];
+    gp.tiles_m[i] = static_cast<int>(ceil_div(g.p[i].M, kBM));
+    gp.tiles_n[i] = static_cast<int>(ceil_div(g.p[i].N, 256));
+    const int t = gp.tiles_m[i] * gp.tiles_n[i] * g.p[i].splits;
+    max_tiles = std::max(max_tiles, t);
+    any_split |= g.p[i].splits > 1;
+  }
+  if (max_tiles == 0) return;
+  tc_gemm_kernel<<<dim3(max_tiles, g.count), kThreads, kSmem, s>>>(gp);
+  TGB_CUDA(cudaGetLastError());
+  if (any_split) {
+    tc_splitk_reduce_kernel<<<dim3(64, g.count), 256, 0, s>>>(gp);
+    TGB_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace tgb

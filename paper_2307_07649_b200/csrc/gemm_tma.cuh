@@ -1,0 +1,76 @@
+// TMA-fed, warp-specialized tcgen05 GEMM over pre-split bf16 operands.
+//
+// Producers of GEMM operands (assemble / activation / backward kernels and the
+// per-step weight pack) write every fp32 value x as a bf16 pair
+// (hi = bf16(x), lo = bf16(x - hi)) into a BfMat. A GEMM operand is a view of a
+// BfMat (column block [col0, col0 + cols) x capacity rows) described by TMA
+// tensor maps with EXACT logical dims, so TMA zero-fills every K / N pad; rows
+// past a runtime count are zeroed by the producers up to the next multiple of
+// 64 (the K-chunk), so split-K reductions never read stale rows.
+// The kernel computes D = A_hi B_hi + A_hi B_lo + A_lo B_hi (fp32 in TMEM).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace tgb {
+
+struct BfMat {
+  __nv_bfloat16* hi = nullptr;
+  __nv_bfloat16* lo = nullptr;
+  int64_t rows = 0;  // capacity rows
+  int64_t ld = 0;    // elements per row (multiple of 8)
+  bool valid() const { return hi != nullptr; }
+};
+
+BfMat bf_alloc(int64_t rows, int64_t cols);
+void bf_free(BfMat& m);
+// Splits a row-major fp32 matrix into an existing BfMat (rows x cols).
+void bf_from_f32(const BfMat& m, const float* src, int64_t rows, int64_t cols, int64_t ld_src, cudaStream_t s);
+
+// Device-side writer (kernels receive BfMat by value; hi == nullptr => skip).
+__device__ __forceinline__ void bf_put(const BfMat& m, int64_t r, int64_t c, float v) {
+  if (m.hi == nullptr) return;
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  m.hi[r * m.ld + c] = h;
+  m.lo[r * m.ld + c] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
+
+struct TmaOp {
+  CUtensorMap hi;
+  CUtensorMap lo;
+  int kmajor = 1;  // 1: contiguous along K (rows = M or N), 0: contiguous along M/N (rows = K)
+  int box_rows = 0;
+};
+
+struct TcProblem {
+  TmaOp a, b;
+  int M = 0, N = 0, K = 0;     // capacities; N includes a bias column when C2 is set
+  const int* M_dev = nullptr;  // runtime M (A K-major rows)
+  const int* K_dev = nullptr;  // runtime K (MN-major reductions over rows)
+  float* C = nullptr;
+  int64_t ldc = 0;
+  float* C2 = nullptr;         // when set, output column N-1 goes to C2[m]
+  float alpha = 1.0f, beta = 0.0f;
+  int splits = 1;
+  float* ws = nullptr;         // split-K partials [splits][M][N]
+  int ntile = 0;               // UMMA N per tile (multiple of 16, <= 256)
+};
+
+constexpr int kMaxTc = 8;
+struct TcGroup {
+  TcProblem p[kMaxTc];
+  int count = 0;
+};
+
+// Operand views. A K-major: matrix [M rows x K cols]; MN-major: stored
+// [K rows x M cols]. B K-major: stored [N rows x K cols]; MN-major: [K x N].
+// (col0 % 8 == 0 so the view base is 16-byte aligned.)
+TmaOp tma_view(const BfMat& m, int64_t col0, int64_t cols, int64_t rows, bool kmajor, int box_rows);
+inline int tc_ntile(int N) { return static_cast<int>(std::min<int64_t>(256, (N + 15) / 16 * 16)); }
+
+void tc_group_launch(const TcGroup& g, cudaStream_t s);
+
+}  // namespace tgb

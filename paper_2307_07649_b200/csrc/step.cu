@@ -65,6 +65,20 @@ __device__ __forceinline__ void flag_if_nonfinite(float v, int* flag) {
   if (!isfinite(v)) atomicExch(flag, 1);
 }
 
+// Zeroes rows [count, min(cap, roundup64(count))) of a pre-split operand so a
+// 64-row K-chunk of a reduction over rows never reads stale values.
+__device__ __forceinline__ void bf_zero_tail(const BfMat& m, int count, int cap, int cols) {
+  if (m.hi == nullptr) return;
+  const int end = min(cap, (count + 63) / 64 * 64);
+  const int64_t total = static_cast<int64_t>(end - count) * cols;
+  for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < total;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = count + x / cols, c = x % cols;
+    m.hi[r * m.ld + c] = __float2bfloat16_rn(0.0f);
+    m.lo[r * m.ld + c] = __float2bfloat16_rn(0.0f);
+  }
+}
+
 struct Dims {  // flattened for kernels
   int d, dt, ds, de, de_pad, da, dh, md, gin, q_in, kv_in;
 };
@@ -89,7 +103,8 @@ Dims make_dims(const ModelDims& m, const DGraph& g) {
 // GRU input rows {mail_mem | cos(dt w) | e(mail event) | s} (make_mail,
 // model.hpp:153-166) and GU = -dt sin(dt w) (time_encode_backward factor).
 __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const float* __restrict__ omega,
-                                    float* __restrict__ Xg, int64_t ldx, float* __restrict__ GU) {
+                                    float* __restrict__ Xg, int64_t ldx, float* __restrict__ GU, StepBf bf,
+                                    int cap_U) {
   const int U = pl.sizes[kSzU];
   const int lane = threadIdx.x & 31;
   for (int64_t u = gwarp(); u < U; u += nwarp()) {
@@ -97,21 +112,40 @@ __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const 
     const bool has = ev >= 0;
     const double dt = vw.mail_dt[u];
     float* row = Xg + u * ldx;
-    for (int x = lane; x < 2 * D.d; x += 32) row[x] = vw.mail_mem[u * 2 * D.d + x];
+    for (int x = lane; x < 2 * D.d; x += 32) {
+      const float v = vw.mail_mem[u * 2 * D.d + x];
+      row[x] = v;
+      bf_put(bf.Xg, u, x, v);
+    }
     for (int i = lane; i < D.dt; i += 32) {
       const double arg = dt * static_cast<double>(omega[i]);
-      row[2 * D.d + i] = static_cast<float>(cos(arg));
-      GU[u * D.dt + i] = has ? static_cast<float>(-dt * sin(arg)) : 0.0f;
+      const float c = static_cast<float>(cos(arg));
+      const float gu = has ? static_cast<float>(-dt * sin(arg)) : 0.0f;
+      row[2 * D.d + i] = c;
+      GU[u * D.dt + i] = gu;
+      bf_put(bf.Xg, u, 2 * D.d + i, c);
+      bf_put(bf.GU, u, i, gu);
     }
     const float* ef = has ? g.efeat + static_cast<int64_t>(ev) * D.de_pad : nullptr;
-    for (int x = lane; x < D.de; x += 32) row[2 * D.d + D.dt + x] = has ? ef[x] : 0.0f;
-    for (int x = lane; x < D.d; x += 32) row[D.md + x] = vw.mem[u * D.d + x];
+    for (int x = lane; x < D.de; x += 32) {
+      const float v = has ? ef[x] : 0.0f;
+      row[2 * D.d + D.dt + x] = v;
+      bf_put(bf.Xg, u, 2 * D.d + D.dt + x, v);
+    }
+    for (int x = lane; x < D.d; x += 32) {
+      const float v = vw.mem[u * D.d + x];
+      row[D.md + x] = v;
+      bf_put(bf.Xg, u, D.md + x, v);
+    }
+    if (lane == 0) bf_put(bf.Xg, u, D.gin, 1.0f);
   }
+  bf_zero_tail(bf.Xg, U, cap_U, D.gin + 1);
+  bf_zero_tail(bf.GU, U, cap_U, D.dt);
 }
 
 // z, r = sigmoid(gates + b) (bias already added by the GEMM); RS = r * s.
 __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
-                               float* __restrict__ RS) {
+                               float* __restrict__ RS, StepBf bf, int cap_U) {
   const int U = pl.sizes[kSzU];
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
@@ -121,8 +155,12 @@ __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
     const float r = sigmoidf_(gr[D.d + i]);
     gr[i] = z;
     gr[D.d + i] = r;
-    RS[x] = r * vw.mem[x];
+    const float rs = r * vw.mem[x];
+    RS[x] = rs;
+    bf_put(bf.RS, u, i, rs);
+    if (i == 0) bf_put(bf.RS, u, D.d, 1.0f);
   }
+  bf_zero_tail(bf.RS, U, cap_U, D.d + 1);
 }
 
 // h = tanh(.), s_hat = (1 - z) s + z h for rows with a mail, else s
@@ -153,7 +191,7 @@ __global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
 __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __restrict__ omega,
                                      const float* __restrict__ stat, const float* __restrict__ s_hat,
                                      float* __restrict__ Qin, int64_t ldq, float* __restrict__ KVin,
-                                     int64_t ldkv, float* __restrict__ Gt) {
+                                     int64_t ldkv, float* __restrict__ Gt, StepBf bf, int cap_R, int cap_P) {
   const int R = pl.sizes[kSzR], P = pl.sizes[kSzP];
   const int lane = threadIdx.x & 31;
   for (int64_t w = gwarp(); w < R + P; w += nwarp()) {
@@ -161,9 +199,20 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
       const int64_t su = pl.root_sup[w];
       const int64_t node = pl.root_node[w];
       float* row = Qin + w * ldq;
-      for (int x = lane; x < D.d; x += 32) row[x] = s_hat[su * D.d + x];
-      for (int x = lane; x < D.ds; x += 32) row[D.d + x] = stat[node * D.ds + x];
-      for (int x = lane; x < D.dt; x += 32) row[D.d + D.ds + x] = 1.0f;
+      for (int x = lane; x < D.d; x += 32) {
+        const float v = s_hat[su * D.d + x];
+        row[x] = v;
+        bf_put(bf.Qin, w, x, v);
+      }
+      for (int x = lane; x < D.ds; x += 32) {
+        const float v = stat[node * D.ds + x];
+        row[D.d + x] = v;
+        bf_put(bf.Qin, w, D.d + x, v);
+      }
+      for (int x = lane; x <= D.dt; x += 32) {
+        if (x < D.dt) row[D.d + D.ds + x] = 1.0f;
+        bf_put(bf.Qin, w, D.d + D.ds + x, 1.0f);  // x == dt: bias column
+      }
     } else {
       const int64_t p = w - R;
       const int64_t su = pl.pair_sup[p];
@@ -171,17 +220,37 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
       const int64_t ev = pl.pair_event[p];
       const double dt = pl.pair_dt[p];
       float* row = KVin + p * ldkv;
-      for (int x = lane; x < D.d; x += 32) row[x] = s_hat[su * D.d + x];
-      for (int x = lane; x < D.ds; x += 32) row[D.d + x] = stat[node * D.ds + x];
+      for (int x = lane; x < D.d; x += 32) {
+        const float v = s_hat[su * D.d + x];
+        row[x] = v;
+        bf_put(bf.KVin, p, x, v);
+      }
+      for (int x = lane; x < D.ds; x += 32) {
+        const float v = stat[node * D.ds + x];
+        row[D.d + x] = v;
+        bf_put(bf.KVin, p, D.d + x, v);
+      }
       const float* ef = g.efeat + ev * D.de_pad;
-      for (int x = lane; x < D.de; x += 32) row[D.d + D.ds + x] = ef[x];
+      for (int x = lane; x < D.de; x += 32) {
+        const float v = ef[x];
+        row[D.d + D.ds + x] = v;
+        bf_put(bf.KVin, p, D.d + D.ds + x, v);
+      }
       for (int i = lane; i < D.dt; i += 32) {
         const double arg = dt * static_cast<double>(omega[i]);
-        row[D.d + D.ds + D.de + i] = static_cast<float>(cos(arg));
-        Gt[p * D.dt + i] = static_cast<float>(-dt * sin(arg));
+        const float c = static_cast<float>(cos(arg));
+        const float gt = static_cast<float>(-dt * sin(arg));
+        row[D.d + D.ds + D.de + i] = c;
+        Gt[p * D.dt + i] = gt;
+        bf_put(bf.KVin, p, D.d + D.ds + D.de + i, c);
+        bf_put(bf.Gt, p, i, gt);
       }
+      if (lane == 0) bf_put(bf.KVin, p, D.kv_in, 1.0f);
     }
   }
+  bf_zero_tail(bf.Qin, R, cap_R, D.q_in + 1);
+  bf_zero_tail(bf.KVin, P, cap_P, D.kv_in + 1);
+  bf_zero_tail(bf.Gt, P, cap_P, D.dt);
 }
 
 constexpr int kMaxDaLanes = 8;  // d_attn <= 256
@@ -190,7 +259,7 @@ constexpr int kMaxDaLanes = 8;  // d_attn <= 256
 // softmax, h = sum a V; n = 0 gives h = 0. One warp per root.
 __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
                                 const float* __restrict__ KV, float* __restrict__ attn_a,
-                                float* __restrict__ H, int* flag) {
+                                float* __restrict__ H, int* flag, StepBf bf) {
   const int R = pl.sizes[kSzR];
   const int lane = threadIdx.x & 31;
   const int da = D.da;
@@ -198,7 +267,10 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
     const int n = pl.nbr_cnt[r];
     float* h = H + r * da;
     if (n == 0) {
-      for (int i = lane; i < da; i += 32) h[i] = 0.0f;
+      for (int i = lane; i < da; i += 32) {
+        h[i] = 0.0f;
+        bf_put(bf.H, r, i, 0.0f);
+      }
       continue;
     }
     const int p0 = pl.pair_ptr[r];
@@ -243,6 +315,7 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
       const int i = lane + 32 * c;
       if (i < da) {
         h[i] = hv[c];
+        bf_put(bf.H, r, i, hv[c]);
         flag_if_nonfinite(hv[c], flag);
       }
     }
@@ -262,7 +335,7 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
                                float* __restrict__ HID, float* __restrict__ Dhid,
                                float* __restrict__ Hin, float* __restrict__ dlogit,
                                float* __restrict__ logits, double* __restrict__ loss_terms,
-                               int* flag) {
+                               int* flag, StepBf bf, int cap_B2) {
   const int B = pl.sizes[kSzB];
   const int lane = threadIdx.x & 31;
   const int dh = D.dh, da = D.da;
@@ -287,8 +360,12 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
     for (int j = lane; j < dh; j += 32) {
       const float hp = HID[e * dh + j];
       const float hn = HID[(B + e) * dh + j];
-      Dhid[e * dh + j] = hp > 0.0f ? dpos * W2[j] : 0.0f;
-      Dhid[(B + e) * dh + j] = hn > 0.0f ? dneg * W2[j] : 0.0f;
+      const float gp = hp > 0.0f ? dpos * W2[j] : 0.0f;
+      const float gn = hn > 0.0f ? dneg * W2[j] : 0.0f;
+      Dhid[e * dh + j] = gp;
+      Dhid[(B + e) * dh + j] = gn;
+      bf_put(bf.Dhid, e, j, gp);
+      bf_put(bf.Dhid, B + e, j, gn);
     }
     const float* hs = H + (3 * e) * da;
     const float* hd = H + (3 * e + 1) * da;
@@ -298,6 +375,14 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
       Hin[e * 2 * da + da + i] = hd[i];
       Hin[(B + e) * 2 * da + i] = hs[i];
       Hin[(B + e) * 2 * da + da + i] = hn[i];
+      bf_put(bf.Hin, e, i, hs[i]);
+      bf_put(bf.Hin, e, da + i, hd[i]);
+      bf_put(bf.Hin, B + e, i, hs[i]);
+      bf_put(bf.Hin, B + e, da + i, hn[i]);
+    }
+    if (lane == 0) {
+      bf_put(bf.Hin, e, 2 * da, 1.0f);
+      bf_put(bf.Hin, B + e, 2 * da, 1.0f);
     }
     if (lane == 0) {
       dlogit[e] = dpos;
@@ -310,6 +395,8 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
       flag_if_nonfinite(neg, flag);
     }
   }
+  bf_zero_tail(bf.Dhid, 2 * B, cap_B2, dh);
+  bf_zero_tail(bf.Hin, 2 * B, cap_B2, 2 * da + 1);
 }
 
 // bce_loss: mean softplus(-pos) + mean softplus(neg), fixed-order f64 reduction.
@@ -344,7 +431,7 @@ __global__ void __launch_bounds__(1024) loss_kernel(DPlan pl, const double* __re
 __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
                                 const float* __restrict__ Q, const float* __restrict__ KV,
                                 const float* __restrict__ attn_a, float* __restrict__ dQ,
-                                float* __restrict__ dKV) {
+                                float* __restrict__ dKV, StepBf bf, int cap_R, int cap_P) {
   const int R = pl.sizes[kSzR];
   const int B = pl.sizes[kSzB];
   const int lane = threadIdx.x & 31;
@@ -366,7 +453,10 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
     }
     const int n = pl.nbr_cnt[r];
     if (n == 0) {
-      for (int i = lane; i < da; i += 32) dQ[r * da + i] = 0.0f;
+      for (int i = lane; i < da; i += 32) {
+        dQ[r * da + i] = 0.0f;
+        bf_put(bf.dQ, r, i, 0.0f);
+      }
       continue;
     }
     const int p0 = pl.pair_ptr[r];
@@ -404,17 +494,25 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
         const int i = lane + 32 * c;
         if (i < da) {
           dq[c] = fmaf(gm, K[i], dq[c]);
-          out[i] = gm * q[c];
-          out[da + i] = am * dh[c];
+          const float dk = gm * q[c], dv = am * dh[c];
+          out[i] = dk;
+          out[da + i] = dv;
+          bf_put(bf.dKV, p, i, dk);
+          bf_put(bf.dKV, p, bf.d8a + i, dv);
         }
       }
     }
 #pragma unroll
     for (int c = 0; c < kMaxDaLanes; ++c) {
       const int i = lane + 32 * c;
-      if (i < da) dQ[r * da + i] = dq[c];
+      if (i < da) {
+        dQ[r * da + i] = dq[c];
+        bf_put(bf.dQ, r, i, dq[c]);
+      }
     }
   }
+  bf_zero_tail(bf.dQ, R, cap_R, da);
+  bf_zero_tail(bf.dKV, pl.sizes[kSzP], cap_P, bf.d8a + da);
 }
 
 // Routing pass 1: fixed chunks of kChunk sorted items; runs fully inside a
@@ -422,7 +520,8 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
 // Row layout of dNodeAcc: {sum dq | sum dK | sum dV} (3 d_attn).
 __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__ dQ,
                                      const float* __restrict__ dKV, float* __restrict__ dNodeAcc,
-                                     float* __restrict__ part_first, float* __restrict__ part_last) {
+                                     float* __restrict__ part_first, float* __restrict__ part_last,
+                                     StepBf bf) {
   const int items = pl.sizes[kSzItems];
   const int R = pl.sizes[kSzR];
   const int nchunks = (items + kChunk - 1) / kChunk;
@@ -462,6 +561,7 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
         float* dst;
         const bool first = run_start == i0 && cont_in;
         const bool last = (i + 1 == i1) && cont_out;
+        const bool direct = !first && !last;
         if (first) dst = part_first + c * w3;
         else if (last) dst = part_last + c * w3;
         else dst = dNodeAcc + static_cast<int64_t>(key) * w3;
@@ -472,6 +572,11 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
             dst[f] = acc[cc];
             dst[da + f] = acc[kMaxDaLanes + cc];
             dst[2 * da + f] = acc[2 * kMaxDaLanes + cc];
+            if (direct) {
+              bf_put(bf.dNA, key, f, acc[cc]);
+              bf_put(bf.dNA, key, da + f, acc[kMaxDaLanes + cc]);
+              bf_put(bf.dNA, key, 2 * da + f, acc[2 * kMaxDaLanes + cc]);
+            }
           }
         }
 #pragma unroll
@@ -486,7 +591,7 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
 // chunk order.
 __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNodeAcc,
                                      const float* __restrict__ part_first,
-                                     const float* __restrict__ part_last) {
+                                     const float* __restrict__ part_last, StepBf bf) {
   const int U = pl.sizes[kSzU];
   const int lane = threadIdx.x & 31;
   const int w3 = 3 * D.da;
@@ -498,6 +603,7 @@ __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNode
       float s = part_last[static_cast<int64_t>(c0) * w3 + f];
       for (int c = c0 + 1; c <= c1; ++c) s += part_first[static_cast<int64_t>(c) * w3 + f];
       dNodeAcc[u * w3 + f] = s;
+      bf_put(bf.dNA, u, f, s);
     }
   }
 }
@@ -506,7 +612,7 @@ __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNode
 // (trainer.hpp:239-253; supports are unique nodes, so rows never collide).
 __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ dNode,
                                 const float* __restrict__ Gates, float* __restrict__ Dg,
-                                float* __restrict__ g_static) {
+                                float* __restrict__ g_static, StepBf bf, int cap_U) {
   const int U = pl.sizes[kSzU];
   const int nd = D.d + D.ds;
   const int64_t total = static_cast<int64_t>(U) * D.d;
@@ -517,10 +623,15 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
     const float ds = dNode[u * nd + i];
     const float z = gr[i], h = gr[2 * D.d + i], s = vw.mem[x];
     float* dg = Dg + u * 3 * D.d;
-    dg[i] = has ? ds * (h - s) * z * (1.0f - z) : 0.0f;
+    const float az = has ? ds * (h - s) * z * (1.0f - z) : 0.0f;
+    const float ah = has ? ds * z * (1.0f - h * h) : 0.0f;
+    dg[i] = az;
     dg[D.d + i] = 0.0f;
-    dg[2 * D.d + i] = has ? ds * z * (1.0f - h * h) : 0.0f;
+    dg[2 * D.d + i] = ah;
+    bf_put(bf.Dg, u, i, az);
+    bf_put(bf.Dg, u, 2 * bf.d8d + i, ah);
   }
+  bf_zero_tail(bf.Dg, U, cap_U, 2 * bf.d8d + D.d);
   if (D.ds > 0) {
     const int64_t tot2 = static_cast<int64_t>(U) * D.ds;
     for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < tot2; x += gridDim.x * blockDim.x) {
@@ -532,14 +643,16 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
 
 // da_r = (Wh^T da_h)[s part] * s * r (1 - r)  (gru.hpp:124-127).
 __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ T1,
-                                const float* __restrict__ Gates, float* __restrict__ Dg) {
+                                const float* __restrict__ Gates, float* __restrict__ Dg, StepBf bf) {
   const int U = pl.sizes[kSzU];
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int64_t u = x / D.d, i = x % D.d;
     const bool has = vw.mail_ev[u] >= 0;
     const float r = Gates[u * 3 * D.d + D.d + i];
-    Dg[u * 3 * D.d + D.d + i] = has ? T1[x] * vw.mem[x] * r * (1.0f - r) : 0.0f;
+    const float ar = has ? T1[x] * vw.mem[x] * r * (1.0f - r) : 0.0f;
+    Dg[u * 3 * D.d + D.d + i] = ar;
+    bf_put(bf.Dg, u, bf.d8d + i, ar);
   }
 }
 
@@ -551,7 +664,8 @@ __global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* _
                                                           int64_t offWk, int64_t offWv, int64_t offWz,
                                                           const float* __restrict__ Mom,
                                                           const float* __restrict__ M2,
-                                                          float* __restrict__ g_omega) {
+                                                          float* __restrict__ g_omega, int v_row0,
+                                                          int blk_stride) {
   __shared__ float red[256];
   const int i = blockIdx.x;
   const int t0 = D.d + D.ds + D.de;
@@ -561,10 +675,12 @@ __global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* _
     if (j < D.da) {
       s = fmaf(params[offWk + static_cast<int64_t>(j) * D.kv_in + t0 + i], Mom[j * D.dt + i], s);
     } else if (j < n1) {
-      s = fmaf(params[offWv + static_cast<int64_t>(j - D.da) * D.kv_in + t0 + i], Mom[j * D.dt + i], s);
+      s = fmaf(params[offWv + static_cast<int64_t>(j - D.da) * D.kv_in + t0 + i],
+               Mom[(v_row0 + j - D.da) * D.dt + i], s);
     } else {
-      const int jj = j - n1;
-      s = fmaf(params[offWz + static_cast<int64_t>(jj) * D.gin + 2 * D.d + i], M2[jj * D.dt + i], s);
+      const int jj = j - n1;  // Wall row: block jj / d (z, r, h), row jj % d
+      const int mrow = (jj / D.d) * blk_stride + jj % D.d;
+      s = fmaf(params[offWz + static_cast<int64_t>(jj) * D.gin + 2 * D.d + i], M2[mrow * D.dt + i], s);
     }
   }
   red[threadIdx.x] = s;
@@ -574,6 +690,31 @@ __global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* _
     __syncthreads();
   }
   if (threadIdx.x == 0) g_omega[i] = red[0];
+}
+
+// ---------------------------------------------------------------- weight pack
+// Per-step bf16 hi/lo copies of the weights in the layouts the TMA GEMMs read
+// ([W | b] for the forward contractions, slices / stacks for the backward).
+struct PackJob {
+  const float* src;
+  int64_t src_ld;
+  int rows, cols;
+  BfMat dst;
+  int r0, c0;
+};
+constexpr int kMaxPack = 20;
+struct PackJobs {
+  PackJob j[kMaxPack];
+  int n;
+};
+
+__global__ void pack_weights_kernel(const __grid_constant__ PackJobs jobs) {
+  const PackJob& J = jobs.j[blockIdx.y];
+  const int64_t total = static_cast<int64_t>(J.rows) * J.cols;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = x / J.cols, c = x % J.cols;
+    bf_put(J.dst, J.r0 + r, J.c0 + c, J.src[r * J.src_ld + c]);
+  }
 }
 
 // ---------------------------------------------------------------- writes
@@ -694,8 +835,8 @@ T* dalloc(size_t n) {
   return p;
 }
 
-int choose_splits(int M, int N, int64_t Kcap) {
-  if (gemm_impl() == kGemmTensor) {
+int choose_splits_engine(int engine, int M, int N, int64_t Kcap) {
+  if (engine == kGemmGather) {
     // tensor tiles are 128 x 256; keep >= ~1024 reduction rows per CTA so the
     // split-K partial traffic stays small next to the MMA work
     const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
@@ -704,12 +845,15 @@ int choose_splits(int M, int N, int64_t Kcap) {
   }
   const int tiles = static_cast<int>(ceil_div(M, 64) * ceil_div(N, 64));
   int s = static_cast<int>(ceil_div(2 * kSMs, tiles));
+  (void)engine;
   const int max_by_k = static_cast<int>(ceil_div(Kcap, 128));
   if (s > max_by_k) s = max_by_k;
   if (s < 1) s = 1;
   if (s > 64) s = 64;
   return s;
 }
+
+int choose_splits(int M, int N, int64_t Kcap) { return choose_splits_engine(gemm_impl(), M, N, Kcap); }
 
 struct WsCarver {
   float* base;
@@ -754,6 +898,68 @@ void add_nn(GemmGroup& gg, int Mcap, const int* M_dev, int N, int K, Operand a, 
 
 Operand ones_op(const float* ones, int K) { return op_dense(ones, 0, 0, K); }
 
+int choose_splits_tma(int M, int N, int64_t Kcap) {
+  const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
+  int64_t s = std::min<int64_t>(ceil_div(2 * kSMs, tiles), ceil_div(Kcap, 256));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 128)));
+}
+
+// Forward-style problem: A K-major [M x K] (runtime rows M_dev), B K-major [N x K].
+void tc_nn(TcGroup& g, int Mcap, const int* M_dev, int N, int K, const BfMat& A, int a_col0,
+           const BfMat& B, int b_col0, int b_rows_cap, float* C, int64_t ldc, float beta = 0.0f) {
+  TcProblem& P = g.p[g.count++];
+  P.M = Mcap;
+  P.M_dev = M_dev;
+  P.N = N;
+  P.K = K;
+  P.ntile = tc_ntile(N);
+  P.a = tma_view(A, a_col0, K, A.rows, true, 128);
+  P.b = tma_view(B, b_col0, K, b_rows_cap, true, P.ntile);
+  P.C = C;
+  P.ldc = ldc;
+  P.beta = beta;
+}
+
+// dX-style problem: A K-major [M x K], B MN-major stored [K x N].
+void tc_nmn(TcGroup& g, int Mcap, const int* M_dev, int N, int K, const BfMat& A, int a_col0,
+            const BfMat& B, int b_col0, float* C, int64_t ldc) {
+  TcProblem& P = g.p[g.count++];
+  P.M = Mcap;
+  P.M_dev = M_dev;
+  P.N = N;
+  P.K = K;
+  P.ntile = tc_ntile(N);
+  P.a = tma_view(A, a_col0, K, A.rows, true, 128);
+  P.b = tma_view(B, b_col0, N, K, false, 64);
+  P.C = C;
+  P.ldc = ldc;
+}
+
+// Weight-gradient problem: C[M x N] = Y^T X reduced over K runtime rows; A is
+// Y (stored [K x M], MN-major), B is X (stored [K x N], MN-major); C2 takes
+// the last output column (bias gradient) when set.
+void tc_tn(TcGroup& g, WsCarver& wc, int M, int N, int Kcap, const int* K_dev, const BfMat& Y, int y_col0,
+           const BfMat& X, int x_col0, float* C, int64_t ldc, float* C2 = nullptr) {
+  TcProblem& P = g.p[g.count++];
+  P.M = M;
+  P.N = N;
+  P.K = Kcap;
+  P.K_dev = K_dev;
+  P.ntile = tc_ntile(N);
+  P.a = tma_view(Y, y_col0, M, Kcap, false, 64);
+  P.b = tma_view(X, x_col0, N, Kcap, false, 64);
+  P.C = C;
+  P.ldc = ldc;
+  P.C2 = C2;
+  P.splits = choose_splits_tma(M, N, Kcap);
+  if (P.splits > 1) P.ws = wc.take(static_cast<size_t>(P.splits) * M * N);
+}
+
+int max_splits(int M, int N, int64_t K) {
+  return std::max(std::max(choose_splits_engine(kGemmSimt, M, N, K), choose_splits_engine(kGemmGather, M, N, K)),
+                  choose_splits_tma(M, N, K));
+}
+
 }  // namespace
 
 void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes) {
@@ -793,8 +999,8 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   w.dNode = dalloc<float>(U * (d + m.d_static));
   w.Dg = dalloc<float>(U * 3 * d);
   w.T1 = dalloc<float>(U * d);
-  w.DMT = dalloc<float>(3 * d * dt);  // M2 = Dg^T GU
-  w.Mom = dalloc<float>(2 * da * dt);
+  w.DMT = dalloc<float>(3 * ((d + 7) / 8 * 8) * dt);  // M2 = Dg^T GU (padded blocks)
+  w.Mom = dalloc<float>(2 * ((da + 7) / 8 * 8) * dt);  // padded dK | dV rows (TMA layout)
   w.omega_chunks = static_cast<int>(ceil_div(U, kOmegaRows));
   w.omega_part = dalloc<float>(static_cast<size_t>(w.omega_chunks) * dt);
   const int64_t max_ones = std::max<int64_t>(std::max<int64_t>(P, U), B2);
@@ -803,10 +1009,39 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   TGB_CUDA(cudaMemcpy(w.ones, &one, sizeof(float), cudaMemcpyHostToDevice));
   (void)max_ones;
   w.loss_terms = dalloc<double>(2 * cap_B);
-  // routing partials live in the split-K arena's tail; size generously
   const int64_t gin = m.gin(), kv = m.kv_in(), q = m.q_in();
+  {
+    StepBf& b = w.bf;
+    b.d8a = static_cast<int>((da + 7) / 8 * 8);
+    b.d8d = static_cast<int>((d + 7) / 8 * 8);
+    const int64_t md = m.mail_dim(), ds = m.d_static;
+    b.Xg = bf_alloc(U, gin + 1);
+    b.GU = bf_alloc(U, std::max<int64_t>(dt, 1));
+    b.RS = bf_alloc(U, d + 1);
+    b.Qin = bf_alloc(R, q + 1);
+    b.KVin = bf_alloc(P, kv + 1);
+    b.Gt = bf_alloc(P, std::max<int64_t>(dt, 1));
+    b.H = bf_alloc(R, da);
+    b.Hin = bf_alloc(B2, 2 * da + 1);
+    b.Dhid = bf_alloc(B2, dh);
+    b.dQ = bf_alloc(R, da);
+    b.dKV = bf_alloc(P, b.d8a + da);
+    b.dNA = bf_alloc(U, 3 * da);
+    b.Dg = bf_alloc(U, 2 * b.d8d + d);
+    b.Wzr = bf_alloc(2 * d, gin + 1);
+    b.Whm = bf_alloc(d, md);
+    b.Whs = bf_alloc(d, d + 1);
+    b.Wq = bf_alloc(da, q + 1);
+    b.Wk = bf_alloc(da, kv + 1);
+    b.Wv = bf_alloc(da, kv + 1);
+    b.W1a = bf_alloc(dh, da);
+    b.W1b = bf_alloc(dh, da);
+    b.W1 = bf_alloc(dh, 2 * da);
+    b.Wst = bf_alloc(3 * da, d + ds);
+  }
+  // split-K arena (max over the engines) + routing partials in its tail
   size_t ws = 0;
-  auto acc = [&](int M, int N, int64_t K) { ws += static_cast<size_t>(choose_splits(M, N, K)) * M * N; };
+  auto acc = [&](int M, int N, int64_t K) { ws += static_cast<size_t>(max_splits(M, N + 1, K)) * M * (N + 1); };
   // decoder bwd
   acc(static_cast<int>(dh), static_cast<int>(2 * da), B2);
   acc(1, static_cast<int>(dh), B2);
@@ -826,6 +1061,11 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   acc(static_cast<int>(d), static_cast<int>(d), U);
   acc(1, static_cast<int>(3 * d), U);
   acc(static_cast<int>(3 * d), static_cast<int>(dt), U);
+  // TMA-engine shapes (padded blocks, separate z / r problems)
+  acc(static_cast<int>(w.bf.d8a + da), static_cast<int>(dt), P);
+  acc(static_cast<int>(d), static_cast<int>(gin), U);
+  acc(static_cast<int>(d), static_cast<int>(gin), U);
+  acc(static_cast<int>(2 * w.bf.d8d + d), static_cast<int>(dt), U);
   const int64_t nchunks = ceil_div(R + P, kChunk) + 1;
   ws += 2 * static_cast<size_t>(nchunks) * 3 * da;
   w.splitk_ws_floats = ws;
@@ -855,6 +1095,10 @@ void step_free(StepWork& w) {
                   w.loss_terms, w.splitk_ws, w.wpack, w.win};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  BfMat* bfs[] = {&w.bf.Xg, &w.bf.GU, &w.bf.RS, &w.bf.Qin, &w.bf.KVin, &w.bf.Gt, &w.bf.H, &w.bf.Hin,
+                  &w.bf.Dhid, &w.bf.dQ, &w.bf.dKV, &w.bf.dNA, &w.bf.Dg, &w.bf.Wzr, &w.bf.Whm, &w.bf.Whs,
+                  &w.bf.Wq, &w.bf.Wk, &w.bf.Wv, &w.bf.W1a, &w.bf.W1b, &w.bf.W1, &w.bf.Wst};
+  for (BfMat* b : bfs) bf_free(*b);
   w = StepWork{};
 }
 
@@ -891,6 +1135,45 @@ void substep_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* 
   substep_rest_launch(c, pl, vw, loss_out, s);
 }
 
+namespace {
+
+void pack_weights_launch(const StepCtx& c, cudaStream_t s) {
+  const ModelDims& m = c.m;
+  const ParamLayout& L = c.L;
+  const StepBf& b = c.w->bf;
+  const float* P = c.params;
+  const int d = static_cast<int>(m.d_mem), gin = static_cast<int>(m.gin()), md = static_cast<int>(m.mail_dim());
+  const int da = static_cast<int>(m.d_attn), q = static_cast<int>(m.q_in()), kv = static_cast<int>(m.kv_in());
+  const int dh = static_cast<int>(m.dh()), nd = static_cast<int>(m.node_dim());
+  PackJobs J{};
+  auto add = [&](int64_t off, int64_t ld, int rows, int cols, const BfMat& dst, int r0, int c0) {
+    if (rows > 0 && cols > 0) J.j[J.n++] = PackJob{P + off, ld, rows, cols, dst, r0, c0};
+  };
+  add(L.off[tWz], gin, d, gin, b.Wzr, 0, 0);
+  add(L.off[tBz], 1, d, 1, b.Wzr, 0, gin);
+  add(L.off[tWr], gin, d, gin, b.Wzr, d, 0);
+  add(L.off[tBr], 1, d, 1, b.Wzr, d, gin);
+  add(L.off[tWh], gin, d, md, b.Whm, 0, 0);
+  add(L.off[tWh] + md, gin, d, d, b.Whs, 0, 0);
+  add(L.off[tBh], 1, d, 1, b.Whs, 0, d);
+  add(L.off[tWq], q, da, q, b.Wq, 0, 0);
+  add(L.off[tBq], 1, da, 1, b.Wq, 0, q);
+  add(L.off[tWk], kv, da, kv, b.Wk, 0, 0);
+  add(L.off[tBk], 1, da, 1, b.Wk, 0, kv);
+  add(L.off[tWv], kv, da, kv, b.Wv, 0, 0);
+  add(L.off[tBv], 1, da, 1, b.Wv, 0, kv);
+  add(L.off[tW1], 2 * da, dh, da, b.W1a, 0, 0);
+  add(L.off[tW1] + da, 2 * da, dh, da, b.W1b, 0, 0);
+  add(L.off[tW1], 2 * da, dh, 2 * da, b.W1, 0, 0);
+  add(L.off[tWq], q, da, nd, b.Wst, 0, 0);
+  add(L.off[tWk], kv, da, nd, b.Wst, da, 0);
+  add(L.off[tWv], kv, da, nd, b.Wst, 2 * da, 0);
+  pack_weights_kernel<<<dim3(32, J.n), 256, 0, s>>>(J);
+  TGB_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
 void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s) {
   const ModelDims& m = c.m;
   const ParamLayout& L = c.L;
@@ -901,11 +1184,22 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   const int d = D.d, md = D.md, gin = D.gin;
   const int U = w.cap_U;
   const int* szU = pl.sizes + kSzU;
+  const bool tma = gemm_impl() == kGemmTma;
+  StepBf bfx;
+  if (tma) bfx = w.bf;
+  bfx.d8a = w.bf.d8a;
+  bfx.d8d = w.bf.d8d;
   // ---- GRU freshen (K5)
   c.mark(phGruFwd, s);
+  if (tma) pack_weights_launch(c, s);
   assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, vw, g, P + L.off[tOmega], w.Xg,
-                                                             w.ldx, w.GU);
-  {
+                                                             w.ldx, w.GU, bfx, U);
+  if (tma) {
+    TcGroup tg;
+    tc_nn(tg, U, szU, 2 * d, gin + 1, w.bf.Xg, 0, w.bf.Wzr, 0, 2 * d, w.Gates, 3 * d);
+    tc_nn(tg, U, szU, d, md, w.bf.Xg, 0, w.bf.Whm, 0, d, w.Gates + 2 * d, 3 * d);
+    tc_group_launch(tg, s);
+  } else {
     GemmGroup gg;
     add_nn(gg, U, szU, 2 * d, gin, A_rows(w.Xg, w.ldx, gin), B_wT(P + L.off[tWz], gin, gin), w.Gates,
            3 * d, P + L.off[tBz]);
@@ -914,8 +1208,12 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
     gemm_group_launch(gg, s);
   }
   const int eblocks = 4 * kSMs;
-  gru_mid_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, w.RS);
-  {
+  gru_mid_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, w.RS, bfx, U);
+  if (tma) {
+    TcGroup tg;  // Gh += [r*s | 1] [Wh_s | bh]^T  (the bias rides the ones column)
+    tc_nn(tg, U, szU, d, d + 1, w.bf.RS, 0, w.bf.Whs, 0, d, w.Gates + 2 * d, 3 * d, 1.0f);
+    tc_group_launch(tg, s);
+  } else {
     GemmGroup gg;
     add_nn(gg, U, szU, d, d, A_rows(w.RS, d, d), B_wT(P + L.off[tWh] + md, gin, d), w.Gates + 2 * d,
            3 * d, nullptr, 1.0f);
@@ -940,6 +1238,12 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   const int* szR = pl.sizes + kSzR;
   const int* szP = pl.sizes + kSzP;
   const int* sz2B = pl.sizes + kSz2B;
+  const bool tma = gemm_impl() == kGemmTma;
+  StepBf bfx;
+  if (tma) bfx = w.bf;
+  bfx.d8a = w.bf.d8a;
+  bfx.d8d = w.bf.d8d;
+  const StepBf& B = w.bf;
 
   TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));
   const int eblocks = 4 * kSMs;
@@ -947,9 +1251,16 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   // ---- attention forward (K6)
   c.mark(phAttnAssemble, s);
   assemble_attn_kernel<<<row_blocks(R + Pc), 32 * kWarps, 0, s>>>(
-      D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, w.Qin, w.ldq, w.KVin, w.ldkv, w.Gt);
+      D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, w.Qin, w.ldq, w.KVin, w.ldkv, w.Gt, bfx, R,
+      Pc);
   c.mark(phAttnProj, s);
-  {
+  if (tma) {
+    TcGroup tg;
+    tc_nn(tg, R, szR, da, D.q_in + 1, B.Qin, 0, B.Wq, 0, da, w.Q, da);
+    tc_nn(tg, Pc, szP, da, D.kv_in + 1, B.KVin, 0, B.Wk, 0, da, w.KV, 2 * da);
+    tc_nn(tg, Pc, szP, da, D.kv_in + 1, B.KVin, 0, B.Wv, 0, da, w.KV + da, 2 * da);
+    tc_group_launch(tg, s);
+  } else {
     GemmGroup gg;
     add_nn(gg, R, szR, da, D.q_in, A_rows(w.Qin, w.ldq, D.q_in), B_wT(P + L.off[tWq], D.q_in, D.q_in),
            w.Q, da, P + L.off[tBq]);
@@ -961,11 +1272,16 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   }
   c.mark(phAttnSoftmax, s);
   attn_fwd_kernel<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.Q, w.KV, w.attn_a, w.H,
-                                                         c.d_numeric_flag);
+                                                         c.d_numeric_flag, bfx);
 
   // ---- decoder + loss (K7)
   c.mark(phDecoder, s);
-  {
+  if (tma) {
+    TcGroup tg;
+    tc_nn(tg, R, szR, dh, da, B.H, 0, B.W1a, 0, dh, w.AB, 2 * dh);
+    tc_nn(tg, R, szR, dh, da, B.H, 0, B.W1b, 0, dh, w.AB + dh, 2 * dh);
+    tc_group_launch(tg, s);
+  } else {
     GemmGroup gg;
     add_nn(gg, R, szR, dh, da, A_rows(w.H, da, da), B_wT(P + L.off[tW1], 2 * da, da), w.AB, 2 * dh);
     add_nn(gg, R, szR, dh, da, A_rows(w.H, da, da), B_wT(P + L.off[tW1] + da, 2 * da, da), w.AB + dh,
@@ -974,38 +1290,56 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   }
   decoder_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(
       D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, w.Dhid, w.Hin,
-      w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag);
+      w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
   loss_kernel<<<1, 1024, 0, s>>>(pl, w.loss_terms, loss_out, c.d_numeric_flag);
 
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
   c.mark(phDecoderBwd, s);
   {
-    GemmGroup gg;
-    add_tn(gg, wc, dh, 2 * da, B2, sz2B, A_trans(w.Dhid, dh, B2), B_w(w.Hin, 2 * da, B2),
-           G + L.off[tW1], 2 * da);
-    add_tn(gg, wc, 1, dh, B2, sz2B, ones_op(w.ones, B2), B_w(w.Dhid, dh, B2), G + L.off[tB1], dh);
+    GemmGroup gg;  // rank-1 reductions (dW2, db2; and on the fp32 engines dW1, db1, dIn)
     add_tn(gg, wc, 1, dh, B2, sz2B, op_dense(w.dlogit, 0, 1, B2), B_w(w.HID, dh, B2), G + L.off[tW2],
            dh);
     add_tn(gg, wc, 1, 1, B2, sz2B, ones_op(w.ones, B2), op_dense(w.dlogit, 1, 0, B2), G + L.off[tB2],
            1);
-    add_nn(gg, B2, sz2B, 2 * da, dh, A_rows(w.Dhid, dh, dh), B_w(P + L.off[tW1], 2 * da, dh), w.dIn,
-           2 * da);
+    if (!tma) {
+      add_tn(gg, wc, dh, 2 * da, B2, sz2B, A_trans(w.Dhid, dh, B2), B_w(w.Hin, 2 * da, B2),
+             G + L.off[tW1], 2 * da);
+      add_tn(gg, wc, 1, dh, B2, sz2B, ones_op(w.ones, B2), B_w(w.Dhid, dh, B2), G + L.off[tB1], dh);
+      add_nn(gg, B2, sz2B, 2 * da, dh, A_rows(w.Dhid, dh, dh), B_w(P + L.off[tW1], 2 * da, dh), w.dIn,
+             2 * da);
+    }
     gemm_group_launch(gg, s);
+  }
+  if (tma) {
+    TcGroup tg;
+    tc_tn(tg, wc, dh, 2 * da + 1, B2, sz2B, B.Dhid, 0, B.Hin, 0, G + L.off[tW1], 2 * da, G + L.off[tB1]);
+    tc_nmn(tg, B2, sz2B, 2 * da, dh, B.Dhid, 0, B.W1, 0, w.dIn, 2 * da);
+    tc_group_launch(tg, s);
   }
 
   // ---- attention backward (K8)
   c.mark(phAttnBwd, s);
   attn_bwd_kernel<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ,
-                                                         w.dKV);
+                                                         w.dKV, bfx, R, Pc);
   const int64_t nchunks = ceil_div(R + Pc, kChunk) + 1;
   float* part_first = wc.take(static_cast<size_t>(nchunks) * 3 * da);
   float* part_last = wc.take(static_cast<size_t>(nchunks) * 3 * da);
   routing_chunk_kernel<<<row_blocks(nchunks), 32 * kWarps, 0, s>>>(D, pl, w.dQ, w.dKV, w.dNodeAcc,
-                                                                    part_first, part_last);
+                                                                    part_first, part_last, bfx);
   routing_fixup_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, w.dNodeAcc, part_first,
-                                                             part_last);
+                                                             part_last, bfx);
   c.mark(phAttnBwdGemm, s);
-  {
+  if (tma) {
+    TcGroup tg;
+    const int nd = d + D.ds;
+    tc_nmn(tg, U, szU, nd, 3 * da, B.dNA, 0, B.Wst, 0, w.dNode, nd);
+    tc_tn(tg, wc, da, D.q_in + 1, R, szR, B.dQ, 0, B.Qin, 0, G + L.off[tWq], D.q_in, G + L.off[tBq]);
+    tc_tn(tg, wc, da, D.kv_in + 1, Pc, szP, B.dKV, 0, B.KVin, 0, G + L.off[tWk], D.kv_in, G + L.off[tBk]);
+    tc_tn(tg, wc, da, D.kv_in + 1, Pc, szP, B.dKV, B.d8a, B.KVin, 0, G + L.off[tWv], D.kv_in,
+          G + L.off[tBv]);
+    if (dt > 0) tc_tn(tg, wc, B.d8a + da, dt, Pc, szP, B.dKV, 0, B.Gt, 0, w.Mom, dt);
+    tc_group_launch(tg, s);
+  } else {
     GemmGroup gg;
     Operand bs;
     op_append(bs, P + L.off[tWq], D.q_in, 1, da);
@@ -1028,14 +1362,26 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 
   // ---- GRU backward (K9)
   c.mark(phGruBwd, s);
-  gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, w.Dg, G + L.off[tStatic]);
-  {
+  gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, w.Dg, G + L.off[tStatic], bfx, U);
+  if (tma) {
+    TcGroup tg;
+    tc_nmn(tg, U, szU, d, d, B.Dg, 2 * B.d8d, B.Whs, 0, w.T1, d);
+    tc_group_launch(tg, s);
+  } else {
     GemmGroup gg;
     add_nn(gg, U, szU, d, d, A_rows(w.Dg + 2 * d, 3 * d, d), B_w(P + L.off[tWh] + md, gin, d), w.T1, d);
     gemm_group_launch(gg, s);
   }
-  gru_bwd2_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.T1, w.Gates, w.Dg);
-  {
+  gru_bwd2_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.T1, w.Gates, w.Dg, bfx);
+  if (tma) {
+    TcGroup tg;
+    tc_tn(tg, wc, d, gin + 1, U, szU, B.Dg, 0, B.Xg, 0, G + L.off[tWz], gin, G + L.off[tBz]);
+    tc_tn(tg, wc, d, gin + 1, U, szU, B.Dg, B.d8d, B.Xg, 0, G + L.off[tWr], gin, G + L.off[tBr]);
+    tc_tn(tg, wc, d, md, U, szU, B.Dg, 2 * B.d8d, B.Xg, 0, G + L.off[tWh], gin);
+    tc_tn(tg, wc, d, d + 1, U, szU, B.Dg, 2 * B.d8d, B.RS, 0, G + L.off[tWh] + md, gin, G + L.off[tBh]);
+    if (dt > 0) tc_tn(tg, wc, 2 * B.d8d + d, dt, U, szU, B.Dg, 0, B.GU, 0, w.DMT, dt);
+    tc_group_launch(tg, s);
+  } else {
     GemmGroup gg;
     add_tn(gg, wc, 2 * d, gin, U, szU, A_trans(w.Dg, 3 * d, U), B_w(w.Xg, w.ldx, U), G + L.off[tWz], gin);
     add_tn(gg, wc, d, md, U, szU, A_trans(w.Dg + 2 * d, 3 * d, U), B_w(w.Xg, w.ldx, U), G + L.off[tWh],
@@ -1048,7 +1394,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   }
   if (dt > 0)
     omega_final_kernel<<<dt, 256, 0, s>>>(D, P, L.off[tWk], L.off[tWv], L.off[tWz], w.Mom, w.DMT,
-                                          G + L.off[tOmega]);
+                                          G + L.off[tOmega], tma ? B.d8a : da, tma ? B.d8d : d);
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "device_types.cuh"
 #include "gemm_simt.cuh"
+#include "gemm_tma.cuh"
 
 namespace tgb {
 
@@ -37,8 +38,21 @@ struct ParamLayout {
   static ParamLayout make(const ModelDims& m);
 };
 
+// Pre-split (bf16 hi/lo) GEMM operands of the TMA engine. Layouts (columns):
+//  Xg [mail2 | phi | ef | mem | 1], RS [r*s | 1], Qin [s_hat | static | 1..1 | 1],
+//  KVin [s_hat | static | ef | cos | 1], Hin [h_u | h_v | 1] -- the trailing 1
+//  column carries the bias: forward GEMMs use packed [W | b] weights, and the
+//  weight-gradient GEMMs emit db as their last output column.
+//  dKV [dK | pad | dV], Dg [da_z | pad | da_r | pad | da_h] (blocks 8-aligned).
+struct StepBf {
+  BfMat Xg, GU, RS, Qin, KVin, Gt, H, Hin, Dhid, dQ, dKV, dNA, Dg;
+  BfMat Wzr, Whm, Whs, Wq, Wk, Wv, W1a, W1b, W1, Wst;
+  int d8a = 0, d8d = 0;
+};
+
 // Per-trainer activation workspace (capacities fixed at creation).
 struct StepWork {
+  StepBf bf;
   int cap_B = 0, cap_R = 0, cap_P = 0, cap_U = 0;
   int64_t ldx = 0, ldq = 0, ldkv = 0;
   float *Xg = nullptr, *GU = nullptr, *Gates = nullptr, *RS = nullptr, *s_hat = nullptr;

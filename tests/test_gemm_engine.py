@@ -1,4 +1,5 @@
-"""GEMM engines on the B200: tcgen05 bf16x3 (default) and exact fp32 SIMT,
+"""GEMM engines on the B200: TMA-fed tcgen05 bf16x3 (default), the gather
+tcgen05 engine and exact fp32 SIMT,
 against a float64 numpy product, over the operand orientations and ragged
 shapes the training step uses (tolerances stated per engine)."""
 from __future__ import annotations
@@ -14,7 +15,7 @@ SHAPES = [(300, 200, 472), (128, 100, 64), (1, 100, 1200), (1800, 300, 100), (77
           (2845, 572, 200), (13, 16, 8)]
 
 
-@pytest.mark.parametrize("impl,tol", [(T.GEMM_TENSOR, 3e-5), (T.GEMM_SIMT, 2e-6)])
+@pytest.mark.parametrize("impl,tol", [(T.GEMM_TMA, 3e-5), (T.GEMM_SIMT, 2e-6), (T.GEMM_GATHER, 3e-5)])
 @pytest.mark.parametrize("M,N,K", SHAPES)
 @pytest.mark.parametrize("at,bt", [(False, True), (True, False), (False, False), (True, True)])
 def test_gemm_engine(impl, tol, M, N, K, at, bt):

@@ -147,7 +147,7 @@ def _substep_case(env, cfg, mdims, begin, B, seed=0):
     return s, rg, g, mc, params, negs, plan, vm, vl
 
 
-@pytest.fixture(params=[T.GEMM_TENSOR, T.GEMM_SIMT], ids=["tcgen05", "simt"])
+@pytest.fixture(params=[T.GEMM_TMA, T.GEMM_SIMT, T.GEMM_GATHER], ids=["tma", "simt", "gather"])
 def engine(request):
     prev = T.get_gemm_impl()
     T.set_gemm_impl(request.param)
