@@ -139,6 +139,7 @@ std::vector<double> host_init_params(const ModelDims& m, uint64_t seed) {
 struct tgnn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // plan-only work overlapped with the step
   int* d_flag = nullptr;
 
   void check_numeric() {
@@ -215,6 +216,8 @@ void plan_alloc(DPlan& pl, int cap_B, int n, int cap_U, int64_t N) {
   pl.sort_bits = bits;
   pl.sort_tmp_bytes = plan_sort_tmp_bytes(items, bits);
   TGB_CUDA(cudaMalloc(&pl.sort_tmp, pl.sort_tmp_bytes > 0 ? pl.sort_tmp_bytes : 1));
+  TGB_CUDA(cudaEventCreateWithFlags(&pl.ev_pairs, cudaEventDisableTiming));
+  TGB_CUDA(cudaEventCreateWithFlags(&pl.ev_sorted, cudaEventDisableTiming));
   pl.bitmap = dalloc<uint32_t>(static_cast<size_t>((N + 31) / 32));
   TGB_CUDA(cudaMemset(pl.bitmap, 0, sizeof(uint32_t) * ((N + 31) / 32)));
 }
@@ -227,6 +230,8 @@ void plan_free(DPlan& pl) {
                   pl.bitmap};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (pl.ev_pairs) cudaEventDestroy(pl.ev_pairs);
+  if (pl.ev_sorted) cudaEventDestroy(pl.ev_sorted);
   pl = DPlan{};
 }
 
@@ -480,7 +485,7 @@ void run_barrier(tgnn_run* r, int64_t b) {
           a.valid = 1;
           DPlan& pl = tr->plans[static_cast<size_t>(sub)];
           set_plan_args_launch(pl.args, a, s);
-          plan_launch(r->g->d, pl, s);
+          plan_launch(r->g->d, pl, s, ctx->side);
           gather_view_launch(pl, r->mem->d, tr->views[static_cast<size_t>(sub)], s);
         }
         substep_gru_launch(sc, tr->plans[0], tr->views[0], s);
@@ -557,6 +562,7 @@ int tgnn_ctx_create(int device, tgnn_ctx** out) {
   auto* c = new tgnn_ctx();
   c->device = device;
   TGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  TGB_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   c->d_flag = dalloc<int>(1);
   TGB_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
   *out = c;
@@ -568,6 +574,8 @@ int tgnn_ctx_destroy(tgnn_ctx* ctx) {
   if (!ctx) return 0;
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_flag);
+  cudaStreamSynchronize(ctx->side);
+  cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   API_END
@@ -1147,7 +1155,7 @@ int tgnn_trainer_iterate(tgnn_trainer* tr, tgnn_memstore* m, int64_t batch_index
   a.valid = 1;
   DPlan& pl = tr->plans[0];
   set_plan_args_launch(pl.args, a, s);
-  plan_launch(tr->g->d, pl, s);
+  plan_launch(tr->g->d, pl, s, ctx->side);
   gather_view_launch(pl, m->d, tr->views[0], s);
   StepCtx sc = tr->sc();
   substep_launch(sc, pl, tr->views[0], tr->d_loss, s);

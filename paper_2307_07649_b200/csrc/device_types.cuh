@@ -12,6 +12,8 @@
 //    mail_mem [N, 2d] fp32, mail_t / mail_dt / last_update f64, mail_event int32.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace tgb {
@@ -84,6 +86,9 @@ struct DPlan {
   size_t sort_tmp_bytes = 0;
   int sort_bits = 1;
   uint32_t* bitmap = nullptr;    // [ceil(N / 32)] support marks, cleared by finalize
+  // The routing sort only depends on the plan: it runs on a side stream,
+  // overlapped with the forward pass; the backward waits on ev_sorted.
+  cudaEvent_t ev_pairs = nullptr, ev_sorted = nullptr;
 };
 
 // Read view (ReadView, shared_buffers.hpp:118-122) in device form.

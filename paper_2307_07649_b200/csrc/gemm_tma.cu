@@ -24,14 +24,17 @@ namespace {
 
 constexpr int kBM = 128, kBK = 64, kThreads = 192, kSt = 2;
 constexpr int kATileB = kBM * kBK * 2;   // 16 KB (one of hi / lo)
-constexpr int kBTileB = 256 * kBK * 2;   // 32 KB
-constexpr int kStageB = 2 * kATileB + 2 * kBTileB;
-constexpr int kSmem = kSt * kStageB + 1024 + 256;
+constexpr int kSmemMax = kSt * (2 * kATileB + 2 * 256 * kBK * 2) + 1024 + 256;
 
+// Shared-memory / TMEM geometry is sized by the group's widest N tile, so
+// narrow-tile groups fit several CTAs per SM.
 struct TcParams {
   TcProblem p[kMaxTc];
   int tiles_m[kMaxTc], tiles_n[kMaxTc];
   int count;
+  int b_tile_bytes;  // per hi / lo B tile: roundup64(max ntile) * 128
+  int stage_bytes;
+  int tmem_cols;     // power of two >= max(32, max ntile)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const int split = tile / (tm * tn);
   const int t2 = tile % (tm * tn);
   const int m0 = (t2 / tn) * kBM;
-  const int n0 = (t2 % tn) * 256;
+  const int n0 = (t2 % tn) * P.ntile;
   const int M = P.M_dev ? min(P.M, *P.M_dev) : P.M;
   if (m0 >= M && P.splits == 1) return;
   const int N = P.N;
@@ -131,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int kStageB = gp.stage_bytes, kBTileB = gp.b_tile_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageB);
   uint64_t* empty = full + kSt;
   uint64_t* accf = empty + kSt;
@@ -146,7 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(256));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "r"(gp.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const int m = m0 + row;
-    const int nvalid = min(256, N - n0);
+    const int nvalid = min(ntile, N - n0);
     for (int c0 = 0; c0 < ntile; c0 += 16) {
       uint32_t v[16];
       if (nk > 0) {
@@ -254,7 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(gp.tmem_cols));
 }
 
 __global__ void tc_splitk_reduce_kernel(const __grid_constant__ TcParams gp) {
@@ -374,24 +380,33 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s) {
   if (g.count == 0) return;
   static bool attr = false;
   if (!attr) {
-    TGB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    TGB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
     attr = true;
   }
   TcParams gp;
   std::memset(&gp, 0, sizeof(gp));
   gp.count = g.count;
-  int max_tiles = 0;
+  int max_tiles = 0, max_ntile = 16;
   bool any_split = false;
   for (int i = 0; i < g.count; ++i) {
     gp.p[i] = g.p[i];
+    TGB_REQUIRE(g.p[i].ntile % 16 == 0 && g.p[i].ntile >= 16 && g.p[i].ntile <= 256, kConfig,
+                "tc gemm: ntile must be a multiple of 16 in [16, 256]");
     gp.tiles_m[i] = static_cast<int>(ceil_div(g.p[i].M, kBM));
-    gp.tiles_n[i] = static_cast<int>(ceil_div(g.p[i].N, 256));
+    gp.tiles_n[i] = static_cast<int>(ceil_div(g.p[i].N, g.p[i].ntile));
     const int t = gp.tiles_m[i] * gp.tiles_n[i] * g.p[i].splits;
     max_tiles = std::max(max_tiles, t);
+    max_ntile = std::max(max_ntile, g.p[i].ntile);
     any_split |= g.p[i].splits > 1;
   }
   if (max_tiles == 0) return;
-  tc_gemm_kernel<<<dim3(max_tiles, g.count), kThreads, kSmem, s>>>(gp);
+  gp.b_tile_bytes = (max_ntile + 63) / 64 * 64 * 128;
+  gp.stage_bytes = 2 * kATileB + 2 * gp.b_tile_bytes;
+  int cols = 32;
+  while (cols < max_ntile) cols *= 2;
+  gp.tmem_cols = cols;
+  const int smem = kSt * gp.stage_bytes + 1024 + 256;
+  tc_gemm_kernel<<<dim3(max_tiles, g.count), kThreads, smem, s>>>(gp);
   TGB_CUDA(cudaGetLastError());
   if (any_split) {
     tc_splitk_reduce_kernel<<<dim3(64, g.count), 256, 0, s>>>(gp);

@@ -69,7 +69,9 @@ struct TcGroup {
 // [K rows x M cols]. B K-major: stored [N rows x K cols]; MN-major: [K x N].
 // (col0 % 8 == 0 so the view base is 16-byte aligned.)
 TmaOp tma_view(const BfMat& m, int64_t col0, int64_t cols, int64_t rows, bool kmajor, int box_rows);
-inline int tc_ntile(int N) { return static_cast<int>(std::min<int64_t>(256, (N + 15) / 16 * 16)); }
+inline int tc_ntile(int N, int cap = 256) {
+  return static_cast<int>(std::min<int64_t>(cap, (N + 15) / 16 * 16));
+}
 
 void tc_group_launch(const TcGroup& g, cudaStream_t s);
 

@@ -310,7 +310,7 @@ size_t plan_sort_tmp_bytes(int cap_items, int bits) {
   return bytes;
 }
 
-void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s) {
+void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) {
   uint32_t* bitmap = pl.bitmap;
   const int B = pl.cap_B;
   negatives_kernel<<<static_cast<int>(ceil_div(B, 256)), 256, 0, s>>>(pl.args, g.N, g.boundary,
@@ -328,12 +328,19 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s) {
   pairs_kernel<<<static_cast<int>(ceil_div(slots, 256)), 256, 0, s>>>(pl);
   TGB_CUDA(cudaGetLastError());
   const int cap_items = pl.cap_R + pl.cap_P;
+  cudaStream_t ss = s;
+  if (side && pl.ev_pairs) {
+    TGB_CUDA(cudaEventRecord(pl.ev_pairs, s));
+    TGB_CUDA(cudaStreamWaitEvent(side, pl.ev_pairs, 0));
+    ss = side;
+  }
   size_t bytes = pl.sort_tmp_bytes;
   TGB_CUDA(cub::DeviceRadixSort::SortPairs(pl.sort_tmp, bytes, pl.item_key, pl.item_key_s,
                                            pl.item_val, pl.item_val_s, cap_items, 0,
-                                           pl.sort_bits, s));
-  routing_ptr_kernel<<<static_cast<int>(ceil_div(cap_items, 256)), 256, 0, s>>>(pl);
+                                           pl.sort_bits, ss));
+  routing_ptr_kernel<<<static_cast<int>(ceil_div(cap_items, 256)), 256, 0, ss>>>(pl);
   TGB_CUDA(cudaGetLastError());
+  if (pl.ev_sorted) TGB_CUDA(cudaEventRecord(pl.ev_sorted, ss));
 }
 
 void gather_view_launch(const DPlan& pl, const DMem& st, DView& vw, cudaStream_t s) {

@@ -8,7 +8,7 @@ namespace tgb {
 
 size_t plan_sort_tmp_bytes(int cap_items, int bits);
 // negatives -> sampler -> support dedup -> pair compaction -> routing CSR
-void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s);
+void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side = nullptr);
 void negatives_only_launch(const DGraph& g, const PlanArgs* args, int count, int32_t* negs,
                            cudaStream_t s);
 void set_plan_args_launch(PlanArgs* dst, const PlanArgs& a, cudaStream_t s);

@@ -111,30 +111,32 @@ __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const 
     const int32_t ev = vw.mail_ev[u];
     const bool has = ev >= 0;
     const double dt = vw.mail_dt[u];
-    float* row = Xg + u * ldx;
+    float* row = Xg ? Xg + u * ldx : nullptr;  // fp32 copy only for the fp32-operand engines
     for (int x = lane; x < 2 * D.d; x += 32) {
       const float v = vw.mail_mem[u * 2 * D.d + x];
-      row[x] = v;
+      if (row) row[x] = v;
       bf_put(bf.Xg, u, x, v);
     }
     for (int i = lane; i < D.dt; i += 32) {
       const double arg = dt * static_cast<double>(omega[i]);
       const float c = static_cast<float>(cos(arg));
       const float gu = has ? static_cast<float>(-dt * sin(arg)) : 0.0f;
-      row[2 * D.d + i] = c;
-      GU[u * D.dt + i] = gu;
+      if (row) {
+        row[2 * D.d + i] = c;
+        GU[u * D.dt + i] = gu;
+      }
       bf_put(bf.Xg, u, 2 * D.d + i, c);
       bf_put(bf.GU, u, i, gu);
     }
     const float* ef = has ? g.efeat + static_cast<int64_t>(ev) * D.de_pad : nullptr;
     for (int x = lane; x < D.de; x += 32) {
       const float v = has ? ef[x] : 0.0f;
-      row[2 * D.d + D.dt + x] = v;
+      if (row) row[2 * D.d + D.dt + x] = v;
       bf_put(bf.Xg, u, 2 * D.d + D.dt + x, v);
     }
     for (int x = lane; x < D.d; x += 32) {
       const float v = vw.mem[u * D.d + x];
-      row[D.md + x] = v;
+      if (row) row[D.md + x] = v;
       bf_put(bf.Xg, u, D.md + x, v);
     }
     if (lane == 0) bf_put(bf.Xg, u, D.gin, 1.0f);
@@ -156,7 +158,7 @@ __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
     gr[i] = z;
     gr[D.d + i] = r;
     const float rs = r * vw.mem[x];
-    RS[x] = rs;
+    if (RS) RS[x] = rs;
     bf_put(bf.RS, u, i, rs);
     if (i == 0) bf_put(bf.RS, u, D.d, 1.0f);
   }
@@ -198,19 +200,19 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
     if (w < R) {
       const int64_t su = pl.root_sup[w];
       const int64_t node = pl.root_node[w];
-      float* row = Qin + w * ldq;
+      float* row = Qin ? Qin + w * ldq : nullptr;
       for (int x = lane; x < D.d; x += 32) {
         const float v = s_hat[su * D.d + x];
-        row[x] = v;
+        if (row) row[x] = v;
         bf_put(bf.Qin, w, x, v);
       }
       for (int x = lane; x < D.ds; x += 32) {
         const float v = stat[node * D.ds + x];
-        row[D.d + x] = v;
+        if (row) row[D.d + x] = v;
         bf_put(bf.Qin, w, D.d + x, v);
       }
       for (int x = lane; x <= D.dt; x += 32) {
-        if (x < D.dt) row[D.d + D.ds + x] = 1.0f;
+        if (row && x < D.dt) row[D.d + D.ds + x] = 1.0f;
         bf_put(bf.Qin, w, D.d + D.ds + x, 1.0f);  // x == dt: bias column
       }
     } else {
@@ -219,29 +221,31 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
       const int64_t node = pl.pair_node[p];
       const int64_t ev = pl.pair_event[p];
       const double dt = pl.pair_dt[p];
-      float* row = KVin + p * ldkv;
+      float* row = KVin ? KVin + p * ldkv : nullptr;
       for (int x = lane; x < D.d; x += 32) {
         const float v = s_hat[su * D.d + x];
-        row[x] = v;
+        if (row) row[x] = v;
         bf_put(bf.KVin, p, x, v);
       }
       for (int x = lane; x < D.ds; x += 32) {
         const float v = stat[node * D.ds + x];
-        row[D.d + x] = v;
+        if (row) row[D.d + x] = v;
         bf_put(bf.KVin, p, D.d + x, v);
       }
       const float* ef = g.efeat + ev * D.de_pad;
       for (int x = lane; x < D.de; x += 32) {
         const float v = ef[x];
-        row[D.d + D.ds + x] = v;
+        if (row) row[D.d + D.ds + x] = v;
         bf_put(bf.KVin, p, D.d + D.ds + x, v);
       }
       for (int i = lane; i < D.dt; i += 32) {
         const double arg = dt * static_cast<double>(omega[i]);
         const float c = static_cast<float>(cos(arg));
         const float gt = static_cast<float>(-dt * sin(arg));
-        row[D.d + D.ds + D.de + i] = c;
-        Gt[p * D.dt + i] = gt;
+        if (row) {
+          row[D.d + D.ds + D.de + i] = c;
+          Gt[p * D.dt + i] = gt;
+        }
         bf_put(bf.KVin, p, D.d + D.ds + D.de + i, c);
         bf_put(bf.Gt, p, i, gt);
       }
@@ -362,8 +366,10 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
       const float hn = HID[(B + e) * dh + j];
       const float gp = hp > 0.0f ? dpos * W2[j] : 0.0f;
       const float gn = hn > 0.0f ? dneg * W2[j] : 0.0f;
-      Dhid[e * dh + j] = gp;
-      Dhid[(B + e) * dh + j] = gn;
+      if (Dhid) {
+        Dhid[e * dh + j] = gp;
+        Dhid[(B + e) * dh + j] = gn;
+      }
       bf_put(bf.Dhid, e, j, gp);
       bf_put(bf.Dhid, B + e, j, gn);
     }
@@ -371,10 +377,12 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
     const float* hd = H + (3 * e + 1) * da;
     const float* hn = H + (3 * e + 2) * da;
     for (int i = lane; i < da; i += 32) {
-      Hin[e * 2 * da + i] = hs[i];
-      Hin[e * 2 * da + da + i] = hd[i];
-      Hin[(B + e) * 2 * da + i] = hs[i];
-      Hin[(B + e) * 2 * da + da + i] = hn[i];
+      if (Hin) {
+        Hin[e * 2 * da + i] = hs[i];
+        Hin[e * 2 * da + da + i] = hd[i];
+        Hin[(B + e) * 2 * da + i] = hs[i];
+        Hin[(B + e) * 2 * da + da + i] = hn[i];
+      }
       bf_put(bf.Hin, e, i, hs[i]);
       bf_put(bf.Hin, e, da + i, hd[i]);
       bf_put(bf.Hin, B + e, i, hs[i]);
@@ -536,52 +544,67 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
 #pragma unroll
     for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] = 0.0f;
     int run_start = i0;
-    for (int i = i0; i < i1; ++i) {
-      const int v = pl.item_val_s[i];
-      if (v < R) {
+    constexpr int kAhead = 4;  // item rows loaded ahead of the in-order accumulation
+    for (int ib = i0; ib < i1; ib += kAhead) {
+      float ld[kAhead][3 * kMaxDaLanes];
+#pragma unroll
+      for (int a = 0; a < kAhead; ++a) {
+        const int i = ib + a;
+        const int v = i < i1 ? pl.item_val_s[i] : -1;
 #pragma unroll
         for (int cc = 0; cc < kMaxDaLanes; ++cc) {
           const int f = lane + 32 * cc;
-          if (f < da) acc[cc] += dQ[static_cast<int64_t>(v) * da + f];
-        }
-      } else {
-        const float* row = dKV + static_cast<int64_t>(v - R) * 2 * da;
-#pragma unroll
-        for (int cc = 0; cc < kMaxDaLanes; ++cc) {
-          const int f = lane + 32 * cc;
-          if (f < da) {
-            acc[kMaxDaLanes + cc] += row[f];
-            acc[2 * kMaxDaLanes + cc] += row[da + f];
-          }
-        }
-      }
-      const bool run_end = (i + 1 == i1) || pl.item_key_s[i + 1] != pl.item_key_s[i];
-      if (run_end) {
-        const int key = pl.item_key_s[i];
-        float* dst;
-        const bool first = run_start == i0 && cont_in;
-        const bool last = (i + 1 == i1) && cont_out;
-        const bool direct = !first && !last;
-        if (first) dst = part_first + c * w3;
-        else if (last) dst = part_last + c * w3;
-        else dst = dNodeAcc + static_cast<int64_t>(key) * w3;
-#pragma unroll
-        for (int cc = 0; cc < kMaxDaLanes; ++cc) {
-          const int f = lane + 32 * cc;
-          if (f < da) {
-            dst[f] = acc[cc];
-            dst[da + f] = acc[kMaxDaLanes + cc];
-            dst[2 * da + f] = acc[2 * kMaxDaLanes + cc];
-            if (direct) {
-              bf_put(bf.dNA, key, f, acc[cc]);
-              bf_put(bf.dNA, key, da + f, acc[kMaxDaLanes + cc]);
-              bf_put(bf.dNA, key, 2 * da + f, acc[2 * kMaxDaLanes + cc]);
+          float q = 0.0f, k = 0.0f, vv = 0.0f;
+          if (v >= 0 && f < da) {
+            if (v < R) {
+              q = dQ[static_cast<int64_t>(v) * da + f];
+            } else {
+              const float* row = dKV + static_cast<int64_t>(v - R) * 2 * da;
+              k = row[f];
+              vv = row[da + f];
             }
           }
+          ld[a][cc] = q;
+          ld[a][kMaxDaLanes + cc] = k;
+          ld[a][2 * kMaxDaLanes + cc] = vv;
         }
+      }
 #pragma unroll
-        for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] = 0.0f;
-        run_start = i + 1;
+      for (int a = 0; a < kAhead; ++a) {
+        const int i = ib + a;
+        if (i >= i1) break;
+#pragma unroll
+        for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] += ld[a][x];
+        const bool run_end = (i + 1 == i1) || pl.item_key_s[i + 1] != pl.item_key_s[i];
+        if (run_end) {
+          const int key = pl.item_key_s[i];
+          float* dst;
+          const bool first = run_start == i0 && cont_in;
+          const bool last = (i + 1 == i1) && cont_out;
+          const bool direct = !first && !last;
+          if (first) dst = part_first + c * w3;
+          else if (last) dst = part_last + c * w3;
+          else dst = dNodeAcc ? dNodeAcc + static_cast<int64_t>(key) * w3 : nullptr;
+#pragma unroll
+          for (int cc = 0; cc < kMaxDaLanes; ++cc) {
+            const int f = lane + 32 * cc;
+            if (f < da) {
+              if (dst) {
+                dst[f] = acc[cc];
+                dst[da + f] = acc[kMaxDaLanes + cc];
+                dst[2 * da + f] = acc[2 * kMaxDaLanes + cc];
+              }
+              if (direct) {
+                bf_put(bf.dNA, key, f, acc[cc]);
+                bf_put(bf.dNA, key, da + f, acc[kMaxDaLanes + cc]);
+                bf_put(bf.dNA, key, 2 * da + f, acc[2 * kMaxDaLanes + cc]);
+              }
+            }
+          }
+#pragma unroll
+          for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] = 0.0f;
+          run_start = i + 1;
+        }
       }
     }
   }
@@ -602,7 +625,7 @@ __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNode
     for (int f = lane; f < w3; f += 32) {
       float s = part_last[static_cast<int64_t>(c0) * w3 + f];
       for (int c = c0 + 1; c <= c1; ++c) s += part_first[static_cast<int64_t>(c) * w3 + f];
-      dNodeAcc[u * w3 + f] = s;
+      if (dNodeAcc) dNodeAcc[u * w3 + f] = s;
       bf_put(bf.dNA, u, f, s);
     }
   }
@@ -622,12 +645,14 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
     const float* gr = Gates + u * 3 * D.d;
     const float ds = dNode[u * nd + i];
     const float z = gr[i], h = gr[2 * D.d + i], s = vw.mem[x];
-    float* dg = Dg + u * 3 * D.d;
     const float az = has ? ds * (h - s) * z * (1.0f - z) : 0.0f;
     const float ah = has ? ds * z * (1.0f - h * h) : 0.0f;
-    dg[i] = az;
-    dg[D.d + i] = 0.0f;
-    dg[2 * D.d + i] = ah;
+    if (Dg) {
+      float* dg = Dg + u * 3 * D.d;
+      dg[i] = az;
+      dg[D.d + i] = 0.0f;
+      dg[2 * D.d + i] = ah;
+    }
     bf_put(bf.Dg, u, i, az);
     bf_put(bf.Dg, u, 2 * bf.d8d + i, ah);
   }
@@ -651,7 +676,7 @@ __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restr
     const bool has = vw.mail_ev[u] >= 0;
     const float r = Gates[u * 3 * D.d + D.d + i];
     const float ar = has ? T1[x] * vw.mem[x] * r * (1.0f - r) : 0.0f;
-    Dg[u * 3 * D.d + D.d + i] = ar;
+    if (Dg) Dg[u * 3 * D.d + D.d + i] = ar;
     bf_put(bf.Dg, u, bf.d8d + i, ar);
   }
 }
@@ -898,13 +923,24 @@ void add_nn(GemmGroup& gg, int Mcap, const int* M_dev, int N, int K, Operand a, 
 
 Operand ones_op(const float* ones, int K) { return op_dense(ones, 0, 0, K); }
 
+// ~64 CTAs per weight-gradient problem (a group runs 4-5 of them at once) and
+// >= 512 reduction rows per split, which keeps the fp32 partial traffic of the
+// deterministic split-K reduction small next to the MMA work.
 int choose_splits_tma(int M, int N, int64_t Kcap) {
   const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
-  int64_t s = std::min<int64_t>(ceil_div(2 * kSMs, tiles), ceil_div(Kcap, 256));
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 128)));
+  int64_t s = std::min<int64_t>(ceil_div(64, tiles), ceil_div(Kcap, 512));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 64)));
 }
 
 // Forward-style problem: A K-major [M x K] (runtime rows M_dev), B K-major [N x K].
+// Narrow N tiles for the short (supports / roots) problems so the grid fills
+// the 148 SMs; full-width tiles for the pair-level projections.
+int g_wide = 0;  // set around the pair-level projections
+int nn_ntile(int Mcap, int N) {
+  (void)Mcap;
+  return tc_ntile(N, g_wide ? 256 : 64);
+}
+
 void tc_nn(TcGroup& g, int Mcap, const int* M_dev, int N, int K, const BfMat& A, int a_col0,
            const BfMat& B, int b_col0, int b_rows_cap, float* C, int64_t ldc, float beta = 0.0f) {
   TcProblem& P = g.p[g.count++];
@@ -912,7 +948,7 @@ void tc_nn(TcGroup& g, int Mcap, const int* M_dev, int N, int K, const BfMat& A,
   P.M_dev = M_dev;
   P.N = N;
   P.K = K;
-  P.ntile = tc_ntile(N);
+  P.ntile = nn_ntile(Mcap, N);
   P.a = tma_view(A, a_col0, K, A.rows, true, 128);
   P.b = tma_view(B, b_col0, K, b_rows_cap, true, P.ntile);
   P.C = C;
@@ -928,7 +964,7 @@ void tc_nmn(TcGroup& g, int Mcap, const int* M_dev, int N, int K, const BfMat& A
   P.M_dev = M_dev;
   P.N = N;
   P.K = K;
-  P.ntile = tc_ntile(N);
+  P.ntile = nn_ntile(Mcap, N);
   P.a = tma_view(A, a_col0, K, A.rows, true, 128);
   P.b = tma_view(B, b_col0, N, K, false, 64);
   P.C = C;
@@ -1192,8 +1228,8 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   // ---- GRU freshen (K5)
   c.mark(phGruFwd, s);
   if (tma) pack_weights_launch(c, s);
-  assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, vw, g, P + L.off[tOmega], w.Xg,
-                                                             w.ldx, w.GU, bfx, U);
+  assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, vw, g, P + L.off[tOmega],
+                                                             tma ? nullptr : w.Xg, w.ldx, w.GU, bfx, U);
   if (tma) {
     TcGroup tg;
     tc_nn(tg, U, szU, 2 * d, gin + 1, w.bf.Xg, 0, w.bf.Wzr, 0, 2 * d, w.Gates, 3 * d);
@@ -1208,7 +1244,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
     gemm_group_launch(gg, s);
   }
   const int eblocks = 4 * kSMs;
-  gru_mid_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, w.RS, bfx, U);
+  gru_mid_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, tma ? nullptr : w.RS, bfx, U);
   if (tma) {
     TcGroup tg;  // Gh += [r*s | 1] [Wh_s | bh]^T  (the bias rides the ones column)
     tc_nn(tg, U, szU, d, d + 1, w.bf.RS, 0, w.bf.Whs, 0, d, w.Gates + 2 * d, 3 * d, 1.0f);
@@ -1251,14 +1287,16 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   // ---- attention forward (K6)
   c.mark(phAttnAssemble, s);
   assemble_attn_kernel<<<row_blocks(R + Pc), 32 * kWarps, 0, s>>>(
-      D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, w.Qin, w.ldq, w.KVin, w.ldkv, w.Gt, bfx, R,
-      Pc);
+      D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, tma ? nullptr : w.Qin, w.ldq,
+      tma ? nullptr : w.KVin, w.ldkv, w.Gt, bfx, R, Pc);
   c.mark(phAttnProj, s);
   if (tma) {
     TcGroup tg;
     tc_nn(tg, R, szR, da, D.q_in + 1, B.Qin, 0, B.Wq, 0, da, w.Q, da);
+    g_wide = 1;
     tc_nn(tg, Pc, szP, da, D.kv_in + 1, B.KVin, 0, B.Wk, 0, da, w.KV, 2 * da);
     tc_nn(tg, Pc, szP, da, D.kv_in + 1, B.KVin, 0, B.Wv, 0, da, w.KV + da, 2 * da);
+    g_wide = 0;
     tc_group_launch(tg, s);
   } else {
     GemmGroup gg;
@@ -1289,8 +1327,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     gemm_group_launch(gg, s);
   }
   decoder_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(
-      D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, w.Dhid, w.Hin,
-      w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
+      D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, tma ? nullptr : w.Dhid,
+      tma ? nullptr : w.Hin, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
   loss_kernel<<<1, 1024, 0, s>>>(pl, w.loss_terms, loss_out, c.d_numeric_flag);
 
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
@@ -1321,12 +1359,13 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   c.mark(phAttnBwd, s);
   attn_bwd_kernel<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ,
                                                          w.dKV, bfx, R, Pc);
+  if (pl.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));  // routing CSR ready
   const int64_t nchunks = ceil_div(R + Pc, kChunk) + 1;
   float* part_first = wc.take(static_cast<size_t>(nchunks) * 3 * da);
   float* part_last = wc.take(static_cast<size_t>(nchunks) * 3 * da);
-  routing_chunk_kernel<<<row_blocks(nchunks), 32 * kWarps, 0, s>>>(D, pl, w.dQ, w.dKV, w.dNodeAcc,
-                                                                    part_first, part_last, bfx);
-  routing_fixup_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, w.dNodeAcc, part_first,
+  routing_chunk_kernel<<<row_blocks(nchunks), 32 * kWarps, 0, s>>>(
+      D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc, part_first, part_last, bfx);
+  routing_fixup_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, tma ? nullptr : w.dNodeAcc, part_first,
                                                              part_last, bfx);
   c.mark(phAttnBwdGemm, s);
   if (tma) {
@@ -1362,7 +1401,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 
   // ---- GRU backward (K9)
   c.mark(phGruBwd, s);
-  gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, w.Dg, G + L.off[tStatic], bfx, U);
+  gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
+                                          G + L.off[tStatic], bfx, U);
   if (tma) {
     TcGroup tg;
     tc_nmn(tg, U, szU, d, d, B.Dg, 2 * B.d8d, B.Whs, 0, w.T1, d);
@@ -1372,7 +1412,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     add_nn(gg, U, szU, d, d, A_rows(w.Dg + 2 * d, 3 * d, d), B_w(P + L.off[tWh] + md, gin, d), w.T1, d);
     gemm_group_launch(gg, s);
   }
-  gru_bwd2_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.T1, w.Gates, w.Dg, bfx);
+  gru_bwd2_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.T1, w.Gates, tma ? nullptr : w.Dg, bfx);
   if (tma) {
     TcGroup tg;
     tc_tn(tg, wc, d, gin + 1, U, szU, B.Dg, 0, B.Xg, 0, G + L.off[tWz], gin, G + L.off[tBz]);
