@@ -155,13 +155,13 @@ def reference_time(cfg, n_groups, barriers, warmup, log=print):
     return out
 
 
-def reference_arm(args, world, rank):
+def reference_arm(args, world, rank, emit):
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
     from oracle import ref
     if not ref.available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref not built"})
         return 0
     # bound the sample: each reference barrier is several seconds of CPU work
     steps = min(args.steps, args.ref_max_steps)
@@ -179,12 +179,27 @@ def reference_arm(args, world, rank):
                                    f"run_{'training' if world > 1 else 'sequential'} (oracle/_ref)"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
 # ----------------------------------------------------------------- B200 arm
+def _claim_stdout():
+    """Routes fd 1 to stderr (NCCL / library banners) and returns a writer for
+    the single JSON result line on the original stdout."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    out = os.fdopen(saved, "w")
+
+    def emit(obj):
+        out.write(json.dumps(obj) + "\n")
+        out.flush()
+    return emit
+
+
 def main():
+    emit = _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -206,7 +221,7 @@ def main():
         print(f"warning: --gpus {args.gpus} without torchrun; running 1 rank", file=sys.stderr)
 
     if args.impl == "reference":
-        return reference_arm(args, world, rank)
+        return reference_arm(args, world, rank, emit)
 
     import torch
     import torch.distributed as dist
@@ -338,7 +353,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (tcgen05 bf16x3 GEMMs, fp32 accumulate; f64 times)",
             "data": "synthetic (bit-identical gen_synthetic, seed 1)",
             "config": {"workload": cfg["workload"],
                        "parallelism": f"(i,j,k)=(1,1,{world}), one trainer per GPU",
@@ -359,7 +374,7 @@ def main():
             "model_tflops": step_model_flops(sz_mean, cfg) * world / (ms_max / args.steps / 1e3) / 1e12,
             "loss_first_last": [float(losses[0]), float(losses[-1])],
         }
-        print(json.dumps(line))
+        emit(line)
     run.close()
     g.close()
     ctx.close()

@@ -365,8 +365,19 @@ struct tgnn_run {
   int64_t launches = -1;
   PhaseMarks marks;
   bool marks_ready = false;
+  // CUDA-graph mode (j == 1): per-barrier descriptors + a device counter make
+  // every barrier the same graph, captured once and relaunched.
+  bool use_graphs = false;
+  BarrierDesc* d_desc = nullptr;
+  int* d_ctr = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
 
   ~tgnn_run() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (d_desc) cudaFree(d_desc);
+    if (d_ctr) cudaFree(d_ctr);
     if (gcomm) nccl::api().CommDestroy(gcomm);
     if (comm) nccl::api().CommDestroy(comm);
     if (d_losses) cudaFree(d_losses);
@@ -533,8 +544,78 @@ void run_barrier(tgnn_run* r, int64_t b) {
                              r->comm, s));
   const int64_t active = r->sched.active_trainers[static_cast<size_t>(b)];
   sc.mark(phAdam, s);
+  tr->adam_t = b;  // Adam's step counter advances on every rank at every barrier
   tr->adam(c.lr_eff(), 1.0f / static_cast<float>(active > 0 ? active : 1));
   sc.mark(phCount, s);
+}
+
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+// Graph body (j == 1): the same launch sequence for every barrier; all
+// per-barrier values come from d_desc[*d_ctr].
+void barrier_body_dev(tgnn_run* r) {
+  tgnn_ctx* ctx = r->ctx;
+  tgnn_trainer* tr = r->tr.get();
+  cudaStream_t s = ctx->stream;
+  StepCtx sc = tr->sc();
+  sc.d_ctr = r->d_ctr;
+  DPlan& pl = tr->plans[0];
+  DView& vw = tr->views[0];
+  reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, s);
+  select_plan_args_launch(pl.args, r->d_desc, r->d_ctr, s);
+  plan_launch(r->g->d, pl, s, ctx->side);
+  gather_view_launch(pl, r->mem->d, vw, s);
+  substep_gru_launch(sc, pl, vw, s);
+  root_writes_launch(sc, pl, vw, s);
+  const size_t pb = tr->w.wpack_bytes;
+  const int cap = 2 * tr->cap_B;
+  if (r->group_size > 1) {
+    NCCL_CHECK(nccl::api().GroupStart());
+    for (int mm = 0; mm < r->tc.i; ++mm)
+      NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb,
+                                       pb, ncclChar, mm, r->gcomm, s));
+    NCCL_CHECK(nccl::api().GroupEnd());
+    std::vector<WriteSet> sets;
+    for (int mm = 0; mm < r->tc.i; ++mm)
+      sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap, tr->m.d_mem));
+    apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+  } else {
+    apply_writes_launch({pack_view(tr->w.wpack, cap, tr->m.d_mem)}, r->mem->d, r->mem->win, s);
+  }
+  substep_rest_launch(sc, pl, vw, r->d_losses, s);
+  if (r->nranks > 1)
+    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
+                                     r->comm, s));
+  adam_launch(tr->params, tr->grads, tr->am, tr->av, tr->L.total, 0.f, 1.f, 1.f, 1.f, s, r->d_desc, r->d_ctr);
+  incr_launch(r->d_ctr, s);
+}
+
+void build_graph(tgnn_run* r) {
+  cudaStream_t s = r->ctx->stream;
+  gemm_kernels_prepare();
+  TGB_CUDA(cudaStreamSynchronize(s));
+  TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    barrier_body_dev(r);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  TGB_CUDA(cudaStreamEndCapture(s, &r->graph));
+  TGB_CUDA(cudaGraphInstantiate(&r->exec, r->graph, 0));
+  size_t n = 0;
+  TGB_CUDA(cudaGraphGetNodes(r->graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  TGB_CUDA(cudaGraphGetNodes(r->graph, nodes.data(), &n));
+  int64_t kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    TGB_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  r->launches = kernels;
 }
 
 }  // namespace
@@ -1236,6 +1317,36 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
   if (r->group_size > 1) {
     TGB_CUDA(cudaMalloc(&r->gathered, r->tr->w.wpack_bytes * static_cast<size_t>(r->tc.i)));
   }
+  r->use_graphs = opt->use_graphs != 0 && r->tc.j == 1;
+  if (r->use_graphs) {
+    const int64_t nb = std::max<int64_t>(r->sched.barriers, 1);
+    std::vector<BarrierDesc> desc(static_cast<size_t>(nb));
+    for (int64_t b = 0; b < r->sched.barriers; ++b) {
+      const host::Task t = r->sched.task(r->rank, b);
+      BarrierDesc& d = desc[static_cast<size_t>(b)];
+      d.args.begin = t.slice_begin;
+      d.args.end = t.slice_end;
+      d.args.batch_begin = t.batch_begin;
+      d.args.batch_index = t.batch;
+      d.args.group = t.active ? t.neg_group[0] : 0;
+      d.args.seed = r->tc.seed;
+      d.args.neg_mode = 1;
+      d.args.valid = t.active ? 1 : 0;
+      // the group's copy resets before the read of its sweep's first pair; every
+      // member of the group sees the same flag (pair index == barrier at j == 1)
+      const host::Task t0 = r->sched.task(r->group * r->tc.i * r->tc.j, b);
+      d.reset = t0.active && t0.reset_before ? 1 : 0;
+      const int64_t active = r->sched.active_trainers[static_cast<size_t>(b)];
+      d.lr = static_cast<float>(r->tc.lr_eff());
+      d.c1 = static_cast<float>(1.0 - std::pow(0.9, static_cast<double>(b + 1)));
+      d.c2 = static_cast<float>(1.0 - std::pow(0.999, static_cast<double>(b + 1)));
+      d.scale = 1.0f / static_cast<float>(active > 0 ? active : 1);
+    }
+    r->d_desc = dalloc<BarrierDesc>(desc.size());
+    TGB_CUDA(cudaMemcpy(r->d_desc, desc.data(), sizeof(BarrierDesc) * desc.size(), cudaMemcpyHostToDevice));
+    r->d_ctr = dalloc<int>(1);
+    TGB_CUDA(cudaMemset(r->d_ctr, 0, sizeof(int)));
+  }
   *out = r.release();
   API_END
 }
@@ -1277,7 +1388,15 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
   TGB_REQUIRE(first == r->next_barrier, kProtocol, "run: barriers must be issued in order");
   TGB_REQUIRE(first + count <= r->sched.barriers, kConfig, "run: barrier range past the schedule");
   TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
-  for (int64_t b = first; b < first + count; ++b) run_barrier(r, b);
+  if (r->use_graphs && count > 0) {
+    if (!r->exec) build_graph(r);
+    set_int_kernel<<<1, 1, 0, r->ctx->stream>>>(r->d_ctr, static_cast<int>(first));
+    TGB_CUDA(cudaGetLastError());
+    for (int64_t b = first; b < first + count; ++b) TGB_CUDA(cudaGraphLaunch(r->exec, r->ctx->stream));
+    r->tr->adam_t = first + count;
+  } else {
+    for (int64_t b = first; b < first + count; ++b) run_barrier(r, b);
+  }
   r->next_barrier = first + count;
   API_END
 }
@@ -1321,6 +1440,11 @@ int tgnn_run_traversed(tgnn_run* r, int64_t first, int64_t count, int64_t* out) 
 int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out) {
   API_BEGIN
   r->ctx->use();
+  if (r->use_graphs) {
+    if (!r->exec) build_graph(r);
+    *out = r->launches;
+    return 0;
+  }
   TGB_REQUIRE(r->next_barrier < r->sched.barriers, kConfig, "run: no barrier left to inspect");
   TGB_REQUIRE(r->nranks == 1, kConfig, "run: launch counting is done on single-rank runs");
   cudaStream_t s = r->ctx->stream;

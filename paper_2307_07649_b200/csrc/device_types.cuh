@@ -53,6 +53,16 @@ struct PlanArgs {
   int32_t valid = 0;               // 0: empty plan (idle trainer)
 };
 
+// Per-barrier parameters of one rank, resident in HBM so a whole barrier can
+// be captured once as a CUDA graph and replayed: kernels read the entry of the
+// device barrier counter.
+struct BarrierDesc {
+  PlanArgs args;      // this rank's sub-0 plan (valid = 0 when the rank is idle)
+  int32_t reset = 0;  // the group's memory copy resets before this read
+  int32_t pad = 0;
+  float lr = 0, c1 = 1, c2 = 1, scale = 1;  // Adam step (lr_eff, bias corrections, 1/active)
+};
+
 // Per-plan runtime sizes, device-resident.
 enum SizeIdx { kSzB = 0, kSzR = 1, kSzP = 2, kSzU = 3, kSzUm = 4, kSzItems = 5, kSz2B = 6, kSzCount = 8 };
 

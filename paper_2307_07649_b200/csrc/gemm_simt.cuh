@@ -86,5 +86,12 @@ void gemm_group_launch(const GemmGroup& g, cudaStream_t s);
 void gemm_group_launch_simt(const GemmGroup& g, cudaStream_t s);
 void gemm_group_launch_tc(const GemmGroup& g, cudaStream_t s);
 void splitk_reduce_launch(const GemmGroup& g, cudaStream_t s);
+void gemm_tc_prepare();
+void tc_gemm_prepare();
+// One-time kernel attributes (call before any stream capture).
+inline void gemm_kernels_prepare() {
+  gemm_tc_prepare();
+  tc_gemm_prepare();
+}
 
 }  // namespace tgb

@@ -343,14 +343,18 @@ __global__ void __launch_bounds__(TNT2, 1) gemm_tc_kernel(const __grid_constant_
 
 void splitk_reduce_launch(const GemmGroup& g, cudaStream_t s);
 
-void gemm_group_launch_tc(const GemmGroup& g, cudaStream_t s) {
-  if (g.count == 0) return;
+void gemm_tc_prepare() {
   static bool attr_set = false;
   if (!attr_set) {
     TGB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBytes));
     attr_set = true;
   }
+}
+
+void gemm_group_launch_tc(const GemmGroup& g, cudaStream_t s) {
+  if (g.count == 0) return;
+  gemm_tc_prepare();
   TcParams gp{};
   gp.count = g.count;
   int max_tiles = 0;

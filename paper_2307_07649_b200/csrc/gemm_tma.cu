@@ -376,13 +376,17 @@ TmaOp tma_view(const BfMat& m, int64_t col0, int64_t cols, int64_t rows, bool km
   return op;
 }
 
-void tc_group_launch(const TcGroup& g, cudaStream_t s) {
-  if (g.count == 0) return;
+void tc_gemm_prepare() {
   static bool attr = false;
   if (!attr) {
     TGB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
     attr = true;
   }
+}
+
+void tc_group_launch(const TcGroup& g, cudaStream_t s) {
+  if (g.count == 0) return;
+  tc_gemm_prepare();
   TcParams gp;
   std::memset(&gp, 0, sizeof(gp));
   gp.count = g.count;

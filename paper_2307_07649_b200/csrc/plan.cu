@@ -253,6 +253,11 @@ __global__ void gather_view_kernel(DPlan pl, DMem st, DView vw) {
 
 __global__ void set_args_kernel(PlanArgs* dst, PlanArgs a) { *dst = a; }
 
+__global__ void select_args_kernel(const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
+                                   PlanArgs* dst) {
+  *dst = desc[*ctr].args;
+}
+
 __global__ void sample_queries_kernel(DGraph g, const int32_t* __restrict__ nodes,
                                       const double* __restrict__ times, int count, int n,
                                       int32_t* __restrict__ nbr_node, int32_t* __restrict__ nbr_event,
@@ -278,6 +283,11 @@ __global__ void sample_queries_kernel(DGraph g, const int32_t* __restrict__ node
 }
 
 }  // namespace
+
+void select_plan_args_launch(PlanArgs* dst, const BarrierDesc* desc, const int* ctr, cudaStream_t s) {
+  select_args_kernel<<<1, 1, 0, s>>>(desc, ctr, dst);
+  TGB_CUDA(cudaGetLastError());
+}
 
 void set_plan_args_launch(PlanArgs* dst, const PlanArgs& a, cudaStream_t s) {
   set_args_kernel<<<1, 1, 0, s>>>(dst, a);

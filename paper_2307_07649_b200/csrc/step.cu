@@ -409,7 +409,8 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
 
 // bce_loss: mean softplus(-pos) + mean softplus(neg), fixed-order f64 reduction.
 __global__ void __launch_bounds__(1024) loss_kernel(DPlan pl, const double* __restrict__ terms,
-                                                    double* loss_out, int* flag) {
+                                                    double* loss_base, const int* ctr, int* flag) {
+  double* loss_out = loss_base + (ctr ? *ctr : 0);
   __shared__ double sp[1024], sn[1024];
   const int B = pl.sizes[kSzB];
   double a = 0.0, b = 0.0;
@@ -838,10 +839,18 @@ __global__ void fill_kernel(int32_t* p, int64_t n, int32_t v) {
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) p[x] = v;
 }
 
-// Dense Adam, optimizer.hpp:40-56 (fp32 state).
+// Dense Adam, optimizer.hpp:40-56 (fp32 state). With a descriptor table the
+// step scalars come from the entry of the device barrier counter.
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, int64_t n, float lr, float c1, float c2,
-                            float scale) {
+                            float scale, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr) {
+  if (desc) {
+    const BarrierDesc& d = desc[*ctr];
+    lr = d.lr;
+    c1 = d.c1;
+    c2 = d.c2;
+    scale = d.scale;
+  }
   const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     const float gr = g[x] * scale;
@@ -852,6 +861,24 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     p[x] -= lr * (mm / c1) / (sqrtf(vv / c2) + eps);
   }
 }
+
+// reset_state (memory_store.hpp:43-50) when the barrier's descriptor asks for it.
+__global__ void reset_cond_kernel(DMem st, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr) {
+  if (!desc[*ctr].reset) return;
+  const int64_t n = st.N * st.d;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 3 * n; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (x < n) st.memory[x] = 0.0f;
+    else st.mail_mem[x - n] = 0.0f;
+  }
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < st.N; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    st.last_update[x] = 0.0;
+    st.mail_t[x] = 0.0;
+    st.mail_dt[x] = 0.0;
+    st.mail_ev[x] = -1;
+  }
+}
+
+__global__ void incr_kernel(int* ctr) { *ctr += 1; }
 
 template <typename T>
 T* dalloc(size_t n) {
@@ -1329,7 +1356,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   decoder_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(
       D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, tma ? nullptr : w.Dhid,
       tma ? nullptr : w.Hin, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
-  loss_kernel<<<1, 1024, 0, s>>>(pl, w.loss_terms, loss_out, c.d_numeric_flag);
+  loss_kernel<<<1, 1024, 0, s>>>(pl, w.loss_terms, loss_out, c.d_ctr, c.d_numeric_flag);
 
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
   c.mark(phDecoderBwd, s);
@@ -1474,9 +1501,20 @@ void reset_state_launch(DMem& st, cudaStream_t s) {
 }
 
 void adam_launch(float* params, const float* grads, float* m, float* v, int64_t n, float lr,
-                 float c1, float c2, float grad_scale, cudaStream_t s) {
+                 float c1, float c2, float grad_scale, cudaStream_t s, const BarrierDesc* desc,
+                 const int* ctr) {
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
-  adam_kernel<<<blocks, 256, 0, s>>>(params, grads, m, v, n, lr, c1, c2, grad_scale);
+  adam_kernel<<<blocks, 256, 0, s>>>(params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s) {
+  reset_cond_kernel<<<4 * kSMs, 256, 0, s>>>(st, desc, ctr);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void incr_launch(int* ctr, cudaStream_t s) {
+  incr_kernel<<<1, 1, 0, s>>>(ctr);
   TGB_CUDA(cudaGetLastError());
 }
 

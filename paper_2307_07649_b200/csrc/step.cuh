@@ -105,6 +105,7 @@ struct StepCtx {
   StepWork* w = nullptr;
   int* d_numeric_flag = nullptr;  // set when a non-finite value escapes a kernel
   PhaseMarks* marks = nullptr;
+  const int* d_ctr = nullptr;  // graph mode: the loss goes to loss_out[*d_ctr]
   void mark(int slot, cudaStream_t s) const {
     if (marks) marks->mark(slot, s);
   }
@@ -148,6 +149,10 @@ void reset_state_launch(DMem& st, cudaStream_t s);
 // Dense Adam over the flat parameters (optimizer.hpp:40-56). Gradients are
 // scaled by grad_scale first (1 / active trainers after an all-reduce sum).
 void adam_launch(float* params, const float* grads, float* m, float* v, int64_t n, float lr,
-                 float c1, float c2, float grad_scale, cudaStream_t s);
+                 float c1, float c2, float grad_scale, cudaStream_t s,
+                 const BarrierDesc* desc = nullptr, const int* ctr = nullptr);
+// Graph mode helpers: reset the memory copy if desc[*ctr].reset; ++*ctr.
+void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s);
+void incr_launch(int* ctr, cudaStream_t s);
 
 }  // namespace tgb
