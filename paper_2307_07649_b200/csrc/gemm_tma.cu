@@ -243,16 +243,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
       } else if (m < M) {
         float* crow = P.C + static_cast<int64_t>(m) * P.ldc;
+        float prev[16];
+        if (P.beta != 0.0f) {  // all loads first: one latency, not sixteen
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int n = n0 + c0 + q;
+            prev[q] = c0 + q < nvalid ? ((P.C2 && n == N - 1) ? P.C2[m] : crow[n]) : 0.0f;
+          }
+        }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const int n = n0 + c0 + q;
           if (c0 + q >= nvalid) continue;
-          const float x = P.alpha * __uint_as_float(v[q]);
-          if (P.C2 && n == N - 1) {
-            P.C2[m] = P.beta != 0.0f ? x + P.beta * P.C2[m] : x;
-          } else {
-            crow[n] = P.beta != 0.0f ? x + P.beta * crow[n] : x;
-          }
+          float x = P.alpha * __uint_as_float(v[q]);
+          if (P.beta != 0.0f) x += P.beta * prev[q];
+          if (P.C2 && n == N - 1)
+            P.C2[m] = x;
+          else
+            crow[n] = x;
         }
       }
     }

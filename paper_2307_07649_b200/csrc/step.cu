@@ -1095,8 +1095,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
     b.Whm = bf_alloc(d, md);
     b.Whs = bf_alloc(d, d + 1);
     b.Wq = bf_alloc(da, q + 1);
-    b.Wk = bf_alloc(da, kv + 1);
-    b.Wv = bf_alloc(da, kv + 1);
+    b.Wkv = bf_alloc(2 * da, kv + 1);
     b.W1a = bf_alloc(dh, da);
     b.W1b = bf_alloc(dh, da);
     b.W1 = bf_alloc(dh, 2 * da);
@@ -1160,7 +1159,7 @@ void step_free(StepWork& w) {
     if (p) cudaFree(p);
   BfMat* bfs[] = {&w.bf.Xg, &w.bf.GU, &w.bf.RS, &w.bf.Qin, &w.bf.KVin, &w.bf.Gt, &w.bf.H, &w.bf.Hin,
                   &w.bf.Dhid, &w.bf.dQ, &w.bf.dKV, &w.bf.dNA, &w.bf.Dg, &w.bf.Wzr, &w.bf.Whm, &w.bf.Whs,
-                  &w.bf.Wq, &w.bf.Wk, &w.bf.Wv, &w.bf.W1a, &w.bf.W1b, &w.bf.W1, &w.bf.Wst};
+                  &w.bf.Wq, &w.bf.Wkv, &w.bf.W1a, &w.bf.W1b, &w.bf.W1, &w.bf.Wst};
   for (BfMat* b : bfs) bf_free(*b);
   w = StepWork{};
 }
@@ -1221,10 +1220,10 @@ void pack_weights_launch(const StepCtx& c, cudaStream_t s) {
   add(L.off[tBh], 1, d, 1, b.Whs, 0, d);
   add(L.off[tWq], q, da, q, b.Wq, 0, 0);
   add(L.off[tBq], 1, da, 1, b.Wq, 0, q);
-  add(L.off[tWk], kv, da, kv, b.Wk, 0, 0);
-  add(L.off[tBk], 1, da, 1, b.Wk, 0, kv);
-  add(L.off[tWv], kv, da, kv, b.Wv, 0, 0);
-  add(L.off[tBv], 1, da, 1, b.Wv, 0, kv);
+  add(L.off[tWk], kv, da, kv, b.Wkv, 0, 0);
+  add(L.off[tBk], 1, da, 1, b.Wkv, 0, kv);
+  add(L.off[tWv], kv, da, kv, b.Wkv, da, 0);
+  add(L.off[tBv], 1, da, 1, b.Wkv, da, kv);
   add(L.off[tW1], 2 * da, dh, da, b.W1a, 0, 0);
   add(L.off[tW1] + da, 2 * da, dh, da, b.W1b, 0, 0);
   add(L.off[tW1], 2 * da, dh, 2 * da, b.W1, 0, 0);
@@ -1320,9 +1319,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   if (tma) {
     TcGroup tg;
     tc_nn(tg, R, szR, da, D.q_in + 1, B.Qin, 0, B.Wq, 0, da, w.Q, da);
-    g_wide = 1;
-    tc_nn(tg, Pc, szP, da, D.kv_in + 1, B.KVin, 0, B.Wk, 0, da, w.KV, 2 * da);
-    tc_nn(tg, Pc, szP, da, D.kv_in + 1, B.KVin, 0, B.Wv, 0, da, w.KV + da, 2 * da);
+    g_wide = 1;  // K and V in one pass over the pair rows: [Wk | bk ; Wv | bv]
+    tc_nn(tg, Pc, szP, 2 * da, D.kv_in + 1, B.KVin, 0, B.Wkv, 0, 2 * da, w.KV, 2 * da);
     g_wide = 0;
     tc_group_launch(tg, s);
   } else {

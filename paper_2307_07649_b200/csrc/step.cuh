@@ -46,7 +46,7 @@ struct ParamLayout {
 //  dKV [dK | pad | dV], Dg [da_z | pad | da_r | pad | da_h] (blocks 8-aligned).
 struct StepBf {
   BfMat Xg, GU, RS, Qin, KVin, Gt, H, Hin, Dhid, dQ, dKV, dNA, Dg;
-  BfMat Wzr, Whm, Whs, Wq, Wk, Wv, W1a, W1b, W1, Wst;
+  BfMat Wzr, Whm, Whs, Wq, Wkv, W1a, W1b, W1, Wst;  // Wkv = [Wk | bk ; Wv | bv]
   int d8a = 0, d8d = 0;
 };
 
