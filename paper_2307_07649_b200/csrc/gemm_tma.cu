@@ -1,11 +1,13 @@
-// TMA-fed, warp-specialized tcgen05 GEMM (see gemm_tma.cuh).
+// TMA-fed, warp-specialized, persistent tcgen05 GEMM (see gemm_tma.cuh).
 //
 // CTA = 6 warps: warp 0 issues TMA loads (one elected lane), warp 1 owns the
 // TMEM allocation and issues tcgen05.mma (one elected lane), warps 2-5 run the
-// epilogue (warp w reads TMEM lanes 32 (w % 4) .. +32). Two shared-memory
+// epilogue (warp w reads TMEM lanes 32 (w % 4) .. +32). Each CTA walks the
+// flattened tiles of all problems of the group round-robin. Two shared-memory
 // stages of {A_hi, A_lo, B_hi, B_lo} (128 B swizzled, K-major or MN-major per
-// operand) form a full/empty mbarrier ring; a final commit releases the
-// accumulator to the epilogue.
+// operand) form a full/empty mbarrier ring that runs across tile boundaries;
+// two TMEM accumulators (tfull/tempty barriers) let the epilogue of tile t
+// overlap the MMAs of tile t+1.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -31,6 +33,7 @@ constexpr int kSmemMax = kSt * (2 * kATileB + 2 * 256 * kBK * 2) + 1024 + 256;
 struct TcParams {
   TcProblem p[kMaxTc];
   int tiles_m[kMaxTc], tiles_n[kMaxTc];
+  int tile_base[kMaxTc + 1];  // flattened tile index of each problem's first tile
   int count;
   int b_tile_bytes;  // per hi / lo B tile: roundup64(max ntile) * 128
   int stage_bytes;
@@ -104,49 +107,55 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcParams gp) {
-  const int pi = blockIdx.y;
-  if (pi >= gp.count) return;
+// Tile geometry of flattened tile index t (identical in every role).
+struct TileInfo {
+  int pi, m0, n0, split, kbeg, nk, M;
+};
+
+__device__ __forceinline__ bool tile_info(const TcParams& gp, int t, TileInfo& ti) {
+  int pi = 0;
+  while (pi + 1 < gp.count && t >= gp.tile_base[pi + 1]) ++pi;
   const TcProblem& P = gp.p[pi];
+  const int local = t - gp.tile_base[pi];
   const int tm = gp.tiles_m[pi], tn = gp.tiles_n[pi];
-  const int tile = blockIdx.x;
-  if (tile >= tm * tn * P.splits) return;
-  const int split = tile / (tm * tn);
-  const int t2 = tile % (tm * tn);
-  const int m0 = (t2 / tn) * kBM;
-  const int n0 = (t2 % tn) * P.ntile;
-  const int M = P.M_dev ? min(P.M, *P.M_dev) : P.M;
-  if (m0 >= M && P.splits == 1) return;
-  const int N = P.N;
+  ti.pi = pi;
+  ti.split = local / (tm * tn);
+  const int t2 = local % (tm * tn);
+  ti.m0 = (t2 / tn) * kBM;
+  ti.n0 = (t2 % tn) * P.ntile;
+  ti.M = P.M_dev ? min(P.M, *P.M_dev) : P.M;
+  if (ti.m0 >= ti.M && P.splits == 1) return false;  // beyond the runtime rows: no work, no output
   const int Kcap = P.K;
   const int K = P.K_dev ? min(Kcap, *P.K_dev) : Kcap;
   const int kper = ((Kcap + P.splits - 1) / P.splits + kBK - 1) / kBK * kBK;
-  const int kbeg = split * kper;
-  const int kend = min(K, kbeg + kper);
-  const int nk = (kend > kbeg && m0 < M) ? (kend - kbeg + kBK - 1) / kBK : 0;
-  const int ntile = P.ntile;
-  const bool a_k = P.a.kmajor != 0, b_k = P.b.kmajor != 0;
-  const int a_boxes = a_k ? 1 : 2;
-  const int b_boxes = b_k ? 1 : (ntile + 63) / 64;
-  const uint32_t a_bytes = a_k ? static_cast<uint32_t>(P.a.box_rows) * 128u : 8192u * 2u;
-  const uint32_t b_bytes = b_k ? static_cast<uint32_t>(P.b.box_rows) * 128u : 8192u * static_cast<uint32_t>(b_boxes);
-  const uint32_t stage_tx = 2u * (a_bytes + b_bytes);
+  ti.kbeg = ti.split * kper;
+  const int kend = min(K, ti.kbeg + kper);
+  ti.nk = (kend > ti.kbeg && ti.m0 < ti.M) ? (kend - ti.kbeg + kBK - 1) / kBK : 0;
+  return true;
+}
 
+// Persistent CTA: static round-robin over the flattened tiles of the group.
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcParams gp) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int kStageB = gp.stage_bytes, kBTileB = gp.b_tile_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageB);
   uint64_t* empty = full + kSt;
-  uint64_t* accf = empty + kSt;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint64_t* tfull = empty + kSt;   // [2] accumulator ready for the epilogue
+  uint64_t* tempty = tfull + 2;    // [2] accumulator drained by the epilogue
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = gp.tile_base[gp.count];
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSt; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(accf, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -158,111 +167,151 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
+  const int acc_cols = gp.tmem_cols / 2;
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc % kSt;
-        if (kc >= kSt) mbar_wait(empty + s, ((kc / kSt) - 1) & 1);
-        uint8_t* st = smem + s * kStageB;
-        mbar_expect_tx(full + s, stage_tx);
-        const int k0 = kbeg + kc * kBK;
-        for (int h = 0; h < 2; ++h) {
-          const CUtensorMap* am = h ? &P.a.lo : &P.a.hi;
-          const CUtensorMap* bm = h ? &P.b.lo : &P.b.hi;
-          uint8_t* ad = st + h * kATileB;
-          uint8_t* bd = st + 2 * kATileB + h * kBTileB;
-          if (a_k) {
-            tma_2d(ad, am, k0, m0, full + s);
-          } else {
-            for (int j = 0; j < a_boxes; ++j) tma_2d(ad + j * 8192, am, m0 + 64 * j, k0, full + s);
-          }
-          if (b_k) {
-            tma_2d(bd, bm, k0, n0, full + s);
-          } else {
-            for (int j = 0; j < b_boxes; ++j) tma_2d(bd + j * 8192, bm, n0 + 64 * j, k0, full + s);
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        TileInfo ti;
+        if (!tile_info(gp, t, ti)) continue;
+        const TcProblem& P = gp.p[ti.pi];
+        const bool a_k = P.a.kmajor != 0, b_k = P.b.kmajor != 0;
+        const int b_boxes = b_k ? 1 : (P.ntile + 63) / 64;
+        const uint32_t a_bytes = a_k ? static_cast<uint32_t>(P.a.box_rows) * 128u : 8192u * 2u;
+        const uint32_t b_bytes = b_k ? static_cast<uint32_t>(P.b.box_rows) * 128u : 8192u * static_cast<uint32_t>(b_boxes);
+        const uint32_t stage_tx = 2u * (a_bytes + b_bytes);
+        for (int kc = 0; kc < ti.nk; ++kc, ++it) {
+          const uint32_t s = it % kSt;
+          if (it >= kSt) mbar_wait(empty + s, ((it / kSt) - 1) & 1);
+          uint8_t* st = smem + s * kStageB;
+          mbar_expect_tx(full + s, stage_tx);
+          const int k0 = ti.kbeg + kc * kBK;
+          for (int h = 0; h < 2; ++h) {
+            const CUtensorMap* am = h ? &P.a.lo : &P.a.hi;
+            const CUtensorMap* bm = h ? &P.b.lo : &P.b.hi;
+            uint8_t* ad = st + h * kATileB;
+            uint8_t* bd = st + 2 * kATileB + h * kBTileB;
+            if (a_k) {
+              tma_2d(ad, am, k0, ti.m0, full + s);
+            } else {
+              tma_2d(ad, am, ti.m0, k0, full + s);
+              tma_2d(ad + 8192, am, ti.m0 + 64, k0, full + s);
+            }
+            if (b_k) {
+              tma_2d(bd, bm, k0, ti.n0, full + s);
+            } else {
+              for (int j = 0; j < b_boxes; ++j) tma_2d(bd + j * 8192, bm, ti.n0 + 64 * j, k0, full + s);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t id = idesc(ntile, a_k, b_k);
-      for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc % kSt;
-        mbar_wait(full + s, (kc / kSt) & 1);
+      uint32_t it = 0, lt = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        TileInfo ti;
+        if (!tile_info(gp, t, ti)) continue;
+        const TcProblem& P = gp.p[ti.pi];
+        const bool a_k = P.a.kmajor != 0, b_k = P.b.kmajor != 0;
+        const uint32_t acc = lt & 1;
+        if (lt >= 2) mbar_wait(tempty + acc, ((lt >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint8_t* st = smem + s * kStageB;
-        const uint32_t ahi = su32(st), alo = su32(st + kATileB);
-        const uint32_t bhi = su32(st + 2 * kATileB), blo = su32(st + 2 * kATileB + kBTileB);
+        const uint32_t dtm = tmem + acc * static_cast<uint32_t>(acc_cols);
+        const uint32_t id = idesc(P.ntile, a_k, b_k);
+        for (int kc = 0; kc < ti.nk; ++kc, ++it) {
+          const uint32_t s = it % kSt;
+          mbar_wait(full + s, (it / kSt) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          uint8_t* st = smem + s * kStageB;
+          const uint32_t ahi = su32(st), alo = su32(st + kATileB);
+          const uint32_t bhi = su32(st + 2 * kATileB), blo = su32(st + 2 * kATileB + kBTileB);
 #pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks) {
-          const uint32_t aoff = a_k ? ks * 32u : ks * 2048u;
-          const uint32_t boff = b_k ? ks * 32u : ks * 2048u;
-          const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
-          umma(tmem, sdesc(ahi + aoff, a_k), sdesc(bhi + boff, b_k), id, acc);
-          umma(tmem, sdesc(ahi + aoff, a_k), sdesc(blo + boff, b_k), id, 1u);
-          umma(tmem, sdesc(alo + aoff, a_k), sdesc(bhi + boff, b_k), id, 1u);
+          for (int ks = 0; ks < kBK / 16; ++ks) {
+            const uint32_t aoff = a_k ? ks * 32u : ks * 2048u;
+            const uint32_t boff = b_k ? ks * 32u : ks * 2048u;
+            const uint32_t accf = (kc > 0 || ks > 0) ? 1u : 0u;
+            umma(dtm, sdesc(ahi + aoff, a_k), sdesc(bhi + boff, b_k), id, accf);
+            umma(dtm, sdesc(ahi + aoff, a_k), sdesc(blo + boff, b_k), id, 1u);
+            umma(dtm, sdesc(alo + aoff, a_k), sdesc(bhi + boff, b_k), id, 1u);
+          }
+          umma_commit(empty + s);
         }
-        umma_commit(empty + s);
+        if (ti.nk > 0)
+          umma_commit(tfull + acc);
+        else
+          mbar_arrive(tfull + acc);
+        ++lt;
       }
-      if (nk > 0)
-        umma_commit(accf);
-      else
-        mbar_arrive(accf);
     }
   } else {
-    // epilogue warps 2..5
-    mbar_wait(accf, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue warps 2..5: warp w reads TMEM lanes 32 (w % 4) .. + 32
     const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const int m = m0 + row;
-    const int nvalid = min(ntile, N - n0);
-    for (int c0 = 0; c0 < ntile; c0 += 16) {
-      uint32_t v[16];
-      if (nk > 0) {
-        const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-              "=r"(v[14]), "=r"(v[15])
-            : "r"(ta));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      } else {
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      TileInfo ti;
+      if (!tile_info(gp, t, ti)) continue;
+      const TcProblem& P = gp.p[ti.pi];
+      const uint32_t acc = lt & 1;
+      mbar_wait(tfull + acc, (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = quarter * 32 + lane;
+      const int m = ti.m0 + row;
+      const int N = P.N;
+      const int ntile = P.ntile;
+      const int nvalid = min(ntile, N - ti.n0);
+      const int n0 = ti.n0;
+      for (int c0 = 0; c0 < ntile; c0 += 16) {
+        uint32_t v[16];
+        if (ti.nk > 0) {
+          const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * static_cast<uint32_t>(acc_cols) +
+                              static_cast<uint32_t>(c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                "=r"(v[14]), "=r"(v[15])
+              : "r"(ta));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        } else {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = 0u;
-      }
-      if (P.splits > 1) {
-        if (m < P.M) {
-          float* w = P.ws + static_cast<int64_t>(split) * P.M * N + static_cast<int64_t>(m) * N;
-#pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (c0 + q < nvalid) w[n0 + c0 + q] = m < M ? __uint_as_float(v[q]) : 0.0f;
+          for (int q = 0; q < 16; ++q) v[q] = 0u;
         }
-      } else if (m < M) {
-        float* crow = P.C + static_cast<int64_t>(m) * P.ldc;
-        float prev[16];
-        if (P.beta != 0.0f) {  // all loads first: one latency, not sixteen
+        if (P.splits > 1) {
+          if (m < P.M) {
+            float* w = P.ws + static_cast<int64_t>(ti.split) * P.M * N + static_cast<int64_t>(m) * N;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (c0 + q < nvalid) w[n0 + c0 + q] = m < ti.M ? __uint_as_float(v[q]) : 0.0f;
+          }
+        } else if (m < ti.M) {
+          float* crow = P.C + static_cast<int64_t>(m) * P.ldc;
+          float prev[16];
+          if (P.beta != 0.0f) {  // all loads first: one latency, not sixteen
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int n = n0 + c0 + q;
+              prev[q] = c0 + q < nvalid ? ((P.C2 && n == N - 1) ? P.C2[m] : crow[n]) : 0.0f;
+            }
+          }
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int n = n0 + c0 + q;
-            prev[q] = c0 + q < nvalid ? ((P.C2 && n == N - 1) ? P.C2[m] : crow[n]) : 0.0f;
+            if (c0 + q >= nvalid) continue;
+            float x = P.alpha * __uint_as_float(v[q]);
+            if (P.beta != 0.0f) x += P.beta * prev[q];
+            if (P.C2 && n == N - 1)
+              P.C2[m] = x;
+            else
+              crow[n] = x;
           }
         }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int n = n0 + c0 + q;
-          if (c0 + q >= nvalid) continue;
-          float x = P.alpha * __uint_as_float(v[q]);
-          if (P.beta != 0.0f) x += P.beta * prev[q];
-          if (P.C2 && n == N - 1)
-            P.C2[m] = x;
-          else
-            crow[n] = x;
-        }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      ++lt;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -412,13 +461,21 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s) {
     any_split |= g.p[i].splits > 1;
   }
   if (max_tiles == 0) return;
+  gp.tile_base[0] = 0;
+  for (int i = 0; i < g.count; ++i)
+    gp.tile_base[i + 1] = gp.tile_base[i] + gp.tiles_m[i] * gp.tiles_n[i] * g.p[i].splits;
   gp.b_tile_bytes = (max_ntile + 63) / 64 * 64 * 128;
   gp.stage_bytes = 2 * kATileB + 2 * gp.b_tile_bytes;
   int cols = 32;
-  while (cols < max_ntile) cols *= 2;
+  while (cols < 2 * max_ntile) cols *= 2;  // two accumulator stages
   gp.tmem_cols = cols;
   const int smem = kSt * gp.stage_bytes + 1024 + 256;
-  tc_gemm_kernel<<<dim3(max_tiles, g.count), kThreads, smem, s>>>(gp);
+  // one persistent CTA per SM (or fewer when the group has fewer tiles)
+  int ctas_per_sm = (228 * 1024) / (smem + 1024);
+  if (ctas_per_sm < 1) ctas_per_sm = 1;
+  if (ctas_per_sm * cols > 512) ctas_per_sm = 512 / cols;
+  const int grid = std::min(gp.tile_base[g.count], kSMs * ctas_per_sm);
+  tc_gemm_kernel<<<grid, kThreads, smem, s>>>(gp);
   TGB_CUDA(cudaGetLastError());
   if (any_split) {
     tc_splitk_reduce_kernel<<<dim3(64, g.count), 256, 0, s>>>(gp);
