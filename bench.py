@@ -56,6 +56,15 @@ def attn_proj_flops(sz, cfg):
     return 2.0 * (sz["R"] * q_in * da + 2 * sz["P"] * kv_in * da)
 
 
+def attn_proj_bytes(sz, cfg):
+    """Compulsory bytes of that launch in fp32-equivalents: the gathered Q / K|V
+    input rows (Qin [R x q_in], KVin [P x kv_in]) in, Q [R x d_a] and K|V
+    [P x 2 d_a] out. (Weights are L2-resident and excluded.)"""
+    d, ds, de, dt, da = 100, cfg["d_static"], cfg["d_e"], 100, 100
+    q_in, kv_in = d + ds + dt, d + ds + de + dt
+    return 4.0 * (sz["R"] * (q_in + da) + sz["P"] * (kv_in + 2 * da))
+
+
 def step_model_flops(sz, cfg):
     """SURVEY.md 8(d) model FLOPs of one sub-iteration (forward + dW + dX ~ 3x
     forward MACs x 2): KV, Q, GRU and decoder contractions."""
@@ -295,13 +304,22 @@ def main():
     sz_mean = {k: float(np.mean([p[1][k] for p in prof])) for k in prof[0][1]}
     proj_ms = ph_mean["attn_proj"]
     flops = attn_proj_flops(sz_mean, cfg)
+    hbm_bytes = attn_proj_bytes(sz_mean, cfg)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
-    achieved_tf = flops / (proj_ms / 1e3) / 1e12
-    roofline = {"kernel": "attention projection GEMM group (Q + K + V, fp32 SIMT)", "bound": "tensor",
-                "achieved": achieved_tf, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved_tf / peaks["bf16_tflops"], "traffic": None,
-                "flops_per_launch": flops, "launch_ms": proj_ms,
+    src = "MEASURED_PEAKS.json" if "when" in peaks else "B200_PROFILING.md fallback"
+    t_tensor = flops / (peaks["bf16_tflops"] * 1e12)
+    t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
+    secs = proj_ms / 1e3
+    tensor_view = {"achieved": flops / secs / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s"}
+    hbm_view = {"achieved": hbm_bytes / secs / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    bound = "hbm" if t_hbm >= t_tensor else "tensor"
+    main = hbm_view if bound == "hbm" else tensor_view
+    roofline = {"kernel": "attention projection GEMM group (Q, fused K|V; tcgen05 bf16x3, TMA)",
+                "bound": bound, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
+                "frac": main["achieved"] / main["peak"], "traffic": None, "peak_source": src,
+                "flops_per_launch": flops, "algorithmic_bytes_per_launch": hbm_bytes,
+                "launch_ms": proj_ms, "tensor_view": tensor_view, "hbm_view": hbm_view,
                 "share_of_step": proj_ms / max(sum(ph_mean.values()), 1e-9)}
     log("phases (ms): " + ", ".join(f"{k}={v:.3f}" for k, v in ph_mean.items()))
     log(f"plan sizes: {sz_mean}")

@@ -79,6 +79,35 @@ __device__ __forceinline__ void bf_zero_tail(const BfMat& m, int count, int cap,
   }
 }
 
+// Writes one staged row (cols floats in shared memory) of a pre-split operand
+// with 16-byte stores: each lane converts 8 consecutive values to bf16 hi/lo.
+// Columns [cols, roundup8(cols)) receive zeros. f32row (nullable) gets the
+// fp32 copy used by the fp32-operand GEMM engines.
+__device__ __forceinline__ void warp_store_row(const BfMat& m, int64_t r, const float* buf, int cols,
+                                               float* f32row, int f32cols) {
+  const int lane = threadIdx.x & 31;
+  if (f32row)
+    for (int x = lane; x < f32cols; x += 32) f32row[x] = buf[x];
+  if (m.hi == nullptr) return;
+  const int chunks = (cols + 7) / 8;
+  for (int c = lane; c < chunks; c += 32) {
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int x0 = c * 8 + 2 * q;
+      const float v0 = x0 < cols ? buf[x0] : 0.0f;
+      const float v1 = x0 + 1 < cols ? buf[x0 + 1] : 0.0f;
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(v0), h1 = __float2bfloat16_rn(v1);
+      const __nv_bfloat16 l0 = __float2bfloat16_rn(v0 - __bfloat162float(h0));
+      const __nv_bfloat16 l1 = __float2bfloat16_rn(v1 - __bfloat162float(h1));
+      h[q] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+      l[q] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+    }
+    *reinterpret_cast<uint4*>(m.hi + r * m.ld + c * 8) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(m.lo + r * m.ld + c * 8) = make_uint4(l[0], l[1], l[2], l[3]);
+  }
+}
+
 struct Dims {  // flattened for kernels
   int d, dt, ds, de, de_pad, da, dh, md, gin, q_in, kv_in;
 };
@@ -100,46 +129,39 @@ Dims make_dims(const ModelDims& m, const DGraph& g) {
 }
 
 // ---------------------------------------------------------------- forward
-// GRU input rows {mail_mem | cos(dt w) | e(mail event) | s} (make_mail,
-// model.hpp:153-166) and GU = -dt sin(dt w) (time_encode_backward factor).
+// GRU input rows {mail_mem | cos(dt w) | e(mail event) | s | 1} (make_mail,
+// model.hpp:153-166) and GU = -dt sin(dt w) (time_encode_backward factor),
+// staged per warp in shared memory and written with 16-byte stores.
 __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const float* __restrict__ omega,
                                     float* __restrict__ Xg, int64_t ldx, float* __restrict__ GU, StepBf bf,
-                                    int cap_U) {
+                                    int cap_U, int stage) {
+  extern __shared__ float sbuf[];
   const int U = pl.sizes[kSzU];
   const int lane = threadIdx.x & 31;
+  float* row = sbuf + (threadIdx.x >> 5) * stage;
+  float* gu = row + D.gin + 1;
   for (int64_t u = gwarp(); u < U; u += nwarp()) {
     const int32_t ev = vw.mail_ev[u];
     const bool has = ev >= 0;
     const double dt = vw.mail_dt[u];
-    float* row = Xg ? Xg + u * ldx : nullptr;  // fp32 copy only for the fp32-operand engines
-    for (int x = lane; x < 2 * D.d; x += 32) {
-      const float v = vw.mail_mem[u * 2 * D.d + x];
-      if (row) row[x] = v;
-      bf_put(bf.Xg, u, x, v);
-    }
+    for (int x = lane; x < 2 * D.d; x += 32) row[x] = vw.mail_mem[u * 2 * D.d + x];
     for (int i = lane; i < D.dt; i += 32) {
       const double arg = dt * static_cast<double>(omega[i]);
-      const float c = static_cast<float>(cos(arg));
-      const float gu = has ? static_cast<float>(-dt * sin(arg)) : 0.0f;
-      if (row) {
-        row[2 * D.d + i] = c;
-        GU[u * D.dt + i] = gu;
-      }
-      bf_put(bf.Xg, u, 2 * D.d + i, c);
-      bf_put(bf.GU, u, i, gu);
+      row[2 * D.d + i] = static_cast<float>(cos(arg));
+      gu[i] = has ? static_cast<float>(-dt * sin(arg)) : 0.0f;
     }
     const float* ef = has ? g.efeat + static_cast<int64_t>(ev) * D.de_pad : nullptr;
-    for (int x = lane; x < D.de; x += 32) {
-      const float v = has ? ef[x] : 0.0f;
-      if (row) row[2 * D.d + D.dt + x] = v;
-      bf_put(bf.Xg, u, 2 * D.d + D.dt + x, v);
+    for (int x = lane; x < D.de; x += 32) row[2 * D.d + D.dt + x] = has ? ef[x] : 0.0f;
+    for (int x = lane; x < D.d; x += 32) row[D.md + x] = vw.mem[u * D.d + x];
+    if (lane == 0) row[D.gin] = 1.0f;
+    __syncwarp();
+    warp_store_row(bf.Xg, u, row, D.gin + 1, nullptr, 0);
+    warp_store_row(bf.GU, u, gu, D.dt, nullptr, 0);
+    if (Xg) {
+      for (int x = lane; x < D.gin; x += 32) Xg[u * ldx + x] = row[x];
+      for (int i = lane; i < D.dt; i += 32) GU[u * D.dt + i] = gu[i];
     }
-    for (int x = lane; x < D.d; x += 32) {
-      const float v = vw.mem[u * D.d + x];
-      if (row) row[D.md + x] = v;
-      bf_put(bf.Xg, u, D.md + x, v);
-    }
-    if (lane == 0) bf_put(bf.Xg, u, D.gin, 1.0f);
+    __syncwarp();
   }
   bf_zero_tail(bf.Xg, U, cap_U, D.gin + 1);
   bf_zero_tail(bf.GU, U, cap_U, D.dt);
@@ -187,70 +209,49 @@ __global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
   }
 }
 
-// Attention inputs: Qin = {s_hat | static | cos(0 w) = 1} per root, KVin =
-// {s_hat | static | e | cos(dt w)} per pair (embed_root, trainer.hpp:128-159),
-// Gt = -dt sin(dt w) per pair.
+// Attention inputs: Qin = {s_hat | static | cos(0 w) = 1 | 1} per root, KVin =
+// {s_hat | static | e | cos(dt w) | 1} per pair (embed_root, trainer.hpp:128-159),
+// Gt = -dt sin(dt w) per pair; staged per warp, written with 16-byte stores.
 __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __restrict__ omega,
                                      const float* __restrict__ stat, const float* __restrict__ s_hat,
                                      float* __restrict__ Qin, int64_t ldq, float* __restrict__ KVin,
-                                     int64_t ldkv, float* __restrict__ Gt, StepBf bf, int cap_R, int cap_P) {
+                                     int64_t ldkv, float* __restrict__ Gt, StepBf bf, int cap_R, int cap_P,
+                                     int stage) {
+  extern __shared__ float sbuf[];
   const int R = pl.sizes[kSzR], P = pl.sizes[kSzP];
   const int lane = threadIdx.x & 31;
+  float* row = sbuf + (threadIdx.x >> 5) * stage;
+  float* gt = row + D.kv_in + 1;
   for (int64_t w = gwarp(); w < R + P; w += nwarp()) {
     if (w < R) {
       const int64_t su = pl.root_sup[w];
       const int64_t node = pl.root_node[w];
-      float* row = Qin ? Qin + w * ldq : nullptr;
-      for (int x = lane; x < D.d; x += 32) {
-        const float v = s_hat[su * D.d + x];
-        if (row) row[x] = v;
-        bf_put(bf.Qin, w, x, v);
-      }
-      for (int x = lane; x < D.ds; x += 32) {
-        const float v = stat[node * D.ds + x];
-        if (row) row[D.d + x] = v;
-        bf_put(bf.Qin, w, D.d + x, v);
-      }
-      for (int x = lane; x <= D.dt; x += 32) {
-        if (row && x < D.dt) row[D.d + D.ds + x] = 1.0f;
-        bf_put(bf.Qin, w, D.d + D.ds + x, 1.0f);  // x == dt: bias column
-      }
+      for (int x = lane; x < D.d; x += 32) row[x] = s_hat[su * D.d + x];
+      for (int x = lane; x < D.ds; x += 32) row[D.d + x] = stat[node * D.ds + x];
+      for (int x = lane; x <= D.dt; x += 32) row[D.d + D.ds + x] = 1.0f;  // cos(0 w) and the bias column
+      __syncwarp();
+      warp_store_row(bf.Qin, w, row, D.q_in + 1, Qin ? Qin + w * ldq : nullptr, D.q_in);
     } else {
       const int64_t p = w - R;
       const int64_t su = pl.pair_sup[p];
       const int64_t node = pl.pair_node[p];
       const int64_t ev = pl.pair_event[p];
       const double dt = pl.pair_dt[p];
-      float* row = KVin ? KVin + p * ldkv : nullptr;
-      for (int x = lane; x < D.d; x += 32) {
-        const float v = s_hat[su * D.d + x];
-        if (row) row[x] = v;
-        bf_put(bf.KVin, p, x, v);
-      }
-      for (int x = lane; x < D.ds; x += 32) {
-        const float v = stat[node * D.ds + x];
-        if (row) row[D.d + x] = v;
-        bf_put(bf.KVin, p, D.d + x, v);
-      }
+      for (int x = lane; x < D.d; x += 32) row[x] = s_hat[su * D.d + x];
+      for (int x = lane; x < D.ds; x += 32) row[D.d + x] = stat[node * D.ds + x];
       const float* ef = g.efeat + ev * D.de_pad;
-      for (int x = lane; x < D.de; x += 32) {
-        const float v = ef[x];
-        if (row) row[D.d + D.ds + x] = v;
-        bf_put(bf.KVin, p, D.d + D.ds + x, v);
-      }
+      for (int x = lane; x < D.de; x += 32) row[D.d + D.ds + x] = ef[x];
       for (int i = lane; i < D.dt; i += 32) {
         const double arg = dt * static_cast<double>(omega[i]);
-        const float c = static_cast<float>(cos(arg));
-        const float gt = static_cast<float>(-dt * sin(arg));
-        if (row) {
-          row[D.d + D.ds + D.de + i] = c;
-          Gt[p * D.dt + i] = gt;
-        }
-        bf_put(bf.KVin, p, D.d + D.ds + D.de + i, c);
-        bf_put(bf.Gt, p, i, gt);
+        row[D.d + D.ds + D.de + i] = static_cast<float>(cos(arg));
+        gt[i] = static_cast<float>(-dt * sin(arg));
       }
-      if (lane == 0) bf_put(bf.KVin, p, D.kv_in, 1.0f);
+      if (lane == 0) row[D.kv_in] = 1.0f;
+      __syncwarp();
+      warp_store_row(bf.KVin, p, row, D.kv_in + 1, KVin ? KVin + p * ldkv : nullptr, D.kv_in);
+      warp_store_row(bf.Gt, p, gt, D.dt, Gt && KVin ? Gt + p * D.dt : nullptr, D.dt);
     }
+    __syncwarp();
   }
   bf_zero_tail(bf.Qin, R, cap_R, D.q_in + 1);
   bf_zero_tail(bf.KVin, P, cap_P, D.kv_in + 1);
@@ -1254,8 +1255,11 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   // ---- GRU freshen (K5)
   c.mark(phGruFwd, s);
   if (tma) pack_weights_launch(c, s);
-  assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, vw, g, P + L.off[tOmega],
-                                                             tma ? nullptr : w.Xg, w.ldx, w.GU, bfx, U);
+  {
+    const int stage = (D.gin + 1 + D.dt + 7) / 8 * 8;
+    assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, sizeof(float) * stage * kWarps, s>>>(
+        D, pl, vw, g, P + L.off[tOmega], tma ? nullptr : w.Xg, w.ldx, w.GU, bfx, U, stage);
+  }
   if (tma) {
     TcGroup tg;
     tc_nn(tg, U, szU, 2 * d, gin + 1, w.bf.Xg, 0, w.bf.Wzr, 0, 2 * d, w.Gates, 3 * d);
@@ -1312,9 +1316,12 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 
   // ---- attention forward (K6)
   c.mark(phAttnAssemble, s);
-  assemble_attn_kernel<<<row_blocks(R + Pc), 32 * kWarps, 0, s>>>(
-      D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, tma ? nullptr : w.Qin, w.ldq,
-      tma ? nullptr : w.KVin, w.ldkv, w.Gt, bfx, R, Pc);
+  {
+    const int stage = (std::max(D.kv_in, D.q_in) + 1 + D.dt + 7) / 8 * 8;
+    assemble_attn_kernel<<<row_blocks(R + Pc), 32 * kWarps, sizeof(float) * stage * kWarps, s>>>(
+        D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, tma ? nullptr : w.Qin, w.ldq,
+        tma ? nullptr : w.KVin, w.ldkv, w.Gt, bfx, R, Pc, stage);
+  }
   c.mark(phAttnProj, s);
   if (tma) {
     TcGroup tg;
