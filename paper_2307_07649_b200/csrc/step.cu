@@ -146,9 +146,12 @@ __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const 
     const double dt = vw.mail_dt[u];
     for (int x = lane; x < 2 * D.d; x += 32) row[x] = vw.mail_mem[u * 2 * D.d + x];
     for (int i = lane; i < D.dt; i += 32) {
-      const double arg = dt * static_cast<double>(omega[i]);
-      row[2 * D.d + i] = static_cast<float>(cos(arg));
-      gu[i] = has ? static_cast<float>(-dt * sin(arg)) : 0.0f;
+      // product in f64 (dt is an f64 time delta), cos/sin in f32: |arg| = O(1)
+      const float arg = static_cast<float>(dt * static_cast<double>(omega[i]));
+      float sn, cs;
+      sincosf(arg, &sn, &cs);
+      row[2 * D.d + i] = cs;
+      gu[i] = has ? static_cast<float>(-dt) * sn : 0.0f;
     }
     const float* ef = has ? g.efeat + static_cast<int64_t>(ev) * D.de_pad : nullptr;
     for (int x = lane; x < D.de; x += 32) row[2 * D.d + D.dt + x] = has ? ef[x] : 0.0f;
@@ -242,9 +245,11 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
       const float* ef = g.efeat + ev * D.de_pad;
       for (int x = lane; x < D.de; x += 32) row[D.d + D.ds + x] = ef[x];
       for (int i = lane; i < D.dt; i += 32) {
-        const double arg = dt * static_cast<double>(omega[i]);
-        row[D.d + D.ds + D.de + i] = static_cast<float>(cos(arg));
-        gt[i] = static_cast<float>(-dt * sin(arg));
+        const float arg = static_cast<float>(dt * static_cast<double>(omega[i]));
+        float sn, cs;
+        sincosf(arg, &sn, &cs);
+        row[D.d + D.ds + D.de + i] = cs;
+        gt[i] = static_cast<float>(-dt) * sn;
       }
       if (lane == 0) row[D.kv_in] = 1.0f;
       __syncwarp();
@@ -259,9 +264,13 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
 }
 
 constexpr int kMaxDaLanes = 8;  // d_attn <= 256
+constexpr int kNbGroup = 4;     // neighbour rows loaded ahead of their use
 
 // attention_forward (attention.hpp:36-91): scores q.K / sqrt(n), stable
-// softmax, h = sum a V; n = 0 gives h = 0. One warp per root.
+// softmax, h = sum a V; n = 0 gives h = 0. One warp per root; LANES = ceil(d_a
+// / 32) features per lane; neighbour rows are fetched kNbGroup at a time so
+// their L2 latencies overlap.
+template <int LANES>
 __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
                                 const float* __restrict__ KV, float* __restrict__ attn_a,
                                 float* __restrict__ H, int* flag, StepBf bf) {
@@ -279,44 +288,64 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
       continue;
     }
     const int p0 = pl.pair_ptr[r];
-    float q[kMaxDaLanes];
+    float q[LANES];
 #pragma unroll
-    for (int c = 0; c < kMaxDaLanes; ++c) {
+    for (int c = 0; c < LANES; ++c) {
       const int i = lane + 32 * c;
       q[c] = i < da ? Q[r * da + i] : 0.0f;
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(n));
     float my_score = -INFINITY;
-    for (int m = 0; m < n; ++m) {
-      const float* K = KV + static_cast<int64_t>(p0 + m) * 2 * da;
-      float acc = 0.0f;
+    for (int m0 = 0; m0 < n; m0 += kNbGroup) {
+      float kr[kNbGroup][LANES];
 #pragma unroll
-      for (int c = 0; c < kMaxDaLanes; ++c) {
-        const int i = lane + 32 * c;
-        if (i < da) acc = fmaf(q[c], K[i], acc);
+      for (int g = 0; g < kNbGroup; ++g) {
+        const float* K = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da;
+#pragma unroll
+        for (int c = 0; c < LANES; ++c) {
+          const int i = lane + 32 * c;
+          kr[g][c] = (m0 + g < n && i < da) ? K[i] : 0.0f;
+        }
       }
-      acc = warp_sum(acc) * scale;
-      if (lane == m) my_score = acc;
+#pragma unroll
+      for (int g = 0; g < kNbGroup; ++g) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < LANES; ++c) acc = fmaf(q[c], kr[g][c], acc);
+        acc = warp_sum(acc) * scale;
+        if (lane == m0 + g && m0 + g < n) my_score = acc;
+      }
     }
     const float mx = warp_max(my_score);
     const float ex = lane < n ? expf(my_score - mx) : 0.0f;
     const float denom = warp_sum(ex);
     const float a = ex / denom;
     if (lane < n) attn_a[p0 + lane] = a;
-    float hv[kMaxDaLanes];
+    float hv[LANES];
 #pragma unroll
-    for (int c = 0; c < kMaxDaLanes; ++c) hv[c] = 0.0f;
-    for (int m = 0; m < n; ++m) {
-      const float am = __shfl_sync(0xffffffffu, a, m);
-      const float* V = KV + static_cast<int64_t>(p0 + m) * 2 * da + da;
+    for (int c = 0; c < LANES; ++c) hv[c] = 0.0f;
+    for (int m0 = 0; m0 < n; m0 += kNbGroup) {
+      float vr[kNbGroup][LANES];
 #pragma unroll
-      for (int c = 0; c < kMaxDaLanes; ++c) {
-        const int i = lane + 32 * c;
-        if (i < da) hv[c] = fmaf(am, V[i], hv[c]);
+      for (int g = 0; g < kNbGroup; ++g) {
+        const float* V = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da + da;
+#pragma unroll
+        for (int c = 0; c < LANES; ++c) {
+          const int i = lane + 32 * c;
+          vr[g][c] = (m0 + g < n && i < da) ? V[i] : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kNbGroup; ++g) {
+        const float am = __shfl_sync(0xffffffffu, a, (m0 + g) & 31);
+        if (m0 + g < n) {
+#pragma unroll
+          for (int c = 0; c < LANES; ++c) hv[c] = fmaf(am, vr[g][c], hv[c]);
+        }
       }
     }
 #pragma unroll
-    for (int c = 0; c < kMaxDaLanes; ++c) {
+    for (int c = 0; c < LANES; ++c) {
       const int i = lane + 32 * c;
       if (i < da) {
         h[i] = hv[c];
@@ -438,6 +467,7 @@ __global__ void __launch_bounds__(1024) loss_kernel(DPlan pl, const double* __re
 
 // attention_backward (attention.hpp:96-140), one warp per root. dh comes from
 // the decoder input gradient: the source root gets both pairs' halves.
+template <int LANES>
 __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
                                 const float* __restrict__ Q, const float* __restrict__ KV,
                                 const float* __restrict__ attn_a, float* __restrict__ dQ,
@@ -449,9 +479,9 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
   for (int64_t r = gwarp(); r < R; r += nwarp()) {
     const int64_t e = r / 3;
     const int side = static_cast<int>(r % 3);
-    float dh[kMaxDaLanes];
+    float dh[LANES];
 #pragma unroll
-    for (int c = 0; c < kMaxDaLanes; ++c) {
+    for (int c = 0; c < LANES; ++c) {
       const int i = lane + 32 * c;
       float v = 0.0f;
       if (i < da) {
@@ -473,47 +503,70 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
     const float scale = 1.0f / sqrtf(static_cast<float>(n));
     const float a_l = lane < n ? attn_a[p0 + lane] : 0.0f;
     float da_l = 0.0f;
-    for (int m = 0; m < n; ++m) {
-      const float* V = KV + static_cast<int64_t>(p0 + m) * 2 * da + da;
-      float acc = 0.0f;
+    for (int m0 = 0; m0 < n; m0 += kNbGroup) {
+      float vr[kNbGroup][LANES];
 #pragma unroll
-      for (int c = 0; c < kMaxDaLanes; ++c) {
-        const int i = lane + 32 * c;
-        if (i < da) acc = fmaf(dh[c], V[i], acc);
+      for (int g = 0; g < kNbGroup; ++g) {
+        const float* V = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da + da;
+#pragma unroll
+        for (int c = 0; c < LANES; ++c) {
+          const int i = lane + 32 * c;
+          vr[g][c] = (m0 + g < n && i < da) ? V[i] : 0.0f;
+        }
       }
-      acc = warp_sum(acc);
-      if (lane == m) da_l = acc;
+#pragma unroll
+      for (int g = 0; g < kNbGroup; ++g) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < LANES; ++c) acc = fmaf(dh[c], vr[g][c], acc);
+        acc = warp_sum(acc);
+        if (lane == m0 + g) da_l = acc;
+      }
     }
     const float mixed = warp_sum(a_l * da_l);
     const float g_l = a_l * (da_l - mixed) * scale;
-    float q[kMaxDaLanes], dq[kMaxDaLanes];
+    float q[LANES], dq[LANES];
 #pragma unroll
-    for (int c = 0; c < kMaxDaLanes; ++c) {
+    for (int c = 0; c < LANES; ++c) {
       const int i = lane + 32 * c;
       q[c] = i < da ? Q[r * da + i] : 0.0f;
       dq[c] = 0.0f;
     }
-    for (int m = 0; m < n; ++m) {
-      const float am = __shfl_sync(0xffffffffu, a_l, m);
-      const float gm = __shfl_sync(0xffffffffu, g_l, m);
-      const int64_t p = p0 + m;
-      const float* K = KV + p * 2 * da;
-      float* out = dKV + p * 2 * da;
+    for (int m0 = 0; m0 < n; m0 += kNbGroup) {
+      float kr[kNbGroup][LANES];
 #pragma unroll
-      for (int c = 0; c < kMaxDaLanes; ++c) {
-        const int i = lane + 32 * c;
-        if (i < da) {
-          dq[c] = fmaf(gm, K[i], dq[c]);
-          const float dk = gm * q[c], dv = am * dh[c];
-          out[i] = dk;
-          out[da + i] = dv;
-          bf_put(bf.dKV, p, i, dk);
-          bf_put(bf.dKV, p, bf.d8a + i, dv);
+      for (int g = 0; g < kNbGroup; ++g) {
+        const float* K = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da;
+#pragma unroll
+        for (int c = 0; c < LANES; ++c) {
+          const int i = lane + 32 * c;
+          kr[g][c] = (m0 + g < n && i < da) ? K[i] : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kNbGroup; ++g) {
+        const int m = m0 + g;
+        const float am = __shfl_sync(0xffffffffu, a_l, m & 31);
+        const float gm = __shfl_sync(0xffffffffu, g_l, m & 31);
+        if (m >= n) continue;
+        const int64_t p = p0 + m;
+        float* out = dKV + p * 2 * da;
+#pragma unroll
+        for (int c = 0; c < LANES; ++c) {
+          const int i = lane + 32 * c;
+          if (i < da) {
+            dq[c] = fmaf(gm, kr[g][c], dq[c]);
+            const float dk = gm * q[c], dv = am * dh[c];
+            out[i] = dk;
+            out[da + i] = dv;
+            bf_put(bf.dKV, p, i, dk);
+            bf_put(bf.dKV, p, bf.d8a + i, dv);
+          }
         }
       }
     }
 #pragma unroll
-    for (int c = 0; c < kMaxDaLanes; ++c) {
+    for (int c = 0; c < LANES; ++c) {
       const int i = lane + 32 * c;
       if (i < da) {
         dQ[r * da + i] = dq[c];
@@ -527,7 +580,9 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
 
 // Routing pass 1: fixed chunks of kChunk sorted items; runs fully inside a
 // chunk are written directly, runs that cross a chunk edge leave partials.
-// Row layout of dNodeAcc: {sum dq | sum dK | sum dV} (3 d_attn).
+// Row layout of dNodeAcc: {sum dq | sum dK | sum dV} (3 d_attn). Item rows are
+// fetched kAhead at a time, then accumulated strictly in item order.
+template <int LANES>
 __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__ dQ,
                                      const float* __restrict__ dKV, float* __restrict__ dNodeAcc,
                                      float* __restrict__ part_first, float* __restrict__ part_last,
@@ -537,24 +592,24 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
   const int nchunks = (items + kChunk - 1) / kChunk;
   const int lane = threadIdx.x & 31;
   const int da = D.da, w3 = 3 * D.da;
+  constexpr int kAhead = 8;
   for (int64_t c = gwarp(); c < nchunks; c += nwarp()) {
     const int i0 = static_cast<int>(c) * kChunk;
     const int i1 = min(items, i0 + kChunk);
     const bool cont_in = i0 > 0 && pl.item_key_s[i0 - 1] == pl.item_key_s[i0];
     const bool cont_out = i1 < items && pl.item_key_s[i1] == pl.item_key_s[i1 - 1];
-    float acc[3 * kMaxDaLanes];
+    float acc[3 * LANES];
 #pragma unroll
-    for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] = 0.0f;
+    for (int x = 0; x < 3 * LANES; ++x) acc[x] = 0.0f;
     int run_start = i0;
-    constexpr int kAhead = 4;  // item rows loaded ahead of the in-order accumulation
     for (int ib = i0; ib < i1; ib += kAhead) {
-      float ld[kAhead][3 * kMaxDaLanes];
+      float ld[kAhead][3 * LANES];
 #pragma unroll
       for (int a = 0; a < kAhead; ++a) {
         const int i = ib + a;
         const int v = i < i1 ? pl.item_val_s[i] : -1;
 #pragma unroll
-        for (int cc = 0; cc < kMaxDaLanes; ++cc) {
+        for (int cc = 0; cc < LANES; ++cc) {
           const int f = lane + 32 * cc;
           float q = 0.0f, k = 0.0f, vv = 0.0f;
           if (v >= 0 && f < da) {
@@ -567,8 +622,8 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
             }
           }
           ld[a][cc] = q;
-          ld[a][kMaxDaLanes + cc] = k;
-          ld[a][2 * kMaxDaLanes + cc] = vv;
+          ld[a][LANES + cc] = k;
+          ld[a][2 * LANES + cc] = vv;
         }
       }
 #pragma unroll
@@ -576,7 +631,7 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
         const int i = ib + a;
         if (i >= i1) break;
 #pragma unroll
-        for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] += ld[a][x];
+        for (int x = 0; x < 3 * LANES; ++x) acc[x] += ld[a][x];
         const bool run_end = (i + 1 == i1) || pl.item_key_s[i + 1] != pl.item_key_s[i];
         if (run_end) {
           const int key = pl.item_key_s[i];
@@ -588,23 +643,23 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
           else if (last) dst = part_last + c * w3;
           else dst = dNodeAcc ? dNodeAcc + static_cast<int64_t>(key) * w3 : nullptr;
 #pragma unroll
-          for (int cc = 0; cc < kMaxDaLanes; ++cc) {
+          for (int cc = 0; cc < LANES; ++cc) {
             const int f = lane + 32 * cc;
             if (f < da) {
               if (dst) {
                 dst[f] = acc[cc];
-                dst[da + f] = acc[kMaxDaLanes + cc];
-                dst[2 * da + f] = acc[2 * kMaxDaLanes + cc];
+                dst[da + f] = acc[LANES + cc];
+                dst[2 * da + f] = acc[2 * LANES + cc];
               }
               if (direct) {
                 bf_put(bf.dNA, key, f, acc[cc]);
-                bf_put(bf.dNA, key, da + f, acc[kMaxDaLanes + cc]);
-                bf_put(bf.dNA, key, 2 * da + f, acc[2 * kMaxDaLanes + cc]);
+                bf_put(bf.dNA, key, da + f, acc[LANES + cc]);
+                bf_put(bf.dNA, key, 2 * da + f, acc[2 * LANES + cc]);
               }
             }
           }
 #pragma unroll
-          for (int x = 0; x < 3 * kMaxDaLanes; ++x) acc[x] = 0.0f;
+          for (int x = 0; x < 3 * LANES; ++x) acc[x] = 0.0f;
           run_start = i + 1;
         }
       }
@@ -612,22 +667,29 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
   }
 }
 
-// Routing pass 2: supports whose item run spans chunks sum their partials in
-// chunk order.
+// Routing pass 2: a support whose item run spans chunks (a hub) sums its
+// partials in chunk order. One block per support, one thread per feature.
 __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNodeAcc,
                                      const float* __restrict__ part_first,
                                      const float* __restrict__ part_last, StepBf bf) {
   const int U = pl.sizes[kSzU];
-  const int lane = threadIdx.x & 31;
   const int w3 = 3 * D.da;
-  for (int64_t u = gwarp(); u < U; u += nwarp()) {
+  for (int u = blockIdx.x; u < U; u += gridDim.x) {
     const int b = pl.sup_item_ptr[u], e = pl.sup_item_ptr[u + 1];
     const int c0 = b / kChunk, c1 = (e - 1) / kChunk;
     if (c0 == c1) continue;
-    for (int f = lane; f < w3; f += 32) {
+    for (int f = threadIdx.x; f < w3; f += blockDim.x) {
       float s = part_last[static_cast<int64_t>(c0) * w3 + f];
-      for (int c = c0 + 1; c <= c1; ++c) s += part_first[static_cast<int64_t>(c) * w3 + f];
-      if (dNodeAcc) dNodeAcc[u * w3 + f] = s;
+      int c = c0 + 1;
+      for (; c + 8 <= c1 + 1; c += 8) {
+        float t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = part_first[static_cast<int64_t>(c + q) * w3 + f];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += t[q];
+      }
+      for (; c <= c1; ++c) s += part_first[static_cast<int64_t>(c) * w3 + f];
+      if (dNodeAcc) dNodeAcc[static_cast<int64_t>(u) * w3 + f] = s;
       bf_put(bf.dNA, u, f, s);
     }
   }
@@ -1341,8 +1403,12 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     gemm_group_launch(gg, s);
   }
   c.mark(phAttnSoftmax, s);
-  attn_fwd_kernel<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.Q, w.KV, w.attn_a, w.H,
-                                                         c.d_numeric_flag, bfx);
+  {
+    const int lanes = (da + 31) / 32;
+    auto fwd = lanes <= 1 ? attn_fwd_kernel<1> : lanes <= 2 ? attn_fwd_kernel<2>
+             : lanes <= 4 ? attn_fwd_kernel<4> : attn_fwd_kernel<8>;
+    fwd<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag, bfx);
+  }
 
   // ---- decoder + loss (K7)
   c.mark(phDecoder, s);
@@ -1389,16 +1455,26 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 
   // ---- attention backward (K8)
   c.mark(phAttnBwd, s);
-  attn_bwd_kernel<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ,
-                                                         w.dKV, bfx, R, Pc);
+  {
+    const int lanes = (da + 31) / 32;
+    auto bwd = lanes <= 1 ? attn_bwd_kernel<1> : lanes <= 2 ? attn_bwd_kernel<2>
+             : lanes <= 4 ? attn_bwd_kernel<4> : attn_bwd_kernel<8>;
+    bwd<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV, bfx, R, Pc);
+  }
   if (pl.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));  // routing CSR ready
   const int64_t nchunks = ceil_div(R + Pc, kChunk) + 1;
   float* part_first = wc.take(static_cast<size_t>(nchunks) * 3 * da);
   float* part_last = wc.take(static_cast<size_t>(nchunks) * 3 * da);
-  routing_chunk_kernel<<<row_blocks(nchunks), 32 * kWarps, 0, s>>>(
-      D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc, part_first, part_last, bfx);
-  routing_fixup_kernel<<<row_blocks(U), 32 * kWarps, 0, s>>>(D, pl, tma ? nullptr : w.dNodeAcc, part_first,
-                                                             part_last, bfx);
+  {
+    const int lanes = (da + 31) / 32;
+    auto chunk = lanes <= 1 ? routing_chunk_kernel<1> : lanes <= 2 ? routing_chunk_kernel<2>
+               : lanes <= 4 ? routing_chunk_kernel<4> : routing_chunk_kernel<8>;
+    chunk<<<row_blocks(nchunks), 32 * kWarps, 0, s>>>(D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
+                                                      part_first, part_last, bfx);
+    const int fix_threads = std::min(1024, (3 * da + 31) / 32 * 32);
+    routing_fixup_kernel<<<std::min(U, 8 * kSMs), fix_threads, 0, s>>>(D, pl, tma ? nullptr : w.dNodeAcc,
+                                                                       part_first, part_last, bfx);
+  }
   c.mark(phAttnBwdGemm, s);
   if (tma) {
     TcGroup tg;
