@@ -501,7 +501,7 @@ void run_barrier(tgnn_run* r, int64_t b) {
         }
         substep_gru_launch(sc, tr->plans[0], tr->views[0], s);
         sc.mark(phWrites, s);
-        root_writes_launch(sc, tr->plans[0], tr->views[0], s);
+        root_writes_launch(sc, tr->plans[0], tr->views[0], s, r->group_size > 1 ? nullptr : &r->mem->d);
       }
       const size_t pb = tr->w.wpack_bytes;
       const int cap = 2 * tr->cap_B;
@@ -518,8 +518,6 @@ void run_barrier(tgnn_run* r, int64_t b) {
           sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap,
                                    tr->m.d_mem));
         apply_writes_launch(sets, r->mem->d, r->mem->win, s);
-      } else {
-        apply_writes_launch({pack_view(tr->w.wpack, cap, tr->m.d_mem)}, r->mem->d, r->mem->win, s);
       }
     }
     if (t.active) {
@@ -566,7 +564,7 @@ void barrier_body_dev(tgnn_run* r) {
   plan_launch(r->g->d, pl, s, ctx->side);
   gather_view_launch(pl, r->mem->d, vw, s);
   substep_gru_launch(sc, pl, vw, s);
-  root_writes_launch(sc, pl, vw, s);
+  root_writes_launch(sc, pl, vw, s, r->group_size > 1 ? nullptr : &r->mem->d);
   const size_t pb = tr->w.wpack_bytes;
   const int cap = 2 * tr->cap_B;
   if (r->group_size > 1) {
@@ -579,8 +577,6 @@ void barrier_body_dev(tgnn_run* r) {
     for (int mm = 0; mm < r->tc.i; ++mm)
       sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap, tr->m.d_mem));
     apply_writes_launch(sets, r->mem->d, r->mem->win, s);
-  } else {
-    apply_writes_launch({pack_view(tr->w.wpack, cap, tr->m.d_mem)}, r->mem->d, r->mem->win, s);
   }
   substep_rest_launch(sc, pl, vw, r->d_losses, s);
   if (r->nranks > 1)
@@ -1240,8 +1236,7 @@ int tgnn_trainer_iterate(tgnn_trainer* tr, tgnn_memstore* m, int64_t batch_index
   gather_view_launch(pl, m->d, tr->views[0], s);
   StepCtx sc = tr->sc();
   substep_launch(sc, pl, tr->views[0], tr->d_loss, s);
-  root_writes_launch(sc, pl, tr->views[0], s);
-  apply_writes_launch({pack_view(tr->w.wpack, 2 * tr->cap_B, tr->m.d_mem)}, m->d, m->win, s);
+  root_writes_launch(sc, pl, tr->views[0], s, &m->d);
   tr->adam(lr, 1.0f);
   double loss = 0;
   d2h(&loss, tr->d_loss, 1, s);

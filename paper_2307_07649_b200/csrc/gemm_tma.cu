@@ -127,7 +127,10 @@ __device__ __forceinline__ bool tile_info(const TcParams& gp, int t, TileInfo& t
   if (ti.m0 >= ti.M && P.splits == 1) return false;  // beyond the runtime rows: no work, no output
   const int Kcap = P.K;
   const int K = P.K_dev ? min(Kcap, *P.K_dev) : Kcap;
-  const int kper = ((Kcap + P.splits - 1) / P.splits + kBK - 1) / kBK * kBK;
+  // split-K partition of the RUNTIME reduction length (64-row chunks): the
+  // splits stay balanced however loose the capacity is; still a fixed
+  // function of the data, so the reduction order is deterministic.
+  const int kper = ((K + P.splits - 1) / P.splits + kBK - 1) / kBK * kBK;
   ti.kbeg = ti.split * kper;
   const int kend = min(K, ti.kbeg + kper);
   ti.nk = (kend > ti.kbeg && ti.m0 < ti.M) ? (kend - ti.kbeg + kBK - 1) / kBK : 0;

@@ -465,6 +465,33 @@ __global__ void __launch_bounds__(1024) loss_kernel(DPlan pl, const double* __re
   }
 }
 
+// dW2 = sum_e dlogit_e hid_e and db2 = sum_e dlogit_e (decoder.hpp:55-60):
+// block j < d_h reduces column j, block d_h reduces db2; fixed-order tree.
+__global__ void __launch_bounds__(256) decoder_small_grads_kernel(DPlan pl, int dh,
+                                                                  const float* __restrict__ dlogit,
+                                                                  const float* __restrict__ HID,
+                                                                  float* __restrict__ gW2,
+                                                                  float* __restrict__ gb2) {
+  __shared__ float red[256];
+  const int rows = pl.sizes[kSz2B];
+  const int j = blockIdx.x;
+  float s = 0.0f;
+  for (int e = threadIdx.x; e < rows; e += blockDim.x)
+    s = fmaf(dlogit[e], j < dh ? HID[static_cast<int64_t>(e) * dh + j] : 1.0f, s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (j < dh)
+      gW2[j] = red[0];
+    else
+      gb2[0] = red[0];
+  }
+}
+
 // attention_backward (attention.hpp:96-140), one warp per root. dh comes from
 // the decoder input gradient: the source root gets both pairs' halves.
 template <int LANES>
@@ -824,7 +851,7 @@ __global__ void rw_mark_kernel(DPlan pl, DGraph g, int32_t* __restrict__ win, in
 }
 
 __global__ void rw_emit_kernel(Dims D, DPlan pl, DGraph g, DView vw, const float* __restrict__ s_hat,
-                               int32_t* __restrict__ win, StepWork w) {
+                               int32_t* __restrict__ win, StepWork w, DMem st, int direct) {
   const PlanArgs a = *pl.args;
   if (!a.valid) return;
   const int64_t B = a.end - a.begin;
@@ -846,6 +873,24 @@ __global__ void rw_emit_kernel(Dims D, DPlan pl, DGraph g, DView vw, const float
     if (slot < 0) continue;
     const int64_t u = pl.sup_row[self], o = pl.sup_row[other];
     const double t = g.t[e];
+    if (direct) {
+      // single memory writer (no exchange): apply_root_write in place; the
+      // stale values come from the read view, not from the state being written
+      const int64_t v = self;
+      for (int i = lane; i < D.d; i += 32) {
+        st.memory[v * D.d + i] = s_hat[u * D.d + i];
+        st.mail_mem[v * 2 * D.d + i] = vw.mem[u * D.d + i];
+        st.mail_mem[v * 2 * D.d + D.d + i] = vw.mem[o * D.d + i];
+      }
+      if (lane == 0) {
+        const double t_minus = vw.mail_ev[u] >= 0 ? vw.mail_t[u] : 0.0;
+        st.mail_t[v] = t;
+        st.mail_dt[v] = t - t_minus;
+        st.mail_ev[v] = static_cast<int32_t>(e);
+        st.last_update[v] = t;
+      }
+      continue;
+    }
     for (int i = lane; i < D.d; i += 32) {
       w.w_mem[static_cast<int64_t>(slot) * D.d + i] = s_hat[u * D.d + i];
       w.w_mail[static_cast<int64_t>(slot) * 2 * D.d + i] = vw.mem[u * D.d + i];
@@ -915,14 +960,31 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     scale = d.scale;
   }
   const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
-  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-    const float gr = g[x] * scale;
-    const float mm = b1 * m[x] + (1.0f - b1) * gr;
-    const float vv = b2 * v[x] + (1.0f - b2) * gr * gr;
-    m[x] = mm;
-    v[x] = vv;
-    p[x] -= lr * (mm / c1) / (sqrtf(vv / c2) + eps);
+  auto upd = [&](float& pp, float gg, float& mm, float& vv) {
+    const float gr = gg * scale;
+    mm = b1 * mm + (1.0f - b1) * gr;
+    vv = b2 * vv + (1.0f - b2) * gr * gr;
+    pp -= lr * (mm / c1) / (sqrtf(vv / c2) + eps);
+  };
+  // 128-bit path over the 16-byte-aligned bulk (cudaMalloc bases), scalar tail
+  const int64_t n4 = n / 4;
+  float4* p4 = reinterpret_cast<float4*>(p);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* m4 = reinterpret_cast<float4*>(m);
+  float4* v4 = reinterpret_cast<float4*>(v);
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n4; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 pp = p4[x], mm = m4[x], vv = v4[x];
+    const float4 gg = g4[x];
+    upd(pp.x, gg.x, mm.x, vv.x);
+    upd(pp.y, gg.y, mm.y, vv.y);
+    upd(pp.z, gg.z, mm.z, vv.z);
+    upd(pp.w, gg.w, mm.w, vv.w);
+    p4[x] = pp;
+    m4[x] = mm;
+    v4[x] = vv;
   }
+  for (int64_t x = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; x < n; x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    upd(p[x], g[x], m[x], v[x]);
 }
 
 // reset_state (memory_store.hpp:43-50) when the barrier's descriptor asks for it.
@@ -1013,13 +1075,13 @@ void add_nn(GemmGroup& gg, int Mcap, const int* M_dev, int N, int K, Operand a, 
 
 Operand ones_op(const float* ones, int K) { return op_dense(ones, 0, 0, K); }
 
-// ~64 CTAs per weight-gradient problem (a group runs 4-5 of them at once) and
-// >= 512 reduction rows per split, which keeps the fp32 partial traffic of the
-// deterministic split-K reduction small next to the MMA work.
+// ~32 CTAs per weight-gradient problem (a group runs 4-5 of them at once) and
+// >= 512 reduction rows of capacity per split, which keeps the fp32 partial
+// traffic of the deterministic split-K reduction small next to the MMA work.
 int choose_splits_tma(int M, int N, int64_t Kcap) {
   const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
-  int64_t s = std::min<int64_t>(ceil_div(64, tiles), ceil_div(Kcap, 512));
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 64)));
+  int64_t s = std::min<int64_t>(ceil_div(32, tiles), ceil_div(Kcap, 512));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 32)));
 }
 
 // Forward-style problem: A K-major [M x K] (runtime rows M_dev), B K-major [N x K].
@@ -1431,13 +1493,10 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
   c.mark(phDecoderBwd, s);
-  {
-    GemmGroup gg;  // rank-1 reductions (dW2, db2; and on the fp32 engines dW1, db1, dIn)
-    add_tn(gg, wc, 1, dh, B2, sz2B, op_dense(w.dlogit, 0, 1, B2), B_w(w.HID, dh, B2), G + L.off[tW2],
-           dh);
-    add_tn(gg, wc, 1, 1, B2, sz2B, ones_op(w.ones, B2), op_dense(w.dlogit, 1, 0, B2), G + L.off[tB2],
-           1);
-    if (!tma) {
+  decoder_small_grads_kernel<<<dh + 1, 256, 0, s>>>(pl, dh, w.dlogit, w.HID, G + L.off[tW2], G + L.off[tB2]);
+  if (!tma) {
+    GemmGroup gg;  // decoder weight gradients on the fp32-operand engines
+    {
       add_tn(gg, wc, dh, 2 * da, B2, sz2B, A_trans(w.Dhid, dh, B2), B_w(w.Hin, 2 * da, B2),
              G + L.off[tW1], 2 * da);
       add_tn(gg, wc, 1, dh, B2, sz2B, ones_op(w.ones, B2), B_w(w.Dhid, dh, B2), G + L.off[tB1], dh);
@@ -1546,12 +1605,13 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   TGB_CUDA(cudaGetLastError());
 }
 
-void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s) {
+void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s, DMem* direct) {
   StepWork& w = *c.w;
   const Dims D = make_dims(c.m, *c.g);
   const int B2 = 2 * w.cap_B;
   rw_mark_kernel<<<static_cast<int>(ceil_div(B2, 256)), 256, 0, s>>>(pl, *c.g, w.win, w.w_count);
-  rw_emit_kernel<<<row_blocks(B2), 32 * kWarps, 0, s>>>(D, pl, *c.g, vw, w.s_hat, w.win, w);
+  rw_emit_kernel<<<row_blocks(B2), 32 * kWarps, 0, s>>>(D, pl, *c.g, vw, w.s_hat, w.win, w,
+                                                        direct ? *direct : DMem{}, direct ? 1 : 0);
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -123,8 +123,10 @@ void substep_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* 
 void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s);
 void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
                          cudaStream_t s);
-// build_root_writes + COMB for the plan's slice into w.w_* (compact rows).
-void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s);
+// build_root_writes + COMB for the plan's slice into w.w_* (compact rows), or
+// straight into `direct` when this trainer is its memory copy's only writer.
+void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s,
+                        DMem* direct = nullptr);
 // Applies compact write rows (one or more row sets, later sets win on equal
 // nodes -- ascending-rank application, memory_daemon.hpp:35-38) to the state.
 struct WriteSet {
