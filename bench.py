@@ -358,6 +358,21 @@ def main():
     e2e_events = run.traversed(first_e2e, args.e2e_steps)
     e2e_value = e2e_events / float(e2e_t.item())
 
+    # diagnostic: a plain NCCL all-reduce of one flat gradient (no overlap)
+    allreduce_us = None
+    if world > 1:
+        buf = torch.zeros(run.nparam, dtype=torch.float32, device="cuda")
+        for _ in range(3):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(20):
+            dist.all_reduce(buf)
+        a1.record()
+        a1.synchronize()
+        allreduce_us = a0.elapsed_time(a1) * 1e3 / 20
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import ref
@@ -391,6 +406,7 @@ def main():
             "plan_sizes": sz_mean,
             "model_tflops": step_model_flops(sz_mean, cfg) * world / (ms_max / args.steps / 1e3) / 1e12,
             "loss_first_last": [float(losses[0]), float(losses[-1])],
+            "grad_allreduce_us_standalone": allreduce_us,
         }
         emit(line)
     run.close()

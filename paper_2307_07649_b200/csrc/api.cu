@@ -140,6 +140,7 @@ struct tgnn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // plan-only work overlapped with the step
+  cudaStream_t comm = nullptr;  // gradient all-reduce buckets overlapped with the GRU backward
   int* d_flag = nullptr;
 
   void check_numeric() {
@@ -372,8 +373,12 @@ struct tgnn_run {
   int* d_ctr = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
 
   ~tgnn_run() {
+    if (ev_tail) cudaEventDestroy(ev_tail);
+    if (ev_head) cudaEventDestroy(ev_head);
+    if (ev_comm) cudaEventDestroy(ev_comm);
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (d_desc) cudaFree(d_desc);
@@ -549,6 +554,23 @@ void run_barrier(tgnn_run* r, int64_t b) {
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
 
+// average_active_grads (trainer.hpp:473-483) as two NCCL buckets on the comm
+// stream: [off[tWq], end) once ev_tail fires (overlapping the GRU backward),
+// then [0, off[tWq]) after the step; the compute stream waits before Adam.
+void allreduce_bucketed(tgnn_run* r, cudaStream_t s) {
+  tgnn_trainer* tr = r->tr.get();
+  cudaStream_t c = r->ctx->comm;
+  const int64_t split = tr->L.off[tWq];
+  TGB_CUDA(cudaStreamWaitEvent(c, r->ev_tail, 0));
+  NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),
+                                   ncclFloat, ncclSum, r->comm, c));
+  TGB_CUDA(cudaEventRecord(r->ev_head, s));
+  TGB_CUDA(cudaStreamWaitEvent(c, r->ev_head, 0));
+  NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(split), ncclFloat, ncclSum, r->comm, c));
+  TGB_CUDA(cudaEventRecord(r->ev_comm, c));
+  TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
+}
+
 // Graph body (j == 1): the same launch sequence for every barrier; all
 // per-barrier values come from d_desc[*d_ctr].
 void barrier_body_dev(tgnn_run* r) {
@@ -578,10 +600,9 @@ void barrier_body_dev(tgnn_run* r) {
       sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap, tr->m.d_mem));
     apply_writes_launch(sets, r->mem->d, r->mem->win, s);
   }
+  if (r->nranks > 1) sc.ev_tail_grads = r->ev_tail;
   substep_rest_launch(sc, pl, vw, r->d_losses, s);
-  if (r->nranks > 1)
-    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
-                                     r->comm, s));
+  if (r->nranks > 1) allreduce_bucketed(r, s);
   adam_launch(tr->params, tr->grads, tr->am, tr->av, tr->L.total, 0.f, 1.f, 1.f, 1.f, s, r->d_desc, r->d_ctr);
   incr_launch(r->d_ctr, s);
 }
@@ -640,6 +661,7 @@ int tgnn_ctx_create(int device, tgnn_ctx** out) {
   c->device = device;
   TGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   TGB_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  TGB_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
   c->d_flag = dalloc<int>(1);
   TGB_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
   *out = c;
@@ -652,7 +674,9 @@ int tgnn_ctx_destroy(tgnn_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_flag);
   cudaStreamSynchronize(ctx->side);
+  cudaStreamSynchronize(ctx->comm);
   cudaStreamDestroy(ctx->side);
+  cudaStreamDestroy(ctx->comm);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   API_END
@@ -1356,6 +1380,9 @@ int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128) {
   if (r->group_size > 1) {
     NCCL_CHECK(nccl::api().CommSplit(r->comm, r->group, r->rank, &r->gcomm, nullptr));
   }
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_tail, cudaEventDisableTiming));
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_head, cudaEventDisableTiming));
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_comm, cudaEventDisableTiming));
   r->comm_ready = true;
   API_END
 }

@@ -1570,6 +1570,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   c.mark(phGruBwd, s);
   gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
                                           G + L.off[tStatic], bfx, U);
+  if (c.ev_tail_grads) TGB_CUDA(cudaEventRecord(c.ev_tail_grads, s));
   if (tma) {
     TcGroup tg;
     tc_nmn(tg, U, szU, d, d, B.Dg, 2 * B.d8d, B.Whs, 0, w.T1, d);

@@ -106,6 +106,10 @@ struct StepCtx {
   int* d_numeric_flag = nullptr;  // set when a non-finite value escapes a kernel
   PhaseMarks* marks = nullptr;
   const int* d_ctr = nullptr;  // graph mode: the loss goes to loss_out[*d_ctr]
+  // When set, recorded once the gradient range [off[tWq], end) is final (after
+  // the attention / decoder weight gradients and the static-table scatter), so
+  // its all-reduce can overlap the rest of the GRU backward.
+  cudaEvent_t ev_tail_grads = nullptr;
   void mark(int slot, cudaStream_t s) const {
     if (marks) marks->mark(slot, s);
   }
