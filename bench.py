@@ -75,6 +75,16 @@ def step_model_flops(sz, cfg):
     return 6.0 * macs
 
 
+def roofline_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of the roofline kernel from
+    the committed ncu --set full capture (profiles/), per launch."""
+    p = os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d["dram_read_bytes"] + d["dram_write_bytes"]
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -317,7 +327,7 @@ def main():
     main = hbm_view if bound == "hbm" else tensor_view
     roofline = {"kernel": "attention projection GEMM group (Q, fused K|V; tcgen05 bf16x3, TMA)",
                 "bound": bound, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
-                "frac": main["achieved"] / main["peak"], "traffic": None, "peak_source": src,
+                "frac": main["achieved"] / main["peak"], "traffic": roofline_traffic(), "peak_source": src,
                 "flops_per_launch": flops, "algorithmic_bytes_per_launch": hbm_bytes,
                 "launch_ms": proj_ms, "tensor_view": tensor_view, "hbm_view": hbm_view,
                 "share_of_step": proj_ms / max(sum(ph_mean.values()), 1e-9)}
