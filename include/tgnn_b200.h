@@ -163,6 +163,11 @@ typedef struct tgnn_run_options {
   int64_t train_begin, train_end;
   int32_t rank, nranks;
   int32_t use_graphs; /* capture barrier steps as CUDA graphs */
+  /* RunOptions validation (ref trainer.hpp:572-588): an empty [val_begin,
+   * val_end) disables MRR evaluation; eval_batch 0 = train.local_batch. */
+  int64_t val_begin, val_end;
+  int32_t eval_negatives, pad0;
+  int64_t eval_batch;
 } tgnn_run_options;
 
 /* build_assignment + Assignment::task (ref parallel.hpp:150-331), host only.
@@ -184,6 +189,15 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count);
  * over active trainers, ref trainer.hpp:713-722; valid on every rank). */
 int tgnn_run_losses(tgnn_run* r, int64_t first, int64_t count, double* out);
 int tgnn_run_params(tgnn_run* r, double* flat);
+/* MetricsRow list (ref trainer.hpp:562-570, one row per eval barrier reached
+ * so far, rank 0 evaluates with its device weights as run_training does,
+ * trainer.hpp:725-743). rows[count x 5] = iter, traversed, loss (mean barrier
+ * loss since the previous row), val_mrr, elapsed_s. Collective when nranks > 1
+ * (the loss means need every rank's slot); rows == NULL returns the count only. */
+int tgnn_run_metrics(tgnn_run* r, int64_t* count, double* rows);
+/* evaluate_mrr of the run's current weights (rank-local, no collective). */
+int tgnn_run_evaluate_mrr(tgnn_run* r, int64_t eval_begin, int64_t eval_end, int64_t batch_size,
+                          int32_t n_negatives, uint64_t seed, double* mrr, int64_t* queries);
 /* Events traversed by ALL ranks in barriers [first, first+count) (ref parallel.hpp:302-314). */
 int tgnn_run_traversed(tgnn_run* r, int64_t first, int64_t count, int64_t* out);
 /* Kernel launches issued per barrier by this rank (counted by capturing the
@@ -221,6 +235,28 @@ int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t
                       const int32_t* dst, const double* t, const float* efeat);
 int tgnn_pinned_alloc(int64_t bytes, void** out);
 int tgnn_pinned_free(void* p);
+
+
+/* ---- validation path: evaluate_mrr + replay_batch (ref trainer.hpp:336-468) */
+typedef struct tgnn_evaluator tgnn_evaluator;
+/* Forward-only workspaces for batches of up to batch_size events with
+ * n_negatives distractors per event, plus a private node-memory copy. */
+int tgnn_evaluator_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_model_config* m, int64_t batch_size,
+                          int32_t n_negatives, tgnn_evaluator** out);
+int tgnn_evaluator_destroy(tgnn_evaluator* ev);
+/* Replaces evaluate_mrr(g, p, eval_begin, eval_end, batch_size, n_negatives, seed)
+ * (ref trainer.hpp:383-468): memory rebuilt from scratch by replaying
+ * [0, eval_begin), then every event ranks its destination against the
+ * distractors; params = flat f64 weights in canonical order. */
+int tgnn_evaluate_mrr(tgnn_evaluator* ev, const double* params, int64_t eval_begin, int64_t eval_end,
+                      uint64_t seed, double* mrr, int64_t* queries);
+/* Replaces replay_batch(g, p, state, begin, end) (ref trainer.hpp:336-371) on a
+ * memstore; end - begin <= batch_size. params NULL keeps the loaded weights. */
+int tgnn_replay_batch(tgnn_evaluator* ev, tgnn_memstore* state, const double* params, int64_t begin,
+                      int64_t end);
+/* The distractors evaluate_mrr draws for events [begin, end) (ref
+ * trainer.hpp:413-423): out[(end - begin) x n_negatives]; end - begin <= batch_size. */
+int tgnn_eval_candidates(tgnn_evaluator* ev, int64_t begin, int64_t end, uint64_t seed, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -219,6 +219,12 @@ class RefGraph:
                                       _p(state["mail_dt"], f64p), _p(state["mail_event"], i64p),
                                       C.c_int64(begin), C.c_int64(end)))
 
+    def eval_candidates(self, begin, end, n_neg, seed):
+        out = np.zeros((end - begin, n_neg), np.int64)
+        _check(lib().ref_eval_candidates(self.h, C.c_int64(begin), C.c_int64(end), C.c_int32(n_neg),
+                                         C.c_uint64(seed), _p(out, i64p)))
+        return out
+
     def evaluate_mrr(self, mcfg, params, begin, end, batch, n_neg, seed):
         mc = model_cfg(mcfg)
         params = np.ascontiguousarray(params, np.float64)

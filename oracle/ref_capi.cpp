@@ -222,6 +222,29 @@ int ref_sample_negatives(void* gp, int64_t batch_index, int64_t group, int64_t c
   })
 }
 
+// The distractors evaluate_mrr draws (its loop at trainer.hpp:413-423, over
+// the reference's own hash64 / Rng / bipartite boundary): evaluate_mrr does
+// not expose its candidate lists, so this driver walks the same stream.
+int ref_eval_candidates(void* gp, int64_t begin, int64_t end, int32_t n_neg, uint64_t seed,
+                        int64_t* out) {
+  REF_GUARD({
+    auto* g = static_cast<TemporalGraph*>(gp);
+    const NodeId lo = g->bipartite() ? g->bipartite_boundary : 0;
+    const NodeId span = g->num_nodes - lo;
+    for (EventId e = begin; e < end; ++e) {
+      const Event& ev = g->events[static_cast<std::size_t>(e)];
+      for (int s = 0; s < n_neg; ++s) {
+        Rng r(hash64(seed, 0x6576616cull, static_cast<std::uint64_t>(e), static_cast<std::uint64_t>(s)));
+        NodeId v;
+        do {
+          v = lo + r.next_below(span);
+        } while (v == ev.dst);
+        *out++ = v;
+      }
+    }
+  })
+}
+
 // Roots are event-major (src, dst, neg); neighbour arrays are [R x n] padded.
 // supports must hold R*(n+1) entries; *num_supports receives U.
 int ref_plan_sub_batch(void* gp, int64_t begin, int64_t end, const int64_t* negatives, int64_t n,

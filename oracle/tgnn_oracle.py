@@ -158,6 +158,24 @@ def sample_negatives(g: Graph, batch_index: int, group: int, count: int, seed: i
     return (lo + (rng_first_u64(h) % np.uint64(span)).astype(np.int64)).astype(np.int64)
 
 
+def eval_candidates(g: Graph, begin: int, end: int, n_neg: int, seed: int):
+    """evaluate_mrr distractors (trainer.hpp:413-423): candidate s of event e is
+    lo + Rng(hash64(seed, "eval", e, s)).next_below(span), redrawn while it
+    equals the event's destination."""
+    lo = g.boundary if g.boundary >= 0 else 0
+    span = g.num_nodes - lo
+    out = np.zeros((end - begin, n_neg), np.int64)
+    for e in range(begin, end):
+        dst = int(g.dst[e])
+        for s in range(n_neg):
+            r = Rng(int(hash64(np.uint64(seed), np.uint64(0x6576616C), np.uint64(e), np.uint64(s))))
+            v = lo + r.next_below(span)
+            while v == dst:
+                v = lo + r.next_below(span)
+            out[e - begin, s] = v
+    return out
+
+
 @dataclass
 class Plan:
     """SubBatchPlan (trainer.hpp:47-56) in padded array form."""
@@ -560,6 +578,72 @@ def replay_batch(c: ModelConfig, flat_params, g: Graph, state: MemoryState, begi
     rows_mem = np.stack([s_hat[ridx[cn[x]]] for x in kept])
     rows_mail = np.stack([np.concatenate([cm[x], [ct[x], cdt[x], float(ce[x])]]) for x in kept])
     state.write([cn[x] for x in kept], rows_mem, rows_mail)
+
+
+def embed_roots(c: ModelConfig, P, g: Graph, root_node, root_t, nodes, s_hat):
+    """embed_root (trainer.hpp:128-159) + attention_forward (attention.hpp:36-91)
+    for each (node, t) root against the freshened support rows s_hat[nodes]."""
+    row_of = {int(v): i for i, v in enumerate(nodes)}
+    de, dtm = c.d_e, c.d_time
+    ones = np.cos(0.0 * P["omega"])
+    h = np.zeros((len(root_node), c.d_attn))
+    for r, (v, t) in enumerate(zip(root_node, root_t)):
+        q_in = np.concatenate([s_hat[row_of[int(v)]], P["static_table"][int(v)], ones])
+        q = P["attn.Wq"] @ q_in + P["attn.bq"]
+        w, ev, dts = sample_recent_neighbors(g, int(v), float(t), c.n_neighbors)
+        n = len(w)
+        if n == 0:
+            continue
+        kv = np.concatenate([s_hat[[row_of[int(x)] for x in w]], P["static_table"][w],
+                             g.efeat[ev] if de else np.zeros((n, 0)),
+                             np.cos(dts[:, None] * P["omega"][None, :])], axis=1)
+        K = kv @ P["attn.Wk"].T + P["attn.bk"]
+        V = kv @ P["attn.Wv"].T + P["attn.bv"]
+        sc = (K @ q) / math.sqrt(n)
+        a = np.exp(sc - sc.max())
+        a /= a.sum()
+        h[r] = a @ V
+    return h
+
+
+def evaluate_mrr(c: ModelConfig, flat_params, g: Graph, eval_begin, eval_end, batch, n_neg, seed):
+    """evaluate_mrr (trainer.hpp:383-468): memory rebuilt by replaying
+    [0, eval_begin); each event ranks its destination against n_neg
+    distractors, ties counting against it. Returns (mrr, queries)."""
+    P = unflatten(c, flat_params)
+    state = MemoryState.init(g.num_nodes, c.d_mem)
+    for b in range(0, eval_begin, batch):
+        replay_batch(c, flat_params, g, state, b, min(eval_begin, b + batch))
+    W1, b1, W2, b2 = P["dec.W1"], P["dec.b1"], P["dec.W2"], P["dec.b2"]
+
+    def decode(hu, hv):
+        return float(np.maximum(W1 @ np.concatenate([hu, hv]) + b1, 0.0) @ W2[0] + b2[0])
+
+    acc, queries = 0.0, 0
+    for b in range(eval_begin, eval_end, batch):
+        e_end = min(eval_end, b + batch)
+        cand = eval_candidates(g, b, e_end, n_neg, seed)
+        root_node, root_t = [], []
+        for e in range(b, e_end):
+            for v in [g.src[e], g.dst[e], *cand[e - b]]:
+                root_node.append(int(v))
+                root_t.append(float(g.t[e]))
+        nodes = set(root_node)
+        for v, t in zip(root_node, root_t):
+            nodes.update(int(x) for x in sample_recent_neighbors(g, v, t, c.n_neighbors)[0])
+        nodes = np.array(sorted(nodes), np.int64)
+        mem, mail = state.read(nodes)
+        s_hat, _ = freshen(c, P, g, mem, mail)
+        h = embed_roots(c, P, g, root_node, root_t, nodes, s_hat)
+        per = 2 + n_neg
+        for x in range(e_end - b):
+            base = x * per
+            truth = decode(h[base], h[base + 1])
+            worse = sum(1 for s_ in range(n_neg) if decode(h[base], h[base + 2 + s_]) >= truth)
+            acc += 1.0 / (1 + worse)
+            queries += 1
+        replay_batch(c, flat_params, g, state, b, e_end)
+    return (acc / queries if queries else 0.0), queries
 
 
 class Adam:

@@ -19,6 +19,7 @@ library raises at import time -- there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -31,7 +32,8 @@ __all__ = [
     "ConfigError", "ParseError", "NumericError", "ProtocolError", "ShapeError", "CudaError",
     "NcclError", "TgnnError", "ModelConfig", "TrainConfig", "SynthParams", "EventStream",
     "gen_synthetic", "Context", "TemporalGraph", "NodeMemoryStore", "ReadView", "TrainerCore",
-    "Run", "run_sequential", "param_count", "init_params", "lr_eff",
+    "Run", "run_sequential", "param_count", "init_params", "lr_eff", "Evaluator",
+    "write_metrics_csv",
 ]
 
 lib()  # fail loudly at import if the native library is absent
@@ -166,6 +168,11 @@ class Context:
         self.h = C.c_void_p()
         check(lib().tgnn_ctx_create(device, C.byref(self.h)))
         self.device = device
+        self._children = []
+
+    def _adopt(self, obj):
+        """Handles created on this context are closed (newest first) before it."""
+        self._children.append(weakref.ref(obj))
 
     def synchronize(self):
         check(lib().tgnn_ctx_synchronize(self.h))
@@ -178,6 +185,14 @@ class Context:
 
     def close(self):
         if self.h:
+            for ref_ in reversed(self._children):
+                obj = ref_()
+                if obj is not None:
+                    try:
+                        obj.close()
+                    except Exception:
+                        pass
+            self._children = []
             lib().tgnn_ctx_destroy(self.h)
             self.h = C.c_void_p()
 
@@ -193,6 +208,7 @@ class TemporalGraph:
 
     def __init__(self, ctx: Context, num_nodes, boundary, src, dst, t, efeat=None):
         self.ctx = ctx
+        ctx._adopt(self)
         src = np.ascontiguousarray(src, np.int64)
         dst = np.ascontiguousarray(dst, np.int64)
         t = np.ascontiguousarray(t, np.float64)
@@ -302,6 +318,7 @@ class NodeMemoryStore:
 
     def __init__(self, ctx: Context, num_nodes: int, d_mem: int):
         self.ctx = ctx
+        ctx._adopt(self)
         self.num_nodes, self.d_mem = num_nodes, d_mem
         self.h = C.c_void_p()
         check(lib().tgnn_memstore_create(ctx.h, num_nodes, d_mem, C.byref(self.h)))
@@ -362,6 +379,7 @@ class TrainerCore:
     def __init__(self, ctx: Context, g: TemporalGraph, model: ModelConfig, max_local_batch: int,
                  seed: int):
         self.ctx, self.g, self.model, self.seed = ctx, g, model, seed
+        ctx._adopt(self)
         if model.num_nodes == 0:
             model.num_nodes = g.num_nodes
         self.h = C.c_void_p()
@@ -504,12 +522,14 @@ class Run:
 
     def __init__(self, ctx: Context, g: TemporalGraph, model: ModelConfig, train: TrainConfig,
                  train_begin: int, train_end: int, rank: int = 0, nranks: int = 1,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, val_begin: int = 0, val_end: int = 0,
+                 eval_negatives: int = 49, eval_batch: int = 0):
         self.ctx, self.g, self.model, self.train = ctx, g, model, train
+        ctx._adopt(self)
         if model.num_nodes == 0:
             model.num_nodes = g.num_nodes
         opt = RunOptionsC(model.c(), train.c(), train_begin, train_end, rank, nranks,
-                          1 if use_graphs else 0)
+                          1 if use_graphs else 0, val_begin, val_end, eval_negatives, 0, eval_batch)
         self.h = C.c_void_p()
         check(lib().tgnn_run_create(ctx.h, g.h, C.byref(opt), C.byref(self.h)))
         b, n = C.c_int64(), C.c_int64()
@@ -541,6 +561,28 @@ class Run:
         check(lib().tgnn_run_traversed(self.h, first, count, C.byref(out)))
         return out.value
 
+    def metrics(self):
+        """MetricsRow list (trainer.hpp:562-570) for the eval barriers run so far:
+        [rows x 5] = iter, traversed, loss, val_mrr, elapsed_s. Collective at nranks > 1."""
+        n = C.c_int64()
+        check(lib().tgnn_run_metrics(self.h, C.byref(n), None))
+        out = np.zeros((n.value, 5))
+        if n.value:
+            check(lib().tgnn_run_metrics(self.h, C.byref(n), _p(out, f64p)))
+        return out
+
+    def write_metrics_csv(self, path_or_file):
+        """metrics.csv in the reference format (trainer.hpp:607-618)."""
+        write_metrics_csv(self.metrics(), path_or_file)
+
+    def evaluate_mrr(self, eval_begin: int, eval_end: int, batch_size: int, n_negatives: int = 49,
+                     seed: int = 1):
+        """evaluate_mrr (trainer.hpp:383-468) of this rank's current device weights."""
+        mrr, q = C.c_double(), C.c_int64()
+        check(lib().tgnn_run_evaluate_mrr(self.h, eval_begin, eval_end, batch_size, n_negatives, seed,
+                                          C.byref(mrr), C.byref(q)))
+        return mrr.value, q.value
+
     PHASES = ["plan", "gru_fwd", "attn_assemble", "attn_proj", "attn_softmax", "decoder",
               "decoder_bwd", "attn_bwd", "attn_bwd_gemm", "gru_bwd", "writes", "allreduce", "adam"]
 
@@ -562,6 +604,63 @@ class Run:
         if self.h:
             lib().tgnn_run_destroy(self.h)
             self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def write_metrics_csv(rows, path_or_file):
+    """Writes MetricsRow rows with the reference's exact header and number
+    formats (write_metrics_header / write_metrics_row, trainer.hpp:607-618)."""
+    lines = ["iter,traversed,loss,val_mrr,elapsed_s\n"]
+    for r in np.asarray(rows, np.float64).reshape(-1, 5):
+        lines.append("%d,%d,%.17g,%.17g,%.3f\n" % (int(r[0]), int(r[1]), r[2], r[3], r[4]))
+    text = "".join(lines)
+    if hasattr(path_or_file, "write"):
+        path_or_file.write(text)
+    else:
+        with open(path_or_file, "w") as f:
+            f.write(text)
+
+
+class Evaluator:
+    """Device evaluate_mrr / replay_batch (trainer.hpp:336-468): forward-only
+    workspaces for batches of batch_size events with n_negatives distractors."""
+
+    def __init__(self, ctx: Context, g: "TemporalGraph", model: ModelConfig, batch_size: int,
+                 n_negatives: int = 49):
+        self.ctx, self.g, self.model = ctx, g, model
+        ctx._adopt(self)
+        if model.num_nodes == 0:
+            model.num_nodes = g.num_nodes
+        self.batch_size, self.n_negatives = batch_size, n_negatives
+        self.h = C.c_void_p()
+        check(lib().tgnn_evaluator_create(ctx.h, g.h, C.byref(model.c()), batch_size, n_negatives,
+                                          C.byref(self.h)))
+
+    def evaluate_mrr(self, params, eval_begin: int, eval_end: int, seed: int = 1):
+        p = None if params is None else np.ascontiguousarray(params, np.float64)
+        mrr, q = C.c_double(), C.c_int64()
+        check(lib().tgnn_evaluate_mrr(self.h, None if p is None else _p(p, f64p), eval_begin, eval_end,
+                                      seed, C.byref(mrr), C.byref(q)))
+        return mrr.value, q.value
+
+    def replay_batch(self, store: "NodeMemoryStore", params, begin: int, end: int):
+        p = None if params is None else np.ascontiguousarray(params, np.float64)
+        check(lib().tgnn_replay_batch(self.h, store.h, None if p is None else _p(p, f64p), begin, end))
+
+    def candidates(self, begin: int, end: int, seed: int = 1):
+        out = np.zeros((end - begin, self.n_negatives), np.int64)
+        check(lib().tgnn_eval_candidates(self.h, begin, end, seed, _p(out, i64p)))
+        return out
+
+    def close(self):
+        if self.h:
+            check(lib().tgnn_evaluator_destroy(self.h))
+            self.h = None
 
     def __del__(self):
         try:

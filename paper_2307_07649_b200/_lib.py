@@ -79,7 +79,9 @@ class SynthParamsC(C.Structure):
 
 class RunOptionsC(C.Structure):
     _fields_ = [("model", ModelConfigC), ("train", TrainConfigC), ("train_begin", i64),
-                ("train_end", i64), ("rank", i32), ("nranks", i32), ("use_graphs", i32)]
+                ("train_end", i64), ("rank", i32), ("nranks", i32), ("use_graphs", i32),
+                ("val_begin", i64), ("val_end", i64), ("eval_negatives", i32), ("pad0", i32),
+                ("eval_batch", i64)]
 
 
 _lib = None
@@ -131,6 +133,13 @@ SIGNATURES = {
     "tgnn_run_losses": [vp, i64, i64, f64p],
     "tgnn_run_params": [vp, f64p],
     "tgnn_run_traversed": [vp, i64, i64, i64p],
+    "tgnn_run_metrics": [vp, i64p, f64p],
+    "tgnn_run_evaluate_mrr": [vp, i64, i64, i64, i32, u64, f64p, i64p],
+    "tgnn_evaluator_create": [vp, vp, C.POINTER(ModelConfigC), i64, i32, C.POINTER(vp)],
+    "tgnn_evaluator_destroy": [vp],
+    "tgnn_evaluate_mrr": [vp, f64p, i64, i64, u64, f64p, i64p],
+    "tgnn_replay_batch": [vp, vp, f64p, i64, i64],
+    "tgnn_eval_candidates": [vp, i64, i64, u64, i64p],
     "tgnn_run_launches_per_barrier": [vp, i64p],
     "tgnn_run_profile_barrier": [vp, f64p, C.POINTER(C.c_int32)],
     "tgnn_graph_ingest": [vp, i64, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), f64p, f32p],

@@ -180,16 +180,20 @@ struct tgnn_memstore {
 
 namespace {
 
-void plan_alloc(DPlan& pl, int cap_B, int n, int cap_U, int64_t N) {
+void plan_alloc(DPlan& pl, int cap_B, int n, int cap_U, int64_t N, int rpe = 3, int routing = 1,
+                int eval_negs = 0) {
   pl.cap_B = cap_B;
   pl.n = n;
-  pl.cap_R = 3 * cap_B;
+  pl.rpe = rpe;
+  pl.routing = routing;
+  pl.eval_negs = eval_negs;
+  pl.cap_R = rpe * cap_B;
   pl.cap_P = pl.cap_R * (n > 0 ? n : 1);
   pl.cap_U = cap_U;
   pl.args = dalloc<PlanArgs>(1);
   pl.sizes = dalloc<int32_t>(kSzCount);
   TGB_CUDA(cudaMemset(pl.sizes, 0, sizeof(int32_t) * kSzCount));
-  pl.negs = dalloc<int32_t>(cap_B);
+  pl.negs = dalloc<int32_t>(static_cast<size_t>(cap_B) * std::max(rpe - 2, 1));
   pl.root_node = dalloc<int32_t>(pl.cap_R);
   pl.root_t = dalloc<double>(pl.cap_R);
   pl.nbr_cnt = dalloc<int32_t>(pl.cap_R);
@@ -349,6 +353,117 @@ struct tgnn_trainer {
   }
 };
 
+// evaluate_mrr / replay_batch (trainer.hpp:336-468) on device: a private
+// memory copy rebuilt by replaying the prefix, forward-only workspaces sized
+// for 2 + n_negatives roots per event, and per-event rank counts that the host
+// folds in event order (acc += 1 / (1 + worse_or_equal), as the reference).
+struct tgnn_evaluator {
+  tgnn_ctx* ctx = nullptr;
+  tgnn_graph* g = nullptr;
+  ModelDims m;
+  ParamLayout L;
+  int cap_B = 0, n_neg = 0;
+  float* params = nullptr;
+  StepWork w;
+  DPlan pe, pr;  // evaluation plan (candidates + neighbours), replay plan (src, dst only)
+  DView vw;
+  std::unique_ptr<tgnn_memstore> st;
+  int32_t* d_cnt = nullptr;
+  int64_t cnt_cap = 0;
+
+  StepCtx sc() {
+    StepCtx c;
+    c.m = m;
+    c.L = L;
+    c.g = &g->d;
+    c.params = params;
+    c.grads = nullptr;
+    c.w = &w;
+    c.d_numeric_flag = ctx->d_flag;
+    return c;
+  }
+
+  void init(tgnn_ctx* cx, tgnn_graph* gr, const ModelDims& md, int64_t batch, int negatives);
+
+  void set_params(const double* flat) {
+    std::vector<float> f(static_cast<size_t>(L.total));
+    for (int64_t x = 0; x < L.total; ++x) f[static_cast<size_t>(x)] = static_cast<float>(flat[x]);
+    TGB_CUDA(cudaMemcpyAsync(params, f.data(), sizeof(float) * f.size(), cudaMemcpyHostToDevice, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+
+  // replay_batch over [begin, end) in slices of at most cap_B events.
+  void replay(DMem& state, int64_t begin, int64_t end, int64_t batch) {
+    cudaStream_t s = ctx->stream;
+    StepCtx c = sc();
+    for (int64_t b = begin; b < end; b += batch) {
+      PlanArgs a;
+      a.begin = b;
+      a.end = std::min(end, b + batch);
+      a.batch_begin = b;
+      a.neg_mode = 0;
+      a.valid = 1;
+      set_plan_args_launch(pr.args, a, s);
+      plan_launch(g->d, pr, s);
+      gather_view_launch(pr, state, vw, s);
+      substep_gru_launch(c, pr, vw, s);
+      root_writes_launch(c, pr, vw, s, &state);
+    }
+  }
+
+  double evaluate(int64_t eval_begin, int64_t eval_end, uint64_t seed, int64_t* queries) {
+    const DGraph& G = g->d;
+    TGB_REQUIRE(eval_begin >= 0 && eval_end <= G.E && eval_begin <= eval_end, kConfig,
+                "evaluate_mrr: event range out of bounds");
+    const int64_t lo = G.boundary >= 0 ? G.boundary : 0;
+    TGB_REQUIRE(n_neg == 0 || G.N - lo >= 2, kConfig,
+                "evaluate_mrr: destination partition too small to sample distractors");
+    cudaStream_t s = ctx->stream;
+    const int64_t Q = eval_end - eval_begin;
+    if (Q > cnt_cap) {
+      if (d_cnt) cudaFree(d_cnt);
+      d_cnt = dalloc<int32_t>(static_cast<size_t>(Q));
+      cnt_cap = Q;
+    }
+    reset_state_launch(st->d, s);
+    replay(st->d, 0, eval_begin, cap_B);
+    StepCtx c = sc();
+    for (int64_t b = eval_begin; b < eval_end; b += cap_B) {
+      PlanArgs a;
+      a.begin = b;
+      a.end = std::min(eval_end, b + cap_B);
+      a.batch_begin = b;
+      a.seed = seed;
+      a.neg_mode = 2;
+      a.valid = 1;
+      set_plan_args_launch(pe.args, a, s);
+      plan_launch(G, pe, s);
+      gather_view_launch(pe, st->d, vw, s);
+      substep_gru_launch(c, pe, vw, s);
+      attn_forward_launch(c, pe, s);
+      eval_rank_launch(c, pe, d_cnt, eval_begin, s);
+      // the batch's replay: its roots' s_hat are the ones just computed
+      root_writes_launch(c, pe, vw, s, &st->d);
+    }
+    std::vector<int32_t> cnt(static_cast<size_t>(Q));
+    d2h(cnt.data(), d_cnt, static_cast<size_t>(Q), s);
+    ctx->check_numeric();
+    double acc = 0.0;
+    for (int64_t q = 0; q < Q; ++q) acc += 1.0 / static_cast<double>(1 + cnt[static_cast<size_t>(q)]);
+    *queries = Q;
+    return Q > 0 ? acc / static_cast<double>(Q) : 0.0;
+  }
+
+  ~tgnn_evaluator() {
+    step_free(w);
+    plan_free(pe);
+    plan_free(pr);
+    view_free(vw);
+    if (params) cudaFree(params);
+    if (d_cnt) cudaFree(d_cnt);
+  }
+};
+
 struct tgnn_run {
   tgnn_ctx* ctx = nullptr;
   tgnn_graph* g = nullptr;
@@ -374,8 +489,23 @@ struct tgnn_run {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
+  // validation / metrics rows (run_training, trainer.hpp:725-743)
+  int64_t val_begin = 0, val_end = 0, eval_batch = 0;
+  int eval_negatives = 49;
+  std::unique_ptr<tgnn_evaluator> ev;
+  size_t eval_cursor = 0;
+  cudaEvent_t ev_t0 = nullptr;
+  struct Row {
+    int64_t barrier = 0;
+    double val_mrr = 0;
+    cudaEvent_t done = nullptr;
+  };
+  std::vector<Row> rows;
 
   ~tgnn_run() {
+    for (Row& row : rows)
+      if (row.done) cudaEventDestroy(row.done);
+    if (ev_t0) cudaEventDestroy(ev_t0);
     if (ev_tail) cudaEventDestroy(ev_tail);
     if (ev_head) cudaEventDestroy(ev_head);
     if (ev_comm) cudaEventDestroy(ev_comm);
@@ -633,6 +763,57 @@ void build_graph(tgnn_run* r) {
     if (ty == cudaGraphNodeTypeKernel) ++kernels;
   }
   r->launches = kernels;
+}
+
+}  // namespace
+
+void tgnn_evaluator::init(tgnn_ctx* cx, tgnn_graph* gr, const ModelDims& md, int64_t batch, int negatives) {
+  ctx = cx;
+  g = gr;
+  m = md;
+  if (m.num_nodes <= 0) m.num_nodes = gr->d.N;
+  TGB_REQUIRE(m.num_nodes == gr->d.N, kConfig, "model num_nodes does not match the dataset");
+  TGB_REQUIRE(m.d_e == gr->d.d_e, kConfig, "model edge feature width does not match the dataset");
+  validate_dims(m);
+  TGB_REQUIRE(batch > 0, kConfig, "evaluate_mrr: batch size must be positive");
+  TGB_REQUIRE(negatives >= 0, kConfig, "evaluate_mrr: negative distractor count");
+  const int64_t rpe = 2 + static_cast<int64_t>(negatives);
+  const int64_t nn = std::max<int64_t>(m.n_neighbors, 1);
+  TGB_REQUIRE(rpe * batch * (nn + 1) < (1ll << 31), kConfig,
+              "evaluate_mrr: batch x candidates x neighbours exceeds the device index range");
+  L = ParamLayout::make(m);
+  cap_B = static_cast<int>(batch);
+  n_neg = negatives;
+  const int64_t N = m.num_nodes;
+  const int cap_U = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, rpe * batch * (m.n_neighbors + 1))));
+  params = dalloc<float>(static_cast<size_t>(L.total));
+  step_alloc(w, m, cap_B, cap_U, N, static_cast<int>(rpe), true);
+  plan_alloc(pe, cap_B, static_cast<int>(m.n_neighbors), cap_U, N, static_cast<int>(rpe), 0, 1);
+  plan_alloc(pr, cap_B, 0, static_cast<int>(std::min<int64_t>(N, 2 * batch)), N, 2, 0);
+  view_alloc(vw, cap_U, m.d_mem);
+  st.reset(memstore_new(ctx, N, m.d_mem));
+}
+
+namespace {
+
+// One metrics row at eval barrier b (rank 0 evaluates with its own weights).
+void run_eval_point(tgnn_run* r, int64_t b) {
+  tgnn_run::Row row;
+  row.barrier = b;
+  if (r->rank == 0 && r->val_end > r->val_begin) {
+    const int64_t batch = r->eval_batch > 0 ? r->eval_batch : r->tc.local_batch;
+    if (!r->ev || r->ev->cap_B != batch || r->ev->n_neg != r->eval_negatives) {
+      r->ev = std::make_unique<tgnn_evaluator>();
+      r->ev->init(r->ctx, r->g, r->tr->m, batch, r->eval_negatives);
+    }
+    TGB_CUDA(cudaMemcpyAsync(r->ev->params, r->tr->params, sizeof(float) * r->tr->L.total,
+                             cudaMemcpyDeviceToDevice, r->ctx->stream));
+    int64_t q = 0;
+    row.val_mrr = r->ev->evaluate(r->val_begin, r->val_end, r->tc.seed, &q);
+  }
+  TGB_CUDA(cudaEventCreate(&row.done));
+  TGB_CUDA(cudaEventRecord(row.done, r->ctx->stream));
+  r->rows.push_back(row);
 }
 
 }  // namespace
@@ -1336,6 +1517,14 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
   if (r->group_size > 1) {
     TGB_CUDA(cudaMalloc(&r->gathered, r->tr->w.wpack_bytes * static_cast<size_t>(r->tc.i)));
   }
+  r->val_begin = opt->val_begin;
+  r->val_end = opt->val_end;
+  r->eval_batch = opt->eval_batch;
+  r->eval_negatives = opt->eval_negatives;
+  TGB_REQUIRE(r->val_end <= r->val_begin || (r->val_begin >= 0 && r->val_end <= g->d.E), kConfig,
+              "run: validation range out of bounds");
+  TGB_REQUIRE(r->eval_negatives >= 0 && r->eval_batch >= 0, kConfig, "run: invalid evaluation options");
+  TGB_CUDA(cudaEventCreate(&r->ev_t0));
   r->use_graphs = opt->use_graphs != 0 && r->tc.j == 1;
   if (r->use_graphs) {
     const int64_t nb = std::max<int64_t>(r->sched.barriers, 1);
@@ -1410,16 +1599,35 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
   TGB_REQUIRE(first == r->next_barrier, kProtocol, "run: barriers must be issued in order");
   TGB_REQUIRE(first + count <= r->sched.barriers, kConfig, "run: barrier range past the schedule");
   TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
-  if (r->use_graphs && count > 0) {
-    if (!r->exec) build_graph(r);
-    set_int_kernel<<<1, 1, 0, r->ctx->stream>>>(r->d_ctr, static_cast<int>(first));
-    TGB_CUDA(cudaGetLastError());
-    for (int64_t b = first; b < first + count; ++b) TGB_CUDA(cudaGraphLaunch(r->exec, r->ctx->stream));
-    r->tr->adam_t = first + count;
-  } else {
-    for (int64_t b = first; b < first + count; ++b) run_barrier(r, b);
+  if (first == 0 && count > 0) TGB_CUDA(cudaEventRecord(r->ev_t0, r->ctx->stream));
+  const auto& evb = r->sched.eval_barriers;
+  int64_t b = first;
+  const int64_t stop = first + count;
+  while (b < stop) {
+    // segments end at eval barriers, where rank 0 evaluates between barriers
+    while (r->eval_cursor < evb.size() && evb[r->eval_cursor] < b) ++r->eval_cursor;
+    int64_t seg_end = stop;
+    bool eval_here = false;
+    if (r->eval_cursor < evb.size() && evb[r->eval_cursor] < stop) {
+      seg_end = evb[r->eval_cursor] + 1;
+      eval_here = true;
+    }
+    if (r->use_graphs) {
+      if (!r->exec) build_graph(r);
+      set_int_kernel<<<1, 1, 0, r->ctx->stream>>>(r->d_ctr, static_cast<int>(b));
+      TGB_CUDA(cudaGetLastError());
+      for (int64_t x = b; x < seg_end; ++x) TGB_CUDA(cudaGraphLaunch(r->exec, r->ctx->stream));
+      r->tr->adam_t = seg_end;
+    } else {
+      for (int64_t x = b; x < seg_end; ++x) run_barrier(r, x);
+    }
+    if (eval_here) {
+      run_eval_point(r, seg_end - 1);
+      ++r->eval_cursor;
+    }
+    b = seg_end;
   }
-  r->next_barrier = first + count;
+  r->next_barrier = stop;
   API_END
 }
 
@@ -1446,6 +1654,51 @@ int tgnn_run_params(tgnn_run* r, double* flat) {
   API_BEGIN
   r->ctx->use();
   r->tr->get_flat(r->tr->params, flat);
+  API_END
+}
+
+int tgnn_run_metrics(tgnn_run* r, int64_t* count, double* rows) {
+  API_BEGIN
+  r->ctx->use();
+  *count = static_cast<int64_t>(r->rows.size());
+  if (!rows) return 0;
+  const int64_t nb = r->next_barrier;
+  std::vector<double> loss(static_cast<size_t>(std::max<int64_t>(nb, 1)));
+  if (nb > 0) {
+    const int rc = tgnn_run_losses(r, 0, nb, loss.data());
+    if (rc) return rc;
+  }
+  TGB_CUDA(cudaStreamSynchronize(r->ctx->stream));
+  int64_t prev = 0;
+  for (size_t x = 0; x < r->rows.size(); ++x) {
+    const tgnn_run::Row& row = r->rows[x];
+    double acc = 0.0;
+    for (int64_t b = prev; b <= row.barrier; ++b) acc += loss[static_cast<size_t>(b)];
+    const int64_t n = row.barrier + 1 - prev;
+    prev = row.barrier + 1;
+    float ms = 0.0f;
+    TGB_CUDA(cudaEventElapsedTime(&ms, r->ev_t0, row.done));
+    double* o = rows + 5 * x;
+    o[0] = static_cast<double>(row.barrier + 1);
+    o[1] = static_cast<double>(r->sched.traversed_after[static_cast<size_t>(row.barrier)]);
+    o[2] = n > 0 ? acc / static_cast<double>(n) : 0.0;
+    o[3] = row.val_mrr;
+    o[4] = static_cast<double>(ms) * 1e-3;
+  }
+  API_END
+}
+
+int tgnn_run_evaluate_mrr(tgnn_run* r, int64_t eval_begin, int64_t eval_end, int64_t batch_size,
+                          int32_t n_negatives, uint64_t seed, double* mrr, int64_t* queries) {
+  API_BEGIN
+  r->ctx->use();
+  if (!r->ev || r->ev->cap_B != batch_size || r->ev->n_neg != n_negatives) {
+    r->ev = std::make_unique<tgnn_evaluator>();
+    r->ev->init(r->ctx, r->g, r->tr->m, batch_size, n_negatives);
+  }
+  TGB_CUDA(cudaMemcpyAsync(r->ev->params, r->tr->params, sizeof(float) * r->tr->L.total,
+                           cudaMemcpyDeviceToDevice, r->ctx->stream));
+  *mrr = r->ev->evaluate(eval_begin, eval_end, seed, queries);
   API_END
 }
 
@@ -1640,6 +1893,79 @@ int tgnn_pinned_alloc(int64_t bytes, void** out) {
 int tgnn_pinned_free(void* p) {
   API_BEGIN
   if (p) TGB_CUDA(cudaFreeHost(p));
+  API_END
+}
+
+
+int tgnn_evaluator_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_model_config* m, int64_t batch_size,
+                          int32_t n_negatives, tgnn_evaluator** out) {
+  API_BEGIN
+  ctx->use();
+  auto ev = std::make_unique<tgnn_evaluator>();
+  ev->init(ctx, g, dims_of(m), batch_size, n_negatives);
+  *out = ev.release();
+  API_END
+}
+
+int tgnn_evaluator_destroy(tgnn_evaluator* ev) {
+  API_BEGIN
+  if (ev) {
+    cudaSetDevice(ev->ctx->device);
+    cudaStreamSynchronize(ev->ctx->stream);
+  }
+  delete ev;
+  API_END
+}
+
+int tgnn_evaluate_mrr(tgnn_evaluator* ev, const double* params, int64_t eval_begin, int64_t eval_end,
+                      uint64_t seed, double* mrr, int64_t* queries) {
+  API_BEGIN
+  ev->ctx->use();
+  if (params) ev->set_params(params);
+  *mrr = ev->evaluate(eval_begin, eval_end, seed, queries);
+  API_END
+}
+
+int tgnn_replay_batch(tgnn_evaluator* ev, tgnn_memstore* state, const double* params, int64_t begin,
+                      int64_t end) {
+  API_BEGIN
+  ev->ctx->use();
+  TGB_REQUIRE(begin >= 0 && end <= ev->g->d.E && begin <= end, kConfig, "replay_batch: event range out of bounds");
+  TGB_REQUIRE(end - begin <= ev->cap_B, kConfig, "replay_batch: batch exceeds the evaluator capacity");
+  TGB_REQUIRE(state->d.N == ev->m.num_nodes && state->d.d == ev->m.d_mem, kShape,
+              "replay_batch: memory store shape does not match the model");
+  if (params) ev->set_params(params);
+  ev->replay(state->d, begin, end, ev->cap_B);
+  TGB_CUDA(cudaStreamSynchronize(ev->ctx->stream));
+  ev->ctx->check_numeric();
+  API_END
+}
+
+int tgnn_eval_candidates(tgnn_evaluator* ev, int64_t begin, int64_t end, uint64_t seed, int64_t* out) {
+  API_BEGIN
+  ev->ctx->use();
+  const DGraph& G = ev->g->d;
+  TGB_REQUIRE(begin >= 0 && end <= G.E && begin <= end, kConfig, "eval_candidates: event range out of bounds");
+  TGB_REQUIRE(end - begin <= ev->cap_B, kConfig, "eval_candidates: range exceeds the evaluator capacity");
+  const int64_t lo = G.boundary >= 0 ? G.boundary : 0;
+  TGB_REQUIRE(ev->n_neg == 0 || G.N - lo >= 2, kConfig,
+              "evaluate_mrr: destination partition too small to sample distractors");
+  const int64_t cnt = (end - begin) * ev->n_neg;
+  if (cnt == 0) return 0;
+  cudaStream_t s = ev->ctx->stream;
+  PlanArgs a;
+  a.begin = begin;
+  a.end = end;
+  a.batch_begin = begin;
+  a.seed = seed;
+  a.neg_mode = 2;
+  a.valid = 1;
+  set_plan_args_launch(ev->pe.args, a, s);
+  plan_launch(G, ev->pe, s);
+  std::vector<int32_t> tmp(static_cast<size_t>(cnt));
+  d2h(tmp.data(), ev->pe.negs, static_cast<size_t>(cnt), s);
+  TGB_CUDA(cudaStreamSynchronize(s));
+  for (int64_t x = 0; x < cnt; ++x) out[x] = tmp[static_cast<size_t>(x)];
   API_END
 }
 

@@ -49,7 +49,8 @@ struct PlanArgs {
   int64_t batch_index = 0;         // stint batch index (sample_negatives batch_index)
   int64_t group = 0;               // negative group
   uint64_t seed = 0;
-  int32_t neg_mode = 1;            // 1: sample negatives on device, 0: use provided
+  int32_t neg_mode = 1;            // 1: sample_negatives on device, 0: use provided,
+                                   // 2: evaluate_mrr distractors (rpe - 2 per event)
   int32_t valid = 0;               // 0: empty plan (idle trainer)
 };
 
@@ -68,9 +69,14 @@ enum SizeIdx { kSzB = 0, kSzR = 1, kSzP = 2, kSzU = 3, kSzUm = 4, kSzItems = 5, 
 
 struct DPlan {
   int cap_B = 0, n = 0, cap_R = 0, cap_P = 0, cap_U = 0;
+  // roots per event: 3 for training (src, dst, negative), 2 + n_negatives for
+  // evaluate_mrr candidates, 2 for replay_batch (trainer.hpp:336-468)
+  int rpe = 3;
+  int routing = 1;               // 0: forward-only plan, no backward routing CSR
+  int eval_negs = 0;             // 1: the rpe - 2 negatives are evaluate_mrr distractors
   PlanArgs* args = nullptr;
   int32_t* sizes = nullptr;      // [kSzCount]
-  int32_t* negs = nullptr;       // [cap_B]
+  int32_t* negs = nullptr;       // [cap_B * max(rpe - 2, 1)]
   int32_t* root_node = nullptr;  // [cap_R]
   double* root_t = nullptr;      // [cap_R]
   int32_t* nbr_cnt = nullptr;    // [cap_R]

@@ -7,6 +7,8 @@
 // All three are integer/f64-compare work bounded by HBM/L2 latency; results are
 // bit-identical to the reference (no floating-point arithmetic except t - t_e,
 // which is the same IEEE f64 subtraction).
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "plan.cuh"
@@ -49,7 +51,7 @@ __device__ int block_excl_scan(int v, int* smem_warp, int& total) {
 __global__ void negatives_kernel(const PlanArgs* __restrict__ args, int64_t N, int64_t boundary,
                                  int32_t* __restrict__ negs) {
   const PlanArgs a = *args;
-  if (!a.valid || a.neg_mode == 0) return;
+  if (!a.valid || a.neg_mode != 1) return;
   const int64_t B = a.end - a.begin;
   const int64_t lo = boundary >= 0 ? boundary : 0;
   const uint64_t span = static_cast<uint64_t>(N - lo);
@@ -58,6 +60,32 @@ __global__ void negatives_kernel(const PlanArgs* __restrict__ args, int64_t N, i
     const uint64_t h = hash64_5(a.seed, kTagNegatives, static_cast<uint64_t>(a.batch_index),
                                 static_cast<uint64_t>(a.group), i);
     negs[x] = static_cast<int32_t>(lo + static_cast<int64_t>(rng_first_u64(h) % span));
+  }
+}
+
+// evaluate_mrr distractors (trainer.hpp:413-423): candidate s of event e draws
+// lo + Rng(hash64(seed, "eval", e, s)).next_below(span) until it differs from
+// the event's destination.
+__global__ void eval_negatives_kernel(const PlanArgs* __restrict__ args, DGraph g, int per_event,
+                                      int32_t* __restrict__ negs) {
+  const PlanArgs a = *args;
+  if (!a.valid || a.neg_mode != 2 || per_event <= 0) return;
+  const int64_t total = (a.end - a.begin) * per_event;
+  const int64_t lo = g.boundary >= 0 ? g.boundary : 0;
+  const uint64_t span = static_cast<uint64_t>(g.N - lo);
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int64_t e = a.begin + x / per_event;
+    const uint64_t s = static_cast<uint64_t>(x % per_event);
+    const int32_t dst = g.dst[e];
+    const uint64_t h =
+        splitmix64(hash_fold(hash_fold(hash_fold(a.seed, kTagEval), static_cast<uint64_t>(e)), s));
+    uint64_t st = splitmix64(h ^ 0xa02bdbf7bb3c0a7ull);  // Rng(h)
+    int64_t v;
+    do {
+      st = splitmix64(st);
+      v = lo + static_cast<int64_t>(st % span);
+    } while (v == dst);
+    negs[x] = static_cast<int32_t>(v);
   }
 }
 
@@ -83,22 +111,24 @@ __device__ __forceinline__ int64_t warp_lower_bound(const double* __restrict__ i
   return lo + __popc(__ballot_sync(0xffffffffu, pred));
 }
 
-// One warp per root: roots are event-major (src, dst, neg). Neighbours are
+// One warp per root: roots are event-major (src, dst, negatives...). Neighbours are
 // the min(n, have) most recent incidence entries strictly before t, newest first.
 __global__ void sample_kernel(const PlanArgs* __restrict__ args, DGraph g, DPlan pl,
                               uint32_t* __restrict__ bitmap) {
   const PlanArgs a = *args;
   if (!a.valid) return;
   const int64_t B = a.end - a.begin;
-  const int64_t R = 3 * B;
+  const int rpe = pl.rpe;
+  const int64_t R = rpe * B;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int n = pl.n;
   for (int64_t r = warp; r < R; r += nwarps) {
-    const int64_t e = a.begin + r / 3;
-    const int side = static_cast<int>(r % 3);
-    const int32_t v = side == 0 ? g.src[e] : (side == 1 ? g.dst[e] : pl.negs[r / 3]);
+    const int64_t e = a.begin + r / rpe;
+    const int side = static_cast<int>(r % rpe);
+    const int32_t v = side == 0 ? g.src[e]
+                    : (side == 1 ? g.dst[e] : pl.negs[(r / rpe) * (rpe - 2) + side - 2]);
     const double t = g.t[e];
     const int64_t base = g.inc_ptr[v];
     const int64_t end = g.inc_ptr[v + 1];
@@ -131,7 +161,7 @@ __global__ void __launch_bounds__(1024) plan_finalize_kernel(const PlanArgs* __r
   __shared__ int sw[33];
   const PlanArgs a = *args;
   const int B = a.valid ? static_cast<int>(a.end - a.begin) : 0;
-  const int R = 3 * B;
+  const int R = pl.rpe * B;
   int carry = 0, total = 0;
   for (int base = 0; base < R; base += 1024) {
     const int r = base + threadIdx.x;
@@ -323,8 +353,14 @@ size_t plan_sort_tmp_bytes(int cap_items, int bits) {
 void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) {
   uint32_t* bitmap = pl.bitmap;
   const int B = pl.cap_B;
-  negatives_kernel<<<static_cast<int>(ceil_div(B, 256)), 256, 0, s>>>(pl.args, g.N, g.boundary,
-                                                                      pl.negs);
+  if (!pl.eval_negs && pl.rpe == 3) {
+    negatives_kernel<<<static_cast<int>(ceil_div(B, 256)), 256, 0, s>>>(pl.args, g.N, g.boundary,
+                                                                        pl.negs);
+  } else if (pl.eval_negs && pl.rpe > 2) {
+    const int64_t total = static_cast<int64_t>(B) * (pl.rpe - 2);
+    eval_negatives_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * kSMs)), 256, 0, s>>>(
+        pl.args, g, pl.rpe - 2, pl.negs);
+  }
   TGB_CUDA(cudaGetLastError());
   const int R = pl.cap_R;
   const int warps_per_block = 8;
@@ -337,6 +373,7 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) 
   const int slots = pl.cap_R * (pl.n > 0 ? pl.n : 1);
   pairs_kernel<<<static_cast<int>(ceil_div(slots, 256)), 256, 0, s>>>(pl);
   TGB_CUDA(cudaGetLastError());
+  if (!pl.routing) return;
   const int cap_items = pl.cap_R + pl.cap_P;
   cudaStream_t ss = s;
   if (side && pl.ev_pairs) {

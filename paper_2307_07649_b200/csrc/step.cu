@@ -906,6 +906,34 @@ __global__ void rw_emit_kernel(Dims D, DPlan pl, DGraph g, DView vw, const float
   }
 }
 
+// evaluate_mrr ranking (trainer.hpp:448-458): per event, the truth logit
+// decode(h_src, h_dst) against decode(h_src, h_cand) for every distractor;
+// ties count against the truth. Every logit is computed by the same lane
+// order, so exactly equal embeddings (e.g. nodes without history) tie exactly.
+__global__ void eval_rank_kernel(Dims D, DPlan pl, const float* __restrict__ AB,
+                                 const float* __restrict__ b1, const float* __restrict__ W2,
+                                 const float* __restrict__ b2, int32_t* __restrict__ cnt, int64_t base) {
+  const PlanArgs a = *pl.args;
+  if (!a.valid) return;
+  const int64_t B = a.end - a.begin;
+  const int rpe = pl.rpe;
+  const int dh = D.dh;
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = gwarp(); e < B; e += nwarp()) {
+    const float* As = AB + (rpe * e) * 2 * dh;
+    auto logit = [&](int c) {
+      const float* Bc = AB + (rpe * e + c) * 2 * dh + dh;
+      float acc = 0.0f;
+      for (int j = lane; j < dh; j += 32) acc = fmaf(W2[j], fmaxf(As[j] + Bc[j] + b1[j], 0.0f), acc);
+      return warp_sum(acc) + b2[0];
+    };
+    const float truth = logit(1);
+    int worse_or_equal = 0;
+    for (int c = 2; c < rpe; ++c) worse_or_equal += logit(c) >= truth ? 1 : 0;
+    if (lane == 0) cnt[a.begin + e - base] = worse_or_equal;
+  }
+}
+
 __global__ void apply_mark_kernel(WriteSet ws, int32_t* __restrict__ win) {
   const int n = *ws.count;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
@@ -1150,10 +1178,12 @@ int max_splits(int M, int N, int64_t K) {
 
 }  // namespace
 
-void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes) {
+void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes, int rpe,
+                bool fwd_only) {
   const int n = static_cast<int>(m.n_neighbors);
   w.cap_B = cap_B;
-  w.cap_R = 3 * cap_B;
+  w.cap_R = rpe * cap_B;
+  w.fwd_only = fwd_only;
   w.cap_P = w.cap_R * (n > 0 ? n : 1);
   w.cap_U = cap_U;
   const int64_t d = m.d_mem, dt = m.d_time, da = m.d_attn, dh = m.dh();
@@ -1162,6 +1192,8 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   w.ldq = r4(m.q_in());
   w.ldkv = r4(m.kv_in());
   const int64_t U = cap_U, R = w.cap_R, P = w.cap_P, B2 = 2 * cap_B;
+  // backward-only buffers are skipped by forward-only (evaluation) workspaces
+  const int64_t bU = fwd_only ? 0 : U, bR = fwd_only ? 0 : R, bP = fwd_only ? 0 : P;
   w.Xg = dalloc<float>(U * w.ldx);
   w.GU = dalloc<float>(U * dt);
   w.Gates = dalloc<float>(U * 3 * d);
@@ -1180,13 +1212,13 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   w.Hin = dalloc<float>(B2 * 2 * da);
   w.dlogit = dalloc<float>(B2);
   w.logits = dalloc<float>(B2);
-  w.dIn = dalloc<float>(B2 * 2 * da);
-  w.dQ = dalloc<float>(R * da);
-  w.dKV = dalloc<float>(P * 2 * da);
-  w.dNodeAcc = dalloc<float>(U * 3 * da);
-  w.dNode = dalloc<float>(U * (d + m.d_static));
-  w.Dg = dalloc<float>(U * 3 * d);
-  w.T1 = dalloc<float>(U * d);
+  w.dIn = dalloc<float>(bR ? B2 * 2 * da : 0);
+  w.dQ = dalloc<float>(bR * da);
+  w.dKV = dalloc<float>(bP * 2 * da);
+  w.dNodeAcc = dalloc<float>(bU * 3 * da);
+  w.dNode = dalloc<float>(bU * (d + m.d_static));
+  w.Dg = dalloc<float>(bU * 3 * d);
+  w.T1 = dalloc<float>(bU * d);
   w.DMT = dalloc<float>(3 * ((d + 7) / 8 * 8) * dt);  // M2 = Dg^T GU (padded blocks)
   w.Mom = dalloc<float>(2 * ((da + 7) / 8 * 8) * dt);  // padded dK | dV rows (TMA layout)
   w.omega_chunks = static_cast<int>(ceil_div(U, kOmegaRows));
@@ -1212,10 +1244,12 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
     b.H = bf_alloc(R, da);
     b.Hin = bf_alloc(B2, 2 * da + 1);
     b.Dhid = bf_alloc(B2, dh);
-    b.dQ = bf_alloc(R, da);
-    b.dKV = bf_alloc(P, b.d8a + da);
-    b.dNA = bf_alloc(U, 3 * da);
-    b.Dg = bf_alloc(U, 2 * b.d8d + d);
+    if (!fwd_only) {
+      b.dQ = bf_alloc(R, da);
+      b.dKV = bf_alloc(P, b.d8a + da);
+      b.dNA = bf_alloc(U, 3 * da);
+      b.Dg = bf_alloc(U, 2 * b.d8d + d);
+    }
     b.Wzr = bf_alloc(2 * d, gin + 1);
     b.Whm = bf_alloc(d, md);
     b.Whs = bf_alloc(d, d + 1);
@@ -1255,6 +1289,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   acc(static_cast<int>(2 * w.bf.d8d + d), static_cast<int>(dt), U);
   const int64_t nchunks = ceil_div(R + P, kChunk) + 1;
   ws += 2 * static_cast<size_t>(nchunks) * 3 * da;
+  if (fwd_only) ws = 1;  // forward GEMMs never split K
   w.splitk_ws_floats = ws;
   w.splitk_ws = dalloc<float>(ws);
   w.wpack_bytes = pack_bytes(static_cast<int>(B2), d);
@@ -1413,31 +1448,23 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   TGB_CUDA(cudaGetLastError());
 }
 
-void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
-                         cudaStream_t s) {
+void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   const ModelDims& m = c.m;
   const ParamLayout& L = c.L;
   StepWork& w = *c.w;
   const DGraph& g = *c.g;
   const Dims D = make_dims(m, g);
   const float* P = c.params;
-  float* G = c.grads;
-  const int d = D.d, dt = D.dt, da = D.da, dh = D.dh, md = D.md, gin = D.gin;
-  const int U = w.cap_U, R = w.cap_R, Pc = w.cap_P, B2 = 2 * w.cap_B;
-  const int* szU = pl.sizes + kSzU;
+  const int da = D.da;
+  const int R = w.cap_R, Pc = w.cap_P;
   const int* szR = pl.sizes + kSzR;
   const int* szP = pl.sizes + kSzP;
-  const int* sz2B = pl.sizes + kSz2B;
   const bool tma = gemm_impl() == kGemmTma;
   StepBf bfx;
   if (tma) bfx = w.bf;
   bfx.d8a = w.bf.d8a;
   bfx.d8d = w.bf.d8d;
   const StepBf& B = w.bf;
-
-  TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));
-  const int eblocks = 4 * kSMs;
-
   // ---- attention forward (K6)
   c.mark(phAttnAssemble, s);
   {
@@ -1471,6 +1498,35 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
              : lanes <= 4 ? attn_fwd_kernel<4> : attn_fwd_kernel<8>;
     fwd<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag, bfx);
   }
+
+}
+
+void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
+                         cudaStream_t s) {
+  const ModelDims& m = c.m;
+  const ParamLayout& L = c.L;
+  StepWork& w = *c.w;
+  const DGraph& g = *c.g;
+  const Dims D = make_dims(m, g);
+  const float* P = c.params;
+  float* G = c.grads;
+  const int d = D.d, dt = D.dt, da = D.da, dh = D.dh, md = D.md, gin = D.gin;
+  const int U = w.cap_U, R = w.cap_R, Pc = w.cap_P, B2 = 2 * w.cap_B;
+  const int* szU = pl.sizes + kSzU;
+  const int* szR = pl.sizes + kSzR;
+  const int* szP = pl.sizes + kSzP;
+  const int* sz2B = pl.sizes + kSz2B;
+  const bool tma = gemm_impl() == kGemmTma;
+  StepBf bfx;
+  if (tma) bfx = w.bf;
+  bfx.d8a = w.bf.d8a;
+  bfx.d8d = w.bf.d8d;
+  const StepBf& B = w.bf;
+
+  TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));
+  const int eblocks = 4 * kSMs;
+
+  attn_forward_launch(c, pl, s);
 
   // ---- decoder + loss (K7)
   c.mark(phDecoder, s);
@@ -1603,6 +1659,32 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   if (dt > 0)
     omega_final_kernel<<<dt, 256, 0, s>>>(D, P, L.off[tWk], L.off[tWv], L.off[tWz], w.Mom, w.DMT,
                                           G + L.off[tOmega], tma ? B.d8a : da, tma ? B.d8d : d);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void eval_rank_launch(const StepCtx& c, const DPlan& pl, int32_t* cnt_out, int64_t base, cudaStream_t s) {
+  const ModelDims& m = c.m;
+  const ParamLayout& L = c.L;
+  StepWork& w = *c.w;
+  const Dims D = make_dims(m, *c.g);
+  const float* P = c.params;
+  const int da = D.da, dh = D.dh, R = w.cap_R;
+  const int* szR = pl.sizes + kSzR;
+  c.mark(phDecoder, s);
+  if (gemm_impl() == kGemmTma) {
+    TcGroup tg;
+    tc_nn(tg, R, szR, dh, da, w.bf.H, 0, w.bf.W1a, 0, dh, w.AB, 2 * dh);
+    tc_nn(tg, R, szR, dh, da, w.bf.H, 0, w.bf.W1b, 0, dh, w.AB + dh, 2 * dh);
+    tc_group_launch(tg, s);
+  } else {
+    GemmGroup gg;
+    add_nn(gg, R, szR, dh, da, A_rows(w.H, da, da), B_wT(P + L.off[tW1], 2 * da, da), w.AB, 2 * dh);
+    add_nn(gg, R, szR, dh, da, A_rows(w.H, da, da), B_wT(P + L.off[tW1] + da, 2 * da, da), w.AB + dh,
+           2 * dh);
+    gemm_group_launch(gg, s);
+  }
+  eval_rank_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(D, pl, w.AB, P + L.off[tB1], P + L.off[tW2],
+                                                               P + L.off[tB2], cnt_out, base);
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -54,6 +54,7 @@ struct StepBf {
 struct StepWork {
   StepBf bf;
   int cap_B = 0, cap_R = 0, cap_P = 0, cap_U = 0;
+  bool fwd_only = false;
   int64_t ldx = 0, ldq = 0, ldkv = 0;
   float *Xg = nullptr, *GU = nullptr, *Gates = nullptr, *RS = nullptr, *s_hat = nullptr;
   float *Qin = nullptr, *KVin = nullptr, *Gt = nullptr, *Q = nullptr, *KV = nullptr;
@@ -115,7 +116,10 @@ struct StepCtx {
   }
 };
 
-void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes);
+// rpe: roots per event of the plans this workspace serves (3 in training,
+// 2 + n_negatives for evaluation); fwd_only skips the backward buffers.
+void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes, int rpe = 3,
+                bool fwd_only = false);
 void step_free(StepWork& w);
 
 // Forward + backward of one sub-iteration on (plan, view). Writes the loss to
@@ -127,6 +131,12 @@ void substep_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* 
 void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s);
 void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
                          cudaStream_t s);
+// Forward-only evaluation pieces (evaluate_mrr, trainer.hpp:383-468).
+// attention embedding of every root (embed_root + attention_forward) into w.H
+void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s);
+// decode_link of (src, dst) and (src, candidate) per event of an evaluation
+// plan (rpe = 2 + n_neg); cnt_out[e - base] = #candidates with logit >= truth.
+void eval_rank_launch(const StepCtx& c, const DPlan& pl, int32_t* cnt_out, int64_t base, cudaStream_t s);
 // build_root_writes + COMB for the plan's slice into w.w_* (compact rows), or
 // straight into `direct` when this trainer is its memory copy's only writer.
 void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s,

@@ -108,6 +108,12 @@ def main():
     r = g.run(mc, ref.train_cfg(local_batch=50, seed=3, epochs=2), 0, 600)
     out.update(run_losses=r["barrier_loss"], run_params=r["params"])
 
+    # evaluate_mrr (trainer.hpp:383-468): distractors, and MRR of the initial
+    # and of the trained weights over [600, 800) in batches of 50, 9 negatives
+    out["eval_cand"] = g.eval_candidates(600, 700, 9, 5)
+    out["eval_mrr_init"] = np.array(g.evaluate_mrr(mc, params, 600, 800, 50, 9, 5))
+    out["eval_mrr_trained"] = np.array(g.evaluate_mrr(mc, r["params"], 600, 800, 50, 9, 5))
+
     # schedules for several (i, j, k)
     shapes = np.array([(1, 1, 1, 2), (2, 1, 1, 1), (1, 2, 1, 2), (1, 1, 2, 1), (2, 2, 2, 3),
                        (1, 4, 2, 2), (1, 1, 8, 8)], np.int64)

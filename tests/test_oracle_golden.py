@@ -135,3 +135,18 @@ def test_run_sequential_golden(og, mc):
     losses, params = O.run_sequential(mc, og, 3, 50, 1e-3, 0, 600, epochs=2)
     assert np.abs(losses - GOLD["run_losses"]).max() < 1e-10
     assert np.abs(params - GOLD["run_params"]).max() < 1e-10
+
+
+def test_eval_candidates_golden(og):
+    """evaluate_mrr distractors (trainer.hpp:413-423) against the reference stream."""
+    assert np.array_equal(O.eval_candidates(og, 600, 700, 9, 5), GOLD["eval_cand"])
+    assert not np.any(GOLD["eval_cand"] == og.dst[600:700, None])
+
+
+def test_evaluate_mrr_golden(og, mc):
+    """evaluate_mrr (trainer.hpp:383-468) of the initial and the trained weights."""
+    for key, params in (("eval_mrr_init", GOLD["init_params_seed7"]),
+                        ("eval_mrr_trained", GOLD["run_params"])):
+        mrr, q = O.evaluate_mrr(mc, params, og, 600, 800, 50, 9, 5)
+        assert q == int(GOLD[key][1])
+        assert abs(mrr - GOLD[key][0]) < 1e-12, (key, mrr, GOLD[key][0])
