@@ -258,6 +258,13 @@ int tgnn_replay_batch(tgnn_evaluator* ev, tgnn_memstore* state, const double* pa
  * trainer.hpp:413-423): out[(end - begin) x n_negatives]; end - begin <= batch_size. */
 int tgnn_eval_candidates(tgnn_evaluator* ev, int64_t begin, int64_t end, uint64_t seed, int64_t* out);
 
+
+/* ---- artifacts: model.ckpt (ref model.hpp:168-222), byte-compatible with
+ * save_checkpoint / load_checkpoint; flat = f64 weights in canonical order.
+ * Load refuses a manifest that does not match the config (TGNN_CONFIG). */
+int tgnn_checkpoint_save(const tgnn_model_config* m, const double* flat, const char* path);
+int tgnn_checkpoint_load(const tgnn_model_config* m, const char* path, double* flat);
+
 #ifdef __cplusplus
 }
 #endif

@@ -261,6 +261,19 @@ def param_count(mcfg) -> int:
     return lib().ref_param_count(C.byref(mc))
 
 
+def save_checkpoint(mcfg, params, path):
+    mc = model_cfg(mcfg)
+    params = np.ascontiguousarray(params, np.float64)
+    _check(lib().ref_save_checkpoint(C.byref(mc), _p(params, f64p), os.fsencode(path)))
+
+
+def load_checkpoint(mcfg, path) -> np.ndarray:
+    mc = model_cfg(mcfg)
+    out = np.empty(lib().ref_param_count(C.byref(mc)), np.float64)
+    _check(lib().ref_load_checkpoint(C.byref(mc), os.fsencode(path), _p(out, f64p)))
+    return out
+
+
 def init_params(mcfg, seed) -> np.ndarray:
     mc = model_cfg(mcfg)
     out = np.empty(lib().ref_param_count(C.byref(mc)), np.float64)

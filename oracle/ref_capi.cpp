@@ -394,6 +394,25 @@ int ref_evaluate_mrr(void* gp, const ref_model_cfg* c, const double* params_flat
   })
 }
 
+// ---------------------------------------------------------------- checkpoint
+int ref_save_checkpoint(const ref_model_cfg* c, const double* params_flat, const char* path) {
+  REF_GUARD({
+    ModelParams p;
+    shape_params(to_mcfg(c), p);
+    params_from_flat(p, params_flat);
+    save_checkpoint(p, path);
+  })
+}
+
+int ref_load_checkpoint(const ref_model_cfg* c, const char* path, double* params_flat) {
+  REF_GUARD({
+    ModelParams p;
+    shape_params(to_mcfg(c), p);
+    load_checkpoint(p, path);
+    params_to_flat(p, params_flat);
+  })
+}
+
 // ---------------------------------------------------------------- optimizer
 void* ref_adam_create(int64_t n) { return new Adam(static_cast<std::size_t>(n)); }
 void ref_adam_free(void* a) { delete static_cast<Adam*>(a); }

@@ -19,6 +19,7 @@ library raises at import time -- there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 from dataclasses import dataclass, field
 
@@ -33,7 +34,7 @@ __all__ = [
     "NcclError", "TgnnError", "ModelConfig", "TrainConfig", "SynthParams", "EventStream",
     "gen_synthetic", "Context", "TemporalGraph", "NodeMemoryStore", "ReadView", "TrainerCore",
     "Run", "run_sequential", "param_count", "init_params", "lr_eff", "Evaluator",
-    "write_metrics_csv",
+    "write_metrics_csv", "save_checkpoint", "load_checkpoint",
 ]
 
 lib()  # fail loudly at import if the native library is absent
@@ -571,6 +572,10 @@ class Run:
             check(lib().tgnn_run_metrics(self.h, C.byref(n), _p(out, f64p)))
         return out
 
+    def save_checkpoint(self, path):
+        """model.ckpt of this rank's current weights (all replicas are identical)."""
+        save_checkpoint(self.model, self.params(), path)
+
     def write_metrics_csv(self, path_or_file):
         """metrics.csv in the reference format (trainer.hpp:607-618)."""
         write_metrics_csv(self.metrics(), path_or_file)
@@ -610,6 +615,21 @@ class Run:
             self.close()
         except Exception:
             pass
+
+
+def save_checkpoint(model: ModelConfig, params, path):
+    """save_checkpoint (model.hpp:170-186): model.ckpt the reference CLI can load."""
+    p = np.ascontiguousarray(params, np.float64)
+    if p.size != param_count(model):
+        raise ShapeError("save_checkpoint: flat parameter vector has the wrong length")
+    check(lib().tgnn_checkpoint_save(C.byref(model.c()), _p(p, f64p), os.fsencode(path)))
+
+
+def load_checkpoint(model: ModelConfig, path) -> np.ndarray:
+    """load_checkpoint (model.hpp:188-222) into the canonical flat f64 vector."""
+    out = np.empty(param_count(model), np.float64)
+    check(lib().tgnn_checkpoint_load(C.byref(model.c()), os.fsencode(path), _p(out, f64p)))
+    return out
 
 
 def write_metrics_csv(rows, path_or_file):

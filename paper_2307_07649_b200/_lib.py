@@ -140,6 +140,8 @@ SIGNATURES = {
     "tgnn_evaluate_mrr": [vp, f64p, i64, i64, u64, f64p, i64p],
     "tgnn_replay_batch": [vp, vp, f64p, i64, i64],
     "tgnn_eval_candidates": [vp, i64, i64, u64, i64p],
+    "tgnn_checkpoint_save": [C.POINTER(ModelConfigC), f64p, C.c_char_p],
+    "tgnn_checkpoint_load": [C.POINTER(ModelConfigC), C.c_char_p, f64p],
     "tgnn_run_launches_per_barrier": [vp, i64p],
     "tgnn_run_profile_barrier": [vp, f64p, C.POINTER(C.c_int32)],
     "tgnn_graph_ingest": [vp, i64, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), f64p, f32p],

@@ -16,6 +16,7 @@
 #include "../../include/tgnn_b200.h"
 #include "common.cuh"
 #include "device_types.cuh"
+#include "host/checkpoint.hpp"
 #include "host/schedule.hpp"
 #include "host/synth.hpp"
 #include "nccl_dyn.hpp"
@@ -1966,6 +1967,25 @@ int tgnn_eval_candidates(tgnn_evaluator* ev, int64_t begin, int64_t end, uint64_
   d2h(tmp.data(), ev->pe.negs, static_cast<size_t>(cnt), s);
   TGB_CUDA(cudaStreamSynchronize(s));
   for (int64_t x = 0; x < cnt; ++x) out[x] = tmp[static_cast<size_t>(x)];
+  API_END
+}
+
+
+int tgnn_checkpoint_save(const tgnn_model_config* m, const double* flat, const char* path) {
+  API_BEGIN
+  const auto man = host::ckpt_manifest(m->d_mem, m->d_time, m->d_static, m->d_attn, m->d_hidden, m->d_e,
+                                       m->num_nodes);
+  const std::string err = host::ckpt_save(man, flat, path);
+  TGB_REQUIRE(err.empty(), kConfig, err);
+  API_END
+}
+
+int tgnn_checkpoint_load(const tgnn_model_config* m, const char* path, double* flat) {
+  API_BEGIN
+  const auto man = host::ckpt_manifest(m->d_mem, m->d_time, m->d_static, m->d_attn, m->d_hidden, m->d_e,
+                                       m->num_nodes);
+  const std::string err = host::ckpt_load(man, path, flat);
+  TGB_REQUIRE(err.empty(), kConfig, err);
   API_END
 }
 

@@ -114,6 +114,9 @@ def main():
     out["eval_mrr_init"] = np.array(g.evaluate_mrr(mc, params, 600, 800, 50, 9, 5))
     out["eval_mrr_trained"] = np.array(g.evaluate_mrr(mc, r["params"], 600, 800, 50, 9, 5))
 
+    # model.ckpt written by the reference's save_checkpoint (model.hpp:170-186)
+    ref.save_checkpoint(mc, r["params"], os.path.join(HERE, "small.ckpt"))
+
     # schedules for several (i, j, k)
     shapes = np.array([(1, 1, 1, 2), (2, 1, 1, 1), (1, 2, 1, 2), (1, 1, 2, 1), (2, 2, 2, 3),
                        (1, 4, 2, 2), (1, 1, 8, 8)], np.int64)

@@ -105,3 +105,28 @@ def test_no_silent_cpu_fallback():
     if n[0] == 0:
         with pytest.raises(T.CudaError):
             T.Context(0)
+
+
+def test_checkpoint_byte_compatible(tmp_path):
+    """model.ckpt (ref model.hpp:168-222): our writer reproduces the reference's
+    bytes, our reader loads the reference's file, and mismatches are refused."""
+    mc = T.ModelConfig(d_e=4, num_nodes=int(GOLD["num_nodes"]), max_t=float(GOLD["t"][-1]), **MODEL)
+    gold_path = os.path.join(ROOT, "tests", "golden", "small.ckpt")
+    out = tmp_path / "model.ckpt"
+    T.save_checkpoint(mc, GOLD["run_params"], out)
+    assert out.read_bytes() == open(gold_path, "rb").read()
+    assert np.array_equal(T.load_checkpoint(mc, gold_path), GOLD["run_params"])
+    other = T.ModelConfig(d_e=4, num_nodes=int(GOLD["num_nodes"]), max_t=1.0,
+                          **dict(MODEL, d_attn=6))
+    with pytest.raises(T.ConfigError, match="manifest mismatch"):
+        T.load_checkpoint(other, gold_path)
+    bad = tmp_path / "bad.ckpt"
+    bad.write_bytes(b"not a checkpoint\n")
+    with pytest.raises(T.ConfigError, match="bad magic"):
+        T.load_checkpoint(mc, bad)
+    trunc = tmp_path / "trunc.ckpt"
+    trunc.write_bytes(open(gold_path, "rb").read()[:-8])
+    with pytest.raises(T.ConfigError, match="truncated payload"):
+        T.load_checkpoint(mc, trunc)
+    with pytest.raises(T.ConfigError, match="cannot open"):
+        T.load_checkpoint(mc, tmp_path / "missing.ckpt")
