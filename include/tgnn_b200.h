@@ -265,6 +265,26 @@ int tgnn_eval_candidates(tgnn_evaluator* ev, int64_t begin, int64_t end, uint64_
 int tgnn_checkpoint_save(const tgnn_model_config* m, const double* flat, const char* path);
 int tgnn_checkpoint_load(const tgnn_model_config* m, const char* path, double* flat);
 
+
+/* ---- input pipeline (ref temporal_graph.hpp:96-274, synthetic.hpp:54-112) */
+/* gen_synthetic streamed straight into a device graph: bit-identical events
+ * and fp32 features, generated chunk by chunk (sequential chain on the calling
+ * thread, feature transform on `threads` workers, overlapped H2D copies), then
+ * the device finalize. Host memory stays O(chunk) at GDELT scale. */
+int tgnn_graph_synthetic(tgnn_ctx* ctx, const tgnn_synth_params* p, int32_t threads, tgnn_graph** out);
+/* load_dataset (ref temporal_graph.hpp:136-258): the event CSV plus its
+ * ".meta" sidecar, parsed by `threads` workers; the reference's grammar and
+ * errors (TGNN_PARSE for malformed input, TGNN_CONFIG for missing files). */
+int tgnn_graph_load_dataset(tgnn_ctx* ctx, const char* csv_path, int32_t threads, tgnn_graph** out);
+/* write_dataset (ref temporal_graph.hpp:237-262): CSV + sidecar, %.17g numbers. */
+int tgnn_write_dataset(const char* csv_path, int64_t num_nodes, int64_t bipartite_boundary, int64_t num_events,
+                       const int64_t* src, const int64_t* dst, const double* t, const double* efeat, int64_t d_e);
+/* TemporalGraph::edge_feat rows [first, first+count) as fp32 (ref temporal_graph.hpp:46-48). */
+int tgnn_graph_edge_feats(tgnn_graph* g, int64_t first, int64_t count, float* out);
+/* chronological_split (ref temporal_graph.hpp:264-279): event-index quantiles. */
+int tgnn_chronological_split(int64_t num_events, double train_frac, double val_frac, int64_t* train_end,
+                             int64_t* val_end);
+
 #ifdef __cplusplus
 }
 #endif

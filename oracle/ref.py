@@ -34,6 +34,7 @@ class RefError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"[{code}] {msg}")
         self.code = code
+        self.msg = msg
 
 
 _lib = None
@@ -121,6 +122,21 @@ class RefGraph:
                                            _p(t, f64p), _p(ef, f64p), C.c_int64(d_e),
                                            C.byref(out)))
         return RefGraph(out.value)
+
+    @staticmethod
+    def load_dataset(csv_path):
+        out = C.c_void_p()
+        _check(lib().ref_load_dataset(os.fsencode(csv_path), C.byref(out)))
+        return RefGraph(out.value)
+
+    def write_dataset(self, csv_path):
+        _check(lib().ref_write_dataset(self.h, os.fsencode(csv_path)))
+
+    def chronological_split(self, train_frac, val_frac):
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib().ref_chronological_split(self.h, C.c_double(train_frac), C.c_double(val_frac),
+                                             C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def export(self, feats=True):
         E = self.num_events

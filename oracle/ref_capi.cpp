@@ -148,6 +148,24 @@ int ref_graph_synthetic(int64_t nodes, int64_t events, double burst_prob, double
   })
 }
 
+// load_dataset / write_dataset (temporal_graph.hpp:136-262), unmodified.
+int ref_load_dataset(const char* csv_path, void** out) {
+  REF_GUARD({ *out = new TemporalGraph(load_dataset(csv_path)); })
+}
+
+int ref_write_dataset(void* gp, const char* csv_path) {
+  REF_GUARD({ write_dataset(*static_cast<TemporalGraph*>(gp), csv_path); })
+}
+
+int ref_chronological_split(void* gp, double train_frac, double val_frac, int64_t* train_end,
+                            int64_t* val_end) {
+  REF_GUARD({
+    SplitRanges r = chronological_split(*static_cast<TemporalGraph*>(gp), train_frac, val_frac);
+    *train_end = r.train_end;
+    *val_end = r.val_end;
+  })
+}
+
 int ref_graph_from_events(int64_t num_nodes, int64_t boundary, int64_t num_events,
                           const int64_t* src, const int64_t* dst, const double* t,
                           const double* efeat, int64_t d_e, void** out) {

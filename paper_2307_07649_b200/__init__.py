@@ -34,7 +34,7 @@ __all__ = [
     "NcclError", "TgnnError", "ModelConfig", "TrainConfig", "SynthParams", "EventStream",
     "gen_synthetic", "Context", "TemporalGraph", "NodeMemoryStore", "ReadView", "TrainerCore",
     "Run", "run_sequential", "param_count", "init_params", "lr_eff", "Evaluator",
-    "write_metrics_csv", "save_checkpoint", "load_checkpoint",
+    "write_metrics_csv", "save_checkpoint", "load_checkpoint", "write_dataset", "chronological_split",
 ]
 
 lib()  # fail loudly at import if the native library is absent
@@ -128,6 +128,11 @@ class EventStream:
     @property
     def num_events(self):
         return len(self.t)
+
+
+def _synth_c(p: SynthParams) -> SynthParamsC:
+    return SynthParamsC(p.nodes, p.events, p.burst_prob, p.pref_prob, p.prefs_per_src, p.src_frac,
+                        1 if p.bipartite else 0, p.d_e, p.zipf_s, p.seed)
 
 
 def gen_synthetic(p: SynthParams, with_features: bool = True) -> EventStream:
@@ -227,13 +232,47 @@ class TemporalGraph:
             check(lib().tgnn_graph_create(ctx.h, num_nodes, boundary, len(t), _p(src, i64p),
                                           _p(dst, i64p), _p(t, f64p), _p(ef, f32p), d_e,
                                           C.byref(self.h)))
+        self._info()
+
+    def _info(self):
         n, b, e, de = (C.c_int64() for _ in range(4))
         check(lib().tgnn_graph_info(self.h, C.byref(n), C.byref(b), C.byref(e), C.byref(de)))
         self.num_nodes, self.boundary, self.num_events, self.d_e = n.value, b.value, e.value, de.value
 
+    @classmethod
+    def _from_handle(cls, ctx: Context, h) -> "TemporalGraph":
+        g = cls.__new__(cls)
+        g.ctx, g.h = ctx, h
+        ctx._adopt(g)
+        g._info()
+        return g
+
     @staticmethod
     def from_stream(ctx: Context, s: EventStream) -> "TemporalGraph":
         return TemporalGraph(ctx, s.num_nodes, s.boundary, s.src, s.dst, s.t, s.efeat)
+
+    @staticmethod
+    def synthetic(ctx: Context, p: SynthParams, threads: int = 0) -> "TemporalGraph":
+        """gen_synthetic (synthetic.hpp:54-112) streamed into HBM chunk by chunk,
+        then finalized on the device (bit-identical to the reference stream)."""
+        h = C.c_void_p()
+        check(lib().tgnn_graph_synthetic(ctx.h, C.byref(_synth_c(p)), threads, C.byref(h)))
+        return TemporalGraph._from_handle(ctx, h)
+
+    @staticmethod
+    def load_dataset(ctx: Context, csv_path, threads: int = 0) -> "TemporalGraph":
+        """load_dataset (temporal_graph.hpp:255-258): event CSV + .meta sidecar."""
+        h = C.c_void_p()
+        check(lib().tgnn_graph_load_dataset(ctx.h if ctx is not None else None, os.fsencode(csv_path),
+                                             threads, C.byref(h)))
+        return TemporalGraph._from_handle(ctx, h)
+
+    def edge_feats(self, first: int = 0, count=None):
+        """fp32 edge-feature rows [first, first + count) (temporal_graph.hpp:46-48)."""
+        count = self.num_events - first if count is None else count
+        out = np.zeros((count, self.d_e), np.float32)
+        check(lib().tgnn_graph_edge_feats(self.h, first, count, _p(out, f32p)))
+        return out
 
     def bipartite(self) -> bool:
         return self.boundary >= 0
@@ -615,6 +654,24 @@ class Run:
             self.close()
         except Exception:
             pass
+
+
+def write_dataset(csv_path, num_nodes: int, boundary: int, src, dst, t, efeat=None):
+    """write_dataset (temporal_graph.hpp:237-262): CSV + .meta sidecar; efeat f64 [E, d_e]."""
+    src = np.ascontiguousarray(src, np.int64)
+    dst = np.ascontiguousarray(dst, np.int64)
+    t = np.ascontiguousarray(t, np.float64)
+    ef = np.zeros((len(t), 0)) if efeat is None else np.ascontiguousarray(efeat, np.float64)
+    check(lib().tgnn_write_dataset(os.fsencode(csv_path), num_nodes, boundary, len(t), _p(src, i64p),
+                                   _p(dst, i64p), _p(t, f64p), _p(ef, f64p) if ef.size else None,
+                                   ef.shape[1] if ef.ndim == 2 else 0))
+
+
+def chronological_split(num_events: int, train_frac: float, val_frac: float):
+    """chronological_split (temporal_graph.hpp:264-279) -> (train_end, val_end)."""
+    a, b = C.c_int64(), C.c_int64()
+    check(lib().tgnn_chronological_split(num_events, train_frac, val_frac, C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def save_checkpoint(model: ModelConfig, params, path):

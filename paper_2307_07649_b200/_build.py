@@ -19,7 +19,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", CSRC, "-I", os.path.join(HERE, "..", "include")]
-SOURCES = ["plan.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_tma.cu", "step.cu", "api.cu"]
+SOURCES = ["plan.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_tma.cu", "step.cu", "graph.cu", "api.cu",
+           "host/dataset.cpp"]
+CXX = os.environ.get("TGNN_HOST_CXX", "g++")
+CXXFLAGS = ["-O2", "-std=c++20", "-fPIC", "-pthread", "-g", "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 
 def _deps_hash(src: str) -> str:
@@ -30,16 +33,19 @@ def _deps_hash(src: str) -> str:
                 h.update(open(os.path.join(root, f), "rb").read())
     h.update(open(os.path.join(HERE, "..", "include", "tgnn_b200.h"), "rb").read())
     h.update(open(os.path.join(CSRC, src), "rb").read())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(" ".join(ARCH + FLAGS + CXXFLAGS).encode())
     return h.hexdigest()[:16]
 
 
 def _compile(src: str) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    obj = os.path.join(OBJ, f"{src}.{_deps_hash(src)}.o")
+    obj = os.path.join(OBJ, f"{src.replace('/', '_')}.{_deps_hash(src)}.o")
     if os.path.exists(obj):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj + ".tmp"]
+    if src.endswith(".cpp"):
+        cmd = [CXX, *CXXFLAGS, "-c", os.path.join(CSRC, src), "-o", obj + ".tmp"]
+    else:
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -54,7 +60,7 @@ def build(verbose: bool = False) -> str:
     stamp_file = OUT + ".stamp"
     if os.path.exists(OUT) and os.path.exists(stamp_file) and open(stamp_file).read() == stamp:
         return OUT
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-ldl", "-cudart", "static",
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-ldl", "-lpthread", "-cudart", "static",
            "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -141,6 +141,11 @@ SIGNATURES = {
     "tgnn_replay_batch": [vp, vp, f64p, i64, i64],
     "tgnn_eval_candidates": [vp, i64, i64, u64, i64p],
     "tgnn_checkpoint_save": [C.POINTER(ModelConfigC), f64p, C.c_char_p],
+    "tgnn_graph_synthetic": [vp, C.POINTER(SynthParamsC), i32, C.POINTER(vp)],
+    "tgnn_graph_load_dataset": [vp, C.c_char_p, i32, C.POINTER(vp)],
+    "tgnn_write_dataset": [C.c_char_p, i64, i64, i64, i64p, i64p, f64p, f64p, i64],
+    "tgnn_chronological_split": [i64, f64, f64, i64p, i64p],
+    "tgnn_graph_edge_feats": [vp, i64, i64, f32p],
     "tgnn_checkpoint_load": [C.POINTER(ModelConfigC), C.c_char_p, f64p],
     "tgnn_run_launches_per_barrier": [vp, i64p],
     "tgnn_run_profile_barrier": [vp, f64p, C.POINTER(C.c_int32)],

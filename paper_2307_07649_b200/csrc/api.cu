@@ -11,15 +11,18 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tgnn_b200.h"
 #include "common.cuh"
 #include "device_types.cuh"
 #include "host/checkpoint.hpp"
+#include "host/dataset.hpp"
 #include "host/schedule.hpp"
 #include "host/synth.hpp"
 #include "nccl_dyn.hpp"
+#include "graph.cuh"
 #include "plan.cuh"
 #include "step.cuh"
 #include "gemm_tma.cuh"
@@ -159,8 +162,6 @@ struct tgnn_ctx {
 struct tgnn_graph {
   tgnn_ctx* ctx = nullptr;
   DGraph d;
-  std::vector<int32_t> h_src, h_dst;
-  std::vector<double> h_t;
   ~tgnn_graph() {
     void* ptrs[] = {d.src, d.dst, d.t, d.inc_ptr, d.inc_t, d.inc_eid, d.inc_nbr, d.efeat};
     for (void* p : ptrs)
@@ -896,57 +897,16 @@ int tgnn_gen_synthetic(const tgnn_synth_params* p, int64_t* src, int64_t* dst, d
 
 namespace {
 
-int graph_create_impl(tgnn_ctx* ctx, int64_t num_nodes, int64_t boundary, int64_t E,
-                      const int64_t* src, const int64_t* dst, const double* t, const float* ef32,
-                      const double* ef64, int64_t d_e, tgnn_graph** out) {
-  API_BEGIN
-  ctx->use();
-  // TemporalGraph::finalize (temporal_graph.hpp:55-91)
+// Allocates the event arrays of an E-event graph (T-CSR built by finalize).
+std::unique_ptr<tgnn_graph> graph_alloc(tgnn_ctx* ctx, int64_t num_nodes, int64_t boundary, int64_t E, int64_t d_e) {
   TGB_REQUIRE(num_nodes > 0, kConfig, "graph: num_nodes must be positive");
-  TGB_REQUIRE(num_nodes < (1ll << 31) && E < (1ll << 31), kConfig, "graph: too large for int32 ids");
+  TGB_REQUIRE(num_nodes < (1ll << 31) && E < (1ll << 30), kConfig, "graph: too large for int32 ids");
   if (boundary >= 0)
     TGB_REQUIRE(boundary > 0 && boundary < num_nodes, kConfig,
                 "graph: bipartite boundary leaves an empty partition");
   TGB_REQUIRE(E >= 0 && d_e >= 0, kConfig, "graph: invalid sizes");
-  std::vector<int64_t> order(static_cast<size_t>(E));
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return t[a] < t[b]; });
   auto g = std::make_unique<tgnn_graph>();
   g->ctx = ctx;
-  g->h_src.resize(static_cast<size_t>(E));
-  g->h_dst.resize(static_cast<size_t>(E));
-  g->h_t.resize(static_cast<size_t>(E));
-  std::vector<int64_t> deg(static_cast<size_t>(num_nodes) + 1, 0);
-  for (int64_t e = 0; e < E; ++e) {
-    const int64_t o = order[static_cast<size_t>(e)];
-    const int64_t s = src[o], d = dst[o];
-    if (s < 0 || s >= num_nodes || d < 0 || d >= num_nodes)
-      throw Error(kConfig, "graph: node id out of range at event " + std::to_string(e));
-    if (boundary >= 0 && !(s < boundary && d >= boundary))
-      throw Error(kConfig, "graph: event " + std::to_string(e) + " does not cross the bipartite boundary");
-    g->h_src[static_cast<size_t>(e)] = static_cast<int32_t>(s);
-    g->h_dst[static_cast<size_t>(e)] = static_cast<int32_t>(d);
-    g->h_t[static_cast<size_t>(e)] = t[o];
-    ++deg[static_cast<size_t>(s) + 1];
-    ++deg[static_cast<size_t>(d) + 1];
-  }
-  for (int64_t v = 0; v < num_nodes; ++v) deg[static_cast<size_t>(v) + 1] += deg[static_cast<size_t>(v)];
-  // T-CSR: per-node ascending (t, event id) incidence; each event is listed
-  // under src then dst (a self-loop twice), temporal_graph.hpp:78-90.
-  const int64_t M = 2 * E;
-  std::vector<int32_t> inc_eid(static_cast<size_t>(M)), inc_nbr(static_cast<size_t>(M));
-  std::vector<double> inc_t(static_cast<size_t>(M));
-  std::vector<int64_t> cur(deg.begin(), deg.end() - 1);
-  for (int64_t e = 0; e < E; ++e) {
-    const int32_t s = g->h_src[static_cast<size_t>(e)], d = g->h_dst[static_cast<size_t>(e)];
-    for (int side = 0; side < 2; ++side) {
-      const int32_t v = side == 0 ? s : d;
-      const int64_t at = cur[static_cast<size_t>(v)]++;
-      inc_eid[static_cast<size_t>(at)] = static_cast<int32_t>(e);
-      inc_nbr[static_cast<size_t>(at)] = s == v ? d : s;
-      inc_t[static_cast<size_t>(at)] = g->h_t[static_cast<size_t>(e)];
-    }
-  }
   DGraph& D = g->d;
   D.N = num_nodes;
   D.boundary = boundary;
@@ -956,34 +916,49 @@ int graph_create_impl(tgnn_ctx* ctx, int64_t num_nodes, int64_t boundary, int64_
   D.src = dalloc<int32_t>(E);
   D.dst = dalloc<int32_t>(E);
   D.t = dalloc<double>(E);
-  D.inc_ptr = dalloc<int64_t>(num_nodes + 1);
-  D.inc_t = dalloc<double>(M);
-  D.inc_eid = dalloc<int32_t>(M);
-  D.inc_nbr = dalloc<int32_t>(M);
   D.efeat = dalloc<float>(static_cast<size_t>(E * std::max<int64_t>(D.d_e_pad, 1)));
-  TGB_CUDA(cudaMemcpy(D.src, g->h_src.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
-  TGB_CUDA(cudaMemcpy(D.dst, g->h_dst.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
-  TGB_CUDA(cudaMemcpy(D.t, g->h_t.data(), sizeof(double) * E, cudaMemcpyHostToDevice));
-  TGB_CUDA(cudaMemcpy(D.inc_ptr, deg.data(), sizeof(int64_t) * (num_nodes + 1), cudaMemcpyHostToDevice));
-  TGB_CUDA(cudaMemcpy(D.inc_t, inc_t.data(), sizeof(double) * M, cudaMemcpyHostToDevice));
-  TGB_CUDA(cudaMemcpy(D.inc_eid, inc_eid.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice));
-  TGB_CUDA(cudaMemcpy(D.inc_nbr, inc_nbr.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice));
-  if (d_e > 0) {
-    // padded fp32 rows, uploaded in chunks to bound host staging
-    const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / (4 * D.d_e_pad));
-    std::vector<float> buf(static_cast<size_t>(std::min(chunk, E) * D.d_e_pad), 0.0f);
-    for (int64_t e0 = 0; e0 < E; e0 += chunk) {
-      const int64_t e1 = std::min(E, e0 + chunk);
-      for (int64_t e = e0; e < e1; ++e) {
-        const int64_t o = order[static_cast<size_t>(e)];
-        float* row = buf.data() + (e - e0) * D.d_e_pad;
-        for (int64_t f = 0; f < d_e; ++f)
-          row[f] = ef32 ? ef32[o * d_e + f] : static_cast<float>(ef64[o * d_e + f]);
-      }
-      TGB_CUDA(cudaMemcpy(D.efeat + e0 * D.d_e_pad, buf.data(), sizeof(float) * (e1 - e0) * D.d_e_pad,
-                          cudaMemcpyHostToDevice));
+  if (D.d_e_pad > D.d_e)
+    TGB_CUDA(cudaMemset(D.efeat, 0, sizeof(float) * static_cast<size_t>(E * D.d_e_pad)));
+  return g;
+}
+
+int graph_create_impl(tgnn_ctx* ctx, int64_t num_nodes, int64_t boundary, int64_t E,
+                      const int64_t* src, const int64_t* dst, const double* t, const float* ef32,
+                      const double* ef64, int64_t d_e, tgnn_graph** out) {
+  API_BEGIN
+  ctx->use();
+  // TemporalGraph::finalize (temporal_graph.hpp:55-91): events and feature
+  // rows go up as given; sort, validation and the T-CSR run on the device.
+  auto g = graph_alloc(ctx, num_nodes, boundary, E, d_e);
+  DGraph& D = g->d;
+  cudaStream_t s = ctx->stream;
+  // ids outside [0, N) become -1 so int32 narrowing cannot hide them
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(E, (64ll << 20) / (4 * std::max<int64_t>(D.d_e_pad, 4))));
+  std::vector<int32_t> s32(static_cast<size_t>(std::min(chunk, std::max<int64_t>(E, 1))));
+  std::vector<int32_t> d32(s32.size());
+  std::vector<float> buf(d_e > 0 ? s32.size() * static_cast<size_t>(D.d_e_pad) : 0, 0.0f);
+  for (int64_t e0 = 0; e0 < E; e0 += chunk) {
+    const int64_t n = std::min(chunk, E - e0);
+    for (int64_t x = 0; x < n; ++x) {
+      const int64_t a = src[e0 + x], b = dst[e0 + x];
+      s32[static_cast<size_t>(x)] = a >= 0 && a < num_nodes ? static_cast<int32_t>(a) : -1;
+      d32[static_cast<size_t>(x)] = b >= 0 && b < num_nodes ? static_cast<int32_t>(b) : -1;
     }
+    TGB_CUDA(cudaMemcpyAsync(D.src + e0, s32.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    TGB_CUDA(cudaMemcpyAsync(D.dst + e0, d32.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    TGB_CUDA(cudaMemcpyAsync(D.t + e0, t + e0, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    if (d_e > 0) {
+      for (int64_t x = 0; x < n; ++x) {
+        float* row = buf.data() + x * D.d_e_pad;
+        for (int64_t f = 0; f < d_e; ++f)
+          row[f] = ef32 ? ef32[(e0 + x) * d_e + f] : static_cast<float>(ef64[(e0 + x) * d_e + f]);
+      }
+      TGB_CUDA(cudaMemcpyAsync(D.efeat + e0 * D.d_e_pad, buf.data(), sizeof(float) * n * D.d_e_pad,
+                               cudaMemcpyHostToDevice, s));
+    }
+    TGB_CUDA(cudaStreamSynchronize(s));  // pageable staging is reused
   }
+  graph_finalize_device(D, s);
   *out = g.release();
   API_END
 }
@@ -1022,10 +997,17 @@ int tgnn_graph_info(tgnn_graph* g, int64_t* num_nodes, int64_t* boundary, int64_
 
 int tgnn_graph_events(tgnn_graph* g, int64_t* src, int64_t* dst, double* t) {
   API_BEGIN
-  for (int64_t e = 0; e < g->d.E; ++e) {
-    src[e] = g->h_src[static_cast<size_t>(e)];
-    dst[e] = g->h_dst[static_cast<size_t>(e)];
-    t[e] = g->h_t[static_cast<size_t>(e)];
+  g->ctx->use();
+  const int64_t E = g->d.E;
+  std::vector<int32_t> a(static_cast<size_t>(E)), b(static_cast<size_t>(E));
+  cudaStream_t s = g->ctx->stream;
+  d2h(a.data(), g->d.src, static_cast<size_t>(E), s);
+  d2h(b.data(), g->d.dst, static_cast<size_t>(E), s);
+  d2h(t, g->d.t, static_cast<size_t>(E), s);
+  TGB_CUDA(cudaStreamSynchronize(s));
+  for (int64_t e = 0; e < E; ++e) {
+    src[e] = a[static_cast<size_t>(e)];
+    dst[e] = b[static_cast<size_t>(e)];
   }
   API_END
 }
@@ -1986,6 +1968,73 @@ int tgnn_checkpoint_load(const tgnn_model_config* m, const char* path, double* f
                                        m->num_nodes);
   const std::string err = host::ckpt_load(man, path, flat);
   TGB_REQUIRE(err.empty(), kConfig, err);
+  API_END
+}
+
+
+int tgnn_graph_synthetic(tgnn_ctx* ctx, const tgnn_synth_params* p, int32_t threads, tgnn_graph** out) {
+  API_BEGIN
+  ctx->use();
+  host::SynthConfig c;
+  c.nodes = p->nodes;
+  c.events = p->events;
+  c.burst_prob = p->burst_prob;
+  c.pref_prob = p->pref_prob;
+  c.prefs_per_src = p->prefs_per_src;
+  c.src_frac = p->src_frac;
+  c.bipartite = p->bipartite != 0;
+  c.d_e = p->d_e;
+  c.zipf_s = p->zipf_s;
+  c.seed = p->seed;
+  const host::Generator probe(c);  // validates and fixes the boundary
+  auto g = graph_alloc(ctx, c.nodes, probe.boundary(), c.events, c.d_e);
+  if (threads <= 0) threads = static_cast<int32_t>(std::max(1u, std::thread::hardware_concurrency() - 1));
+  synth_stream_to_device(c, g->d, ctx->stream, threads);
+  graph_finalize_device(g->d, ctx->stream);
+  *out = g.release();
+  API_END
+}
+
+int tgnn_graph_load_dataset(tgnn_ctx* ctx, const char* csv_path, int32_t threads, tgnn_graph** out) {
+  API_BEGIN
+  const std::string path(csv_path);
+  const host::DatasetMeta meta = host::load_sidecar(host::sidecar_path(path));
+  host::EventTable tab;
+  if (threads <= 0) threads = static_cast<int32_t>(std::max(1u, std::thread::hardware_concurrency()));
+  host::load_events(path, meta, threads, tab);  // parse errors surface before any device work
+  TGB_REQUIRE(ctx != nullptr, kConfig, "load_dataset: a device context is required");
+  ctx->use();
+  const int64_t E = static_cast<int64_t>(tab.t.size());
+  const int rc = graph_create_impl(ctx, meta.num_nodes, meta.boundary, E, tab.src.data(), tab.dst.data(),
+                                   tab.t.data(), tab.efeat.data(), nullptr, meta.d_e, out);
+  if (rc) return rc;
+  API_END
+}
+
+int tgnn_write_dataset(const char* csv_path, int64_t num_nodes, int64_t bipartite_boundary, int64_t num_events,
+                       const int64_t* src, const int64_t* dst, const double* t, const double* efeat, int64_t d_e) {
+  API_BEGIN
+  host::write_dataset(csv_path, num_nodes, bipartite_boundary, num_events, src, dst, t, efeat, d_e);
+  API_END
+}
+
+int tgnn_chronological_split(int64_t num_events, double train_frac, double val_frac, int64_t* train_end,
+                             int64_t* val_end) {
+  API_BEGIN
+  host::chronological_split(num_events, train_frac, val_frac, train_end, val_end);
+  API_END
+}
+
+
+int tgnn_graph_edge_feats(tgnn_graph* g, int64_t first, int64_t count, float* out) {
+  API_BEGIN
+  g->ctx->use();
+  const DGraph& D = g->d;
+  TGB_REQUIRE(first >= 0 && count >= 0 && first + count <= D.E, kConfig, "edge_feats: range out of bounds");
+  if (D.d_e == 0 || count == 0) return 0;
+  TGB_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * D.d_e, D.efeat + first * D.d_e_pad, sizeof(float) * D.d_e_pad,
+                             sizeof(float) * D.d_e, static_cast<size_t>(count), cudaMemcpyDeviceToHost, g->ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(g->ctx->stream));
   API_END
 }
 

@@ -69,6 +69,7 @@ constexpr uint64_t kTagEval = 0x6576616cull;       // "eval", trainer.hpp:417
 
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+#ifdef __CUDACC__
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -88,6 +89,8 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+#endif  // __CUDACC__
 
 constexpr int kSMs = 148;
 
