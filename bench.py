@@ -37,9 +37,15 @@ CONFIGS = {
     "c5p": dict(workload="synthetic GDELT-shape CTDG (C5, 5M-event prefix): 16,682 nodes, "
                          "186-d edge feats, TGN + static memory, batch 600",
                 nodes=16682, events=5_000_000, d_e=186, d_static=100),
+    # BASELINE.json configs[4] at full size: 191M events x 186 fp32 features
+    # (143 GB) streamed into HBM by the chunked generator
+    "c5": dict(workload="synthetic GDELT-shape CTDG (C5): 16,682 nodes, 191,290,882 events, "
+                        "186-d edge feats, TGN + static memory, batch 600",
+               nodes=16682, events=191_290_882, d_e=186, d_static=100),
 }
 LOCAL_BATCH = 600
 TRAIN_FRAC = 0.70
+REF_MAX_EVENTS = 5_000_000  # f64 host copy of a GDELT-shape prefix: ~7.5 GB
 
 
 def model_dims(cfg):
@@ -152,12 +158,15 @@ def reference_time(cfg, n_groups, barriers, warmup, log=print):
     from oracle import tgnn_oracle as O
 
     t0 = time.time()
-    g = ref.RefGraph.synthetic(cfg["nodes"], cfg["events"], d_e=cfg["d_e"], seed=1)
+    # the generator is sequential, so a prefix of the stream is the full
+    # stream's prefix: the f64 reference holds at most REF_MAX_EVENTS of it
+    n_ev = min(cfg["events"], REF_MAX_EVENTS)
+    g = ref.RefGraph.synthetic(cfg["nodes"], n_ev, d_e=cfg["d_e"], seed=1)
     _, _, t, _ = g.export(feats=False)
     log(f"[ref] graph ready in {time.time() - t0:.1f}s")
     mc = O.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(t[-1]), **model_dims(cfg))
     gb = LOCAL_BATCH
-    mid = int(cfg["events"] * TRAIN_FRAC) // 2
+    mid = int(n_ev * TRAIN_FRAC) // 2
     out = None
     for phase, nbar in (("warmup", warmup), ("timed", barriers)):
         if nbar <= 0:
@@ -257,11 +266,13 @@ def main():
 
     cfg = CONFIGS[args.config]
     t0 = time.time()
-    s = T.gen_synthetic(T.SynthParams(nodes=cfg["nodes"], events=cfg["events"], d_e=cfg["d_e"], seed=1))
-    log(f"stream generated in {time.time() - t0:.1f}s")
     ctx = T.Context(local_rank)
-    g = T.TemporalGraph.from_stream(ctx, s)
-    mc = T.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(s.t[-1]), **model_dims(cfg))
+    # gen_synthetic streamed into HBM (bit-identical to the reference stream)
+    g = T.TemporalGraph.synthetic(ctx, T.SynthParams(nodes=cfg["nodes"], events=cfg["events"], d_e=cfg["d_e"],
+                                                     seed=1))
+    ev_src, ev_dst, ev_t = g.events()
+    log(f"stream generated into HBM in {time.time() - t0:.1f}s")
+    mc = T.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(ev_t[-1]), **model_dims(cfg))
     train_end = int(round(cfg["events"] * TRAIN_FRAC))
     tc = T.TrainConfig(i=1, j=1, k=world, local_batch=LOCAL_BATCH, lr_base=1e-3, seed=1, epochs=world)
     run = T.Run(ctx, g, mc, tc, 0, train_end, rank=rank, nranks=world)
@@ -344,6 +355,10 @@ def main():
     p_t = T.pinned_empty((maxb,), np.float64)
     p_f = T.pinned_empty((maxb, d_e), np.float32)
     h2d = 0
+    act = [x for x in range(args.e2e_steps) if sched["active"][x]]
+    w_lo = min([int(sched["slice_begin"][x]) for x in act], default=0)
+    w_hi = max([int(sched["slice_end"][x]) for x in act], default=0)
+    host_feats = g.edge_feats(w_lo, w_hi - w_lo)  # the host-side copy of the steps' inputs
     if world > 1:
         dist.barrier()
     ctx.synchronize()
@@ -353,10 +368,10 @@ def main():
         b0, b1 = int(sched["slice_begin"][x]), int(sched["slice_end"][x])
         n = b1 - b0
         if sched["active"][x] and n > 0:
-            p_src[:n] = s.src[b0:b1]
-            p_dst[:n] = s.dst[b0:b1]
-            p_t[:n] = s.t[b0:b1]
-            p_f[:n] = s.efeat[b0:b1]
+            p_src[:n] = ev_src[b0:b1]
+            p_dst[:n] = ev_dst[b0:b1]
+            p_t[:n] = ev_t[b0:b1]
+            p_f[:n] = host_feats[b0 - w_lo:b1 - w_lo]
             g.ingest(b0, p_src[:n], p_dst[:n], p_t[:n], p_f[:n])
             h2d += n * (4 + 4 + 8 + 4 * d_e)
         run.step(1)
