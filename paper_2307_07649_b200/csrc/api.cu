@@ -145,6 +145,8 @@ struct tgnn_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // plan-only work overlapped with the step
   cudaStream_t comm = nullptr;  // gradient all-reduce buckets overlapped with the GRU backward
+  cudaStream_t aux = nullptr;   // next barrier's plan / read, overlapped with this barrier's step
+  cudaStream_t br = nullptr;    // leaves of the step (gradient zeroing, root writes, loss)
   int* d_flag = nullptr;
 
   void check_numeric() {
@@ -316,6 +318,8 @@ struct tgnn_trainer {
     TGB_CUDA(cudaMemset(av, 0, sizeof(float) * L.total));
     set_params(host_init_params(m, seed).data());
     step_alloc(w, m, cap_B, cap_U, m.num_nodes);
+    // >= 2 slots: the graph-mode pipeline plans barrier b + 1 into the other slot
+    subs = std::max(subs, 2);
     plans.resize(static_cast<size_t>(subs));
     views.resize(static_cast<size_t>(subs));
     for (int s = 0; s < subs; ++s) {
@@ -488,8 +492,11 @@ struct tgnn_run {
   bool use_graphs = false;
   BarrierDesc* d_desc = nullptr;
   int* d_ctr = nullptr;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // barrier b runs exec[b % 2]
+  int64_t prepared = -1;  // barrier whose plan + read view are ready in plans/views[b % 2]
+  cudaEvent_t ev_fork = nullptr, ev_written = nullptr, ev_next = nullptr;
+  cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
   // validation / metrics rows (run_training, trainer.hpp:725-743)
   int64_t val_begin = 0, val_end = 0, eval_batch = 0;
@@ -511,8 +518,16 @@ struct tgnn_run {
     if (ev_tail) cudaEventDestroy(ev_tail);
     if (ev_head) cudaEventDestroy(ev_head);
     if (ev_comm) cudaEventDestroy(ev_comm);
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
+    for (int p = 0; p < 2; ++p) {
+      if (exec[p]) cudaGraphExecDestroy(exec[p]);
+      if (graph[p]) cudaGraphDestroy(graph[p]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_written) cudaEventDestroy(ev_written);
+    if (ev_next) cudaEventDestroy(ev_next);
+    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin};
+    for (cudaEvent_t e : more)
+      if (e) cudaEventDestroy(e);
     if (d_desc) cudaFree(d_desc);
     if (d_ctr) cudaFree(d_ctr);
     if (gcomm) nccl::api().CommDestroy(gcomm);
@@ -600,6 +615,7 @@ void plan_explicit(tgnn_trainer* tr, int slot, int64_t begin, int64_t end, const
 // One barrier of a run on this rank (TrainerCore::iterate + the daemon's
 // read/write brackets + average_active_grads + Adam::step).
 void run_barrier(tgnn_run* r, int64_t b) {
+  r->prepared = -1;  // the direct path reuses slot 0
   tgnn_ctx* ctx = r->ctx;
   tgnn_trainer* tr = r->tr.get();
   cudaStream_t s = ctx->stream;
@@ -704,60 +720,109 @@ void allreduce_bucketed(tgnn_run* r, cudaStream_t s) {
 }
 
 // Graph body (j == 1): the same launch sequence for every barrier; all
-// per-barrier values come from d_desc[*d_ctr].
-void barrier_body_dev(tgnn_run* r) {
+// per-barrier values come from d_desc[*d_ctr]. Barrier b runs on slot p =
+// b % 2 (plan + read view prepared by the previous barrier) and prepares
+// barrier b + 1 in slot 1 - p on the aux stream: its sampling / plan / routing
+// sort overlaps this barrier's GRU, and its memory read (after this barrier's
+// writes, and the next sweep's reset) overlaps this barrier's backward.
+void barrier_body_dev(tgnn_run* r, int p) {
   tgnn_ctx* ctx = r->ctx;
   tgnn_trainer* tr = r->tr.get();
-  cudaStream_t s = ctx->stream;
+  cudaStream_t s = ctx->stream, aux = ctx->aux;
   StepCtx sc = tr->sc();
   sc.d_ctr = r->d_ctr;
-  DPlan& pl = tr->plans[0];
-  DView& vw = tr->views[0];
-  reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, s);
-  select_plan_args_launch(pl.args, r->d_desc, r->d_ctr, s);
-  plan_launch(r->g->d, pl, s, ctx->side);
-  gather_view_launch(pl, r->mem->d, vw, s);
-  substep_gru_launch(sc, pl, vw, s);
-  root_writes_launch(sc, pl, vw, s, r->group_size > 1 ? nullptr : &r->mem->d);
-  const size_t pb = tr->w.wpack_bytes;
-  const int cap = 2 * tr->cap_B;
-  if (r->group_size > 1) {
-    NCCL_CHECK(nccl::api().GroupStart());
-    for (int mm = 0; mm < r->tc.i; ++mm)
-      NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb,
-                                       pb, ncclChar, mm, r->gcomm, s));
-    NCCL_CHECK(nccl::api().GroupEnd());
-    std::vector<WriteSet> sets;
-    for (int mm = 0; mm < r->tc.i; ++mm)
-      sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap, tr->m.d_mem));
-    apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+  sc.packed = true;  // by the previous barrier's Adam (or the prologue)
+  DPlan& pl = tr->plans[static_cast<size_t>(p)];
+  DView& vw = tr->views[static_cast<size_t>(p)];
+  DPlan& nx = tr->plans[static_cast<size_t>(1 - p)];
+  DView& nv = tr->views[static_cast<size_t>(1 - p)];
+  // fork: plan of barrier b + 1 (routing sort on the side stream)
+  TGB_CUDA(cudaEventRecord(r->ev_fork, s));
+  TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_fork, 0));
+  select_plan_args_launch(nx.args, r->d_desc, r->d_ctr, aux, 1);
+  plan_launch(r->g->d, nx, aux, ctx->side);
+  // branch: gradient zeroing now, the root writes after the GRU, the loss later
+  cudaStream_t br = ctx->br;
+  TGB_CUDA(cudaStreamWaitEvent(br, r->ev_fork, 0));
+  TGB_CUDA(cudaMemsetAsync(tr->grads, 0, sizeof(float) * tr->L.total, br));
+  TGB_CUDA(cudaEventRecord(r->ev_gzero, br));
+  sc.br = br;
+  sc.ev_g_zero = r->ev_gzero;
+  sc.ev_br_dec = r->ev_dec;
+  sc.ev_br_join = r->ev_brjoin;
+  // this barrier: its plan was sorted inside the previous graph
+  cudaEvent_t sorted = pl.ev_sorted;
+  pl.ev_sorted = nullptr;
+  try {
+    substep_gru_launch(sc, pl, vw, s);
+    cudaStream_t ws = s;
+    if (r->group_size == 1) {  // single writer: direct writes on the branch
+      TGB_CUDA(cudaEventRecord(r->ev_gru, s));
+      TGB_CUDA(cudaStreamWaitEvent(br, r->ev_gru, 0));
+      ws = br;
+    }
+    root_writes_launch(sc, pl, vw, ws, r->group_size > 1 ? nullptr : &r->mem->d);
+    const size_t pb = tr->w.wpack_bytes;
+    const int cap = 2 * tr->cap_B;
+    if (r->group_size > 1) {
+      NCCL_CHECK(nccl::api().GroupStart());
+      for (int mm = 0; mm < r->tc.i; ++mm)
+        NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb,
+                                         pb, ncclChar, mm, r->gcomm, s));
+      NCCL_CHECK(nccl::api().GroupEnd());
+      std::vector<WriteSet> sets;
+      for (int mm = 0; mm < r->tc.i; ++mm)
+        sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap, tr->m.d_mem));
+      apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+    }
+    // join: the next barrier reads the memory copy once this barrier's writes landed
+    TGB_CUDA(cudaEventRecord(r->ev_written, ws));
+    TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_written, 0));
+    reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, aux, 1);
+    gather_view_launch(nx, r->mem->d, nv, aux);
+    TGB_CUDA(cudaStreamWaitEvent(aux, nx.ev_sorted, 0));
+    TGB_CUDA(cudaEventRecord(r->ev_next, aux));
+    if (r->nranks > 1) sc.ev_tail_grads = r->ev_tail;
+    substep_rest_launch(sc, pl, vw, r->d_losses, s);
+    if (r->nranks > 1) allreduce_bucketed(r, s);
+    adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr);
+    TGB_CUDA(cudaStreamWaitEvent(s, r->ev_next, 0));
+    incr_launch(r->d_ctr, s);
+  } catch (...) {
+    pl.ev_sorted = sorted;
+    throw;
   }
-  if (r->nranks > 1) sc.ev_tail_grads = r->ev_tail;
-  substep_rest_launch(sc, pl, vw, r->d_losses, s);
-  if (r->nranks > 1) allreduce_bucketed(r, s);
-  adam_launch(tr->params, tr->grads, tr->am, tr->av, tr->L.total, 0.f, 1.f, 1.f, 1.f, s, r->d_desc, r->d_ctr);
-  incr_launch(r->d_ctr, s);
+  pl.ev_sorted = sorted;
 }
 
 void build_graph(tgnn_run* r) {
   cudaStream_t s = r->ctx->stream;
   gemm_kernels_prepare();
   TGB_CUDA(cudaStreamSynchronize(s));
-  TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  try {
-    barrier_body_dev(r);
-  } catch (...) {
-    cudaGraph_t g = nullptr;
-    cudaStreamEndCapture(s, &g);
-    if (g) cudaGraphDestroy(g);
-    throw;
+  if (!r->ev_fork) {
+    TGB_CUDA(cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming));
+    TGB_CUDA(cudaEventCreateWithFlags(&r->ev_written, cudaEventDisableTiming));
+    TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
+    cudaEvent_t* more[] = {&r->ev_gru, &r->ev_gzero, &r->ev_dec, &r->ev_brjoin};
+    for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
-  TGB_CUDA(cudaStreamEndCapture(s, &r->graph));
-  TGB_CUDA(cudaGraphInstantiate(&r->exec, r->graph, 0));
+  for (int p = 0; p < 2; ++p) {
+    TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      barrier_body_dev(r, p);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    TGB_CUDA(cudaStreamEndCapture(s, &r->graph[p]));
+    TGB_CUDA(cudaGraphInstantiate(&r->exec[p], r->graph[p], 0));
+  }
   size_t n = 0;
-  TGB_CUDA(cudaGraphGetNodes(r->graph, nullptr, &n));
+  TGB_CUDA(cudaGraphGetNodes(r->graph[0], nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
-  TGB_CUDA(cudaGraphGetNodes(r->graph, nodes.data(), &n));
+  TGB_CUDA(cudaGraphGetNodes(r->graph[0], nodes.data(), &n));
   int64_t kernels = 0;
   for (auto nd : nodes) {
     cudaGraphNodeType ty;
@@ -765,6 +830,24 @@ void build_graph(tgnn_run* r) {
     if (ty == cudaGraphNodeTypeKernel) ++kernels;
   }
   r->launches = kernels;
+}
+
+// Graph-mode prologue: plan + read of barrier b into slot b % 2 (the reset of
+// its sweep first), as barrier b - 1's graph would have left them.
+void prepare_barrier(tgnn_run* r, int64_t b) {
+  tgnn_ctx* ctx = r->ctx;
+  tgnn_trainer* tr = r->tr.get();
+  cudaStream_t s = ctx->stream;
+  DPlan& pl = tr->plans[static_cast<size_t>(b & 1)];
+  set_int_kernel<<<1, 1, 0, s>>>(r->d_ctr, static_cast<int>(b));
+  TGB_CUDA(cudaGetLastError());
+  reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, s, 0);
+  select_plan_args_launch(pl.args, r->d_desc, r->d_ctr, s, 0);
+  plan_launch(r->g->d, pl, s, ctx->side);
+  gather_view_launch(pl, r->mem->d, tr->views[static_cast<size_t>(b & 1)], s);
+  TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));
+  pack_weights(tr->sc(), s);
+  r->prepared = b;
 }
 
 }  // namespace
@@ -845,6 +928,8 @@ int tgnn_ctx_create(int device, tgnn_ctx** out) {
   TGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   TGB_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   TGB_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
+  TGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  TGB_CUDA(cudaStreamCreateWithFlags(&c->br, cudaStreamNonBlocking));
   c->d_flag = dalloc<int>(1);
   TGB_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
   *out = c;
@@ -858,6 +943,10 @@ int tgnn_ctx_destroy(tgnn_ctx* ctx) {
   cudaFree(ctx->d_flag);
   cudaStreamSynchronize(ctx->side);
   cudaStreamSynchronize(ctx->comm);
+  cudaStreamSynchronize(ctx->aux);
+  cudaStreamSynchronize(ctx->br);
+  cudaStreamDestroy(ctx->aux);
+  cudaStreamDestroy(ctx->br);
   cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->comm);
   cudaStreamDestroy(ctx->stream);
@@ -1510,7 +1599,8 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
   TGB_CUDA(cudaEventCreate(&r->ev_t0));
   r->use_graphs = opt->use_graphs != 0 && r->tc.j == 1;
   if (r->use_graphs) {
-    const int64_t nb = std::max<int64_t>(r->sched.barriers, 1);
+    // one idle entry past the end: the last barrier prepares an empty plan
+    const int64_t nb = r->sched.barriers + 1;
     std::vector<BarrierDesc> desc(static_cast<size_t>(nb));
     for (int64_t b = 0; b < r->sched.barriers; ++b) {
       const host::Task t = r->sched.task(r->rank, b);
@@ -1596,10 +1686,10 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
       eval_here = true;
     }
     if (r->use_graphs) {
-      if (!r->exec) build_graph(r);
-      set_int_kernel<<<1, 1, 0, r->ctx->stream>>>(r->d_ctr, static_cast<int>(b));
-      TGB_CUDA(cudaGetLastError());
-      for (int64_t x = b; x < seg_end; ++x) TGB_CUDA(cudaGraphLaunch(r->exec, r->ctx->stream));
+      if (!r->exec[0]) build_graph(r);
+      if (r->prepared != b) prepare_barrier(r, b);
+      for (int64_t x = b; x < seg_end; ++x) TGB_CUDA(cudaGraphLaunch(r->exec[x & 1], r->ctx->stream));
+      r->prepared = seg_end;
       r->tr->adam_t = seg_end;
     } else {
       for (int64_t x = b; x < seg_end; ++x) run_barrier(r, x);
@@ -1699,7 +1789,7 @@ int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out) {
   API_BEGIN
   r->ctx->use();
   if (r->use_graphs) {
-    if (!r->exec) build_graph(r);
+    if (!r->exec[0]) build_graph(r);
     *out = r->launches;
     return 0;
   }

@@ -284,8 +284,8 @@ __global__ void gather_view_kernel(DPlan pl, DMem st, DView vw) {
 __global__ void set_args_kernel(PlanArgs* dst, PlanArgs a) { *dst = a; }
 
 __global__ void select_args_kernel(const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
-                                   PlanArgs* dst) {
-  *dst = desc[*ctr].args;
+                                   int offset, PlanArgs* dst) {
+  *dst = desc[*ctr + offset].args;
 }
 
 __global__ void sample_queries_kernel(DGraph g, const int32_t* __restrict__ nodes,
@@ -314,8 +314,9 @@ __global__ void sample_queries_kernel(DGraph g, const int32_t* __restrict__ node
 
 }  // namespace
 
-void select_plan_args_launch(PlanArgs* dst, const BarrierDesc* desc, const int* ctr, cudaStream_t s) {
-  select_args_kernel<<<1, 1, 0, s>>>(desc, ctr, dst);
+void select_plan_args_launch(PlanArgs* dst, const BarrierDesc* desc, const int* ctr, cudaStream_t s,
+                             int offset) {
+  select_args_kernel<<<1, 1, 0, s>>>(desc, ctr, offset, dst);
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -13,7 +13,9 @@ void negatives_only_launch(const DGraph& g, const PlanArgs* args, int count, int
                            cudaStream_t s);
 void set_plan_args_launch(PlanArgs* dst, const PlanArgs& a, cudaStream_t s);
 // Graph mode: the plan args of barrier *ctr from the descriptor table.
-void select_plan_args_launch(PlanArgs* dst, const BarrierDesc* desc, const int* ctr, cudaStream_t s);
+// (offset 1: the next barrier's plan, prepared one barrier ahead)
+void select_plan_args_launch(PlanArgs* dst, const BarrierDesc* desc, const int* ctr, cudaStream_t s,
+                             int offset = 0);
 // Batched sample_recent_neighbors over arbitrary (node, time) queries.
 void sample_queries_launch(const DGraph& g, const int32_t* nodes, const double* times, int count,
                            int n, int32_t* nbr_node, int32_t* nbr_event, double* nbr_dt,

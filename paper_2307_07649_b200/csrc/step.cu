@@ -607,7 +607,9 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
 
 // Routing pass 1: fixed chunks of kChunk sorted items; runs fully inside a
 // chunk are written directly, runs that cross a chunk edge leave partials.
-// Row layout of dNodeAcc: {sum dq | sum dK | sum dV} (3 d_attn). Item rows are
+// Row layout of dNodeAcc: {sum dq | sum dK | sum dV} (3 d_attn). One warp per
+// (chunk, part): part 0 sums the dq rows of root items, parts 1 / 2 the dK /
+// dV rows of pair items, so three warps share a chunk's latency. Item rows are
 // fetched kAhead at a time, then accumulated strictly in item order.
 template <int LANES>
 __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__ dQ,
@@ -619,52 +621,59 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
   const int nchunks = (items + kChunk - 1) / kChunk;
   const int lane = threadIdx.x & 31;
   const int da = D.da, w3 = 3 * D.da;
-  constexpr int kAhead = 8;
-  for (int64_t c = gwarp(); c < nchunks; c += nwarp()) {
+  constexpr int kAhead = 16;
+  static_assert(kChunk == 32, "one sorted item per lane");
+  for (int64_t gw = gwarp(); gw < 3ll * nchunks; gw += nwarp()) {
+    const int64_t c = gw / 3;
+    const int part = static_cast<int>(gw % 3);
     const int i0 = static_cast<int>(c) * kChunk;
     const int i1 = min(items, i0 + kChunk);
-    const bool cont_in = i0 > 0 && pl.item_key_s[i0 - 1] == pl.item_key_s[i0];
-    const bool cont_out = i1 < items && pl.item_key_s[i1] == pl.item_key_s[i1 - 1];
-    float acc[3 * LANES];
+    const int n = i1 - i0;
+    // the chunk's keys / values, one per lane, and where each run ends
+    const int it = i0 + lane;
+    const int my_key = it < i1 ? pl.item_key_s[it] : -1;
+    const int my_val = it < i1 ? pl.item_val_s[it] : -1;
+    const int nxt_key = it + 1 < items ? pl.item_key_s[it + 1] : -2;
+    const unsigned ends = __ballot_sync(0xffffffffu, it < i1 && (it + 1 == i1 || nxt_key != my_key));
+    const int prev_key = (lane == 0 && i0 > 0) ? pl.item_key_s[i0 - 1] : -3;
+    const bool cont_in = __shfl_sync(0xffffffffu, prev_key == my_key, 0) && i0 > 0;
+    const bool cont_out =
+        i1 < items && __shfl_sync(0xffffffffu, nxt_key == my_key ? 1 : 0, n - 1) != 0;
+    // this part's rows: dq of roots (part 0), dK / dV of pairs (parts 1 / 2)
+    const bool mine = my_val >= 0 && (part == 0 ? my_val < R : my_val >= R);
+    const float* my_row = !mine ? nullptr
+                        : part == 0 ? dQ + static_cast<int64_t>(my_val) * da
+                                    : dKV + static_cast<int64_t>(my_val - R) * 2 * da + (part - 1) * da;
+    const unsigned have = __ballot_sync(0xffffffffu, mine);
+    float acc[LANES];
 #pragma unroll
-    for (int x = 0; x < 3 * LANES; ++x) acc[x] = 0.0f;
-    int run_start = i0;
-    for (int ib = i0; ib < i1; ib += kAhead) {
-      float ld[kAhead][3 * LANES];
+    for (int x = 0; x < LANES; ++x) acc[x] = 0.0f;
+    bool at_start = true;  // the current run starts at i0
+    for (int ib = 0; ib < n; ib += kAhead) {
+      float ld[kAhead][LANES];
 #pragma unroll
       for (int a = 0; a < kAhead; ++a) {
-        const int i = ib + a;
-        const int v = i < i1 ? pl.item_val_s[i] : -1;
+        const int x = (ib + a) & 31;
+        const float* row = reinterpret_cast<const float*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_row), x));
+        const bool ok = ib + a < n && ((have >> x) & 1u);
 #pragma unroll
         for (int cc = 0; cc < LANES; ++cc) {
           const int f = lane + 32 * cc;
-          float q = 0.0f, k = 0.0f, vv = 0.0f;
-          if (v >= 0 && f < da) {
-            if (v < R) {
-              q = dQ[static_cast<int64_t>(v) * da + f];
-            } else {
-              const float* row = dKV + static_cast<int64_t>(v - R) * 2 * da;
-              k = row[f];
-              vv = row[da + f];
-            }
-          }
-          ld[a][cc] = q;
-          ld[a][LANES + cc] = k;
-          ld[a][2 * LANES + cc] = vv;
+          ld[a][cc] = (ok && f < da) ? row[f] : 0.0f;
         }
       }
 #pragma unroll
       for (int a = 0; a < kAhead; ++a) {
-        const int i = ib + a;
-        if (i >= i1) break;
+        const int x = ib + a;
+        if (x >= n) break;
 #pragma unroll
-        for (int x = 0; x < 3 * LANES; ++x) acc[x] += ld[a][x];
-        const bool run_end = (i + 1 == i1) || pl.item_key_s[i + 1] != pl.item_key_s[i];
-        if (run_end) {
-          const int key = pl.item_key_s[i];
+        for (int y = 0; y < LANES; ++y) acc[y] += ld[a][y];
+        if ((ends >> x) & 1u) {
+          const int key = __shfl_sync(0xffffffffu, my_key, x & 31);
           float* dst;
-          const bool first = run_start == i0 && cont_in;
-          const bool last = (i + 1 == i1) && cont_out;
+          const bool first = at_start && cont_in;
+          const bool last = (x + 1 == n) && cont_out;
           const bool direct = !first && !last;
           if (first) dst = part_first + c * w3;
           else if (last) dst = part_last + c * w3;
@@ -673,21 +682,13 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
           for (int cc = 0; cc < LANES; ++cc) {
             const int f = lane + 32 * cc;
             if (f < da) {
-              if (dst) {
-                dst[f] = acc[cc];
-                dst[da + f] = acc[LANES + cc];
-                dst[2 * da + f] = acc[2 * LANES + cc];
-              }
-              if (direct) {
-                bf_put(bf.dNA, key, f, acc[cc]);
-                bf_put(bf.dNA, key, da + f, acc[LANES + cc]);
-                bf_put(bf.dNA, key, 2 * da + f, acc[2 * LANES + cc]);
-              }
+              if (dst) dst[part * da + f] = acc[cc];
+              if (direct) bf_put(bf.dNA, key, part * da + f, acc[cc]);
             }
           }
 #pragma unroll
-          for (int x = 0; x < 3 * LANES; ++x) acc[x] = 0.0f;
-          run_start = i + 1;
+          for (int y = 0; y < LANES; ++y) acc[y] = 0.0f;
+          at_start = false;
         }
       }
     }
@@ -975,11 +976,46 @@ __global__ void fill_kernel(int32_t* p, int64_t n, int32_t v) {
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) p[x] = v;
 }
 
+// Weight-pack map for the fused Adam: every flat parameter of the tensors the
+// TMA engine consumes is also written, as a bf16 hi/lo pair, into its packed
+// operand(s) (the same placements as pack_weights_kernel). Per tensor: up to
+// three column ranges [c_lo, c_hi) -> (dst, r0, dst col = c0 + c - c_lo).
+struct PackDest {
+  BfMat dst;
+  int r0, c0, c_lo, c_hi;
+};
+struct PackTensor {
+  int64_t off, n;
+  int cols, nd;
+  PackDest d[3];
+};
+constexpr int kMaxPackT = 16;
+struct PackMap {
+  PackTensor t[kMaxPackT];
+  int count;
+};
+
+__device__ __forceinline__ void pack_elem(const PackMap& pm, int64_t x, float v) {
+  for (int k = 0; k < pm.count; ++k) {
+    const PackTensor& T = pm.t[k];
+    const int64_t local = x - T.off;
+    if (local < 0 || local >= T.n) continue;
+    const int r = static_cast<int>(local / T.cols), c = static_cast<int>(local % T.cols);
+    for (int q = 0; q < T.nd; ++q) {
+      const PackDest& D = T.d[q];
+      if (c >= D.c_lo && c < D.c_hi) bf_put(D.dst, D.r0 + r, D.c0 + (c - D.c_lo), v);
+    }
+    return;
+  }
+}
+
 // Dense Adam, optimizer.hpp:40-56 (fp32 state). With a descriptor table the
 // step scalars come from the entry of the device barrier counter.
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, int64_t n, float lr, float c1, float c2,
-                            float scale, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr) {
+                            float scale, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
+                            const __grid_constant__ PackMap pm, int64_t pack_lo, int64_t pack_hi,
+                            int64_t skip_lo, int64_t skip_hi) {
   if (desc) {
     const BarrierDesc& d = desc[*ctr];
     lr = d.lr;
@@ -1010,14 +1046,23 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     p4[x] = pp;
     m4[x] = mm;
     v4[x] = vv;
+    if (pm.count && 4 * x + 3 >= pack_lo && 4 * x < pack_hi && !(4 * x >= skip_lo && 4 * x + 3 < skip_hi)) {
+      pack_elem(pm, 4 * x, pp.x);
+      pack_elem(pm, 4 * x + 1, pp.y);
+      pack_elem(pm, 4 * x + 2, pp.z);
+      pack_elem(pm, 4 * x + 3, pp.w);
+    }
   }
-  for (int64_t x = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; x < n; x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+  for (int64_t x = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; x < n; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     upd(p[x], g[x], m[x], v[x]);
+    if (pm.count) pack_elem(pm, x, p[x]);
+  }
 }
 
 // reset_state (memory_store.hpp:43-50) when the barrier's descriptor asks for it.
-__global__ void reset_cond_kernel(DMem st, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr) {
-  if (!desc[*ctr].reset) return;
+__global__ void reset_cond_kernel(DMem st, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
+                                  int offset) {
+  if (!desc[*ctr + offset].reset) return;
   const int64_t n = st.N * st.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 3 * n; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (x < n) st.memory[x] = 0.0f;
@@ -1394,7 +1439,61 @@ void pack_weights_launch(const StepCtx& c, cudaStream_t s) {
   TGB_CUDA(cudaGetLastError());
 }
 
+// The same placements per source tensor, for the fused Adam.
+PackMap make_pack_map(const StepCtx& c, int64_t& lo, int64_t& hi, int64_t& skip_lo, int64_t& skip_hi) {
+  const ModelDims& m = c.m;
+  const ParamLayout& L = c.L;
+  const StepBf& b = c.w->bf;
+  const int d = static_cast<int>(m.d_mem), gin = static_cast<int>(m.gin()), md = static_cast<int>(m.mail_dim());
+  const int da = static_cast<int>(m.d_attn), q = static_cast<int>(m.q_in()), kv = static_cast<int>(m.kv_in());
+  const int nd = static_cast<int>(m.node_dim());
+  PackMap pm{};
+  auto tensor = [&](int id) -> PackTensor& {
+    PackTensor& T = pm.t[pm.count++];
+    T.off = L.off[id];
+    T.n = L.rows[id] * L.cols[id];
+    T.cols = static_cast<int>(L.cols[id]);
+    T.nd = 0;
+    return T;
+  };
+  auto dest = [](PackTensor& T, const BfMat& dst, int r0, int c0, int c_lo, int c_hi) {
+    if (c_hi > c_lo) T.d[T.nd++] = PackDest{dst, r0, c0, c_lo, c_hi};
+  };
+  { PackTensor& T = tensor(tWz); dest(T, b.Wzr, 0, 0, 0, gin); }
+  { PackTensor& T = tensor(tBz); dest(T, b.Wzr, 0, gin, 0, 1); }
+  { PackTensor& T = tensor(tWr); dest(T, b.Wzr, d, 0, 0, gin); }
+  { PackTensor& T = tensor(tBr); dest(T, b.Wzr, d, gin, 0, 1); }
+  { PackTensor& T = tensor(tWh); dest(T, b.Whm, 0, 0, 0, md); dest(T, b.Whs, 0, 0, md, gin); }
+  { PackTensor& T = tensor(tBh); dest(T, b.Whs, 0, d, 0, 1); }
+  { PackTensor& T = tensor(tWq); dest(T, b.Wq, 0, 0, 0, q); dest(T, b.Wst, 0, 0, 0, nd); }
+  { PackTensor& T = tensor(tBq); dest(T, b.Wq, 0, q, 0, 1); }
+  { PackTensor& T = tensor(tWk); dest(T, b.Wkv, 0, 0, 0, kv); dest(T, b.Wst, da, 0, 0, nd); }
+  { PackTensor& T = tensor(tBk); dest(T, b.Wkv, 0, kv, 0, 1); }
+  { PackTensor& T = tensor(tWv); dest(T, b.Wkv, da, 0, 0, kv); dest(T, b.Wst, 2 * da, 0, 0, nd); }
+  { PackTensor& T = tensor(tBv); dest(T, b.Wkv, da, kv, 0, 1); }
+  { PackTensor& T = tensor(tW1); dest(T, b.W1a, 0, 0, 0, da); dest(T, b.W1b, 0, 0, da, 2 * da); dest(T, b.W1, 0, 0, 0, 2 * da); }
+  lo = L.off[tWz];
+  hi = L.off[tW1] + L.rows[tW1] * L.cols[tW1];
+  skip_lo = L.off[tStatic];  // the static table (the bulk) has no packed copy
+  skip_hi = L.off[tW1];
+  return pm;
+}
+
 }  // namespace
+
+void pack_weights(const StepCtx& c, cudaStream_t s) {
+  if (gemm_impl() == kGemmTma) pack_weights_launch(c, s);
+}
+
+void adam_pack_launch(const StepCtx& c, float* m, float* v, cudaStream_t s, const BarrierDesc* desc,
+                      const int* ctr) {
+  int64_t lo = 0, hi = 0, slo = 0, shi = 0;
+  const PackMap pm = gemm_impl() == kGemmTma ? make_pack_map(c, lo, hi, slo, shi) : PackMap{};
+  const int64_t n = c.L.total;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
+  adam_kernel<<<blocks, 256, 0, s>>>(c.params, c.grads, m, v, n, 0.f, 1.f, 1.f, 1.f, desc, ctr, pm, lo, hi, slo, shi);
+  TGB_CUDA(cudaGetLastError());
+}
 
 void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s) {
   const ModelDims& m = c.m;
@@ -1413,7 +1512,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   bfx.d8d = w.bf.d8d;
   // ---- GRU freshen (K5)
   c.mark(phGruFwd, s);
-  if (tma) pack_weights_launch(c, s);
+  if (tma && !c.packed) pack_weights_launch(c, s);
   {
     const int stage = (D.gin + 1 + D.dt + 7) / 8 * 8;
     assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, sizeof(float) * stage * kWarps, s>>>(
@@ -1523,7 +1622,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   bfx.d8d = w.bf.d8d;
   const StepBf& B = w.bf;
 
-  TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));
+  if (!c.br) TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));  // else zeroed on the branch
   const int eblocks = 4 * kSMs;
 
   attn_forward_launch(c, pl, s);
@@ -1545,11 +1644,23 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   decoder_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(
       D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, tma ? nullptr : w.Dhid,
       tma ? nullptr : w.Hin, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
-  loss_kernel<<<1, 1024, 0, s>>>(pl, w.loss_terms, loss_out, c.d_ctr, c.d_numeric_flag);
-
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
   c.mark(phDecoderBwd, s);
-  decoder_small_grads_kernel<<<dh + 1, 256, 0, s>>>(pl, dh, w.dlogit, w.HID, G + L.off[tW2], G + L.off[tB2]);
+  {
+    // the loss and the W2 / b2 gradient are leaves: on the branch stream when given
+    cudaStream_t ls = s;
+    if (c.br) {
+      TGB_CUDA(cudaEventRecord(c.ev_br_dec, s));
+      TGB_CUDA(cudaStreamWaitEvent(c.br, c.ev_br_dec, 0));
+      ls = c.br;
+    }
+    loss_kernel<<<1, 1024, 0, ls>>>(pl, w.loss_terms, loss_out, c.d_ctr, c.d_numeric_flag);
+    decoder_small_grads_kernel<<<dh + 1, 256, 0, ls>>>(pl, dh, w.dlogit, w.HID, G + L.off[tW2], G + L.off[tB2]);
+    if (c.br) {
+      TGB_CUDA(cudaEventRecord(c.ev_br_join, c.br));
+      TGB_CUDA(cudaStreamWaitEvent(s, c.ev_g_zero, 0));
+    }
+  }
   if (!tma) {
     GemmGroup gg;  // decoder weight gradients on the fp32-operand engines
     {
@@ -1584,7 +1695,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     const int lanes = (da + 31) / 32;
     auto chunk = lanes <= 1 ? routing_chunk_kernel<1> : lanes <= 2 ? routing_chunk_kernel<2>
                : lanes <= 4 ? routing_chunk_kernel<4> : routing_chunk_kernel<8>;
-    chunk<<<row_blocks(nchunks), 32 * kWarps, 0, s>>>(D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
+    chunk<<<row_blocks(3 * nchunks), 32 * kWarps, 0, s>>>(D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
                                                       part_first, part_last, bfx);
     const int fix_threads = std::min(1024, (3 * da + 31) / 32 * 32);
     routing_fixup_kernel<<<std::min(U, 8 * kSMs), fix_threads, 0, s>>>(D, pl, tma ? nullptr : w.dNodeAcc,
@@ -1626,6 +1737,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   c.mark(phGruBwd, s);
   gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
                                           G + L.off[tStatic], bfx, U);
+  if (c.br) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_br_join, 0));
   if (c.ev_tail_grads) TGB_CUDA(cudaEventRecord(c.ev_tail_grads, s));
   if (tma) {
     TcGroup tg;
@@ -1728,12 +1840,12 @@ void adam_launch(float* params, const float* grads, float* m, float* v, int64_t 
                  float c1, float c2, float grad_scale, cudaStream_t s, const BarrierDesc* desc,
                  const int* ctr) {
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
-  adam_kernel<<<blocks, 256, 0, s>>>(params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr);
+  adam_kernel<<<blocks, 256, 0, s>>>(params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr, PackMap{}, 0, 0, 0, 0);
   TGB_CUDA(cudaGetLastError());
 }
 
-void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s) {
-  reset_cond_kernel<<<4 * kSMs, 256, 0, s>>>(st, desc, ctr);
+void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s, int offset) {
+  reset_cond_kernel<<<4 * kSMs, 256, 0, s>>>(st, desc, ctr, offset);
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -111,6 +111,12 @@ struct StepCtx {
   // the attention / decoder weight gradients and the static-table scatter), so
   // its all-reduce can overlap the rest of the GRU backward.
   cudaEvent_t ev_tail_grads = nullptr;
+  // Branch stream (graph mode): the caller zeroes the gradients on it
+  // (recording ev_g_zero); substep_rest runs the loss and the W2 / b2
+  // gradient there (ev_br_dec -> ev_br_join), off the critical path.
+  cudaStream_t br = nullptr;
+  bool packed = false;  // the TMA weight operands are current (packed by the fused Adam)
+  cudaEvent_t ev_g_zero = nullptr, ev_br_dec = nullptr, ev_br_join = nullptr;
   void mark(int slot, cudaStream_t s) const {
     if (marks) marks->mark(slot, s);
   }
@@ -167,8 +173,15 @@ void reset_state_launch(DMem& st, cudaStream_t s);
 void adam_launch(float* params, const float* grads, float* m, float* v, int64_t n, float lr,
                  float c1, float c2, float grad_scale, cudaStream_t s,
                  const BarrierDesc* desc = nullptr, const int* ctr = nullptr);
+// Graph mode: Adam with the step scalars of desc[*ctr] that also refreshes the
+// packed bf16 hi/lo weight operands of the TMA engine (pack_weights), so the
+// next step's GEMMs need no separate pack.
+void adam_pack_launch(const StepCtx& c, float* m, float* v, cudaStream_t s, const BarrierDesc* desc,
+                      const int* ctr);
+// Packs the TMA engine's weight operands from the fp32 parameters.
+void pack_weights(const StepCtx& c, cudaStream_t s);
 // Graph mode helpers: reset the memory copy if desc[*ctr].reset; ++*ctr.
-void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s);
+void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s, int offset = 0);
 void incr_launch(int* ctr, cudaStream_t s);
 
 }  // namespace tgb
