@@ -139,6 +139,8 @@ __device__ __forceinline__ bool tile_info(const TcParams& gp, int t, TileInfo& t
 
 // Persistent CTA: static round-robin over the flattened tiles of the group.
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcParams gp) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int kStageB = gp.stage_bytes, kBTileB = gp.b_tile_bytes;
@@ -324,6 +326,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 }
 
 __global__ void tc_splitk_reduce_kernel(const __grid_constant__ TcParams gp) {
+  pdl_wait();
+  pdl_trigger();
   const TcProblem& P = gp.p[blockIdx.y];
   if (P.splits <= 1) return;
   const int64_t total = static_cast<int64_t>(P.M) * P.N;
@@ -343,6 +347,8 @@ __global__ void tc_splitk_reduce_kernel(const __grid_constant__ TcParams gp) {
 
 __global__ void bf_from_f32_kernel(BfMat m, const float* __restrict__ src, int64_t rows, int64_t cols,
                                    int64_t ld_src) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = rows * cols;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x)
     bf_put(m, x / cols, x % cols, src[(x / cols) * ld_src + x % cols]);
@@ -406,7 +412,7 @@ BfMat bf_alloc(int64_t rows, int64_t cols) {
 void bf_from_f32(const BfMat& m, const float* src, int64_t rows, int64_t cols, int64_t ld_src, cudaStream_t s) {
   if (rows * cols == 0) return;
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(rows * cols, 256), 4 * kSMs));
-  bf_from_f32_kernel<<<blocks, 256, 0, s>>>(m, src, rows, cols, ld_src);
+  launch_pdl(bf_from_f32_kernel, dim3(blocks), dim3(256), 0, s, m, src, rows, cols, ld_src);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -478,10 +484,10 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s) {
   if (ctas_per_sm < 1) ctas_per_sm = 1;
   if (ctas_per_sm * cols > 512) ctas_per_sm = 512 / cols;
   const int grid = std::min(gp.tile_base[g.count], kSMs * ctas_per_sm);
-  tc_gemm_kernel<<<grid, kThreads, smem, s>>>(gp);
+  launch_pdl(tc_gemm_kernel, dim3(grid), dim3(kThreads), smem, s, gp);
   TGB_CUDA(cudaGetLastError());
   if (any_split) {
-    tc_splitk_reduce_kernel<<<dim3(64, g.count), 256, 0, s>>>(gp);
+    launch_pdl(tc_splitk_reduce_kernel, dim3(dim3(64, g.count)), dim3(256), 0, s, gp);
     TGB_CUDA(cudaGetLastError());
   }
 }

@@ -50,6 +50,8 @@ __device__ int block_excl_scan(int v, int* smem_warp, int& total) {
 // global-batch stream (trainer.hpp:539-544).
 __global__ void negatives_kernel(const PlanArgs* __restrict__ args, int64_t N, int64_t boundary,
                                  int32_t* __restrict__ negs) {
+  pdl_wait();
+  pdl_trigger();
   const PlanArgs a = *args;
   if (!a.valid || a.neg_mode != 1) return;
   const int64_t B = a.end - a.begin;
@@ -68,6 +70,8 @@ __global__ void negatives_kernel(const PlanArgs* __restrict__ args, int64_t N, i
 // the event's destination.
 __global__ void eval_negatives_kernel(const PlanArgs* __restrict__ args, DGraph g, int per_event,
                                       int32_t* __restrict__ negs) {
+  pdl_wait();
+  pdl_trigger();
   const PlanArgs a = *args;
   if (!a.valid || a.neg_mode != 2 || per_event <= 0) return;
   const int64_t total = (a.end - a.begin) * per_event;
@@ -115,6 +119,8 @@ __device__ __forceinline__ int64_t warp_lower_bound(const double* __restrict__ i
 // the min(n, have) most recent incidence entries strictly before t, newest first.
 __global__ void sample_kernel(const PlanArgs* __restrict__ args, DGraph g, DPlan pl,
                               uint32_t* __restrict__ bitmap) {
+  pdl_wait();
+  pdl_trigger();
   const PlanArgs a = *args;
   if (!a.valid) return;
   const int64_t B = a.end - a.begin;
@@ -158,6 +164,8 @@ __global__ void sample_kernel(const PlanArgs* __restrict__ args, DGraph g, DPlan
 __global__ void __launch_bounds__(1024) plan_finalize_kernel(const PlanArgs* __restrict__ args,
                                                              int64_t N, DPlan pl,
                                                              uint32_t* __restrict__ bitmap) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int sw[33];
   const PlanArgs a = *args;
   const int B = a.valid ? static_cast<int>(a.end - a.begin) : 0;
@@ -204,6 +212,8 @@ __global__ void __launch_bounds__(1024) plan_finalize_kernel(const PlanArgs* __r
 // Compacts pairs (root-major), resolves support rows, and emits the routing
 // items (roots then pairs) keyed by support row.
 __global__ void pairs_kernel(DPlan pl) {
+  pdl_wait();
+  pdl_trigger();
   const int R = pl.sizes[kSzR];
   const int n = pl.n;
   const int cap_items = pl.cap_R + pl.cap_P;
@@ -242,6 +252,8 @@ __global__ void pairs_kernel(DPlan pl) {
 }
 
 __global__ void routing_ptr_kernel(DPlan pl) {
+  pdl_wait();
+  pdl_trigger();
   const int items = pl.sizes[kSzItems];
   const int U = pl.sizes[kSzU];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < items; i += gridDim.x * blockDim.x) {
@@ -255,6 +267,8 @@ __global__ void routing_ptr_kernel(DPlan pl) {
 // pack_mail_row, memory_store.hpp:73-80): one warp per support row, 128-bit
 // vectorised when d % 4 == 0.
 __global__ void gather_view_kernel(DPlan pl, DMem st, DView vw) {
+  pdl_wait();
+  pdl_trigger();
   const int U = pl.sizes[kSzU];
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -281,10 +295,14 @@ __global__ void gather_view_kernel(DPlan pl, DMem st, DView vw) {
   }
 }
 
-__global__ void set_args_kernel(PlanArgs* dst, PlanArgs a) { *dst = a; }
+__global__ void set_args_kernel(PlanArgs* dst, PlanArgs a) {
+  pdl_wait();
+  pdl_trigger(); *dst = a; }
 
 __global__ void select_args_kernel(const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
                                    int offset, PlanArgs* dst) {
+  pdl_wait();
+  pdl_trigger();
   *dst = desc[*ctr + offset].args;
 }
 
@@ -292,6 +310,8 @@ __global__ void sample_queries_kernel(DGraph g, const int32_t* __restrict__ node
                                       const double* __restrict__ times, int count, int n,
                                       int32_t* __restrict__ nbr_node, int32_t* __restrict__ nbr_event,
                                       double* __restrict__ nbr_dt, int32_t* __restrict__ nbr_count) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -316,12 +336,12 @@ __global__ void sample_queries_kernel(DGraph g, const int32_t* __restrict__ node
 
 void select_plan_args_launch(PlanArgs* dst, const BarrierDesc* desc, const int* ctr, cudaStream_t s,
                              int offset) {
-  select_args_kernel<<<1, 1, 0, s>>>(desc, ctr, offset, dst);
+  launch_pdl(select_args_kernel, dim3(1), dim3(1), 0, s, desc, ctr, offset, dst);
   TGB_CUDA(cudaGetLastError());
 }
 
 void set_plan_args_launch(PlanArgs* dst, const PlanArgs& a, cudaStream_t s) {
-  set_args_kernel<<<1, 1, 0, s>>>(dst, a);
+  launch_pdl(set_args_kernel, dim3(1), dim3(1), 0, s, dst, a);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -331,14 +351,14 @@ void sample_queries_launch(const DGraph& g, const int32_t* nodes, const double* 
   if (count <= 0) return;
   int blocks = static_cast<int>(ceil_div(count, 8));
   if (blocks > 8 * kSMs) blocks = 8 * kSMs;
-  sample_queries_kernel<<<blocks, 256, 0, s>>>(g, nodes, times, count, n, nbr_node, nbr_event,
+  launch_pdl(sample_queries_kernel, dim3(blocks), dim3(256), 0, s, g, nodes, times, count, n, nbr_node, nbr_event,
                                                nbr_dt, nbr_count);
   TGB_CUDA(cudaGetLastError());
 }
 
 void negatives_only_launch(const DGraph& g, const PlanArgs* args, int count, int32_t* negs,
                            cudaStream_t s) {
-  negatives_kernel<<<static_cast<int>(ceil_div(count, 256)), 256, 0, s>>>(args, g.N, g.boundary, negs);
+  launch_pdl(negatives_kernel, dim3(static_cast<int>(ceil_div(count, 256))), dim3(256), 0, s, args, g.N, g.boundary, negs);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -355,11 +375,11 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) 
   uint32_t* bitmap = pl.bitmap;
   const int B = pl.cap_B;
   if (!pl.eval_negs && pl.rpe == 3) {
-    negatives_kernel<<<static_cast<int>(ceil_div(B, 256)), 256, 0, s>>>(pl.args, g.N, g.boundary,
+    launch_pdl(negatives_kernel, dim3(static_cast<int>(ceil_div(B, 256))), dim3(256), 0, s, pl.args, g.N, g.boundary,
                                                                         pl.negs);
   } else if (pl.eval_negs && pl.rpe > 2) {
     const int64_t total = static_cast<int64_t>(B) * (pl.rpe - 2);
-    eval_negatives_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * kSMs)), 256, 0, s>>>(
+    launch_pdl(eval_negatives_kernel, dim3(static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * kSMs))), dim3(256), 0, s, 
         pl.args, g, pl.rpe - 2, pl.negs);
   }
   TGB_CUDA(cudaGetLastError());
@@ -367,12 +387,12 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) 
   const int warps_per_block = 8;
   int blocks = static_cast<int>(ceil_div(R, warps_per_block));
   if (blocks > 4 * kSMs * 8) blocks = 4 * kSMs * 8;
-  sample_kernel<<<blocks, 32 * warps_per_block, 0, s>>>(pl.args, g, pl, bitmap);
+  launch_pdl(sample_kernel, dim3(blocks), dim3(32 * warps_per_block), 0, s, pl.args, g, pl, bitmap);
   TGB_CUDA(cudaGetLastError());
-  plan_finalize_kernel<<<1, 1024, 0, s>>>(pl.args, g.N, pl, bitmap);
+  launch_pdl(plan_finalize_kernel, dim3(1), dim3(1024), 0, s, pl.args, g.N, pl, bitmap);
   TGB_CUDA(cudaGetLastError());
   const int slots = pl.cap_R * (pl.n > 0 ? pl.n : 1);
-  pairs_kernel<<<static_cast<int>(ceil_div(slots, 256)), 256, 0, s>>>(pl);
+  launch_pdl(pairs_kernel, dim3(static_cast<int>(ceil_div(slots, 256))), dim3(256), 0, s, pl);
   TGB_CUDA(cudaGetLastError());
   if (!pl.routing) return;
   const int cap_items = pl.cap_R + pl.cap_P;
@@ -386,7 +406,7 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) 
   TGB_CUDA(cub::DeviceRadixSort::SortPairs(pl.sort_tmp, bytes, pl.item_key, pl.item_key_s,
                                            pl.item_val, pl.item_val_s, cap_items, 0,
                                            pl.sort_bits, ss));
-  routing_ptr_kernel<<<static_cast<int>(ceil_div(cap_items, 256)), 256, 0, ss>>>(pl);
+  launch_pdl(routing_ptr_kernel, dim3(static_cast<int>(ceil_div(cap_items, 256))), dim3(256), 0, ss, pl);
   TGB_CUDA(cudaGetLastError());
   if (pl.ev_sorted) TGB_CUDA(cudaEventRecord(pl.ev_sorted, ss));
 }
@@ -394,7 +414,7 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) 
 void gather_view_launch(const DPlan& pl, const DMem& st, DView& vw, cudaStream_t s) {
   int blocks = static_cast<int>(ceil_div(pl.cap_U, 8));
   if (blocks > 8 * kSMs) blocks = 8 * kSMs;
-  gather_view_kernel<<<blocks, 256, 0, s>>>(pl, st, vw);
+  launch_pdl(gather_view_kernel, dim3(blocks), dim3(256), 0, s, pl, st, vw);
   TGB_CUDA(cudaGetLastError());
 }
 

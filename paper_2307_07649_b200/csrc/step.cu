@@ -135,6 +135,8 @@ Dims make_dims(const ModelDims& m, const DGraph& g) {
 __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const float* __restrict__ omega,
                                     float* __restrict__ Xg, int64_t ldx, float* __restrict__ GU, StepBf bf,
                                     int cap_U, int stage) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sbuf[];
   const int U = pl.sizes[kSzU];
   const int lane = threadIdx.x & 31;
@@ -173,6 +175,8 @@ __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const 
 // z, r = sigmoid(gates + b) (bias already added by the GEMM); RS = r * s.
 __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
                                float* __restrict__ RS, StepBf bf, int cap_U) {
+  pdl_wait();
+  pdl_trigger();
   const int U = pl.sizes[kSzU];
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
@@ -194,6 +198,8 @@ __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
 // (freshen_memory, trainer.hpp:111-124; gru_update, gru.hpp:59-85).
 __global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
                                float* __restrict__ s_hat, int* flag) {
+  pdl_wait();
+  pdl_trigger();
   const int U = pl.sizes[kSzU];
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
@@ -220,6 +226,8 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
                                      float* __restrict__ Qin, int64_t ldq, float* __restrict__ KVin,
                                      int64_t ldkv, float* __restrict__ Gt, StepBf bf, int cap_R, int cap_P,
                                      int stage) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sbuf[];
   const int R = pl.sizes[kSzR], P = pl.sizes[kSzP];
   const int lane = threadIdx.x & 31;
@@ -274,6 +282,8 @@ template <int LANES>
 __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
                                 const float* __restrict__ KV, float* __restrict__ attn_a,
                                 float* __restrict__ H, int* flag, StepBf bf) {
+  pdl_wait();
+  pdl_trigger();
   const int R = pl.sizes[kSzR];
   const int lane = threadIdx.x & 31;
   const int da = D.da;
@@ -370,6 +380,8 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
                                float* __restrict__ Hin, float* __restrict__ dlogit,
                                float* __restrict__ logits, double* __restrict__ loss_terms,
                                int* flag, StepBf bf, int cap_B2) {
+  pdl_wait();
+  pdl_trigger();
   const int B = pl.sizes[kSzB];
   const int lane = threadIdx.x & 31;
   const int dh = D.dh, da = D.da;
@@ -440,6 +452,8 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
 // bce_loss: mean softplus(-pos) + mean softplus(neg), fixed-order f64 reduction.
 __global__ void __launch_bounds__(1024) loss_kernel(DPlan pl, const double* __restrict__ terms,
                                                     double* loss_base, const int* ctr, int* flag) {
+  pdl_wait();
+  pdl_trigger();
   double* loss_out = loss_base + (ctr ? *ctr : 0);
   __shared__ double sp[1024], sn[1024];
   const int B = pl.sizes[kSzB];
@@ -472,6 +486,8 @@ __global__ void __launch_bounds__(256) decoder_small_grads_kernel(DPlan pl, int 
                                                                   const float* __restrict__ HID,
                                                                   float* __restrict__ gW2,
                                                                   float* __restrict__ gb2) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[256];
   const int rows = pl.sizes[kSz2B];
   const int j = blockIdx.x;
@@ -499,6 +515,8 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
                                 const float* __restrict__ Q, const float* __restrict__ KV,
                                 const float* __restrict__ attn_a, float* __restrict__ dQ,
                                 float* __restrict__ dKV, StepBf bf, int cap_R, int cap_P) {
+  pdl_wait();
+  pdl_trigger();
   const int R = pl.sizes[kSzR];
   const int B = pl.sizes[kSzB];
   const int lane = threadIdx.x & 31;
@@ -616,6 +634,8 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
                                      const float* __restrict__ dKV, float* __restrict__ dNodeAcc,
                                      float* __restrict__ part_first, float* __restrict__ part_last,
                                      StepBf bf) {
+  pdl_wait();
+  pdl_trigger();
   const int items = pl.sizes[kSzItems];
   const int R = pl.sizes[kSzR];
   const int nchunks = (items + kChunk - 1) / kChunk;
@@ -700,6 +720,8 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
 __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNodeAcc,
                                      const float* __restrict__ part_first,
                                      const float* __restrict__ part_last, StepBf bf) {
+  pdl_wait();
+  pdl_trigger();
   const int U = pl.sizes[kSzU];
   const int w3 = 3 * D.da;
   for (int u = blockIdx.x; u < U; u += gridDim.x) {
@@ -728,6 +750,8 @@ __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNode
 __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ dNode,
                                 const float* __restrict__ Gates, float* __restrict__ Dg,
                                 float* __restrict__ g_static, StepBf bf, int cap_U) {
+  pdl_wait();
+  pdl_trigger();
   const int U = pl.sizes[kSzU];
   const int nd = D.d + D.ds;
   const int64_t total = static_cast<int64_t>(U) * D.d;
@@ -761,6 +785,8 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
 // da_r = (Wh^T da_h)[s part] * s * r (1 - r)  (gru.hpp:124-127).
 __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ T1,
                                 const float* __restrict__ Gates, float* __restrict__ Dg, StepBf bf) {
+  pdl_wait();
+  pdl_trigger();
   const int U = pl.sizes[kSzU];
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
@@ -783,6 +809,8 @@ __global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* _
                                                           const float* __restrict__ M2,
                                                           float* __restrict__ g_omega, int v_row0,
                                                           int blk_stride) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[256];
   const int i = blockIdx.x;
   const int t0 = D.d + D.ds + D.de;
@@ -826,6 +854,8 @@ struct PackJobs {
 };
 
 __global__ void pack_weights_kernel(const __grid_constant__ PackJobs jobs) {
+  pdl_wait();
+  pdl_trigger();
   const PackJob& J = jobs.j[blockIdx.y];
   const int64_t total = static_cast<int64_t>(J.rows) * J.cols;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -839,6 +869,8 @@ __global__ void pack_weights_kernel(const __grid_constant__ PackJobs jobs) {
 // events are sorted by (t, id), so the kept mail of a node is the one of its
 // largest event index.
 __global__ void rw_mark_kernel(DPlan pl, DGraph g, int32_t* __restrict__ win, int32_t* count) {
+  pdl_wait();
+  pdl_trigger();
   const PlanArgs a = *pl.args;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = 0;
   if (!a.valid) return;
@@ -853,6 +885,8 @@ __global__ void rw_mark_kernel(DPlan pl, DGraph g, int32_t* __restrict__ win, in
 
 __global__ void rw_emit_kernel(Dims D, DPlan pl, DGraph g, DView vw, const float* __restrict__ s_hat,
                                int32_t* __restrict__ win, StepWork w, DMem st, int direct) {
+  pdl_wait();
+  pdl_trigger();
   const PlanArgs a = *pl.args;
   if (!a.valid) return;
   const int64_t B = a.end - a.begin;
@@ -914,6 +948,8 @@ __global__ void rw_emit_kernel(Dims D, DPlan pl, DGraph g, DView vw, const float
 __global__ void eval_rank_kernel(Dims D, DPlan pl, const float* __restrict__ AB,
                                  const float* __restrict__ b1, const float* __restrict__ W2,
                                  const float* __restrict__ b2, int32_t* __restrict__ cnt, int64_t base) {
+  pdl_wait();
+  pdl_trigger();
   const PlanArgs a = *pl.args;
   if (!a.valid) return;
   const int64_t B = a.end - a.begin;
@@ -936,6 +972,8 @@ __global__ void eval_rank_kernel(Dims D, DPlan pl, const float* __restrict__ AB,
 }
 
 __global__ void apply_mark_kernel(WriteSet ws, int32_t* __restrict__ win) {
+  pdl_wait();
+  pdl_trigger();
   const int n = *ws.count;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
     atomicMax(&win[ws.node[x]], ws.event[x] + 1);
@@ -944,6 +982,8 @@ __global__ void apply_mark_kernel(WriteSet ws, int32_t* __restrict__ win) {
 // apply_root_write (memory_store.hpp:168-181). With several row sets, a row
 // is applied only if it carries the node's largest event (== later rank wins).
 __global__ void apply_rows_kernel(WriteSet ws, DMem st, int32_t* __restrict__ win, int use_win) {
+  pdl_wait();
+  pdl_trigger();
   const int n = *ws.count;
   const int lane = threadIdx.x & 31;
   const int64_t d = st.d;
@@ -967,12 +1007,16 @@ __global__ void apply_rows_kernel(WriteSet ws, DMem st, int32_t* __restrict__ wi
 }
 
 __global__ void apply_clear_kernel(WriteSet ws, int32_t* __restrict__ win) {
+  pdl_wait();
+  pdl_trigger();
   const int n = *ws.count;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
     win[ws.node[x]] = 0;
 }
 
 __global__ void fill_kernel(int32_t* p, int64_t n, int32_t v) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) p[x] = v;
 }
 
@@ -1016,6 +1060,8 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
                             float scale, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
                             const __grid_constant__ PackMap pm, int64_t pack_lo, int64_t pack_hi,
                             int64_t skip_lo, int64_t skip_hi) {
+  pdl_wait();
+  pdl_trigger();
   if (desc) {
     const BarrierDesc& d = desc[*ctr];
     lr = d.lr;
@@ -1062,6 +1108,8 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
 // reset_state (memory_store.hpp:43-50) when the barrier's descriptor asks for it.
 __global__ void reset_cond_kernel(DMem st, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
                                   int offset) {
+  pdl_wait();
+  pdl_trigger();
   if (!desc[*ctr + offset].reset) return;
   const int64_t n = st.N * st.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 3 * n; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1076,7 +1124,9 @@ __global__ void reset_cond_kernel(DMem st, const BarrierDesc* __restrict__ desc,
   }
 }
 
-__global__ void incr_kernel(int* ctr) { *ctr += 1; }
+__global__ void incr_kernel(int* ctr) {
+  pdl_wait();
+  pdl_trigger(); *ctr += 1; }
 
 template <typename T>
 T* dalloc(size_t n) {
@@ -1435,7 +1485,7 @@ void pack_weights_launch(const StepCtx& c, cudaStream_t s) {
   add(L.off[tWq], q, da, nd, b.Wst, 0, 0);
   add(L.off[tWk], kv, da, nd, b.Wst, da, 0);
   add(L.off[tWv], kv, da, nd, b.Wst, 2 * da, 0);
-  pack_weights_kernel<<<dim3(32, J.n), 256, 0, s>>>(J);
+  launch_pdl(pack_weights_kernel, dim3(dim3(32, J.n)), dim3(256), 0, s, J);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -1491,7 +1541,7 @@ void adam_pack_launch(const StepCtx& c, float* m, float* v, cudaStream_t s, cons
   const PackMap pm = gemm_impl() == kGemmTma ? make_pack_map(c, lo, hi, slo, shi) : PackMap{};
   const int64_t n = c.L.total;
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
-  adam_kernel<<<blocks, 256, 0, s>>>(c.params, c.grads, m, v, n, 0.f, 1.f, 1.f, 1.f, desc, ctr, pm, lo, hi, slo, shi);
+  launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, c.params, c.grads, m, v, n, 0.f, 1.f, 1.f, 1.f, desc, ctr, pm, lo, hi, slo, shi);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -1515,7 +1565,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   if (tma && !c.packed) pack_weights_launch(c, s);
   {
     const int stage = (D.gin + 1 + D.dt + 7) / 8 * 8;
-    assemble_gru_kernel<<<row_blocks(U), 32 * kWarps, sizeof(float) * stage * kWarps, s>>>(
+    launch_pdl(assemble_gru_kernel, dim3(row_blocks(U)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, 
         D, pl, vw, g, P + L.off[tOmega], tma ? nullptr : w.Xg, w.ldx, w.GU, bfx, U, stage);
   }
   if (tma) {
@@ -1532,7 +1582,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
     gemm_group_launch(gg, s);
   }
   const int eblocks = 4 * kSMs;
-  gru_mid_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, tma ? nullptr : w.RS, bfx, U);
+  launch_pdl(gru_mid_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, tma ? nullptr : w.RS, bfx, U);
   if (tma) {
     TcGroup tg;  // Gh += [r*s | 1] [Wh_s | bh]^T  (the bias rides the ones column)
     tc_nn(tg, U, szU, d, d + 1, w.bf.RS, 0, w.bf.Whs, 0, d, w.Gates + 2 * d, 3 * d, 1.0f);
@@ -1543,7 +1593,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
            3 * d, nullptr, 1.0f);
     gemm_group_launch(gg, s);
   }
-  gru_out_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.Gates, w.s_hat, c.d_numeric_flag);
+  launch_pdl(gru_out_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, w.s_hat, c.d_numeric_flag);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -1568,7 +1618,7 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   c.mark(phAttnAssemble, s);
   {
     const int stage = (std::max(D.kv_in, D.q_in) + 1 + D.dt + 7) / 8 * 8;
-    assemble_attn_kernel<<<row_blocks(R + Pc), 32 * kWarps, sizeof(float) * stage * kWarps, s>>>(
+    launch_pdl(assemble_attn_kernel, dim3(row_blocks(R + Pc)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, 
         D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, tma ? nullptr : w.Qin, w.ldq,
         tma ? nullptr : w.KVin, w.ldkv, w.Gt, bfx, R, Pc, stage);
   }
@@ -1595,7 +1645,7 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
     const int lanes = (da + 31) / 32;
     auto fwd = lanes <= 1 ? attn_fwd_kernel<1> : lanes <= 2 ? attn_fwd_kernel<2>
              : lanes <= 4 ? attn_fwd_kernel<4> : attn_fwd_kernel<8>;
-    fwd<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag, bfx);
+    launch_pdl(fwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag, bfx);
   }
 
 }
@@ -1641,7 +1691,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
            2 * dh);
     gemm_group_launch(gg, s);
   }
-  decoder_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(
+  launch_pdl(decoder_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s, 
       D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, tma ? nullptr : w.Dhid,
       tma ? nullptr : w.Hin, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
@@ -1654,8 +1704,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
       TGB_CUDA(cudaStreamWaitEvent(c.br, c.ev_br_dec, 0));
       ls = c.br;
     }
-    loss_kernel<<<1, 1024, 0, ls>>>(pl, w.loss_terms, loss_out, c.d_ctr, c.d_numeric_flag);
-    decoder_small_grads_kernel<<<dh + 1, 256, 0, ls>>>(pl, dh, w.dlogit, w.HID, G + L.off[tW2], G + L.off[tB2]);
+    launch_pdl(loss_kernel, dim3(1), dim3(1024), 0, ls, pl, w.loss_terms, loss_out, c.d_ctr, c.d_numeric_flag);
+    launch_pdl(decoder_small_grads_kernel, dim3(dh + 1), dim3(256), 0, ls, pl, dh, w.dlogit, w.HID, G + L.off[tW2], G + L.off[tB2]);
     if (c.br) {
       TGB_CUDA(cudaEventRecord(c.ev_br_join, c.br));
       TGB_CUDA(cudaStreamWaitEvent(s, c.ev_g_zero, 0));
@@ -1685,7 +1735,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     const int lanes = (da + 31) / 32;
     auto bwd = lanes <= 1 ? attn_bwd_kernel<1> : lanes <= 2 ? attn_bwd_kernel<2>
              : lanes <= 4 ? attn_bwd_kernel<4> : attn_bwd_kernel<8>;
-    bwd<<<row_blocks(R), 32 * kWarps, 0, s>>>(D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV, bfx, R, Pc);
+    launch_pdl(bwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV, bfx, R, Pc);
   }
   if (pl.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));  // routing CSR ready
   const int64_t nchunks = ceil_div(R + Pc, kChunk) + 1;
@@ -1695,10 +1745,10 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     const int lanes = (da + 31) / 32;
     auto chunk = lanes <= 1 ? routing_chunk_kernel<1> : lanes <= 2 ? routing_chunk_kernel<2>
                : lanes <= 4 ? routing_chunk_kernel<4> : routing_chunk_kernel<8>;
-    chunk<<<row_blocks(3 * nchunks), 32 * kWarps, 0, s>>>(D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
+    launch_pdl(chunk, dim3(row_blocks(3 * nchunks)), dim3(32 * kWarps), 0, s, D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
                                                       part_first, part_last, bfx);
     const int fix_threads = std::min(1024, (3 * da + 31) / 32 * 32);
-    routing_fixup_kernel<<<std::min(U, 8 * kSMs), fix_threads, 0, s>>>(D, pl, tma ? nullptr : w.dNodeAcc,
+    launch_pdl(routing_fixup_kernel, dim3(std::min(U, 8 * kSMs)), dim3(fix_threads), 0, s, D, pl, tma ? nullptr : w.dNodeAcc,
                                                                        part_first, part_last, bfx);
   }
   c.mark(phAttnBwdGemm, s);
@@ -1735,7 +1785,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 
   // ---- GRU backward (K9)
   c.mark(phGruBwd, s);
-  gru_bwd1_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
+  launch_pdl(gru_bwd1_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
                                           G + L.off[tStatic], bfx, U);
   if (c.br) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_br_join, 0));
   if (c.ev_tail_grads) TGB_CUDA(cudaEventRecord(c.ev_tail_grads, s));
@@ -1748,7 +1798,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     add_nn(gg, U, szU, d, d, A_rows(w.Dg + 2 * d, 3 * d, d), B_w(P + L.off[tWh] + md, gin, d), w.T1, d);
     gemm_group_launch(gg, s);
   }
-  gru_bwd2_kernel<<<eblocks, 256, 0, s>>>(D, pl, vw, w.T1, w.Gates, tma ? nullptr : w.Dg, bfx);
+  launch_pdl(gru_bwd2_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.T1, w.Gates, tma ? nullptr : w.Dg, bfx);
   if (tma) {
     TcGroup tg;
     tc_tn(tg, wc, d, gin + 1, U, szU, B.Dg, 0, B.Xg, 0, G + L.off[tWz], gin, G + L.off[tBz]);
@@ -1769,7 +1819,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     gemm_group_launch(gg, s);
   }
   if (dt > 0)
-    omega_final_kernel<<<dt, 256, 0, s>>>(D, P, L.off[tWk], L.off[tWv], L.off[tWz], w.Mom, w.DMT,
+    launch_pdl(omega_final_kernel, dim3(dt), dim3(256), 0, s, D, P, L.off[tWk], L.off[tWv], L.off[tWz], w.Mom, w.DMT,
                                           G + L.off[tOmega], tma ? B.d8a : da, tma ? B.d8d : d);
   TGB_CUDA(cudaGetLastError());
 }
@@ -1795,7 +1845,7 @@ void eval_rank_launch(const StepCtx& c, const DPlan& pl, int32_t* cnt_out, int64
            2 * dh);
     gemm_group_launch(gg, s);
   }
-  eval_rank_kernel<<<row_blocks(w.cap_B), 32 * kWarps, 0, s>>>(D, pl, w.AB, P + L.off[tB1], P + L.off[tW2],
+  launch_pdl(eval_rank_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s, D, pl, w.AB, P + L.off[tB1], P + L.off[tW2],
                                                                P + L.off[tB2], cnt_out, base);
   TGB_CUDA(cudaGetLastError());
 }
@@ -1804,8 +1854,8 @@ void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   StepWork& w = *c.w;
   const Dims D = make_dims(c.m, *c.g);
   const int B2 = 2 * w.cap_B;
-  rw_mark_kernel<<<static_cast<int>(ceil_div(B2, 256)), 256, 0, s>>>(pl, *c.g, w.win, w.w_count);
-  rw_emit_kernel<<<row_blocks(B2), 32 * kWarps, 0, s>>>(D, pl, *c.g, vw, w.s_hat, w.win, w,
+  launch_pdl(rw_mark_kernel, dim3(static_cast<int>(ceil_div(B2, 256))), dim3(256), 0, s, pl, *c.g, w.win, w.w_count);
+  launch_pdl(rw_emit_kernel, dim3(row_blocks(B2)), dim3(32 * kWarps), 0, s, D, pl, *c.g, vw, w.s_hat, w.win, w,
                                                         direct ? *direct : DMem{}, direct ? 1 : 0);
   TGB_CUDA(cudaGetLastError());
 }
@@ -1814,13 +1864,13 @@ void apply_writes_launch(const std::vector<WriteSet>& sets, DMem& st, int32_t* w
   const bool multi = sets.size() > 1;
   if (multi) {
     for (const WriteSet& ws : sets)
-      apply_mark_kernel<<<static_cast<int>(ceil_div(ws.cap, 256)), 256, 0, s>>>(ws, win);
+      launch_pdl(apply_mark_kernel, dim3(static_cast<int>(ceil_div(ws.cap, 256))), dim3(256), 0, s, ws, win);
   }
   for (const WriteSet& ws : sets)
-    apply_rows_kernel<<<row_blocks(ws.cap), 32 * kWarps, 0, s>>>(ws, st, win, multi ? 1 : 0);
+    launch_pdl(apply_rows_kernel, dim3(row_blocks(ws.cap)), dim3(32 * kWarps), 0, s, ws, st, win, multi ? 1 : 0);
   if (multi) {
     for (const WriteSet& ws : sets)
-      apply_clear_kernel<<<static_cast<int>(ceil_div(ws.cap, 256)), 256, 0, s>>>(ws, win);
+      launch_pdl(apply_clear_kernel, dim3(static_cast<int>(ceil_div(ws.cap, 256))), dim3(256), 0, s, ws, win);
   }
   TGB_CUDA(cudaGetLastError());
 }
@@ -1831,7 +1881,7 @@ void reset_state_launch(DMem& st, cudaStream_t s) {
   TGB_CUDA(cudaMemsetAsync(st.last_update, 0, sizeof(double) * st.N, s));
   TGB_CUDA(cudaMemsetAsync(st.mail_t, 0, sizeof(double) * st.N, s));
   TGB_CUDA(cudaMemsetAsync(st.mail_dt, 0, sizeof(double) * st.N, s));
-  fill_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(st.N, 256), 4 * kSMs)), 256, 0, s>>>(
+  launch_pdl(fill_kernel, dim3(static_cast<int>(std::min<int64_t>(ceil_div(st.N, 256), 4 * kSMs))), dim3(256), 0, s, 
       st.mail_ev, st.N, -1);
   TGB_CUDA(cudaGetLastError());
 }
@@ -1840,17 +1890,17 @@ void adam_launch(float* params, const float* grads, float* m, float* v, int64_t 
                  float c1, float c2, float grad_scale, cudaStream_t s, const BarrierDesc* desc,
                  const int* ctr) {
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
-  adam_kernel<<<blocks, 256, 0, s>>>(params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr, PackMap{}, 0, 0, 0, 0);
+  launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr, PackMap{}, 0, 0, 0, 0);
   TGB_CUDA(cudaGetLastError());
 }
 
 void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s, int offset) {
-  reset_cond_kernel<<<4 * kSMs, 256, 0, s>>>(st, desc, ctr, offset);
+  launch_pdl(reset_cond_kernel, dim3(4 * kSMs), dim3(256), 0, s, st, desc, ctr, offset);
   TGB_CUDA(cudaGetLastError());
 }
 
 void incr_launch(int* ctr, cudaStream_t s) {
-  incr_kernel<<<1, 1, 0, s>>>(ctr);
+  launch_pdl(incr_kernel, dim3(1), dim3(1), 0, s, ctr);
   TGB_CUDA(cudaGetLastError());
 }
 
