@@ -233,6 +233,12 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
  * end-to-end measurement. Pinned buffers make the copies asynchronous. */
 int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t* src,
                       const int32_t* dst, const double* t, const float* efeat);
+/* Debug: timing (us per launch) of the tcgen05 engine on an M x N x K
+ * K-major problem; trace (nullable) receives 16 globaltimer stamps per CTA for
+ * up to 296 CTAs: entry, setup done, first TMA landed (MMA), last MMA issued,
+ * epilogue start, epilogue end, exit, first TMA issued. */
+int tgnn_debug_gemm_bench(int64_t M, int64_t N, int64_t K, int32_t ntile, int32_t iters, double* us,
+                          uint64_t* trace, int32_t* grid);
 int tgnn_pinned_alloc(int64_t bytes, void** out);
 int tgnn_pinned_free(void* p);
 

@@ -151,6 +151,7 @@ SIGNATURES = {
     "tgnn_run_profile_barrier": [vp, f64p, C.POINTER(C.c_int32)],
     "tgnn_graph_ingest": [vp, i64, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), f64p, f32p],
     "tgnn_pinned_alloc": [i64, C.POINTER(vp)],
+    "tgnn_debug_gemm_bench": [i64, i64, i64, i32, i32, f64p, C.POINTER(C.c_uint64), C.POINTER(i32)],
     "tgnn_set_gemm_impl": [C.c_int],
     "tgnn_get_gemm_impl": [C.POINTER(C.c_int)],
     "tgnn_debug_gemm": [C.c_int, i64, i64, i64, f32p, C.c_int, f32p, C.c_int, f32p, C.c_int],

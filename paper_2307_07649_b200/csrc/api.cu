@@ -147,6 +147,7 @@ struct tgnn_ctx {
   cudaStream_t comm = nullptr;  // gradient all-reduce buckets overlapped with the GRU backward
   cudaStream_t aux = nullptr;   // next barrier's plan / read, overlapped with this barrier's step
   cudaStream_t br = nullptr;    // leaves of the step (gradient zeroing, root writes, loss)
+  cudaStream_t edge = nullptr;  // per-pair edge projection, overlapped with the GRU
   int* d_flag = nullptr;
 
   void check_numeric() {
@@ -496,7 +497,7 @@ struct tgnn_run {
   cudaGraphExec_t exec[2] = {nullptr, nullptr};  // barrier b runs exec[b % 2]
   int64_t prepared = -1;  // barrier whose plan + read view are ready in plans/views[b % 2]
   cudaEvent_t ev_fork = nullptr, ev_written = nullptr, ev_next = nullptr;
-  cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr;
+  cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
   // validation / metrics rows (run_training, trainer.hpp:725-743)
   int64_t val_begin = 0, val_end = 0, eval_batch = 0;
@@ -525,7 +526,7 @@ struct tgnn_run {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_written) cudaEventDestroy(ev_written);
     if (ev_next) cudaEventDestroy(ev_next);
-    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin};
+    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin, ev_edge};
     for (cudaEvent_t e : more)
       if (e) cudaEventDestroy(e);
     if (d_desc) cudaFree(d_desc);
@@ -750,6 +751,13 @@ void barrier_body_dev(tgnn_run* r, int p) {
   sc.ev_g_zero = r->ev_gzero;
   sc.ev_br_dec = r->ev_dec;
   sc.ev_br_join = r->ev_brjoin;
+  // edge branch: the plan-only half of the attention projection runs beside the GRU
+  if (gemm_impl() == kGemmTma) {
+    TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_fork, 0));
+    attn_edge_launch(sc, pl, ctx->edge);
+    TGB_CUDA(cudaEventRecord(r->ev_edge, ctx->edge));
+    sc.ev_edge = r->ev_edge;
+  }
   // this barrier: its plan was sorted inside the previous graph
   cudaEvent_t sorted = pl.ev_sorted;
   pl.ev_sorted = nullptr;
@@ -803,7 +811,7 @@ void build_graph(tgnn_run* r) {
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming));
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_written, cudaEventDisableTiming));
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
-    cudaEvent_t* more[] = {&r->ev_gru, &r->ev_gzero, &r->ev_dec, &r->ev_brjoin};
+    cudaEvent_t* more[] = {&r->ev_gru, &r->ev_gzero, &r->ev_dec, &r->ev_brjoin, &r->ev_edge};
     for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   for (int p = 0; p < 2; ++p) {
@@ -930,6 +938,7 @@ int tgnn_ctx_create(int device, tgnn_ctx** out) {
   TGB_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
   TGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   TGB_CUDA(cudaStreamCreateWithFlags(&c->br, cudaStreamNonBlocking));
+  TGB_CUDA(cudaStreamCreateWithFlags(&c->edge, cudaStreamNonBlocking));
   c->d_flag = dalloc<int>(1);
   TGB_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
   *out = c;
@@ -945,8 +954,10 @@ int tgnn_ctx_destroy(tgnn_ctx* ctx) {
   cudaStreamSynchronize(ctx->comm);
   cudaStreamSynchronize(ctx->aux);
   cudaStreamSynchronize(ctx->br);
+  cudaStreamSynchronize(ctx->edge);
   cudaStreamDestroy(ctx->aux);
   cudaStreamDestroy(ctx->br);
+  cudaStreamDestroy(ctx->edge);
   cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->comm);
   cudaStreamDestroy(ctx->stream);
@@ -2125,6 +2136,15 @@ int tgnn_graph_edge_feats(tgnn_graph* g, int64_t first, int64_t count, float* ou
   TGB_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * D.d_e, D.efeat + first * D.d_e_pad, sizeof(float) * D.d_e_pad,
                              sizeof(float) * D.d_e, static_cast<size_t>(count), cudaMemcpyDeviceToHost, g->ctx->stream));
   TGB_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  API_END
+}
+
+
+int tgnn_debug_gemm_bench(int64_t M, int64_t N, int64_t K, int32_t ntile, int32_t iters, double* us,
+                          uint64_t* trace, int32_t* grid) {
+  API_BEGIN
+  tc_debug_bench(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), ntile, iters, us,
+                 reinterpret_cast<unsigned long long*>(trace), grid);
   API_END
 }
 

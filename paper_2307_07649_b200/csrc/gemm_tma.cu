@@ -24,9 +24,10 @@ namespace tgb {
 
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kThreads = 192, kSt = 2;
+constexpr int kBM = 128, kBK = 64, kThreads = 192, kStMax = 6;
 constexpr int kATileB = kBM * kBK * 2;   // 16 KB (one of hi / lo)
-constexpr int kSmemMax = kSt * (2 * kATileB + 2 * 256 * kBK * 2) + 1024 + 256;
+constexpr int kEpiStageB = 4 * 32 * 33 * 4;  // static epilogue transpose buffers
+constexpr int kSmemMax = 232448 - kEpiStageB;  // opt-in dynamic maximum per CTA
 
 // Shared-memory / TMEM geometry is sized by the group's widest N tile, so
 // narrow-tile groups fit several CTAs per SM.
@@ -38,6 +39,7 @@ struct TcParams {
   int b_tile_bytes;  // per hi / lo B tile: roundup64(max ntile) * 128
   int stage_bytes;
   int tmem_cols;     // power of two >= max(32, max ntile)
+  int stages;        // shared-memory ring depth (2..kStMax), as deep as the CTA budget allows
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -107,6 +109,18 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Optional per-CTA timeline (debug benchmark only): 8 globaltimer stamps per CTA.
+__device__ unsigned long long* g_tc_trace = nullptr;
+__device__ int g_tc_epi_mode = 0;  // debug: 1 skips global stores, 2 skips TMEM loads
+__device__ __forceinline__ void trace(int slot) {
+  unsigned long long* t = g_tc_trace;
+  if (t) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    t[blockIdx.x * 16 + slot] = v;
+  }
+}
+
 // Tile geometry of flattened tile index t (identical in every role).
 struct TileInfo {
   int pi, m0, n0, split, kbeg, nk, M;
@@ -139,21 +153,24 @@ __device__ __forceinline__ bool tile_info(const TcParams& gp, int t, TileInfo& t
 
 // Persistent CTA: static round-robin over the flattened tiles of the group.
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcParams gp) {
+  if (threadIdx.x == 0) trace(0);
   pdl_wait();
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int kStageB = gp.stage_bytes, kBTileB = gp.b_tile_bytes;
+  const uint32_t kSt = static_cast<uint32_t>(gp.stages);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageB);
   uint64_t* empty = full + kSt;
   uint64_t* tfull = empty + kSt;   // [2] accumulator ready for the epilogue
   uint64_t* tempty = tfull + 2;    // [2] accumulator drained by the epilogue
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ float epi_stage[4 * 32 * 33];  // epilogue transposes (static: LDS / STS, not generic)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = gp.tile_base[gp.count];
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSt; ++s) {
+    for (uint32_t s = 0; s < kSt; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
@@ -173,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
   const int acc_cols = gp.tmem_cols / 2;
+  if (threadIdx.x == 0) trace(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -190,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           const uint32_t s = it % kSt;
           if (it >= kSt) mbar_wait(empty + s, ((it / kSt) - 1) & 1);
           uint8_t* st = smem + s * kStageB;
+          if (it == 0) trace(7);
           mbar_expect_tx(full + s, stage_tx);
           const int k0 = ti.kbeg + kc * kBK;
           for (int h = 0; h < 2; ++h) {
@@ -228,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         for (int kc = 0; kc < ti.nk; ++kc, ++it) {
           const uint32_t s = it % kSt;
           mbar_wait(full + s, (it / kSt) & 1);
+          if (it == 0) trace(2);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           uint8_t* st = smem + s * kStageB;
           const uint32_t ahi = su32(st), alo = su32(st + kATileB);
@@ -247,12 +267,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           umma_commit(tfull + acc);
         else
           mbar_arrive(tfull + acc);
+        trace(3);
         ++lt;
       }
     }
   } else {
     // epilogue warps 2..5: warp w reads TMEM lanes 32 (w % 4) .. + 32
     const int quarter = warp & 3;
+    const int epi_mode = g_tc_epi_mode;
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       TileInfo ti;
@@ -260,62 +282,115 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const TcProblem& P = gp.p[ti.pi];
       const uint32_t acc = lt & 1;
       mbar_wait(tfull + acc, (lt >> 1) & 1);
+      if (warp == 2 && lane == 0) trace(4);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = quarter * 32 + lane;
-      const int m = ti.m0 + row;
       const int N = P.N;
       const int ntile = P.ntile;
       const int nvalid = min(ntile, N - ti.n0);
       const int n0 = ti.n0;
-      for (int c0 = 0; c0 < ntile; c0 += 16) {
-        uint32_t v[16];
-        if (ti.nk > 0) {
-          const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * static_cast<uint32_t>(acc_cols) +
-                              static_cast<uint32_t>(c0);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                "=r"(v[14]), "=r"(v[15])
-              : "r"(ta));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        } else {
+      // TMEM -> registers (thread = row) -> shared-memory transpose -> global
+      // stores with lane = column: every store instruction writes one row's
+      // 128 contiguous bytes instead of 32 scattered rows.
+      float* stg = epi_stage + quarter * (32 * 33);
+      const int mb = ti.m0 + quarter * 32;  // first row of this warp
+      for (int c0 = 0; c0 < ntile; c0 += 32) {
+        const int halves = min(2, (ntile - c0) / 16);
+        for (int h = 0; h < halves; ++h) {
+          uint32_t v[16];
+          if (ti.nk > 0 && epi_mode != 2) {
+            const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                acc * static_cast<uint32_t>(acc_cols) + static_cast<uint32_t>(c0 + 16 * h);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                  "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                  "=r"(v[14]), "=r"(v[15])
+                : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          } else {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] = 0u;
-        }
-        if (P.splits > 1) {
-          if (m < P.M) {
-            float* w = P.ws + static_cast<int64_t>(ti.split) * P.M * N + static_cast<int64_t>(m) * N;
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (c0 + q < nvalid) w[n0 + c0 + q] = m < ti.M ? __uint_as_float(v[q]) : 0.0f;
+            for (int q = 0; q < 16; ++q) v[q] = 0u;
           }
-        } else if (m < ti.M) {
-          float* crow = P.C + static_cast<int64_t>(m) * P.ldc;
-          float prev[16];
-          if (P.beta != 0.0f) {  // all loads first: one latency, not sixteen
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const int n = n0 + c0 + q;
-              prev[q] = c0 + q < nvalid ? ((P.C2 && n == N - 1) ? P.C2[m] : crow[n]) : 0.0f;
+          for (int q = 0; q < 16; ++q) stg[lane * 33 + 16 * h + q] = __uint_as_float(v[q]);
+        }
+        __syncwarp();
+        if (warp == 2 && lane == 0 && c0 < 96) trace(8 + 2 * (c0 / 32));
+        // fast path: a full 32-column chunk of 16-byte aligned fp32 rows -- each
+        // lane stores a float4, four rows of 128 B per instruction
+        const int npart = P.splits > 1 ? N : static_cast<int>(P.ldc);
+        float* vbase = P.splits > 1 ? P.ws + static_cast<int64_t>(ti.split) * P.M * N : P.C;
+        const bool vec = epi_mode == 0 && halves == 2 && c0 + 32 <= nvalid && (npart & 3) == 0 &&
+                         ((n0 + c0) & 3) == 0 && (reinterpret_cast<uintptr_t>(vbase) & 15) == 0 &&
+                         P.beta == 0.0f && !(P.C2 && n0 + c0 + 32 > N - 1);
+        if (vec) {
+          const int rmax = P.splits > 1 ? P.M : ti.M;  // rows to write (zeros past ti.M for partials)
+          const int rr = lane >> 3, cc = (lane & 7) * 4;
+          for (int r0 = 0; r0 < 32; r0 += 4) {
+            const int m = mb + r0 + rr;
+            if (m < rmax) {
+              float4 o;
+              const float* src = stg + (r0 + rr) * 33 + cc;
+              const bool live = m < ti.M;
+              o.x = live ? P.alpha * src[0] : 0.0f;
+              o.y = live ? P.alpha * src[1] : 0.0f;
+              o.z = live ? P.alpha * src[2] : 0.0f;
+              o.w = live ? P.alpha * src[3] : 0.0f;
+              *reinterpret_cast<float4*>(vbase + static_cast<int64_t>(m) * npart + n0 + c0 + cc) = o;
             }
           }
+          __syncwarp();
+          continue;
+        }
+        const int col = c0 + lane;                 // this lane's column in the tile
+        const bool col_ok = lane < 16 * halves && col < nvalid && epi_mode != 1;
+        const int n = n0 + col;
+        if (P.splits > 1) {
+          const int rows = min(32, P.M - mb);
+          float* wrow = P.ws + (static_cast<int64_t>(ti.split) * P.M + mb) * N + n;
+          for (int r0 = 0; r0 < rows; r0 += 8) {
+            float val[8];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int n = n0 + c0 + q;
-            if (c0 + q >= nvalid) continue;
-            float x = P.alpha * __uint_as_float(v[q]);
-            if (P.beta != 0.0f) x += P.beta * prev[q];
-            if (P.C2 && n == N - 1)
-              P.C2[m] = x;
-            else
-              crow[n] = x;
+            for (int k = 0; k < 8; ++k) val[k] = stg[(r0 + k) * 33 + lane];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (r0 + k < rows && col_ok) wrow[static_cast<int64_t>(r0 + k) * N] = mb + r0 + k < ti.M ? val[k] : 0.0f;
+          }
+        } else {
+          const bool to_c2 = P.C2 && n == N - 1;
+          const int rows = min(32, ti.M - mb);
+          const int64_t ldc = P.ldc;
+          float* crow = P.C + static_cast<int64_t>(mb) * ldc + n;
+          const float alpha = P.alpha, beta = P.beta;
+          for (int r0 = 0; r0 < rows; r0 += 8) {
+            float val[8], prev[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              val[k] = stg[(r0 + k) * 33 + lane];
+              prev[k] = 0.0f;
+            }
+            if (beta != 0.0f) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (r0 + k < rows && col_ok) prev[k] = to_c2 ? P.C2[mb + r0 + k] : crow[(r0 + k) * ldc];
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (r0 + k < rows && col_ok) {
+                const float x = alpha * val[k] + beta * prev[k];
+                if (to_c2) P.C2[mb + r0 + k] = x;
+                else crow[(r0 + k) * ldc] = x;
+              }
+            }
           }
         }
+        if (warp == 2 && lane == 0 && c0 < 96) trace(9 + 2 * (c0 / 32));
+        __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
+      if (warp == 2 && lane == 0) trace(5);
       ++lt;
     }
   }
@@ -323,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(gp.tmem_cols));
+  if (threadIdx.x == 0) trace(6);
 }
 
 __global__ void tc_splitk_reduce_kernel(const __grid_constant__ TcParams gp) {
@@ -478,9 +554,17 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s) {
   int cols = 32;
   while (cols < 2 * max_ntile) cols *= 2;  // two accumulator stages
   gp.tmem_cols = cols;
-  const int smem = kSt * gp.stage_bytes + 1024 + 256;
-  // one persistent CTA per SM (or fewer when the group has fewer tiles)
-  int ctas_per_sm = (228 * 1024) / (smem + 1024);
+  // Ring depth: as many stages as fit. Groups with more tiles than SMs keep
+  // two CTAs per SM (one's epilogue overlaps the other's loads) when two
+  // stages each still fit; otherwise one CTA per SM with a deeper ring.
+  const int total_tiles = gp.tile_base[g.count];
+  const int fixed = 1024 + 256;
+  int budget = kSmemMax - fixed;
+  const int half = 113 * 1024 - kEpiStageB - fixed;  // two CTAs per SM
+  if (total_tiles > kSMs && half / gp.stage_bytes >= 2 && cols <= 256) budget = half;
+  gp.stages = std::max(2, std::min(kStMax, budget / gp.stage_bytes));
+  const int smem = gp.stages * gp.stage_bytes + fixed;
+  int ctas_per_sm = (228 * 1024) / (smem + kEpiStageB + 1024);
   if (ctas_per_sm < 1) ctas_per_sm = 1;
   if (ctas_per_sm * cols > 512) ctas_per_sm = 512 / cols;
   const int grid = std::min(gp.tile_base[g.count], kSMs * ctas_per_sm);
@@ -490,6 +574,58 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s) {
     launch_pdl(tc_splitk_reduce_kernel, dim3(dim3(64, g.count)), dim3(256), 0, s, gp);
     TGB_CUDA(cudaGetLastError());
   }
+}
+
+void tc_debug_bench(int M, int N, int K, int ntile, int iters, double* us, unsigned long long* trace_out,
+                    int* grid_out) {
+  const int mode = iters >= 1000 ? iters / 1000 : 0;  // debug epilogue mode rides on iters
+  iters = iters % 1000;
+  TGB_CUDA(cudaMemcpyToSymbol(g_tc_epi_mode, &mode, sizeof(int)));
+  BfMat a = bf_alloc(M, K), b = bf_alloc(N, K);
+  float* c = nullptr;
+  TGB_CUDA(cudaMalloc(&c, sizeof(float) * static_cast<size_t>(M) * N));
+  TcGroup tg;
+  TcProblem& T = tg.p[tg.count++];
+  T.M = M;
+  T.N = N;
+  T.K = K;
+  T.ntile = ntile > 0 ? ntile : tc_ntile(N);
+  T.a = tma_view(a, 0, K, M, true, 128);
+  T.b = tma_view(b, 0, K, N, true, T.ntile);
+  T.C = c;
+  T.ldc = N;
+  cudaEvent_t e0, e1;
+  TGB_CUDA(cudaEventCreate(&e0));
+  TGB_CUDA(cudaEventCreate(&e1));
+  for (int w = 0; w < 3; ++w) tc_group_launch(tg, nullptr);
+  TGB_CUDA(cudaEventRecord(e0, nullptr));
+  for (int x = 0; x < iters; ++x) tc_group_launch(tg, nullptr);
+  TGB_CUDA(cudaEventRecord(e1, nullptr));
+  TGB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  TGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *us = 1e3 * ms / iters;
+  const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, T.ntile));
+  *grid_out = std::min(tiles, kSMs * 2);
+  if (trace_out) {
+    unsigned long long* d = nullptr;
+    TGB_CUDA(cudaMalloc(&d, sizeof(unsigned long long) * 16 * 2 * kSMs));
+    TGB_CUDA(cudaMemset(d, 0, sizeof(unsigned long long) * 16 * 2 * kSMs));
+    TGB_CUDA(cudaMemcpyToSymbol(g_tc_trace, &d, sizeof(d)));
+    tc_group_launch(tg, nullptr);
+    TGB_CUDA(cudaDeviceSynchronize());
+    unsigned long long* z = nullptr;
+    TGB_CUDA(cudaMemcpyToSymbol(g_tc_trace, &z, sizeof(z)));
+    TGB_CUDA(cudaMemcpy(trace_out, d, sizeof(unsigned long long) * 16 * 2 * kSMs, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(c);
+  bf_free(a);
+  bf_free(b);
+  const int zero = 0;
+  TGB_CUDA(cudaMemcpyToSymbol(g_tc_epi_mode, &zero, sizeof(int)));
 }
 
 }  // namespace tgb

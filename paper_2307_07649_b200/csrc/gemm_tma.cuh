@@ -74,5 +74,9 @@ inline int tc_ntile(int N, int cap = 256) {
 }
 
 void tc_group_launch(const TcGroup& g, cudaStream_t s);
+// Debug: average microseconds of one launch of an M x N x K K-major problem
+// and (optionally) a per-CTA globaltimer trace [2*148 x 8].
+void tc_debug_bench(int M, int N, int K, int ntile, int iters, double* us, unsigned long long* trace_out,
+                    int* grid_out);
 
 }  // namespace tgb

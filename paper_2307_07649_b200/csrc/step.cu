@@ -196,8 +196,11 @@ __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
 
 // h = tanh(.), s_hat = (1 - z) s + z h for rows with a mail, else s
 // (freshen_memory, trainer.hpp:111-124; gru_update, gru.hpp:59-85).
+// With the TMA engine it also writes the node-feature operand NF = [s_hat |
+// static | 1] of every support (the node half of the attention projections).
 __global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
-                               float* __restrict__ s_hat, int* flag) {
+                               float* __restrict__ s_hat, int* flag, const float* __restrict__ stat,
+                               StepBf bf, int cap_U) {
   pdl_wait();
   pdl_trigger();
   const int U = pl.sizes[kSzU];
@@ -215,6 +218,62 @@ __global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
       flag_if_nonfinite(out, flag);
     }
     s_hat[x] = out;
+    bf_put(bf.NF, u, i, out);
+  }
+  if (bf.NF.hi != nullptr) {
+    const int64_t tot2 = static_cast<int64_t>(U) * (D.ds + 1);
+    for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < tot2; x += gridDim.x * blockDim.x) {
+      const int64_t u = x / (D.ds + 1), j = x % (D.ds + 1);
+      bf_put(bf.NF, u, D.d + j, j < D.ds ? stat[static_cast<int64_t>(pl.supports[u]) * D.ds + j] : 1.0f);
+    }
+    bf_zero_tail(bf.NF, U, cap_U, D.d + D.ds + 1);
+  }
+}
+
+// Edge operand EF = [e(event) | cos(dt w) | 1] and Gt = -dt sin(dt w) per pair
+// (the node-independent columns of embed_root's K/V inputs, trainer.hpp:140-152).
+__global__ void assemble_edge_kernel(Dims D, DPlan pl, DGraph g, const float* __restrict__ omega, StepBf bf,
+                                     int cap_P, int stage) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float sbuf[];
+  const int P = pl.sizes[kSzP];
+  const int lane = threadIdx.x & 31;
+  float* row = sbuf + (threadIdx.x >> 5) * stage;
+  float* gt = row + D.de + D.dt + 1;
+  for (int64_t p = gwarp(); p < P; p += nwarp()) {
+    const int64_t ev = pl.pair_event[p];
+    const double dt = pl.pair_dt[p];
+    const float* ef = g.efeat + ev * D.de_pad;
+    for (int x = lane; x < D.de; x += 32) row[x] = ef[x];
+    for (int i = lane; i < D.dt; i += 32) {
+      const float arg = static_cast<float>(dt * static_cast<double>(omega[i]));
+      float sn, cs;
+      sincosf(arg, &sn, &cs);
+      row[D.de + i] = cs;
+      gt[i] = static_cast<float>(-dt) * sn;
+    }
+    if (lane == 0) row[D.de + D.dt] = 1.0f;
+    __syncwarp();
+    warp_store_row(bf.EF, p, row, D.de + D.dt + 1, nullptr, 0);
+    warp_store_row(bf.Gt, p, gt, D.dt, nullptr, 0);
+    __syncwarp();
+  }
+  bf_zero_tail(bf.EF, P, cap_P, D.de + D.dt + 1);
+  bf_zero_tail(bf.Gt, P, cap_P, D.dt);
+}
+
+// Query constant cq = W_q[:, time] 1 + b_q: every root's query time encoding
+// is cos(0 w) = 1 (trainer.hpp:133-136).
+__global__ void query_const_kernel(Dims D, const float* __restrict__ Wq, const float* __restrict__ bq,
+                                   float* __restrict__ cq) {
+  pdl_wait();
+  pdl_trigger();
+  const int nd = D.d + D.ds;
+  for (int i = threadIdx.x; i < D.da; i += blockDim.x) {
+    float s = bq[i];
+    for (int j = 0; j < D.dt; ++j) s += Wq[static_cast<int64_t>(i) * D.q_in + nd + j];
+    cq[i] = s;
   }
 }
 
@@ -278,10 +337,13 @@ constexpr int kNbGroup = 4;     // neighbour rows loaded ahead of their use
 // softmax, h = sum a V; n = 0 gives h = 0. One warp per root; LANES = ceil(d_a
 // / 32) features per lane; neighbour rows are fetched kNbGroup at a time so
 // their L2 latencies overlap.
+// Node / edge split (TMA engine): q = QKVn[sup(r)] + cq, K / V = KE[p] +
+// QKVn[sup(p)] (node parts d8a apart); the summed Q and K|V rows are written
+// back for the backward pass.
 template <int LANES>
-__global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
-                                const float* __restrict__ KV, float* __restrict__ attn_a,
-                                float* __restrict__ H, int* flag, StepBf bf) {
+__global__ void attn_fwd_kernel(Dims D, DPlan pl, float* Q, const float* __restrict__ KV, float* __restrict__ attn_a,
+                                float* __restrict__ H, int* flag, StepBf bf,
+                                const float* __restrict__ QKVn, const float* __restrict__ cq) {
   pdl_wait();
   pdl_trigger();
   const int R = pl.sizes[kSzR];
@@ -298,11 +360,23 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
       continue;
     }
     const int p0 = pl.pair_ptr[r];
+    const int ldn = 3 * bf.d8a;
+    const int my_sup = (QKVn && lane < n) ? pl.pair_sup[p0 + lane] : 0;
     float q[LANES];
+    if (QKVn) {
+      const float* qn = QKVn + static_cast<int64_t>(pl.root_sup[r]) * ldn;
 #pragma unroll
-    for (int c = 0; c < LANES; ++c) {
-      const int i = lane + 32 * c;
-      q[c] = i < da ? Q[r * da + i] : 0.0f;
+      for (int c = 0; c < LANES; ++c) {
+        const int i = lane + 32 * c;
+        q[c] = i < da ? qn[i] + cq[i] : 0.0f;
+        if (i < da) Q[r * da + i] = q[c];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < LANES; ++c) {
+        const int i = lane + 32 * c;
+        q[c] = i < da ? Q[r * da + i] : 0.0f;
+      }
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(n));
     float my_score = -INFINITY;
@@ -311,10 +385,12 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
 #pragma unroll
       for (int g = 0; g < kNbGroup; ++g) {
         const float* K = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da;
+        const int su = __shfl_sync(0xffffffffu, my_sup, (m0 + g) & 31);
+        const float* kn = QKVn ? QKVn + static_cast<int64_t>(su) * ldn + bf.d8a : nullptr;
 #pragma unroll
         for (int c = 0; c < LANES; ++c) {
           const int i = lane + 32 * c;
-          kr[g][c] = (m0 + g < n && i < da) ? K[i] : 0.0f;
+          kr[g][c] = (m0 + g < n && i < da) ? K[i] + (kn ? kn[i] : 0.0f) : 0.0f;
         }
       }
 #pragma unroll
@@ -339,10 +415,12 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, const float* __restrict__ Q,
 #pragma unroll
       for (int g = 0; g < kNbGroup; ++g) {
         const float* V = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da + da;
+        const int su = __shfl_sync(0xffffffffu, my_sup, (m0 + g) & 31);
+        const float* vn = QKVn ? QKVn + static_cast<int64_t>(su) * ldn + 2 * bf.d8a : nullptr;
 #pragma unroll
         for (int c = 0; c < LANES; ++c) {
           const int i = lane + 32 * c;
-          vr[g][c] = (m0 + g < n && i < da) ? V[i] : 0.0f;
+          vr[g][c] = (m0 + g < n && i < da) ? V[i] + (vn ? vn[i] : 0.0f) : 0.0f;
         }
       }
 #pragma unroll
@@ -514,7 +592,8 @@ template <int LANES>
 __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
                                 const float* __restrict__ Q, const float* __restrict__ KV,
                                 const float* __restrict__ attn_a, float* __restrict__ dQ,
-                                float* __restrict__ dKV, StepBf bf, int cap_R, int cap_P) {
+                                float* __restrict__ dKV, StepBf bf, int cap_R, int cap_P,
+                                const float* __restrict__ QKVn) {
   pdl_wait();
   pdl_trigger();
   const int R = pl.sizes[kSzR];
@@ -545,6 +624,8 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
       continue;
     }
     const int p0 = pl.pair_ptr[r];
+    const int ldn = 3 * bf.d8a;
+    const int my_sup = (QKVn && lane < n) ? pl.pair_sup[p0 + lane] : 0;
     const float scale = 1.0f / sqrtf(static_cast<float>(n));
     const float a_l = lane < n ? attn_a[p0 + lane] : 0.0f;
     float da_l = 0.0f;
@@ -553,10 +634,12 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
 #pragma unroll
       for (int g = 0; g < kNbGroup; ++g) {
         const float* V = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da + da;
+        const int su = __shfl_sync(0xffffffffu, my_sup, (m0 + g) & 31);
+        const float* vn = QKVn ? QKVn + static_cast<int64_t>(su) * ldn + 2 * bf.d8a : nullptr;
 #pragma unroll
         for (int c = 0; c < LANES; ++c) {
           const int i = lane + 32 * c;
-          vr[g][c] = (m0 + g < n && i < da) ? V[i] : 0.0f;
+          vr[g][c] = (m0 + g < n && i < da) ? V[i] + (vn ? vn[i] : 0.0f) : 0.0f;
         }
       }
 #pragma unroll
@@ -582,10 +665,12 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
 #pragma unroll
       for (int g = 0; g < kNbGroup; ++g) {
         const float* K = KV + static_cast<int64_t>(p0 + m0 + g) * 2 * da;
+        const int su = __shfl_sync(0xffffffffu, my_sup, (m0 + g) & 31);
+        const float* kn = QKVn ? QKVn + static_cast<int64_t>(su) * ldn + bf.d8a : nullptr;
 #pragma unroll
         for (int c = 0; c < LANES; ++c) {
           const int i = lane + 32 * c;
-          kr[g][c] = (m0 + g < n && i < da) ? K[i] : 0.0f;
+          kr[g][c] = (m0 + g < n && i < da) ? K[i] + (kn ? kn[i] : 0.0f) : 0.0f;
         }
       }
 #pragma unroll
@@ -703,7 +788,7 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
             const int f = lane + 32 * cc;
             if (f < da) {
               if (dst) dst[part * da + f] = acc[cc];
-              if (direct) bf_put(bf.dNA, key, part * da + f, acc[cc]);
+              if (direct) bf_put(bf.dNA, key, part * bf.d8a + f, acc[cc]);
             }
           }
 #pragma unroll
@@ -740,7 +825,7 @@ __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNode
       }
       for (; c <= c1; ++c) s += part_first[static_cast<int64_t>(c) * w3 + f];
       if (dNodeAcc) dNodeAcc[static_cast<int64_t>(u) * w3 + f] = s;
-      bf_put(bf.dNA, u, f, s);
+      bf_put(bf.dNA, u, (f / D.da) * bf.d8a + f % D.da, s);
     }
   }
 }
@@ -749,11 +834,19 @@ __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNode
 // (trainer.hpp:239-253; supports are unique nodes, so rows never collide).
 __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ dNode,
                                 const float* __restrict__ Gates, float* __restrict__ Dg,
-                                float* __restrict__ g_static, StepBf bf, int cap_U) {
+                                float* __restrict__ g_static, StepBf bf, int cap_U,
+                                float* __restrict__ gWq, const float* __restrict__ gBq) {
   pdl_wait();
   pdl_trigger();
   const int U = pl.sizes[kSzU];
   const int nd = D.d + D.ds;
+  if (gWq) {  // node / edge split: dW_q[:, time] = sum_r dq_r = db_q (cos(0 w) = 1)
+    for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < static_cast<int64_t>(D.da) * D.dt;
+         x += gridDim.x * blockDim.x) {
+      const int64_t r = x / D.dt, j = x % D.dt;
+      gWq[r * D.q_in + nd + j] = gBq[r];
+    }
+  }
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int64_t u = x / D.d, i = x % D.d;
@@ -813,6 +906,7 @@ __global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* _
   pdl_trigger();
   __shared__ float red[256];
   const int i = blockIdx.x;
+
   const int t0 = D.d + D.ds + D.de;
   const int n1 = 2 * D.da, n2 = 3 * D.d;
   float s = 0.0f;
@@ -1039,17 +1133,41 @@ struct PackMap {
   int count;
 };
 
+__device__ __forceinline__ int pack_find(const PackMap& pm, int64_t x) {
+  for (int k = 0; k < pm.count; ++k)
+    if (x >= pm.t[k].off && x < pm.t[k].off + pm.t[k].n) return k;
+  return -1;
+}
+
+__device__ __forceinline__ void pack_put(const PackTensor& T, int64_t x, float v) {
+  const uint32_t local = static_cast<uint32_t>(x - T.off);
+  const uint32_t cols = static_cast<uint32_t>(T.cols);
+  const int r = static_cast<int>(local / cols), c = static_cast<int>(local - (local / cols) * cols);
+  for (int q = 0; q < T.nd; ++q) {
+    const PackDest& D = T.d[q];
+    if (c >= D.c_lo && c < D.c_hi) bf_put(D.dst, D.r0 + r, D.c0 + (c - D.c_lo), v);
+  }
+}
+
 __device__ __forceinline__ void pack_elem(const PackMap& pm, int64_t x, float v) {
-  for (int k = 0; k < pm.count; ++k) {
+  const int k = pack_find(pm, x);
+  if (k >= 0) pack_put(pm.t[k], x, v);
+}
+
+// four consecutive parameters, usually inside one tensor: one lookup
+__device__ __forceinline__ void pack_elem4(const PackMap& pm, int64_t x, float4 v) {
+  const int k = pack_find(pm, x);
+  if (k >= 0 && x + 3 < pm.t[k].off + pm.t[k].n) {
     const PackTensor& T = pm.t[k];
-    const int64_t local = x - T.off;
-    if (local < 0 || local >= T.n) continue;
-    const int r = static_cast<int>(local / T.cols), c = static_cast<int>(local % T.cols);
-    for (int q = 0; q < T.nd; ++q) {
-      const PackDest& D = T.d[q];
-      if (c >= D.c_lo && c < D.c_hi) bf_put(D.dst, D.r0 + r, D.c0 + (c - D.c_lo), v);
-    }
-    return;
+    pack_put(T, x, v.x);
+    pack_put(T, x + 1, v.y);
+    pack_put(T, x + 2, v.z);
+    pack_put(T, x + 3, v.w);
+  } else {
+    pack_elem(pm, x, v.x);
+    pack_elem(pm, x + 1, v.y);
+    pack_elem(pm, x + 2, v.z);
+    pack_elem(pm, x + 3, v.w);
   }
 }
 
@@ -1093,10 +1211,7 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     m4[x] = mm;
     v4[x] = vv;
     if (pm.count && 4 * x + 3 >= pack_lo && 4 * x < pack_hi && !(4 * x >= skip_lo && 4 * x + 3 < skip_hi)) {
-      pack_elem(pm, 4 * x, pp.x);
-      pack_elem(pm, 4 * x + 1, pp.y);
-      pack_elem(pm, 4 * x + 2, pp.z);
-      pack_elem(pm, 4 * x + 3, pp.w);
+      pack_elem4(pm, 4 * x, pp);
     }
   }
   for (int64_t x = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; x < n; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1342,7 +1457,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
     if (!fwd_only) {
       b.dQ = bf_alloc(R, da);
       b.dKV = bf_alloc(P, b.d8a + da);
-      b.dNA = bf_alloc(U, 3 * da);
+      b.dNA = bf_alloc(U, 3 * b.d8a);
       b.Dg = bf_alloc(U, 2 * b.d8d + d);
     }
     b.Wzr = bf_alloc(2 * d, gin + 1);
@@ -1353,8 +1468,13 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
     b.W1a = bf_alloc(dh, da);
     b.W1b = bf_alloc(dh, da);
     b.W1 = bf_alloc(dh, 2 * da);
-    b.Wst = bf_alloc(3 * da, d + ds);
+    b.Wst = bf_alloc(3 * b.d8a, d + ds);
+    b.NF = bf_alloc(U, d + ds + 1);
+    b.EF = bf_alloc(P, m.d_e + dt + 1);
+    b.Wkve = bf_alloc(2 * da, m.d_e + dt + 1);
   }
+  w.QKVn = dalloc<float>(U * 3 * w.bf.d8a);
+  w.cq = dalloc<float>(da);
   // split-K arena (max over the engines) + routing partials in its tail
   size_t ws = 0;
   auto acc = [&](int M, int N, int64_t K) { ws += static_cast<size_t>(max_splits(M, N + 1, K)) * M * (N + 1); };
@@ -1377,6 +1497,12 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   acc(static_cast<int>(d), static_cast<int>(d), U);
   acc(1, static_cast<int>(3 * d), U);
   acc(static_cast<int>(3 * d), static_cast<int>(dt), U);
+  // node / edge split attention weight gradients (TMA)
+  acc(static_cast<int>(da), static_cast<int>(d + m.d_static + 1), U);
+  acc(static_cast<int>(da), static_cast<int>(d + m.d_static + 1), U);
+  acc(static_cast<int>(da), static_cast<int>(d + m.d_static + 1), U);
+  acc(static_cast<int>(da), static_cast<int>(m.d_e + dt), P);
+  acc(static_cast<int>(da), static_cast<int>(m.d_e + dt), P);
   // TMA-engine shapes (padded blocks, separate z / r problems)
   acc(static_cast<int>(w.bf.d8a + da), static_cast<int>(dt), P);
   acc(static_cast<int>(d), static_cast<int>(gin), U);
@@ -1406,7 +1532,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
 }
 
 void step_free(StepWork& w) {
-  void* ptrs[] = {w.Xg, w.GU, w.Gates, w.RS, w.s_hat, w.Qin, w.KVin, w.Gt, w.Q, w.KV, w.attn_a,
+  void* ptrs[] = {w.QKVn, w.cq, w.Xg, w.GU, w.Gates, w.RS, w.s_hat, w.Qin, w.KVin, w.Gt, w.Q, w.KV, w.attn_a,
                   w.H, w.AB, w.HID, w.Dhid, w.Hin, w.dlogit, w.logits, w.dIn, w.dQ, w.dKV,
                   w.dNodeAcc, w.dNode, w.Dg, w.T1, w.DMT, w.Mom, w.omega_part, w.ones,
                   w.loss_terms, w.splitk_ws, w.wpack, w.win};
@@ -1414,7 +1540,8 @@ void step_free(StepWork& w) {
     if (p) cudaFree(p);
   BfMat* bfs[] = {&w.bf.Xg, &w.bf.GU, &w.bf.RS, &w.bf.Qin, &w.bf.KVin, &w.bf.Gt, &w.bf.H, &w.bf.Hin,
                   &w.bf.Dhid, &w.bf.dQ, &w.bf.dKV, &w.bf.dNA, &w.bf.Dg, &w.bf.Wzr, &w.bf.Whm, &w.bf.Whs,
-                  &w.bf.Wq, &w.bf.Wkv, &w.bf.W1a, &w.bf.W1b, &w.bf.W1, &w.bf.Wst};
+                  &w.bf.Wq, &w.bf.Wkv, &w.bf.W1a, &w.bf.W1b, &w.bf.W1, &w.bf.Wst, &w.bf.NF,
+                  &w.bf.EF, &w.bf.Wkve};
   for (BfMat* b : bfs) bf_free(*b);
   w = StepWork{};
 }
@@ -1473,18 +1600,17 @@ void pack_weights_launch(const StepCtx& c, cudaStream_t s) {
   add(L.off[tWh], gin, d, md, b.Whm, 0, 0);
   add(L.off[tWh] + md, gin, d, d, b.Whs, 0, 0);
   add(L.off[tBh], 1, d, 1, b.Whs, 0, d);
-  add(L.off[tWq], q, da, q, b.Wq, 0, 0);
-  add(L.off[tBq], 1, da, 1, b.Wq, 0, q);
-  add(L.off[tWk], kv, da, kv, b.Wkv, 0, 0);
-  add(L.off[tBk], 1, da, 1, b.Wkv, 0, kv);
-  add(L.off[tWv], kv, da, kv, b.Wkv, da, 0);
-  add(L.off[tBv], 1, da, 1, b.Wkv, da, kv);
+  const int et = kv - nd;  // edge + time columns of Wk / Wv
+  add(L.off[tWk] + nd, kv, da, et, b.Wkve, 0, 0);
+  add(L.off[tBk], 1, da, 1, b.Wkve, 0, et);
+  add(L.off[tWv] + nd, kv, da, et, b.Wkve, da, 0);
+  add(L.off[tBv], 1, da, 1, b.Wkve, da, et);
   add(L.off[tW1], 2 * da, dh, da, b.W1a, 0, 0);
   add(L.off[tW1] + da, 2 * da, dh, da, b.W1b, 0, 0);
   add(L.off[tW1], 2 * da, dh, 2 * da, b.W1, 0, 0);
   add(L.off[tWq], q, da, nd, b.Wst, 0, 0);
-  add(L.off[tWk], kv, da, nd, b.Wst, da, 0);
-  add(L.off[tWv], kv, da, nd, b.Wst, 2 * da, 0);
+  add(L.off[tWk], kv, da, nd, b.Wst, b.d8a, 0);
+  add(L.off[tWv], kv, da, nd, b.Wst, 2 * b.d8a, 0);
   launch_pdl(pack_weights_kernel, dim3(dim3(32, J.n)), dim3(256), 0, s, J);
   TGB_CUDA(cudaGetLastError());
 }
@@ -1515,12 +1641,11 @@ PackMap make_pack_map(const StepCtx& c, int64_t& lo, int64_t& hi, int64_t& skip_
   { PackTensor& T = tensor(tBr); dest(T, b.Wzr, d, gin, 0, 1); }
   { PackTensor& T = tensor(tWh); dest(T, b.Whm, 0, 0, 0, md); dest(T, b.Whs, 0, 0, md, gin); }
   { PackTensor& T = tensor(tBh); dest(T, b.Whs, 0, d, 0, 1); }
-  { PackTensor& T = tensor(tWq); dest(T, b.Wq, 0, 0, 0, q); dest(T, b.Wst, 0, 0, 0, nd); }
-  { PackTensor& T = tensor(tBq); dest(T, b.Wq, 0, q, 0, 1); }
-  { PackTensor& T = tensor(tWk); dest(T, b.Wkv, 0, 0, 0, kv); dest(T, b.Wst, da, 0, 0, nd); }
-  { PackTensor& T = tensor(tBk); dest(T, b.Wkv, 0, kv, 0, 1); }
-  { PackTensor& T = tensor(tWv); dest(T, b.Wkv, da, 0, 0, kv); dest(T, b.Wst, 2 * da, 0, 0, nd); }
-  { PackTensor& T = tensor(tBv); dest(T, b.Wkv, da, kv, 0, 1); }
+  { PackTensor& T = tensor(tWq); dest(T, b.Wst, 0, 0, 0, nd); }
+  { PackTensor& T = tensor(tWk); dest(T, b.Wkve, 0, 0, nd, kv); dest(T, b.Wst, b.d8a, 0, 0, nd); }
+  { PackTensor& T = tensor(tBk); dest(T, b.Wkve, 0, kv - nd, 0, 1); }
+  { PackTensor& T = tensor(tWv); dest(T, b.Wkve, da, 0, nd, kv); dest(T, b.Wst, 2 * b.d8a, 0, 0, nd); }
+  { PackTensor& T = tensor(tBv); dest(T, b.Wkve, da, kv - nd, 0, 1); }
   { PackTensor& T = tensor(tW1); dest(T, b.W1a, 0, 0, 0, da); dest(T, b.W1b, 0, 0, da, 2 * da); dest(T, b.W1, 0, 0, 0, 2 * da); }
   lo = L.off[tWz];
   hi = L.off[tW1] + L.rows[tW1] * L.cols[tW1];
@@ -1593,8 +1718,29 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
            3 * d, nullptr, 1.0f);
     gemm_group_launch(gg, s);
   }
-  launch_pdl(gru_out_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, w.s_hat, c.d_numeric_flag);
+  launch_pdl(gru_out_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, w.s_hat, c.d_numeric_flag,
+             P + L.off[tStatic], bfx, U);
   TGB_CUDA(cudaGetLastError());
+}
+
+void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
+  const ModelDims& m = c.m;
+  const ParamLayout& L = c.L;
+  StepWork& w = *c.w;
+  const DGraph& g = *c.g;
+  const Dims D = make_dims(m, g);
+  const float* P = c.params;
+  const int da = D.da, Pc = w.cap_P;
+  const int ke = D.de + D.dt + 1;
+  const int stage = (ke + D.dt + 7) / 8 * 8;
+  launch_pdl(assemble_edge_kernel, dim3(row_blocks(Pc)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, D,
+             pl, g, P + L.off[tOmega], w.bf, Pc, stage);
+  launch_pdl(query_const_kernel, dim3(1), dim3(128), 0, s, D, P + L.off[tWq], P + L.off[tBq], w.cq);
+  TcGroup tg;
+  g_wide = 1;  // per-pair K and V edge parts in one pass: [Wk_e Wk_t bk ; Wv_e Wv_t bv]
+  tc_nn(tg, Pc, pl.sizes + kSzP, 2 * da, ke, w.bf.EF, 0, w.bf.Wkve, 0, 2 * da, w.KV, 2 * da);
+  g_wide = 0;
+  tc_group_launch(tg, s);
 }
 
 void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
@@ -1605,7 +1751,7 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   const Dims D = make_dims(m, g);
   const float* P = c.params;
   const int da = D.da;
-  const int R = w.cap_R, Pc = w.cap_P;
+  const int R = w.cap_R, Pc = w.cap_P, U = w.cap_U;
   const int* szR = pl.sizes + kSzR;
   const int* szP = pl.sizes + kSzP;
   const bool tma = gemm_impl() == kGemmTma;
@@ -1613,24 +1759,25 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   if (tma) bfx = w.bf;
   bfx.d8a = w.bf.d8a;
   bfx.d8d = w.bf.d8d;
-  const StepBf& B = w.bf;
   // ---- attention forward (K6)
   c.mark(phAttnAssemble, s);
-  {
-    const int stage = (std::max(D.kv_in, D.q_in) + 1 + D.dt + 7) / 8 * 8;
-    launch_pdl(assemble_attn_kernel, dim3(row_blocks(R + Pc)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, 
-        D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, tma ? nullptr : w.Qin, w.ldq,
-        tma ? nullptr : w.KVin, w.ldkv, w.Gt, bfx, R, Pc, stage);
-  }
-  c.mark(phAttnProj, s);
   if (tma) {
+    // node / edge split: the per-pair edge part (plan-only) is either enqueued
+    // here or already running on another stream; the per-support node part
+    // QKVn = NF Wst^T follows the GRU
+    if (c.ev_edge) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_edge, 0));
+    else attn_edge_launch(c, pl, s);
+    c.mark(phAttnProj, s);
     TcGroup tg;
-    tc_nn(tg, R, szR, da, D.q_in + 1, B.Qin, 0, B.Wq, 0, da, w.Q, da);
-    g_wide = 1;  // K and V in one pass over the pair rows: [Wk | bk ; Wv | bv]
-    tc_nn(tg, Pc, szP, 2 * da, D.kv_in + 1, B.KVin, 0, B.Wkv, 0, 2 * da, w.KV, 2 * da);
-    g_wide = 0;
+    tc_nn(tg, U, pl.sizes + kSzU, 3 * w.bf.d8a, D.d + D.ds, w.bf.NF, 0, w.bf.Wst, 0, 3 * w.bf.d8a, w.QKVn,
+          3 * w.bf.d8a);
     tc_group_launch(tg, s);
   } else {
+    const int stage = (std::max(D.kv_in, D.q_in) + 1 + D.dt + 7) / 8 * 8;
+    launch_pdl(assemble_attn_kernel, dim3(row_blocks(R + Pc)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s,
+        D, pl, g, P + L.off[tOmega], P + L.off[tStatic], w.s_hat, w.Qin, w.ldq, w.KVin, w.ldkv, w.Gt, bfx, R, Pc,
+        stage);
+    c.mark(phAttnProj, s);
     GemmGroup gg;
     add_nn(gg, R, szR, da, D.q_in, A_rows(w.Qin, w.ldq, D.q_in), B_wT(P + L.off[tWq], D.q_in, D.q_in),
            w.Q, da, P + L.off[tBq]);
@@ -1645,9 +1792,9 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
     const int lanes = (da + 31) / 32;
     auto fwd = lanes <= 1 ? attn_fwd_kernel<1> : lanes <= 2 ? attn_fwd_kernel<2>
              : lanes <= 4 ? attn_fwd_kernel<4> : attn_fwd_kernel<8>;
-    launch_pdl(fwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag, bfx);
+    launch_pdl(fwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag,
+               bfx, tma ? w.QKVn : nullptr, w.cq);
   }
-
 }
 
 void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, double* loss_out,
@@ -1735,7 +1882,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     const int lanes = (da + 31) / 32;
     auto bwd = lanes <= 1 ? attn_bwd_kernel<1> : lanes <= 2 ? attn_bwd_kernel<2>
              : lanes <= 4 ? attn_bwd_kernel<4> : attn_bwd_kernel<8>;
-    launch_pdl(bwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV, bfx, R, Pc);
+    launch_pdl(bwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV, bfx, R, Pc,
+               tma ? w.QKVn : nullptr);
   }
   if (pl.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));  // routing CSR ready
   const int64_t nchunks = ceil_div(R + Pc, kChunk) + 1;
@@ -1754,12 +1902,18 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   c.mark(phAttnBwdGemm, s);
   if (tma) {
     TcGroup tg;
-    const int nd = d + D.ds;
-    tc_nmn(tg, U, szU, nd, 3 * da, B.dNA, 0, B.Wst, 0, w.dNode, nd);
-    tc_tn(tg, wc, da, D.q_in + 1, R, szR, B.dQ, 0, B.Qin, 0, G + L.off[tWq], D.q_in, G + L.off[tBq]);
-    tc_tn(tg, wc, da, D.kv_in + 1, Pc, szP, B.dKV, 0, B.KVin, 0, G + L.off[tWk], D.kv_in, G + L.off[tBk]);
-    tc_tn(tg, wc, da, D.kv_in + 1, Pc, szP, B.dKV, B.d8a, B.KVin, 0, G + L.off[tWv], D.kv_in,
-          G + L.off[tBv]);
+    const int nd = d + D.ds, et = D.de + dt;
+    // dX of the node features (once per support) ...
+    tc_nmn(tg, U, szU, nd, 3 * B.d8a, B.dNA, 0, B.Wst, 0, w.dNode, nd);
+    // ... node-column weight gradients and the biases from the per-support sums ...
+    tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, 0, B.NF, 0, G + L.off[tWq], D.q_in, G + L.off[tBq]);
+    tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, B.d8a, B.NF, 0, G + L.off[tWk], D.kv_in, G + L.off[tBk]);
+    tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, 2 * B.d8a, B.NF, 0, G + L.off[tWv], D.kv_in, G + L.off[tBv]);
+    // ... edge / time-column weight gradients and the omega moments per pair
+    if (et > 0) {
+      tc_tn(tg, wc, da, et, Pc, szP, B.dKV, 0, B.EF, 0, G + L.off[tWk] + nd, D.kv_in);
+      tc_tn(tg, wc, da, et, Pc, szP, B.dKV, B.d8a, B.EF, 0, G + L.off[tWv] + nd, D.kv_in);
+    }
     if (dt > 0) tc_tn(tg, wc, B.d8a + da, dt, Pc, szP, B.dKV, 0, B.Gt, 0, w.Mom, dt);
     tc_group_launch(tg, s);
   } else {
@@ -1786,7 +1940,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   // ---- GRU backward (K9)
   c.mark(phGruBwd, s);
   launch_pdl(gru_bwd1_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
-                                          G + L.off[tStatic], bfx, U);
+                                          G + L.off[tStatic], bfx, U, tma ? G + L.off[tWq] : nullptr,
+                                          G + L.off[tBq]);
   if (c.br) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_br_join, 0));
   if (c.ev_tail_grads) TGB_CUDA(cudaEventRecord(c.ev_tail_grads, s));
   if (tma) {

@@ -44,9 +44,14 @@ struct ParamLayout {
 //  column carries the bias: forward GEMMs use packed [W | b] weights, and the
 //  weight-gradient GEMMs emit db as their last output column.
 //  dKV [dK | pad | dV], Dg [da_z | pad | da_r | pad | da_h] (blocks 8-aligned).
+//  TMA engine, node / edge split of the attention projections (linearity):
+//  NF [s_hat | static | 1] per support, EF [e | cos(dt w) | 1] per pair;
+//  Wst = [Wq_n ; Wk_n ; Wv_n] (node columns, row blocks d8a apart) gives the
+//  per-support node parts QKVn = NF Wst^T, Wkve = [Wk_e Wk_t bk ; Wv_e Wv_t bv]
+//  the per-pair edge parts; dNA [dq | pad | dK | pad | dV] per support.
 struct StepBf {
-  BfMat Xg, GU, RS, Qin, KVin, Gt, H, Hin, Dhid, dQ, dKV, dNA, Dg;
-  BfMat Wzr, Whm, Whs, Wq, Wkv, W1a, W1b, W1, Wst;  // Wkv = [Wk | bk ; Wv | bv]
+  BfMat Xg, GU, RS, Qin, KVin, Gt, H, Hin, Dhid, dQ, dKV, dNA, Dg, NF, EF;
+  BfMat Wzr, Whm, Whs, Wq, Wkv, W1a, W1b, W1, Wst, Wkve;  // Wkv = [Wk | bk ; Wv | bv]
   int d8a = 0, d8d = 0;
 };
 
@@ -62,6 +67,7 @@ struct StepWork {
   float *Hin = nullptr, *dlogit = nullptr, *logits = nullptr, *dIn = nullptr, *dQ = nullptr;
   float *dKV = nullptr, *dNodeAcc = nullptr, *dNode = nullptr, *Dg = nullptr, *T1 = nullptr;
   float *DMT = nullptr, *Mom = nullptr, *omega_part = nullptr, *ones = nullptr;
+  float *QKVn = nullptr, *cq = nullptr;  // node parts [U, 3 d8a]; query constant W_q,t 1 + b_q [d_a]
   double* loss_terms = nullptr;
   float* splitk_ws = nullptr;
   size_t splitk_ws_floats = 0;
@@ -116,6 +122,9 @@ struct StepCtx {
   // gradient there (ev_br_dec -> ev_br_join), off the critical path.
   cudaStream_t br = nullptr;
   bool packed = false;  // the TMA weight operands are current (packed by the fused Adam)
+  // Graph mode: the per-pair edge half of the attention projection was
+  // enqueued on another stream (attn_edge_launch); wait for ev_edge first.
+  cudaEvent_t ev_edge = nullptr;
   cudaEvent_t ev_g_zero = nullptr, ev_br_dec = nullptr, ev_br_join = nullptr;
   void mark(int slot, cudaStream_t s) const {
     if (marks) marks->mark(slot, s);
@@ -140,6 +149,9 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 // Forward-only evaluation pieces (evaluate_mrr, trainer.hpp:383-468).
 // attention embedding of every root (embed_root + attention_forward) into w.H
 void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s);
+// TMA engine: the plan-only half of it -- edge operands EF / Gt, the query
+// constant and the per-pair edge projection KE = EF Wkve^T (into w.KV).
+void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s);
 // decode_link of (src, dst) and (src, candidate) per event of an evaluation
 // plan (rpe = 2 + n_neg); cnt_out[e - base] = #candidates with logit >= truth.
 void eval_rank_launch(const StepCtx& c, const DPlan& pl, int32_t* cnt_out, int64_t base, cudaStream_t s);
