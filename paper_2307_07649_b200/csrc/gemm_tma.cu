@@ -1,8 +1,8 @@
 // TMA-fed, warp-specialized, persistent tcgen05 GEMM (see gemm_tma.cuh).
 //
-// CTA = 6 warps: warp 0 issues TMA loads (one elected lane), warp 1 owns the
-// TMEM allocation and issues tcgen05.mma (one elected lane), warps 2-5 run the
-// epilogue (warp w reads TMEM lanes 32 (w % 4) .. +32). Each CTA walks the
+// CTA = 10 warps: warp 0 issues TMA loads (one elected lane), warp 1 owns the
+// TMEM allocation and issues tcgen05.mma (one elected lane), warps 2-9 run the
+// epilogue (warp w reads TMEM lanes 32 (w % 4) .. +32, alternate 32-column chunks). Each CTA walks the
 // flattened tiles of all problems of the group round-robin. Two shared-memory
 // stages of {A_hi, A_lo, B_hi, B_lo} (128 B swizzled, K-major or MN-major per
 // operand) form a full/empty mbarrier ring that runs across tile boundaries;
@@ -24,9 +24,11 @@ namespace tgb {
 
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kThreads = 192, kStMax = 6;
+constexpr int kBM = 128, kBK = 64, kStMax = 6;
+constexpr int kEpiWarps = 8;                      // two warps per TMEM lane quarter
+constexpr int kThreads = 64 + 32 * kEpiWarps;     // producer, MMA, epilogue
 constexpr int kATileB = kBM * kBK * 2;   // 16 KB (one of hi / lo)
-constexpr int kEpiStageB = 4 * 32 * 33 * 4;  // static epilogue transpose buffers
+constexpr int kEpiStageB = kEpiWarps * 32 * 33 * 4;  // static epilogue transpose buffers
 constexpr int kSmemMax = 232448 - kEpiStageB;  // opt-in dynamic maximum per CTA
 
 // Shared-memory / TMEM geometry is sized by the group's widest N tile, so
@@ -154,8 +156,6 @@ __device__ __forceinline__ bool tile_info(const TcParams& gp, int t, TileInfo& t
 // Persistent CTA: static round-robin over the flattened tiles of the group.
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcParams gp) {
   if (threadIdx.x == 0) trace(0);
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int kStageB = gp.stage_bytes, kBTileB = gp.b_tile_bytes;
@@ -165,10 +165,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint64_t* tfull = empty + kSt;   // [2] accumulator ready for the epilogue
   uint64_t* tempty = tfull + 2;    // [2] accumulator drained by the epilogue
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ float epi_stage[4 * 32 * 33];  // epilogue transposes (static: LDS / STS, not generic)
+  __shared__ float epi_stage[kEpiWarps * 32 * 33];  // epilogue transposes (static: LDS / STS, not generic)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = gp.tile_base[gp.count];
 
+  // Prologue independent of the predecessor's output (it overlaps its tail
+  // under programmatic dependent launch): descriptor prefetch, barriers, TMEM.
+  if (warp == 0 && lane < gp.count) {
+    const TcProblem& Q = gp.p[lane];
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&Q.a.hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&Q.a.lo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&Q.b.hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&Q.b.lo)) : "memory");
+  }
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < kSt; ++s) {
       mbar_init(full + s, 1);
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, 4);  // one arrival per epilogue warp
+      mbar_init(tempty + a, kEpiWarps);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -190,6 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
   const int acc_cols = gp.tmem_cols / 2;
+  pdl_wait();  // operands and runtime sizes come from the predecessor
+  pdl_trigger();
   if (threadIdx.x == 0) trace(1);
 
   if (warp == 0) {
@@ -272,8 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       }
     }
   } else {
-    // epilogue warps 2..5: warp w reads TMEM lanes 32 (w % 4) .. + 32
+    // epilogue warps 2..9: warp w reads TMEM lanes 32 (w % 4) .. + 32
     const int quarter = warp & 3;
+    const int ehalf = (warp - 2) >> 2;  // the two warps of a quarter take alternate 32-column chunks
     const int epi_mode = g_tc_epi_mode;
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -284,16 +296,28 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       mbar_wait(tfull + acc, (lt >> 1) & 1);
       if (warp == 2 && lane == 0) trace(4);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // problem fields in registers (P lives in parameter space, indexed)
       const int N = P.N;
       const int ntile = P.ntile;
       const int nvalid = min(ntile, N - ti.n0);
       const int n0 = ti.n0;
+      const int splits = P.splits;
+      const int PM = P.M;
+      const float alpha = P.alpha, beta = P.beta;
+      float* const Cp = P.C;
+      float* const C2p = P.C2;
+      float* const wsp = P.ws;
+      const int64_t ldcp = P.ldc;
       // TMEM -> registers (thread = row) -> shared-memory transpose -> global
-      // stores with lane = column: every store instruction writes one row's
-      // 128 contiguous bytes instead of 32 scattered rows.
-      float* stg = epi_stage + quarter * (32 * 33);
+      // stores with lane = column (or float4 per lane, four rows per instruction)
+      float* stg = epi_stage + (warp - 2) * (32 * 33);
       const int mb = ti.m0 + quarter * 32;  // first row of this warp
-      for (int c0 = 0; c0 < ntile; c0 += 32) {
+      const int npart = splits > 1 ? N : static_cast<int>(ldcp);
+      float* const vbase = splits > 1 ? wsp + static_cast<int64_t>(ti.split) * PM * N : Cp;
+      const int rmax = splits > 1 ? PM : ti.M;  // rows to write (zeros past ti.M for partials)
+      const bool vec_ok = epi_mode == 0 && (npart & 3) == 0 && (reinterpret_cast<uintptr_t>(vbase) & 15) == 0 &&
+                          beta == 0.0f;
+      for (int c0 = 32 * ehalf; c0 < ntile; c0 += 64) {
         const int halves = min(2, (ntile - c0) / 16);
         for (int h = 0; h < halves; ++h) {
           uint32_t v[16];
@@ -316,38 +340,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
         __syncwarp();
         if (warp == 2 && lane == 0 && c0 < 96) trace(8 + 2 * (c0 / 32));
-        // fast path: a full 32-column chunk of 16-byte aligned fp32 rows -- each
-        // lane stores a float4, four rows of 128 B per instruction
-        const int npart = P.splits > 1 ? N : static_cast<int>(P.ldc);
-        float* vbase = P.splits > 1 ? P.ws + static_cast<int64_t>(ti.split) * P.M * N : P.C;
-        const bool vec = epi_mode == 0 && halves == 2 && c0 + 32 <= nvalid && (npart & 3) == 0 &&
-                         ((n0 + c0) & 3) == 0 && (reinterpret_cast<uintptr_t>(vbase) & 15) == 0 &&
-                         P.beta == 0.0f && !(P.C2 && n0 + c0 + 32 > N - 1);
-        if (vec) {
-          const int rmax = P.splits > 1 ? P.M : ti.M;  // rows to write (zeros past ti.M for partials)
+        if (vec_ok && halves == 2 && c0 + 32 <= nvalid && ((n0 + c0) & 3) == 0 && !(C2p && n0 + c0 + 32 > N - 1)) {
           const int rr = lane >> 3, cc = (lane & 7) * 4;
-          for (int r0 = 0; r0 < 32; r0 += 4) {
-            const int m = mb + r0 + rr;
-            if (m < rmax) {
-              float4 o;
-              const float* src = stg + (r0 + rr) * 33 + cc;
-              const bool live = m < ti.M;
-              o.x = live ? P.alpha * src[0] : 0.0f;
-              o.y = live ? P.alpha * src[1] : 0.0f;
-              o.z = live ? P.alpha * src[2] : 0.0f;
-              o.w = live ? P.alpha * src[3] : 0.0f;
-              *reinterpret_cast<float4*>(vbase + static_cast<int64_t>(m) * npart + n0 + c0 + cc) = o;
-            }
+          float* dst0 = vbase + static_cast<int64_t>(mb + rr) * npart + n0 + c0 + cc;
+          float4 o[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float* src = stg + (4 * k + rr) * 33 + cc;
+            const bool live = mb + 4 * k + rr < ti.M;
+            o[k].x = live ? alpha * src[0] : 0.0f;
+            o[k].y = live ? alpha * src[1] : 0.0f;
+            o[k].z = live ? alpha * src[2] : 0.0f;
+            o[k].w = live ? alpha * src[3] : 0.0f;
           }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (mb + 4 * k + rr < rmax) *reinterpret_cast<float4*>(dst0 + static_cast<int64_t>(4 * k) * npart) = o[k];
+          if (warp == 2 && lane == 0 && c0 < 96) trace(9 + 2 * (c0 / 32));
           __syncwarp();
           continue;
         }
         const int col = c0 + lane;                 // this lane's column in the tile
         const bool col_ok = lane < 16 * halves && col < nvalid && epi_mode != 1;
         const int n = n0 + col;
-        if (P.splits > 1) {
-          const int rows = min(32, P.M - mb);
-          float* wrow = P.ws + (static_cast<int64_t>(ti.split) * P.M + mb) * N + n;
+        if (splits > 1) {
+          const int rows = min(32, PM - mb);
+          float* wrow = wsp + (static_cast<int64_t>(ti.split) * PM + mb) * N + n;
           for (int r0 = 0; r0 < rows; r0 += 8) {
             float val[8];
 #pragma unroll
@@ -357,11 +375,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
               if (r0 + k < rows && col_ok) wrow[static_cast<int64_t>(r0 + k) * N] = mb + r0 + k < ti.M ? val[k] : 0.0f;
           }
         } else {
-          const bool to_c2 = P.C2 && n == N - 1;
+          const bool to_c2 = C2p && n == N - 1;
           const int rows = min(32, ti.M - mb);
-          const int64_t ldc = P.ldc;
-          float* crow = P.C + static_cast<int64_t>(mb) * ldc + n;
-          const float alpha = P.alpha, beta = P.beta;
+          const int64_t ldc = ldcp;
+          float* crow = Cp + static_cast<int64_t>(mb) * ldc + n;
           for (int r0 = 0; r0 < rows; r0 += 8) {
             float val[8], prev[8];
 #pragma unroll
@@ -372,13 +389,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
             if (beta != 0.0f) {
 #pragma unroll
               for (int k = 0; k < 8; ++k)
-                if (r0 + k < rows && col_ok) prev[k] = to_c2 ? P.C2[mb + r0 + k] : crow[(r0 + k) * ldc];
+                if (r0 + k < rows && col_ok) prev[k] = to_c2 ? C2p[mb + r0 + k] : crow[(r0 + k) * ldc];
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               if (r0 + k < rows && col_ok) {
                 const float x = alpha * val[k] + beta * prev[k];
-                if (to_c2) P.C2[mb + r0 + k] = x;
+                if (to_c2) C2p[mb + r0 + k] = x;
                 else crow[(r0 + k) * ldc] = x;
               }
             }
