@@ -55,20 +55,21 @@ def model_dims(cfg):
 
 # ----------------------------------------------------------------- roofline bookkeeping
 def attn_proj_flops(sz, cfg):
-    """Algorithmic FLOPs of the attention projection launch (Q for R roots,
-    K and V for P pairs): 2 * (R * q_in * d_attn + 2 * P * kv_in * d_attn)."""
+    """Algorithmic FLOPs of the attention projection GEMMs (node / edge split,
+    SURVEY 8(a) a8 by linearity): per pair the edge part [e | cos(dt w) | 1] ->
+    K|V, per support the node part [s_hat | static] -> Q|K|V:
+    2 * (P * (d_e + d_t + 1) * 2 d_a + U * (d + d_s) * 3 d_a)."""
     d, ds, de, dt, da = 100, cfg["d_static"], cfg["d_e"], 100, 100
-    q_in, kv_in = d + ds + dt, d + ds + de + dt
-    return 2.0 * (sz["R"] * q_in * da + 2 * sz["P"] * kv_in * da)
+    return 2.0 * (sz["P"] * (de + dt + 1) * 2 * da + sz["U"] * (d + ds) * 3 * da)
 
 
 def attn_proj_bytes(sz, cfg):
-    """Compulsory bytes of that launch in fp32-equivalents: the gathered Q / K|V
-    input rows (Qin [R x q_in], KVin [P x kv_in]) in, Q [R x d_a] and K|V
-    [P x 2 d_a] out. (Weights are L2-resident and excluded.)"""
+    """Compulsory bytes of those launches in fp32-equivalents (a bf16 hi/lo
+    pair is 4 bytes): the edge rows EF [P x (d_e + d_t + 1)] and node rows NF
+    [U x (d + d_s)] in, K|V edge parts [P x 2 d_a] and node parts [U x 3 d_a]
+    out. (Weights are L2-resident and excluded.)"""
     d, ds, de, dt, da = 100, cfg["d_static"], cfg["d_e"], 100, 100
-    q_in, kv_in = d + ds + dt, d + ds + de + dt
-    return 4.0 * (sz["R"] * (q_in + da) + sz["P"] * (kv_in + 2 * da))
+    return 4.0 * (sz["P"] * (de + dt + 1 + 2 * da) + sz["U"] * (d + ds + 3 * da))
 
 
 def step_model_flops(sz, cfg):
@@ -84,7 +85,7 @@ def step_model_flops(sz, cfg):
 def roofline_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of the roofline kernel from
     the committed ncu --set full capture (profiles/), per launch."""
-    p = os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r01b_roofline_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
@@ -336,7 +337,7 @@ def main():
     hbm_view = {"achieved": hbm_bytes / secs / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
     bound = "hbm" if t_hbm >= t_tensor else "tensor"
     main = hbm_view if bound == "hbm" else tensor_view
-    roofline = {"kernel": "attention projection GEMM group (Q, fused K|V; tcgen05 bf16x3, TMA)",
+    roofline = {"kernel": "attention projection GEMMs (tcgen05 bf16x3, TMA): per-pair edge K|V + per-support node Q|K|V",
                 "bound": bound, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
                 "frac": main["achieved"] / main["peak"], "traffic": roofline_traffic(), "peak_source": src,
                 "flops_per_launch": flops, "algorithmic_bytes_per_launch": hbm_bytes,

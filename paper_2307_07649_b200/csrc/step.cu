@@ -1736,6 +1736,7 @@ void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   launch_pdl(assemble_edge_kernel, dim3(row_blocks(Pc)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, D,
              pl, g, P + L.off[tOmega], w.bf, Pc, stage);
   launch_pdl(query_const_kernel, dim3(1), dim3(128), 0, s, D, P + L.off[tWq], P + L.off[tBq], w.cq);
+  c.mark(phAttnProj, s);
   TcGroup tg;
   g_wide = 1;  // per-pair K and V edge parts in one pass: [Wk_e Wk_t bk ; Wv_e Wv_t bv]
   tc_nn(tg, Pc, pl.sizes + kSzP, 2 * da, ke, w.bf.EF, 0, w.bf.Wkve, 0, 2 * da, w.KV, 2 * da);
@@ -1766,8 +1767,7 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
     // here or already running on another stream; the per-support node part
     // QKVn = NF Wst^T follows the GRU
     if (c.ev_edge) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_edge, 0));
-    else attn_edge_launch(c, pl, s);
-    c.mark(phAttnProj, s);
+    else attn_edge_launch(c, pl, s);  // marks phAttnProj before its GEMM
     TcGroup tg;
     tc_nn(tg, U, pl.sizes + kSzU, 3 * w.bf.d8a, D.d + D.ds, w.bf.NF, 0, w.bf.Wst, 0, 3 * w.bf.d8a, w.QKVn,
           3 * w.bf.d8a);
