@@ -498,6 +498,7 @@ struct tgnn_run {
   int64_t prepared = -1;  // barrier whose plan + read view are ready in plans/views[b % 2]
   cudaEvent_t ev_fork = nullptr, ev_written = nullptr, ev_next = nullptr;
   cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
+  cudaEvent_t ev_red = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
   // validation / metrics rows (run_training, trainer.hpp:725-743)
   int64_t val_begin = 0, val_end = 0, eval_batch = 0;
@@ -526,7 +527,7 @@ struct tgnn_run {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_written) cudaEventDestroy(ev_written);
     if (ev_next) cudaEventDestroy(ev_next);
-    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin, ev_edge};
+    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin, ev_edge, ev_red};
     for (cudaEvent_t e : more)
       if (e) cudaEventDestroy(e);
     if (d_desc) cudaFree(d_desc);
@@ -751,6 +752,7 @@ void barrier_body_dev(tgnn_run* r, int p) {
   sc.ev_g_zero = r->ev_gzero;
   sc.ev_br_dec = r->ev_dec;
   sc.ev_br_join = r->ev_brjoin;
+  sc.ev_red = r->ev_red;
   // edge branch: the plan-only half of the attention projection runs beside the GRU
   if (gemm_impl() == kGemmTma) {
     TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_fork, 0));
@@ -811,7 +813,7 @@ void build_graph(tgnn_run* r) {
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming));
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_written, cudaEventDisableTiming));
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
-    cudaEvent_t* more[] = {&r->ev_gru, &r->ev_gzero, &r->ev_dec, &r->ev_brjoin, &r->ev_edge};
+    cudaEvent_t* more[] = {&r->ev_gru, &r->ev_gzero, &r->ev_dec, &r->ev_brjoin, &r->ev_edge, &r->ev_red};
     for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   for (int p = 0; p < 2; ++p) {

@@ -543,7 +543,7 @@ void tc_gemm_prepare() {
   }
 }
 
-void tc_group_launch(const TcGroup& g, cudaStream_t s) {
+void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_stream, cudaEvent_t ev) {
   if (g.count == 0) return;
   tc_gemm_prepare();
   TcParams gp;
@@ -588,7 +588,13 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s) {
   launch_pdl(tc_gemm_kernel, dim3(grid), dim3(kThreads), smem, s, gp);
   TGB_CUDA(cudaGetLastError());
   if (any_split) {
-    launch_pdl(tc_splitk_reduce_kernel, dim3(dim3(64, g.count)), dim3(256), 0, s, gp);
+    cudaStream_t rs = s;
+    if (reduce_stream && ev) {  // the split outputs are leaves: reduce them off the critical path
+      TGB_CUDA(cudaEventRecord(ev, s));
+      TGB_CUDA(cudaStreamWaitEvent(reduce_stream, ev, 0));
+      rs = reduce_stream;
+    }
+    launch_pdl(tc_splitk_reduce_kernel, dim3(dim3(64, g.count)), dim3(256), 0, rs, gp);
     TGB_CUDA(cudaGetLastError());
   }
 }

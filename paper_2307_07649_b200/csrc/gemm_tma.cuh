@@ -73,7 +73,10 @@ inline int tc_ntile(int N, int cap = 256) {
   return static_cast<int>(std::min<int64_t>(cap, (N + 15) / 16 * 16));
 }
 
-void tc_group_launch(const TcGroup& g, cudaStream_t s);
+// reduce_stream / ev (optional): the split-K reduction of the group's split
+// problems runs on reduce_stream after ev (recorded on s past the GEMM).
+void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_stream = nullptr,
+                     cudaEvent_t ev = nullptr);
 // Debug: average microseconds of one launch of an M x N x K K-major problem
 // and (optionally) a per-CTA globaltimer trace [2*148 x 8].
 void tc_debug_bench(int M, int N, int K, int ntile, int iters, double* us, unsigned long long* trace_out,

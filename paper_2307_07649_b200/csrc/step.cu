@@ -875,6 +875,19 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
   }
 }
 
+// Node / edge split: the query's time block is the constant cos(0 w) = 1, so
+// its weight gradient is db_q in every column (trainer.hpp:133-136).
+__global__ void qtime_grad_kernel(Dims D, float* __restrict__ gWq, const float* __restrict__ gBq) {
+  pdl_wait();
+  pdl_trigger();
+  const int nd = D.d + D.ds;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < static_cast<int64_t>(D.da) * D.dt;
+       x += gridDim.x * blockDim.x) {
+    const int64_t r = x / D.dt, j = x % D.dt;
+    gWq[r * D.q_in + nd + j] = gBq[r];
+  }
+}
+
 // da_r = (Wh^T da_h)[s part] * s * r (1 - r)  (gru.hpp:124-127).
 __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ T1,
                                 const float* __restrict__ Gates, float* __restrict__ Dg, StepBf bf) {
@@ -1873,7 +1886,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     TcGroup tg;
     tc_tn(tg, wc, dh, 2 * da + 1, B2, sz2B, B.Dhid, 0, B.Hin, 0, G + L.off[tW1], 2 * da, G + L.off[tB1]);
     tc_nmn(tg, B2, sz2B, 2 * da, dh, B.Dhid, 0, B.W1, 0, w.dIn, 2 * da);
-    tc_group_launch(tg, s);
+    tc_group_launch(tg, s, c.br, c.ev_red);
   }
 
   // ---- attention backward (K8)
@@ -1915,7 +1928,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
       tc_tn(tg, wc, da, et, Pc, szP, B.dKV, B.d8a, B.EF, 0, G + L.off[tWv] + nd, D.kv_in);
     }
     if (dt > 0) tc_tn(tg, wc, B.d8a + da, dt, Pc, szP, B.dKV, 0, B.Gt, 0, w.Mom, dt);
-    tc_group_launch(tg, s);
+    tc_group_launch(tg, s, c.br, c.ev_red);
   } else {
     GemmGroup gg;
     Operand bs;
@@ -1940,9 +1953,17 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   // ---- GRU backward (K9)
   c.mark(phGruBwd, s);
   launch_pdl(gru_bwd1_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
-                                          G + L.off[tStatic], bfx, U, tma ? G + L.off[tWq] : nullptr,
-                                          G + L.off[tBq]);
-  if (c.br) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_br_join, 0));
+                                          G + L.off[tStatic], bfx, U, nullptr, nullptr);
+  if (tma) {
+    // node / edge split: dW_q[:, time] = sum_r dq_r = db_q (cos(0 w) = 1), after
+    // db_q's split-K reduction (on the branch when there is one)
+    launch_pdl(qtime_grad_kernel, dim3(ceil_div(static_cast<int64_t>(da) * dt, 256)), dim3(256), 0,
+               c.br ? c.br : s, D, G + L.off[tWq], G + L.off[tBq]);
+  }
+  if (c.br) {  // the branch's loss, W2 / b2 gradient and split-K reductions so far
+    TGB_CUDA(cudaEventRecord(c.ev_br_join, c.br));
+    TGB_CUDA(cudaStreamWaitEvent(s, c.ev_br_join, 0));
+  }
   if (c.ev_tail_grads) TGB_CUDA(cudaEventRecord(c.ev_tail_grads, s));
   if (tma) {
     TcGroup tg;

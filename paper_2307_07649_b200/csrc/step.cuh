@@ -126,6 +126,7 @@ struct StepCtx {
   // enqueued on another stream (attn_edge_launch); wait for ev_edge first.
   cudaEvent_t ev_edge = nullptr;
   cudaEvent_t ev_g_zero = nullptr, ev_br_dec = nullptr, ev_br_join = nullptr;
+  cudaEvent_t ev_red = nullptr;  // split-K reductions of the weight gradients on the branch
   void mark(int slot, cudaStream_t s) const {
     if (marks) marks->mark(slot, s);
   }

@@ -1,0 +1,34 @@
+"""GPU: the pipelined CUDA-graph barrier (plan-ahead on an aux stream, edge
+projection / root writes / loss / split-K reductions on branch streams,
+programmatic dependent launch, fused Adam + weight pack) must be a pure
+schedule change: bitwise the same losses and weights as the direct,
+single-stream path. A race between branches shows up here first."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2307_07649_b200 as T
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg", [dict(nodes=10984, events=60000, d_e=172, d_static=100),
+                                 dict(nodes=2000, events=30000, d_e=0, d_static=0)])
+def test_graph_barriers_bitwise_equal_direct(ctx, cfg):
+    g = T.TemporalGraph.synthetic(ctx, T.SynthParams(nodes=cfg["nodes"], events=cfg["events"], d_e=cfg["d_e"],
+                                                     seed=4))
+    _, _, t = g.events()
+    mc = T.ModelConfig(d_mem=100, d_time=100, d_static=cfg["d_static"], d_attn=100, d_hidden=100, d_e=cfg["d_e"],
+                       n_neighbors=10, num_nodes=cfg["nodes"], max_t=float(t[-1]))
+    tc = T.TrainConfig(local_batch=600, lr_base=1e-3, seed=2, epochs=2)
+    res = {}
+    for graphs in (True, False):
+        run = T.Run(ctx, g, mc, tc, 0, cfg["events"] * 7 // 10, use_graphs=graphs)
+        n = min(run.barriers, 60)
+        run.step(n // 2)
+        run.step(n - n // 2)  # across a re-entry of the graph pipeline (and an epoch reset)
+        res[graphs] = (run.losses(), run.params())
+        run.close()
+    assert np.array_equal(res[True][0], res[False][0])
+    assert np.array_equal(res[True][1], res[False][1])
