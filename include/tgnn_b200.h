@@ -168,6 +168,9 @@ typedef struct tgnn_run_options {
   int64_t val_begin, val_end;
   int32_t eval_negatives, pad0;
   int64_t eval_batch;
+  /* record the daemon op-log of this rank's reads and writes (ref
+   * memory_daemon.hpp:73,90, oplog.hpp:15-45); read with tgnn_run_oplog */
+  int32_t oplog, pad1;
 } tgnn_run_options;
 
 /* build_assignment + Assignment::task (ref parallel.hpp:150-331), host only.
@@ -195,6 +198,11 @@ int tgnn_run_params(tgnn_run* r, double* flat);
  * loss since the previous row), val_mrr, elapsed_s. Collective when nranks > 1
  * (the loss means need every rank's slot); rows == NULL returns the count only. */
 int tgnn_run_metrics(tgnn_run* r, int64_t* count, double* rows);
+/* This rank's op-log records so far, rows[count x 6] = epoch (sweep), iter
+ * (pair), kind (0 = 'R', 1 = 'W'), rank within the memory copy, first, len
+ * (ref OpRecord, oplog.hpp:15-24). A memory copy's op-log is the union of its
+ * ranks' rows ordered by (iter, kind, rank). rows == NULL returns the count. */
+int tgnn_run_oplog(tgnn_run* r, int64_t* count, int64_t* rows);
 /* evaluate_mrr of the run's current weights (rank-local, no collective). */
 int tgnn_run_evaluate_mrr(tgnn_run* r, int64_t eval_begin, int64_t eval_end, int64_t batch_size,
                           int32_t n_negatives, uint64_t seed, double* mrr, int64_t* queries);

@@ -132,6 +132,12 @@ class RefGraph:
     def write_dataset(self, csv_path):
         _check(lib().ref_write_dataset(self.h, os.fsencode(csv_path)))
 
+    def run_oplog(self, mcfg, tcfg, train_begin, train_end, prefix):
+        """run_training with one op-log file per memory copy: <prefix>.<r>.oplog."""
+        mc = model_cfg(mcfg)
+        _check(lib().ref_run_oplog(self.h, C.byref(mc), C.byref(tcfg), C.c_int64(train_begin),
+                                   C.c_int64(train_end), os.fsencode(prefix)))
+
     def chronological_split(self, train_frac, val_frac):
         a, b = C.c_int64(), C.c_int64()
         _check(lib().ref_chronological_split(self.h, C.c_double(train_frac), C.c_double(val_frac),
@@ -270,6 +276,15 @@ class RefGraph:
                              _p(metrics, f64p), C.c_int64(4096), C.byref(nm), C.byref(el)))
         return dict(barrier_loss=bl[:nb.value].copy(), params=params,
                     metrics=metrics[:nm.value].copy(), elapsed_s=el.value, barriers=nb.value)
+
+
+def validate_oplog(path, i, j):
+    """validate_oplog_file (oplog.hpp:105-160) -> (ok, line, message)."""
+    line = C.c_int64()
+    msg = C.create_string_buffer(512)
+    _check(lib().ref_validate_oplog(os.fsencode(path), C.c_int32(i), C.c_int32(j), C.byref(line), msg,
+                                    C.c_int64(512)))
+    return line.value == 0, line.value, msg.value.decode()
 
 
 def param_count(mcfg) -> int:

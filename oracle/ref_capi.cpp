@@ -24,6 +24,9 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
+#include <memory>
+#include <cstdio>
 #include <string>
 #include <vector>
 
@@ -531,6 +534,35 @@ int ref_run(void* gp, const ref_model_cfg* c, const ref_train_cfg* tc, int64_t t
       metrics[x * 5 + 3] = res.metrics[x].val_mrr;
       metrics[x * 5 + 4] = res.metrics[x].elapsed_s;
     }
+  })
+}
+
+// run_training with op-log sinks (trainer.hpp:583, 643-667): one file per
+// memory copy, "<prefix>.<r>.oplog"; and validate_oplog (oplog.hpp:105-156).
+int ref_run_oplog(void* gp, const ref_model_cfg* c, const ref_train_cfg* tc, int64_t train_begin,
+                  int64_t train_end, const char* prefix) {
+  REF_GUARD({
+    auto* g = static_cast<TemporalGraph*>(gp);
+    RunOptions opt;
+    opt.model = to_mcfg(c);
+    opt.train = to_tcfg(tc);
+    opt.train_begin = train_begin;
+    opt.train_end = train_end;
+    std::vector<std::unique_ptr<std::ofstream>> files;
+    for (int r = 0; r < opt.train.k; ++r) {
+      files.push_back(std::make_unique<std::ofstream>(std::string(prefix) + "." + std::to_string(r) + ".oplog"));
+      opt.oplog_out.push_back(files.back().get());
+    }
+    run_training(*g, opt);
+    for (auto& f : files) f->flush();
+  })
+}
+
+int ref_validate_oplog(const char* path, int32_t i, int32_t j, int64_t* bad_line, char* msg, int64_t msg_cap) {
+  REF_GUARD({
+    OplogVerdict v = validate_oplog_file(path, i, j);
+    *bad_line = v.ok ? 0 : static_cast<int64_t>(v.line);
+    std::snprintf(msg, static_cast<size_t>(msg_cap), "%s", v.message.c_str());
   })
 }
 

@@ -35,6 +35,7 @@ __all__ = [
     "gen_synthetic", "Context", "TemporalGraph", "NodeMemoryStore", "ReadView", "TrainerCore",
     "Run", "run_sequential", "param_count", "init_params", "lr_eff", "Evaluator",
     "write_metrics_csv", "save_checkpoint", "load_checkpoint", "write_dataset", "chronological_split",
+    "write_oplog",
 ]
 
 lib()  # fail loudly at import if the native library is absent
@@ -563,13 +564,14 @@ class Run:
     def __init__(self, ctx: Context, g: TemporalGraph, model: ModelConfig, train: TrainConfig,
                  train_begin: int, train_end: int, rank: int = 0, nranks: int = 1,
                  use_graphs: bool = True, val_begin: int = 0, val_end: int = 0,
-                 eval_negatives: int = 49, eval_batch: int = 0):
+                 eval_negatives: int = 49, eval_batch: int = 0, oplog: bool = False):
         self.ctx, self.g, self.model, self.train = ctx, g, model, train
         ctx._adopt(self)
         if model.num_nodes == 0:
             model.num_nodes = g.num_nodes
         opt = RunOptionsC(model.c(), train.c(), train_begin, train_end, rank, nranks,
-                          1 if use_graphs else 0, val_begin, val_end, eval_negatives, 0, eval_batch)
+                          1 if use_graphs else 0, val_begin, val_end, eval_negatives, 0, eval_batch,
+                          1 if oplog else 0, 0)
         self.h = C.c_void_p()
         check(lib().tgnn_run_create(ctx.h, g.h, C.byref(opt), C.byref(self.h)))
         b, n = C.c_int64(), C.c_int64()
@@ -609,6 +611,16 @@ class Run:
         out = np.zeros((n.value, 5))
         if n.value:
             check(lib().tgnn_run_metrics(self.h, C.byref(n), _p(out, f64p)))
+        return out
+
+    def oplog(self):
+        """This rank's daemon op-log rows [n x 6]: epoch, iter, kind (0 R / 1 W),
+        rank within the memory copy, first, len (OpRecord, oplog.hpp:15-24)."""
+        n = C.c_int64()
+        check(lib().tgnn_run_oplog(self.h, C.byref(n), None))
+        out = np.zeros((n.value, 6), np.int64)
+        if n.value:
+            check(lib().tgnn_run_oplog(self.h, C.byref(n), _p(out, i64p)))
         return out
 
     def save_checkpoint(self, path):
@@ -672,6 +684,20 @@ def chronological_split(num_events: int, train_frac: float, val_frac: float):
     a, b = C.c_int64(), C.c_int64()
     check(lib().tgnn_chronological_split(num_events, train_frac, val_frac, C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def write_oplog(path_or_file, rows):
+    """A memory copy's op-log (OpLogWriter::append, oplog.hpp:31-35) from the
+    rows of all its ranks (Run.oplog()), ordered by (iter, kind, rank): each
+    pair's read bracket, then its write bracket, ranks ascending."""
+    rows = np.asarray(rows, np.int64).reshape(-1, 6)
+    order = np.lexsort((rows[:, 3], rows[:, 2], rows[:, 1]))
+    text = "".join("%d,%d,%s,%d,%d,%d\n" % (r[0], r[1], "RW"[r[2]], r[3], r[4], r[5]) for r in rows[order])
+    if hasattr(path_or_file, "write"):
+        path_or_file.write(text)
+    else:
+        with open(path_or_file, "w") as f:
+            f.write(text)
 
 
 def save_checkpoint(model: ModelConfig, params, path):

@@ -81,7 +81,7 @@ class RunOptionsC(C.Structure):
     _fields_ = [("model", ModelConfigC), ("train", TrainConfigC), ("train_begin", i64),
                 ("train_end", i64), ("rank", i32), ("nranks", i32), ("use_graphs", i32),
                 ("val_begin", i64), ("val_end", i64), ("eval_negatives", i32), ("pad0", i32),
-                ("eval_batch", i64)]
+                ("eval_batch", i64), ("oplog", i32), ("pad1", i32)]
 
 
 _lib = None
@@ -134,6 +134,7 @@ SIGNATURES = {
     "tgnn_run_params": [vp, f64p],
     "tgnn_run_traversed": [vp, i64, i64, i64p],
     "tgnn_run_metrics": [vp, i64p, f64p],
+    "tgnn_run_oplog": [vp, i64p, i64p],
     "tgnn_run_evaluate_mrr": [vp, i64, i64, i64, i32, u64, f64p, i64p],
     "tgnn_evaluator_create": [vp, vp, C.POINTER(ModelConfigC), i64, i32, C.POINTER(vp)],
     "tgnn_evaluator_destroy": [vp],

@@ -500,6 +500,9 @@ struct tgnn_run {
   cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
   cudaEvent_t ev_red = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
+  // daemon op-log records [barriers x 4] (R first, R len, W first, W len)
+  bool oplog = false;
+  int64_t* d_oplog = nullptr;
   // validation / metrics rows (run_training, trainer.hpp:725-743)
   int64_t val_begin = 0, val_end = 0, eval_batch = 0;
   int eval_negatives = 49;
@@ -514,6 +517,7 @@ struct tgnn_run {
   std::vector<Row> rows;
 
   ~tgnn_run() {
+    if (d_oplog) cudaFree(d_oplog);
     for (Row& row : rows)
       if (row.done) cudaEventDestroy(row.done);
     if (ev_t0) cudaEventDestroy(ev_t0);
@@ -657,6 +661,15 @@ void run_barrier(tgnn_run* r, int64_t b) {
         substep_gru_launch(sc, tr->plans[0], tr->views[0], s);
         sc.mark(phWrites, s);
         root_writes_launch(sc, tr->plans[0], tr->views[0], s, r->group_size > 1 ? nullptr : &r->mem->d);
+        if (r->oplog) {
+          OplogPlans op;
+          op.n = std::min(t.subs, 8);
+          for (int x = 0; x < op.n; ++x) {
+            op.sizes[x] = tr->plans[static_cast<size_t>(x)].sizes;
+            op.supports[x] = tr->plans[static_cast<size_t>(x)].supports;
+          }
+          oplog_record_launch(sc, op, r->d_oplog, b, s);
+        }
       }
       const size_t pb = tr->w.wpack_bytes;
       const int cap = 2 * tr->cap_B;
@@ -772,6 +785,13 @@ void barrier_body_dev(tgnn_run* r, int p) {
       ws = br;
     }
     root_writes_launch(sc, pl, vw, ws, r->group_size > 1 ? nullptr : &r->mem->d);
+    if (r->oplog) {
+      OplogPlans op;
+      op.n = 1;
+      op.sizes[0] = pl.sizes;
+      op.supports[0] = pl.supports;
+      oplog_record_launch(sc, op, r->d_oplog, 0, ws);
+    }
     const size_t pb = tr->w.wpack_bytes;
     const int cap = 2 * tr->cap_B;
     if (r->group_size > 1) {
@@ -1602,6 +1622,12 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
   if (r->group_size > 1) {
     TGB_CUDA(cudaMalloc(&r->gathered, r->tr->w.wpack_bytes * static_cast<size_t>(r->tc.i)));
   }
+  r->oplog = opt->oplog != 0;
+  if (r->oplog) {
+    const int64_t nb = std::max<int64_t>(r->sched.barriers, 1);
+    r->d_oplog = dalloc<int64_t>(static_cast<size_t>(4 * nb));
+    TGB_CUDA(cudaMemset(r->d_oplog, 0, sizeof(int64_t) * 4 * nb));
+  }
   r->val_begin = opt->val_begin;
   r->val_end = opt->val_end;
   r->eval_batch = opt->eval_batch;
@@ -2147,6 +2173,30 @@ int tgnn_debug_gemm_bench(int64_t M, int64_t N, int64_t K, int32_t ntile, int32_
   API_BEGIN
   tc_debug_bench(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), ntile, iters, us,
                  reinterpret_cast<unsigned long long*>(trace), grid);
+  API_END
+}
+
+
+int tgnn_run_oplog(tgnn_run* r, int64_t* count, int64_t* rows) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(r->oplog, kConfig, "run: op-log recording was not enabled (tgnn_run_options.oplog)");
+  std::vector<int64_t> log(static_cast<size_t>(4 * std::max<int64_t>(r->sched.barriers, 1)));
+  TGB_CUDA(cudaStreamSynchronize(r->ctx->stream));
+  TGB_CUDA(cudaMemcpy(log.data(), r->d_oplog, sizeof(int64_t) * log.size(), cudaMemcpyDeviceToHost));
+  const int local = r->rank % (r->tc.i * r->tc.j);
+  int64_t n = 0;
+  for (int64_t b = 0; b < r->next_barrier; ++b) {
+    const host::Task t = r->sched.task(r->rank, b);
+    if (!t.active || t.sub != 0) continue;
+    if (rows) {
+      const int64_t* l = log.data() + 4 * b;
+      const int64_t rr[2][6] = {{t.sweep, t.pair, 0, local, l[0], l[1]}, {t.sweep, t.pair, 1, local, l[2], l[3]}};
+      std::memcpy(rows + 6 * n, rr, sizeof(rr));
+    }
+    n += 2;
+  }
+  *count = n;
   API_END
 }
 

@@ -979,7 +979,10 @@ __global__ void rw_mark_kernel(DPlan pl, DGraph g, int32_t* __restrict__ win, in
   pdl_wait();
   pdl_trigger();
   const PlanArgs a = *pl.args;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    count[0] = 0;
+    count[1] = 0x7fffffff;  // smallest written node (the op-log's W "first")
+  }
   if (!a.valid) return;
   const int64_t B = a.end - a.begin;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * B; x += gridDim.x * blockDim.x) {
@@ -1008,6 +1011,7 @@ __global__ void rw_emit_kernel(Dims D, DPlan pl, DGraph g, DView vw, const float
     if (lane == 0) {
       if (win[self] == static_cast<int32_t>(e + 1)) {
         slot = atomicAdd(w.w_count, 1);
+        atomicMin(w.w_count + 1, self);
         win[self] = 0;
       }
     }
@@ -2024,6 +2028,38 @@ void eval_rank_launch(const StepCtx& c, const DPlan& pl, int32_t* cnt_out, int64
   launch_pdl(eval_rank_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s, D, pl, w.AB, P + L.off[tB1], P + L.off[tW2],
                                                                P + L.off[tB2], cnt_out, base);
   TGB_CUDA(cudaGetLastError());
+}
+
+namespace {
+// Daemon op-log record of one stint read / write (memory_daemon.hpp:48-93): R
+// first = first node of the first non-empty sub's (ascending) read list, len =
+// total rows over the subs; W first = smallest written node, len = rows.
+__global__ void oplog_record_kernel(OplogPlans op, const int32_t* __restrict__ wcount, int64_t* __restrict__ log,
+                                    const int* __restrict__ ctr, int64_t b) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t idx = ctr ? *ctr : b;
+  int64_t first = 0, total = 0;
+  bool have = false;
+  for (int x = 0; x < op.n; ++x) {
+    const int U = op.sizes[x][kSzU];
+    if (U > 0 && !have) {
+      first = op.supports[x][0];
+      have = true;
+    }
+    total += U;
+  }
+  const int w = wcount[0];
+  log[idx * 4 + 0] = first;
+  log[idx * 4 + 1] = total;
+  log[idx * 4 + 2] = w > 0 ? wcount[1] : 0;
+  log[idx * 4 + 3] = w;
+}
+}  // namespace
+
+void oplog_record_launch(const StepCtx& c, const OplogPlans& op, int64_t* log, int64_t b, cudaStream_t s) {
+  launch_pdl(oplog_record_kernel, dim3(1), dim3(1), 0, s, op, static_cast<const int32_t*>(c.w->w_count), log,
+             c.d_ctr, b);
 }
 
 void root_writes_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cudaStream_t s, DMem* direct) {

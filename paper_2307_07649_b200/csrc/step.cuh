@@ -172,6 +172,14 @@ struct WriteSet {
   const float* mail;
   int cap;
 };
+// Op-log record (sub plans of the stint + this rank's write rows) into
+// log[(*ctr or b) * 4 .. +4): {R first, R len, W first, W len}.
+struct OplogPlans {
+  const int32_t* sizes[8];
+  const int32_t* supports[8];
+  int n = 0;
+};
+void oplog_record_launch(const StepCtx& c, const OplogPlans& op, int64_t* log, int64_t b, cudaStream_t s);
 void apply_writes_launch(const std::vector<WriteSet>& sets, DMem& st, int32_t* win,
                          cudaStream_t s);
 

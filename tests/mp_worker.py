@@ -35,7 +35,7 @@ def main():
                        num_nodes=20, max_t=float(s.t[-1]))
     tc = T.TrainConfig(i=a.i, j=a.j, k=a.k, local_batch=a.local_batch, epochs=a.epochs, seed=3,
                        lr_base=a.lr)
-    run = T.Run(ctx, g, mc, tc, 0, a.train_end, rank=rank, nranks=world)
+    run = T.Run(ctx, g, mc, tc, 0, a.train_end, rank=rank, nranks=world, oplog=True)
     uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
     if rank == 0:
         uid.copy_(torch.frombuffer(bytearray(T.comm_unique_id()), dtype=torch.uint8))
@@ -47,8 +47,12 @@ def main():
     allp = [torch.zeros(len(params), dtype=torch.float64, device="cuda") for _ in range(world)]
     dist.all_gather(allp, torch.tensor(params, device="cuda"))
     same = all(torch.equal(allp[0], x) for x in allp)
+    logs = [None] * world
+    dist.all_gather_object(logs, (rank // (a.i * a.j), run.oplog().tolist()))
     if rank == 0:
-        np.savez(a.out, losses=losses, params=params, replicas_identical=same, barriers=run.barriers)
+        oplog_rows = np.array([[grp] + row for grp, rows in logs for row in rows], np.int64).reshape(-1, 7)
+        np.savez(a.out, losses=losses, params=params, replicas_identical=same, barriers=run.barriers,
+                 oplog=oplog_rows)
     run.close()
     dist.destroy_process_group()
 

@@ -32,3 +32,23 @@ def test_graph_barriers_bitwise_equal_direct(ctx, cfg):
         run.close()
     assert np.array_equal(res[True][0], res[False][0])
     assert np.array_equal(res[True][1], res[False][1])
+
+
+def test_oplog_matches_reference(ctx, tmp_path):
+    """(1,1,1) graph-mode run: the daemon op-log (oplog.hpp) equals the reference
+    run_training's, byte for byte, and passes validate_oplog."""
+    from oracle import ref
+    from oracle import tgnn_oracle as O
+    rg = ref.RefGraph.synthetic(60, 800, d_e=4, seed=3)
+    src, dst, t, ef = rg.export()
+    g = T.TemporalGraph(ctx, rg.num_nodes, rg.boundary, src, dst, t, ef)
+    kw = dict(d_mem=6, d_time=4, d_static=3, d_attn=5, d_hidden=4, n_neighbors=5)
+    mc = T.ModelConfig(d_e=4, num_nodes=60, max_t=float(t[-1]), **kw)
+    run = T.Run(ctx, g, mc, T.TrainConfig(local_batch=50, seed=3, epochs=2), 0, 600, oplog=True)
+    run.step(run.barriers)
+    T.write_oplog(tmp_path / "ours.oplog", run.oplog())
+    run.close()
+    rg.run_oplog(O.ModelConfig(d_e=4, num_nodes=60, max_t=float(t[-1]), **kw),
+                 ref.train_cfg(local_batch=50, seed=3, epochs=2), 0, 600, str(tmp_path / "ref"))
+    assert (tmp_path / "ours.oplog").read_text() == (tmp_path / "ref.0.oplog").read_text()
+    assert ref.validate_oplog(str(tmp_path / "ours.oplog"), 1, 1)[0]

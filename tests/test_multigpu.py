@@ -53,3 +53,13 @@ def test_parallel_run_matches_reference(i, j, k, epochs, tmp_path):
     lr = 1e-3 * T_
     assert np.abs(res["params"] - rr["params"]).max() <= 2.5 * lr * rr["barriers"]
     assert np.median(np.abs(res["params"] - rr["params"])) <= 1e-5
+    # the daemon op-log of every memory copy, byte for byte (memory_daemon.hpp:73,90)
+    import paper_2307_07649_b200 as T
+    rg.run_oplog(mc, tc, 0, 90, str(tmp_path / "ref"))
+    rows = res["oplog"]
+    for grp in range(k):
+        ours = tmp_path / f"ours.{grp}.oplog"
+        T.write_oplog(ours, rows[rows[:, 0] == grp][:, 1:])
+        want = (tmp_path / f"ref.{grp}.oplog").read_text()
+        assert ours.read_text() == want, grp
+        assert ref.validate_oplog(str(ours), i, j)[0]
