@@ -277,7 +277,7 @@ def main():
     train_end = int(round(cfg["events"] * TRAIN_FRAC))
     tc = T.TrainConfig(i=1, j=1, k=world, local_batch=LOCAL_BATCH, lr_base=1e-3, seed=1, epochs=world)
     run = T.Run(ctx, g, mc, tc, 0, train_end, rank=rank, nranks=world)
-    need = args.warmup + args.steps + args.profile_steps + args.e2e_steps + 1
+    need = args.warmup + args.steps + 2 * args.profile_steps + args.e2e_steps + 1
     if run.barriers < need:
         raise SystemExit(f"schedule has {run.barriers} barriers, need {need}")
     if world > 1:
@@ -320,8 +320,10 @@ def main():
     # ---- phase profile (dominant kernel for the roofline)
     prof = []
     for _ in range(args.profile_steps):
-        ph, sz = run.profile_barrier()
+        ph, sz = run.profile_barrier(direct=True)
         prof.append((ph, sz))
+    gprof = [run.profile_barrier(direct=False)[0] for _ in range(args.profile_steps)] if world == 1 else []
+    ph_graph = {k: float(np.mean([p[k] for p in gprof])) for k in gprof[0]} if gprof else None
     ph_mean = {k: float(np.mean([p[0][k] for p in prof])) for k in prof[0][0]}
     sz_mean = {k: float(np.mean([p[1][k] for p in prof])) for k in prof[0][1]}
     proj_ms = ph_mean["attn_proj"]
@@ -429,6 +431,7 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "phases_ms": ph_mean,
+            "phases_ms_graph_critical_path": ph_graph,
             "plan_sizes": sz_mean,
             "model_tflops": step_model_flops(sz_mean, cfg) * world / (ms_max / args.steps / 1e3) / 1e12,
             "loss_first_last": [float(losses[0]), float(losses[-1])],

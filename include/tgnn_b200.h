@@ -214,9 +214,11 @@ int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out);
 /* Runs the next barrier with CUDA-event phase markers and returns per-phase
  * device milliseconds [TGNN_PHASES] (plan, gru_fwd, attn_assemble, attn_proj,
  * attn_softmax, decoder, decoder_bwd, attn_bwd, attn_bwd_gemm, gru_bwd,
- * writes, allreduce, adam) and the plan sizes [8] (B, R, P, U, -, items, 2B, -). */
+ * writes, allreduce, adam) and the plan sizes [8] (B, R, P, U, -, items, 2B, -).
+ * direct != 0: the single-stream path (each phase alone); 0: the production
+ * CUDA-graph schedule (markers on the critical-path stream). */
 #define TGNN_PHASES 13
-int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes);
+int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes, int32_t direct);
 
 /* ------------------------------------------------------------------ GEMM engine
  * Process-wide choice for the step's dense contractions:

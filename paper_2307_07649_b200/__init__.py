@@ -642,11 +642,14 @@ class Run:
     PHASES = ["plan", "gru_fwd", "attn_assemble", "attn_proj", "attn_softmax", "decoder",
               "decoder_bwd", "attn_bwd", "attn_bwd_gemm", "gru_bwd", "writes", "allreduce", "adam"]
 
-    def profile_barrier(self):
-        """Runs the next barrier with phase markers: ({phase: ms}, plan sizes)."""
+    def profile_barrier(self, direct: bool = True):
+        """Runs the next barrier with phase markers: ({phase: ms}, plan sizes).
+        direct: the single-stream path (every phase timed alone); otherwise the
+        production graph schedule (markers on the critical-path stream)."""
         ms = np.zeros(len(self.PHASES))
         sz = np.zeros(8, np.int32)
-        check(lib().tgnn_run_profile_barrier(self.h, _p(ms, f64p), sz.ctypes.data_as(C.POINTER(C.c_int32))))
+        check(lib().tgnn_run_profile_barrier(self.h, _p(ms, f64p), sz.ctypes.data_as(C.POINTER(C.c_int32)),
+                                             1 if direct else 0))
         self.next += 1
         return dict(zip(self.PHASES, ms.tolist())), dict(B=int(sz[0]), R=int(sz[1]), P=int(sz[2]),
                                                          U=int(sz[3]))

@@ -149,7 +149,7 @@ SIGNATURES = {
     "tgnn_graph_edge_feats": [vp, i64, i64, f32p],
     "tgnn_checkpoint_load": [C.POINTER(ModelConfigC), C.c_char_p, f64p],
     "tgnn_run_launches_per_barrier": [vp, i64p],
-    "tgnn_run_profile_barrier": [vp, f64p, C.POINTER(C.c_int32)],
+    "tgnn_run_profile_barrier": [vp, f64p, C.POINTER(C.c_int32), i32],
     "tgnn_graph_ingest": [vp, i64, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), f64p, f32p],
     "tgnn_pinned_alloc": [i64, C.POINTER(vp)],
     "tgnn_debug_gemm_bench": [i64, i64, i64, i32, i32, f64p, C.POINTER(C.c_uint64), C.POINTER(i32)],

@@ -747,6 +747,8 @@ void barrier_body_dev(tgnn_run* r, int p) {
   StepCtx sc = tr->sc();
   sc.d_ctr = r->d_ctr;
   sc.packed = true;  // by the previous barrier's Adam (or the prologue)
+  sc.marks = r->marks.on ? &r->marks : nullptr;  // profiling graph only
+  sc.mark(phPlan, s);
   DPlan& pl = tr->plans[static_cast<size_t>(p)];
   DView& vw = tr->views[static_cast<size_t>(p)];
   DPlan& nx = tr->plans[static_cast<size_t>(1 - p)];
@@ -769,7 +771,9 @@ void barrier_body_dev(tgnn_run* r, int p) {
   // edge branch: the plan-only half of the attention projection runs beside the GRU
   if (gemm_impl() == kGemmTma) {
     TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_fork, 0));
-    attn_edge_launch(sc, pl, ctx->edge);
+    StepCtx se = sc;
+    se.marks = nullptr;  // phase markers live on the main stream
+    attn_edge_launch(se, pl, ctx->edge);
     TGB_CUDA(cudaEventRecord(r->ev_edge, ctx->edge));
     sc.ev_edge = r->ev_edge;
   }
@@ -815,9 +819,11 @@ void barrier_body_dev(tgnn_run* r, int p) {
     if (r->nranks > 1) sc.ev_tail_grads = r->ev_tail;
     substep_rest_launch(sc, pl, vw, r->d_losses, s);
     if (r->nranks > 1) allreduce_bucketed(r, s);
+    sc.mark(phAdam, s);
     adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr);
     TGB_CUDA(cudaStreamWaitEvent(s, r->ev_next, 0));
     incr_launch(r->d_ctr, s);
+    sc.mark(phCount, s);
   } catch (...) {
     pl.ev_sorted = sorted;
     throw;
@@ -955,12 +961,16 @@ int tgnn_ctx_create(int device, tgnn_ctx** out) {
   TGB_CUDA(cudaSetDevice(device));
   auto* c = new tgnn_ctx();
   c->device = device;
-  TGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  TGB_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-  TGB_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
-  TGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
-  TGB_CUDA(cudaStreamCreateWithFlags(&c->br, cudaStreamNonBlocking));
-  TGB_CUDA(cudaStreamCreateWithFlags(&c->edge, cudaStreamNonBlocking));
+  // the step's critical path runs at the highest stream priority (carried into
+  // every launch and captured graph node by launch_pdl); branches at the lowest
+  int lo_prio = 0, hi_prio = 0;
+  TGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, hi_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->br, cudaStreamNonBlocking, lo_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->edge, cudaStreamNonBlocking, lo_prio));
   c->d_flag = dalloc<int>(1);
   TGB_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
   *out = c;
@@ -1865,7 +1875,7 @@ int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out) {
   API_END
 }
 
-int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes) {
+int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes, int32_t direct) {
   API_BEGIN
   r->ctx->use();
   TGB_REQUIRE(r->next_barrier < r->sched.barriers, kConfig, "run: no barrier left to profile");
@@ -1876,8 +1886,45 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes) {
   }
   for (auto& h : r->marks.hit) h = false;
   r->marks.on = true;
+  const int64_t b = r->next_barrier;
+  unsigned long long ts_host[phCount + 1] = {};
+  bool have_ts = false;
   try {
-    run_barrier(r, r->next_barrier);
+    if (r->use_graphs && !direct) {
+      // the production graph body, captured once more with phase stamps on
+      // the main stream, replayed for this barrier
+      if (!r->exec[0]) build_graph(r);
+      if (r->prepared != b) prepare_barrier(r, b);
+      cudaStream_t s = r->ctx->stream;
+      cudaGraph_t gph = nullptr;
+      cudaGraphExec_t ex = nullptr;
+      unsigned long long* d_ts = dalloc<unsigned long long>(phCount + 1);
+      r->marks.d_ts = d_ts;
+      TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      try {
+        barrier_body_dev(r, static_cast<int>(b & 1));
+      } catch (...) {
+        cudaStreamEndCapture(s, &gph);
+        if (gph) cudaGraphDestroy(gph);
+        r->marks.d_ts = nullptr;
+        cudaFree(d_ts);
+        throw;
+      }
+      r->marks.d_ts = nullptr;
+      TGB_CUDA(cudaStreamEndCapture(s, &gph));
+      TGB_CUDA(cudaGraphInstantiate(&ex, gph, 0));
+      TGB_CUDA(cudaGraphLaunch(ex, s));
+      TGB_CUDA(cudaStreamSynchronize(s));
+      cudaGraphExecDestroy(ex);
+      cudaGraphDestroy(gph);
+      TGB_CUDA(cudaMemcpy(ts_host, d_ts, sizeof(ts_host), cudaMemcpyDeviceToHost));
+      cudaFree(d_ts);
+      have_ts = true;
+      r->prepared = b + 1;
+      r->tr->adam_t = b + 1;
+    } else {
+      run_barrier(r, b);
+    }
   } catch (...) {
     r->marks.on = false;
     throw;
@@ -1891,7 +1938,8 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes) {
   for (int x = 0; x <= phCount; ++x) {
     if (!r->marks.hit[x]) continue;
     float ms = 0;
-    TGB_CUDA(cudaEventElapsedTime(&ms, r->marks.ev[phPlan], r->marks.ev[x]));
+    if (have_ts) ms = static_cast<float>(static_cast<double>(ts_host[x] - ts_host[phPlan]) * 1e-6);
+    else TGB_CUDA(cudaEventElapsedTime(&ms, r->marks.ev[phPlan], r->marks.ev[x]));
     at.push_back({ms, x});
   }
   std::stable_sort(at.begin(), at.end());
@@ -1899,7 +1947,8 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes) {
   for (size_t q = 0; q + 1 < at.size(); ++q)
     if (at[q].second < phCount) phase_ms[at[q].second] += at[q + 1].first - at[q].first;
   int32_t sz[kSzCount];
-  TGB_CUDA(cudaMemcpy(sz, r->tr->plans[0].sizes, sizeof(sz), cudaMemcpyDeviceToHost));
+  TGB_CUDA(cudaMemcpy(sz, r->tr->plans[r->use_graphs && !direct ? static_cast<size_t>(b & 1) : 0].sizes, sizeof(sz),
+                      cudaMemcpyDeviceToHost));
   for (int x = 0; x < kSzCount; ++x) sizes[x] = sz[x];
   API_END
 }

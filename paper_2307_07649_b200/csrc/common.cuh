@@ -111,11 +111,17 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  // carry the stream's priority into the launch (and into captured graph
+  // nodes): the critical path outranks the overlapped branches for SMs
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  at[1].id = cudaLaunchAttributePriority;
+  at[1].val.priority = prio;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   TGB_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 #endif

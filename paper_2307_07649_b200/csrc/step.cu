@@ -1783,8 +1783,12 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
     // node / edge split: the per-pair edge part (plan-only) is either enqueued
     // here or already running on another stream; the per-support node part
     // QKVn = NF Wst^T follows the GRU
-    if (c.ev_edge) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_edge, 0));
-    else attn_edge_launch(c, pl, s);  // marks phAttnProj before its GEMM
+    if (c.ev_edge) {
+      TGB_CUDA(cudaStreamWaitEvent(s, c.ev_edge, 0));
+      c.mark(phAttnProj, s);
+    } else {
+      attn_edge_launch(c, pl, s);  // marks phAttnProj before its GEMM
+    }
     TcGroup tg;
     tc_nn(tg, U, pl.sizes + kSzU, 3 * w.bf.d8a, D.d + D.ds, w.bf.NF, 0, w.bf.Wst, 0, 3 * w.bf.d8a, w.QKVn,
           3 * w.bf.d8a);
@@ -2103,6 +2107,19 @@ void adam_launch(float* params, const float* grads, float* m, float* v, int64_t 
                  const int* ctr) {
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
   launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr, PackMap{}, 0, 0, 0, 0);
+  TGB_CUDA(cudaGetLastError());
+}
+
+namespace {
+__global__ void stamp_kernel(unsigned long long* dst) {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  *dst = v;
+}
+}  // namespace
+
+void stamp_launch(unsigned long long* dst, cudaStream_t s) {
+  stamp_kernel<<<1, 1, 0, s>>>(dst);
   TGB_CUDA(cudaGetLastError());
 }
 

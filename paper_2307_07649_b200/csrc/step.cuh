@@ -91,13 +91,18 @@ enum Phase {
   phPlan = 0, phGruFwd, phAttnAssemble, phAttnProj, phAttnSoftmax, phDecoder, phDecoderBwd,
   phAttnBwd, phAttnBwdGemm, phGruBwd, phWrites, phAllreduce, phAdam, phCount
 };
+// Graph-captured barriers stamp %globaltimer from a one-thread kernel instead
+// (event records inside a graph are not timing events).
+void stamp_launch(unsigned long long* dst, cudaStream_t s);
 struct PhaseMarks {
   bool on = false;
+  unsigned long long* d_ts = nullptr;  // set: stamp kernels (graph capture); null: events
   cudaEvent_t ev[phCount + 1] = {};
   bool hit[phCount + 1] = {};
   void mark(int slot, cudaStream_t s) {
     if (on) {
-      cudaEventRecord(ev[slot], s);
+      if (d_ts) stamp_launch(d_ts + slot, s);
+      else cudaEventRecord(ev[slot], s);
       hit[slot] = true;
     }
   }
