@@ -720,18 +720,33 @@ __global__ void set_int_kernel(int* p, int v) { *p = v; }
 // average_active_grads (trainer.hpp:473-483) as two NCCL buckets on the comm
 // stream: [off[tWq], end) once ev_tail fires (overlapping the GRU backward),
 // then [0, off[tWq]) after the step; the compute stream waits before Adam.
-void allreduce_bucketed(tgnn_run* r, cudaStream_t s) {
+// Split-phase update: the tail range [off[tWq], end) -- attention, static
+// table, decoder, 88 % of the parameters -- is final once ev_tail fires
+// (after gru_bwd1): it is all-reduced (N > 1) and Adam-updated on a side
+// stream while the GRU backward still runs; the head range [0, off[tWq))
+// follows after the step. (The omega gradient's attention part reads the old
+// Wk / Wv time rows before ev_tail.)
+void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
   tgnn_trainer* tr = r->tr.get();
-  cudaStream_t c = r->ctx->comm;
+  cudaStream_t c = r->nranks > 1 ? r->ctx->comm : r->ctx->br;
   const int64_t split = tr->L.off[tWq];
   TGB_CUDA(cudaStreamWaitEvent(c, r->ev_tail, 0));
-  NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),
-                                   ncclFloat, ncclSum, r->comm, c));
-  TGB_CUDA(cudaEventRecord(r->ev_head, s));
-  TGB_CUDA(cudaStreamWaitEvent(c, r->ev_head, 0));
-  NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(split), ncclFloat, ncclSum, r->comm, c));
-  TGB_CUDA(cudaEventRecord(r->ev_comm, c));
-  TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
+  if (r->nranks > 1)
+    NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),
+                                     ncclFloat, ncclSum, r->comm, c));
+  adam_pack_launch(sc, tr->am, tr->av, c, r->d_desc, r->d_ctr, split, tr->L.total);
+  if (r->nranks > 1) {
+    TGB_CUDA(cudaEventRecord(r->ev_head, s));
+    TGB_CUDA(cudaStreamWaitEvent(c, r->ev_head, 0));
+    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(split), ncclFloat, ncclSum, r->comm, c));
+    adam_pack_launch(sc, tr->am, tr->av, c, r->d_desc, r->d_ctr, 0, split);
+    TGB_CUDA(cudaEventRecord(r->ev_comm, c));
+    TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
+  } else {
+    adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr, 0, split);
+    TGB_CUDA(cudaEventRecord(r->ev_comm, c));
+    TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
+  }
 }
 
 // Graph body (j == 1): the same launch sequence for every barrier; all
@@ -816,11 +831,10 @@ void barrier_body_dev(tgnn_run* r, int p) {
     gather_view_launch(nx, r->mem->d, nv, aux);
     TGB_CUDA(cudaStreamWaitEvent(aux, nx.ev_sorted, 0));
     TGB_CUDA(cudaEventRecord(r->ev_next, aux));
-    if (r->nranks > 1) sc.ev_tail_grads = r->ev_tail;
+    sc.ev_tail_grads = r->ev_tail;
     substep_rest_launch(sc, pl, vw, r->d_losses, s);
-    if (r->nranks > 1) allreduce_bucketed(r, s);
     sc.mark(phAdam, s);
-    adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr);
+    update_split(r, sc, s);
     TGB_CUDA(cudaStreamWaitEvent(s, r->ev_next, 0));
     incr_launch(r->d_ctr, s);
     sc.mark(phCount, s);
@@ -841,6 +855,9 @@ void build_graph(tgnn_run* r) {
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
     cudaEvent_t* more[] = {&r->ev_gru, &r->ev_gzero, &r->ev_dec, &r->ev_brjoin, &r->ev_edge, &r->ev_red};
     for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    cudaEvent_t* upd[] = {&r->ev_tail, &r->ev_head, &r->ev_comm};
+    for (cudaEvent_t* e : upd)
+      if (!*e) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   for (int p = 0; p < 2; ++p) {
     TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));

@@ -914,16 +914,19 @@ __global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* _
                                                           const float* __restrict__ Mom,
                                                           const float* __restrict__ M2,
                                                           float* __restrict__ g_omega, int v_row0,
-                                                          int blk_stride) {
+                                                          int blk_stride, int j_lo, int j_hi,
+                                                          const float* __restrict__ base) {
   pdl_wait();
   pdl_trigger();
+  // j in [j_lo, j_hi) of the joint (Wk, Wv time rows | Wall rows) contraction;
+  // g_omega[i] = base[i] + the fixed-order tree sum (two calls: the attention
+  // part once Mom is final, the GRU part at the end)
   __shared__ float red[256];
   const int i = blockIdx.x;
-
   const int t0 = D.d + D.ds + D.de;
-  const int n1 = 2 * D.da, n2 = 3 * D.d;
+  const int n1 = 2 * D.da;
   float s = 0.0f;
-  for (int j = threadIdx.x; j < n1 + n2; j += blockDim.x) {
+  for (int j = j_lo + threadIdx.x; j < j_hi; j += blockDim.x) {
     if (j < D.da) {
       s = fmaf(params[offWk + static_cast<int64_t>(j) * D.kv_in + t0 + i], Mom[j * D.dt + i], s);
     } else if (j < n1) {
@@ -941,7 +944,7 @@ __global__ void __launch_bounds__(256) omega_final_kernel(Dims D, const float* _
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) g_omega[i] = red[0];
+  if (threadIdx.x == 0) g_omega[i] = (base ? base[i] : 0.0f) + red[0];
 }
 
 // ---------------------------------------------------------------- weight pack
@@ -1194,7 +1197,7 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
                             float* __restrict__ v, int64_t n, float lr, float c1, float c2,
                             float scale, const BarrierDesc* __restrict__ desc, const int* __restrict__ ctr,
                             const __grid_constant__ PackMap pm, int64_t pack_lo, int64_t pack_hi,
-                            int64_t skip_lo, int64_t skip_hi) {
+                            int64_t skip_lo, int64_t skip_hi, int64_t r_lo) {
   pdl_wait();
   pdl_trigger();
   if (desc) {
@@ -1211,13 +1214,19 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     vv = b2 * vv + (1.0f - b2) * gr * gr;
     pp -= lr * (mm / c1) / (sqrtf(vv / c2) + eps);
   };
-  // 128-bit path over the 16-byte-aligned bulk (cudaMalloc bases), scalar tail
-  const int64_t n4 = n / 4;
+  // elements [r_lo, n): 128-bit path over the 16-byte-aligned bulk (cudaMalloc
+  // bases), scalar head and tail
+  const int64_t a4 = (r_lo + 3) / 4, n4 = n / 4;
   float4* p4 = reinterpret_cast<float4*>(p);
   const float4* g4 = reinterpret_cast<const float4*>(g);
   float4* m4 = reinterpret_cast<float4*>(m);
   float4* v4 = reinterpret_cast<float4*>(v);
-  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n4; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t x = r_lo + blockIdx.x * blockDim.x + threadIdx.x; x < std::min(4 * a4, n);
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    upd(p[x], g[x], m[x], v[x]);
+    if (pm.count) pack_elem(pm, x, p[x]);
+  }
+  for (int64_t x = a4 + blockIdx.x * blockDim.x + threadIdx.x; x < n4; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float4 pp = p4[x], mm = m4[x], vv = v4[x];
     const float4 gg = g4[x];
     upd(pp.x, gg.x, mm.x, vv.x);
@@ -1231,7 +1240,8 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
       pack_elem4(pm, 4 * x, pp);
     }
   }
-  for (int64_t x = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; x < n; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t x = std::max(4 * n4, 4 * a4) + blockIdx.x * blockDim.x + threadIdx.x; x < n;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     upd(p[x], g[x], m[x], v[x]);
     if (pm.count) pack_elem(pm, x, p[x]);
   }
@@ -1450,6 +1460,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   w.Mom = dalloc<float>(2 * ((da + 7) / 8 * 8) * dt);  // padded dK | dV rows (TMA layout)
   w.omega_chunks = static_cast<int>(ceil_div(U, kOmegaRows));
   w.omega_part = dalloc<float>(static_cast<size_t>(w.omega_chunks) * dt);
+  w.omega_att = dalloc<float>(std::max<int64_t>(dt, 1));
   const int64_t max_ones = std::max<int64_t>(std::max<int64_t>(P, U), B2);
   w.ones = dalloc<float>(1);
   const float one = 1.0f;
@@ -1549,7 +1560,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
 }
 
 void step_free(StepWork& w) {
-  void* ptrs[] = {w.QKVn, w.cq, w.Xg, w.GU, w.Gates, w.RS, w.s_hat, w.Qin, w.KVin, w.Gt, w.Q, w.KV, w.attn_a,
+  void* ptrs[] = {w.omega_att, w.QKVn, w.cq, w.Xg, w.GU, w.Gates, w.RS, w.s_hat, w.Qin, w.KVin, w.Gt, w.Q, w.KV, w.attn_a,
                   w.H, w.AB, w.HID, w.Dhid, w.Hin, w.dlogit, w.logits, w.dIn, w.dQ, w.dKV,
                   w.dNodeAcc, w.dNode, w.Dg, w.T1, w.DMT, w.Mom, w.omega_part, w.ones,
                   w.loss_terms, w.splitk_ws, w.wpack, w.win};
@@ -1678,12 +1689,13 @@ void pack_weights(const StepCtx& c, cudaStream_t s) {
 }
 
 void adam_pack_launch(const StepCtx& c, float* m, float* v, cudaStream_t s, const BarrierDesc* desc,
-                      const int* ctr) {
+                      const int* ctr, int64_t r_lo, int64_t r_hi) {
   int64_t lo = 0, hi = 0, slo = 0, shi = 0;
   const PackMap pm = gemm_impl() == kGemmTma ? make_pack_map(c, lo, hi, slo, shi) : PackMap{};
-  const int64_t n = c.L.total;
-  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
-  launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, c.params, c.grads, m, v, n, 0.f, 1.f, 1.f, 1.f, desc, ctr, pm, lo, hi, slo, shi);
+  const int64_t n = r_hi < 0 ? c.L.total : r_hi;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n - r_lo, 256), 8 * kSMs)));
+  launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, c.params, c.grads, m, v, n, 0.f, 1.f, 1.f, 1.f, desc, ctr, pm, lo, hi,
+             slo, shi, r_lo);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -1958,6 +1970,16 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     gemm_group_launch(gg, s);
   }
 
+  // omega gradient, attention part (Wk / Wv time rows x Mom): read before the
+  // split-phase Adam may update those rows (on the branch with Mom's reduction)
+  if (dt > 0 && c.br) {  // Mom is final once the group (and its branch reduction) is done
+    TGB_CUDA(cudaEventRecord(c.ev_red, s));
+    TGB_CUDA(cudaStreamWaitEvent(c.br, c.ev_red, 0));
+  }
+  if (dt > 0)
+    launch_pdl(omega_final_kernel, dim3(dt), dim3(256), 0, c.br ? c.br : s, D, P, L.off[tWk], L.off[tWv], L.off[tWz],
+               w.Mom, w.DMT, w.omega_att, tma ? B.d8a : da, tma ? B.d8d : d, 0, 2 * da,
+               static_cast<const float*>(nullptr));
   // ---- GRU backward (K9)
   c.mark(phGruBwd, s);
   launch_pdl(gru_bwd1_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
@@ -2004,7 +2026,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   }
   if (dt > 0)
     launch_pdl(omega_final_kernel, dim3(dt), dim3(256), 0, s, D, P, L.off[tWk], L.off[tWv], L.off[tWz], w.Mom, w.DMT,
-                                          G + L.off[tOmega], tma ? B.d8a : da, tma ? B.d8d : d);
+               G + L.off[tOmega], tma ? B.d8a : da, tma ? B.d8d : d, 2 * da, 2 * da + 3 * d,
+               static_cast<const float*>(w.omega_att));
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -2106,7 +2129,8 @@ void adam_launch(float* params, const float* grads, float* m, float* v, int64_t 
                  float c1, float c2, float grad_scale, cudaStream_t s, const BarrierDesc* desc,
                  const int* ctr) {
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
-  launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr, PackMap{}, 0, 0, 0, 0);
+  launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr, PackMap{}, 0, 0, 0, 0,
+             static_cast<int64_t>(0));
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -67,7 +67,8 @@ struct StepWork {
   float *Hin = nullptr, *dlogit = nullptr, *logits = nullptr, *dIn = nullptr, *dQ = nullptr;
   float *dKV = nullptr, *dNodeAcc = nullptr, *dNode = nullptr, *Dg = nullptr, *T1 = nullptr;
   float *DMT = nullptr, *Mom = nullptr, *omega_part = nullptr, *ones = nullptr;
-  float *QKVn = nullptr, *cq = nullptr;  // node parts [U, 3 d8a]; query constant W_q,t 1 + b_q [d_a]
+  float *QKVn = nullptr, *cq = nullptr;
+  float* omega_att = nullptr;  // attention part of the omega gradient [d_t]  // node parts [U, 3 d8a]; query constant W_q,t 1 + b_q [d_a]
   double* loss_terms = nullptr;
   float* splitk_ws = nullptr;
   size_t splitk_ws_floats = 0;
@@ -202,8 +203,10 @@ void adam_launch(float* params, const float* grads, float* m, float* v, int64_t 
 // Graph mode: Adam with the step scalars of desc[*ctr] that also refreshes the
 // packed bf16 hi/lo weight operands of the TMA engine (pack_weights), so the
 // next step's GEMMs need no separate pack.
+// r_lo / r_hi: the flat parameter range [r_lo, r_hi) this launch updates
+// (r_hi < 0: to the end), for the split-phase update of the graph barrier.
 void adam_pack_launch(const StepCtx& c, float* m, float* v, cudaStream_t s, const BarrierDesc* desc,
-                      const int* ctr);
+                      const int* ctr, int64_t r_lo = 0, int64_t r_hi = -1);
 // Packs the TMA engine's weight operands from the fp32 parameters.
 void pack_weights(const StepCtx& c, cudaStream_t s);
 // Graph mode helpers: reset the memory copy if desc[*ctr].reset; ++*ctr.
