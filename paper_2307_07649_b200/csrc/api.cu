@@ -360,6 +360,14 @@ struct tgnn_trainer {
   }
 };
 
+// j > 1 graph mode: the stint-start barrier's per-sub plan args of this rank
+// and, per team in pair order, whether the group's copy resets before its read.
+constexpr int kMaxStintJ = 8;
+struct StintDesc {
+  PlanArgs args[kMaxStintJ];
+  int32_t reset[kMaxStintJ];
+};
+
 // evaluate_mrr / replay_batch (trainer.hpp:336-468) on device: a private
 // memory copy rebuilt by replaying the prefix, forward-only workspaces sized
 // for 2 + n_negatives roots per event, and per-event rank counts that the host
@@ -495,6 +503,11 @@ struct tgnn_run {
   int* d_ctr = nullptr;
   cudaGraph_t graph[2] = {nullptr, nullptr};
   cudaGraphExec_t exec[2] = {nullptr, nullptr};  // barrier b runs exec[b % 2]
+  // j > 1: one graph per sub-iteration position s = b % j (a whole stint is
+  // j consecutive launches); per-stint plan args and team resets in d_stint
+  std::vector<cudaGraph_t> sgraph;
+  std::vector<cudaGraphExec_t> sexec;
+  StintDesc* d_stint = nullptr;
   int64_t prepared = -1;  // barrier whose plan + read view are ready in plans/views[b % 2]
   cudaEvent_t ev_fork = nullptr, ev_written = nullptr, ev_next = nullptr;
   cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
@@ -528,6 +541,11 @@ struct tgnn_run {
       if (exec[p]) cudaGraphExecDestroy(exec[p]);
       if (graph[p]) cudaGraphDestroy(graph[p]);
     }
+    for (auto e : sexec)
+      if (e) cudaGraphExecDestroy(e);
+    for (auto g : sgraph)
+      if (g) cudaGraphDestroy(g);
+    if (d_stint) cudaFree(d_stint);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_written) cudaEventDestroy(ev_written);
     if (ev_next) cudaEventDestroy(ev_next);
@@ -843,6 +861,133 @@ void barrier_body_dev(tgnn_run* r, int p) {
     throw;
   }
   pl.ev_sorted = sorted;
+}
+
+__global__ void select_stint_args_kernel(const StintDesc* __restrict__ sd, const int* __restrict__ ctr, int sub,
+                                         PlanArgs* dst) {
+  *dst = sd[*ctr].args[sub];
+}
+
+__global__ void reset_stint_kernel(DMem st, const StintDesc* __restrict__ sd, const int* __restrict__ ctr, int team) {
+  if (!sd[*ctr].reset[team]) return;
+  const int64_t n = st.N * st.d;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 3 * n; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (x < n) st.memory[x] = 0.0f;
+    else st.mail_mem[x - n] = 0.0f;
+  }
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < st.N; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    st.last_update[x] = 0.0;
+    st.mail_t[x] = 0.0;
+    st.mail_dt[x] = 0.0;
+    st.mail_ev[x] = -1;
+  }
+}
+
+// Graph body for j > 1 at stint position sidx: the direct path's launch
+// sequence with every per-barrier value taken from the device tables. At the
+// stint start the group's teams run the daemon's R/W chain in pair order (an
+// idle team contributes an empty plan and an empty write pack, so every rank
+// issues the same collectives); later positions run their pre-planned sub.
+void barrier_body_stint(tgnn_run* r, int sidx) {
+  tgnn_ctx* ctx = r->ctx;
+  tgnn_trainer* tr = r->tr.get();
+  cudaStream_t s = ctx->stream;
+  StepCtx sc = tr->sc();
+  sc.d_ctr = r->d_ctr;
+  const int i = r->tc.i, j = r->tc.j;
+  std::vector<cudaEvent_t> saved(static_cast<size_t>(j));
+  for (int x = 0; x < j; ++x) saved[static_cast<size_t>(x)] = tr->plans[static_cast<size_t>(x)].ev_sorted;
+  auto restore = [&]() {
+    for (int x = 0; x < j; ++x) tr->plans[static_cast<size_t>(x)].ev_sorted = saved[static_cast<size_t>(x)];
+  };
+  try {
+    if (sidx == 0) {
+      for (int tt = 0; tt < j; ++tt) {
+        reset_stint_kernel<<<4 * kSMs, 256, 0, s>>>(r->mem->d, r->d_stint, r->d_ctr, tt);
+        TGB_CUDA(cudaGetLastError());
+        if (tt == r->team) {
+          for (int sub = 0; sub < j; ++sub) {
+            DPlan& pl = tr->plans[static_cast<size_t>(sub)];
+            select_stint_args_kernel<<<1, 1, 0, s>>>(r->d_stint, r->d_ctr, sub, pl.args);
+            TGB_CUDA(cudaGetLastError());
+            plan_launch(r->g->d, pl, s, ctx->side);
+            gather_view_launch(pl, r->mem->d, tr->views[static_cast<size_t>(sub)], s);
+          }
+          substep_gru_launch(sc, tr->plans[0], tr->views[0], s);
+          root_writes_launch(sc, tr->plans[0], tr->views[0], s, nullptr);
+          if (r->oplog) {
+            OplogPlans op;
+            op.n = j;
+            for (int x = 0; x < j; ++x) {
+              op.sizes[x] = tr->plans[static_cast<size_t>(x)].sizes;
+              op.supports[x] = tr->plans[static_cast<size_t>(x)].supports;
+            }
+            oplog_record_launch(sc, op, r->d_oplog, 0, s);
+          }
+        }
+        const size_t pb = tr->w.wpack_bytes;
+        NCCL_CHECK(nccl::api().GroupStart());
+        for (int mm = 0; mm < i; ++mm)
+          NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, pb,
+                                           ncclChar, tt * i + mm, r->gcomm, s));
+        NCCL_CHECK(nccl::api().GroupEnd());
+        std::vector<WriteSet> sets;
+        for (int mm = 0; mm < i; ++mm)
+          sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, 2 * tr->cap_B,
+                                   tr->m.d_mem));
+        apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+      }
+      substep_rest_launch(sc, tr->plans[0], tr->views[0], r->d_losses, s);
+      // the later subs' routing sorts ran on the side stream: join them here
+      for (int sub = 1; sub < j; ++sub) TGB_CUDA(cudaStreamWaitEvent(s, tr->plans[static_cast<size_t>(sub)].ev_sorted, 0));
+    } else {
+      DPlan& pl = tr->plans[static_cast<size_t>(sidx)];
+      pl.ev_sorted = nullptr;  // sorted inside the stint-start graph
+      substep_launch(sc, pl, tr->views[static_cast<size_t>(sidx)], r->d_losses, s);
+    }
+    if (r->nranks > 1)
+      NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
+                                       r->comm, s));
+    adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr);
+    incr_launch(r->d_ctr, s);
+  } catch (...) {
+    restore();
+    throw;
+  }
+  restore();
+}
+
+void build_stint_graphs(tgnn_run* r) {
+  cudaStream_t s = r->ctx->stream;
+  gemm_kernels_prepare();
+  TGB_CUDA(cudaStreamSynchronize(s));
+  const int j = r->tc.j;
+  r->sgraph.assign(static_cast<size_t>(j), nullptr);
+  r->sexec.assign(static_cast<size_t>(j), nullptr);
+  for (int x = 0; x < j; ++x) {
+    TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      barrier_body_stint(r, x);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    TGB_CUDA(cudaStreamEndCapture(s, &r->sgraph[static_cast<size_t>(x)]));
+    TGB_CUDA(cudaGraphInstantiate(&r->sexec[static_cast<size_t>(x)], r->sgraph[static_cast<size_t>(x)], 0));
+  }
+  size_t n = 0;
+  TGB_CUDA(cudaGraphGetNodes(r->sgraph[0], nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  TGB_CUDA(cudaGraphGetNodes(r->sgraph[0], nodes.data(), &n));
+  int64_t kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    TGB_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  r->launches = kernels;
 }
 
 void build_graph(tgnn_run* r) {
@@ -1663,7 +1808,31 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
               "run: validation range out of bounds");
   TGB_REQUIRE(r->eval_negatives >= 0 && r->eval_batch >= 0, kConfig, "run: invalid evaluation options");
   TGB_CUDA(cudaEventCreate(&r->ev_t0));
-  r->use_graphs = opt->use_graphs != 0 && r->tc.j == 1;
+  r->use_graphs = opt->use_graphs != 0 && r->tc.j <= kMaxStintJ;
+  if (r->use_graphs && r->tc.j > 1) {
+    std::vector<StintDesc> sd(static_cast<size_t>(r->sched.barriers + 1));
+    for (int64_t b = 0; b < r->sched.barriers; b += r->tc.j) {
+      StintDesc& e = sd[static_cast<size_t>(b)];
+      const host::Task t = r->sched.task(r->rank, b);
+      for (int sub = 0; sub < r->tc.j; ++sub) {
+        PlanArgs& a = e.args[sub];
+        a.begin = t.slice_begin;
+        a.end = t.slice_end;
+        a.batch_begin = t.batch_begin;
+        a.batch_index = t.batch;
+        a.seed = r->tc.seed;
+        a.neg_mode = 1;
+        a.valid = t.active && sub < t.subs ? 1 : 0;
+        a.group = a.valid ? t.neg_group[static_cast<size_t>(sub)] : 0;
+      }
+      for (int tt = 0; tt < r->tc.j; ++tt) {
+        const host::Task tk = r->sched.task(r->group * r->tc.i * r->tc.j + tt * r->tc.i, b);
+        e.reset[tt] = tk.active && tk.reset_before ? 1 : 0;
+      }
+    }
+    r->d_stint = dalloc<StintDesc>(sd.size());
+    TGB_CUDA(cudaMemcpy(r->d_stint, sd.data(), sizeof(StintDesc) * sd.size(), cudaMemcpyHostToDevice));
+  }
   if (r->use_graphs) {
     // one idle entry past the end: the last barrier prepares an empty plan
     const int64_t nb = r->sched.barriers + 1;
@@ -1751,7 +1920,14 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
       seg_end = evb[r->eval_cursor] + 1;
       eval_here = true;
     }
-    if (r->use_graphs) {
+    if (r->use_graphs && r->tc.j > 1) {
+      if (r->sexec.empty()) build_stint_graphs(r);
+      set_int_kernel<<<1, 1, 0, r->ctx->stream>>>(r->d_ctr, static_cast<int>(b));
+      TGB_CUDA(cudaGetLastError());
+      for (int64_t x = b; x < seg_end; ++x)
+        TGB_CUDA(cudaGraphLaunch(r->sexec[static_cast<size_t>(x % r->tc.j)], r->ctx->stream));
+      r->tr->adam_t = seg_end;
+    } else if (r->use_graphs) {
       if (!r->exec[0]) build_graph(r);
       if (r->prepared != b) prepare_barrier(r, b);
       for (int64_t x = b; x < seg_end; ++x) TGB_CUDA(cudaGraphLaunch(r->exec[x & 1], r->ctx->stream));
@@ -1855,7 +2031,11 @@ int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out) {
   API_BEGIN
   r->ctx->use();
   if (r->use_graphs) {
-    if (!r->exec[0]) build_graph(r);
+    if (r->tc.j > 1) {
+      if (r->sexec.empty()) build_stint_graphs(r);
+    } else if (!r->exec[0]) {
+      build_graph(r);
+    }
     *out = r->launches;
     return 0;
   }
@@ -1907,7 +2087,7 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes, int3
   unsigned long long ts_host[phCount + 1] = {};
   bool have_ts = false;
   try {
-    if (r->use_graphs && !direct) {
+    if (r->use_graphs && r->tc.j == 1 && !direct) {
       // the production graph body, captured once more with phase stamps on
       // the main stream, replayed for this barrier
       if (!r->exec[0]) build_graph(r);
@@ -1964,7 +2144,7 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes, int3
   for (size_t q = 0; q + 1 < at.size(); ++q)
     if (at[q].second < phCount) phase_ms[at[q].second] += at[q + 1].first - at[q].first;
   int32_t sz[kSzCount];
-  TGB_CUDA(cudaMemcpy(sz, r->tr->plans[r->use_graphs && !direct ? static_cast<size_t>(b & 1) : 0].sizes, sizeof(sz),
+  TGB_CUDA(cudaMemcpy(sz, r->tr->plans[r->use_graphs && r->tc.j == 1 && !direct ? static_cast<size_t>(b & 1) : 0].sizes, sizeof(sz),
                       cudaMemcpyDeviceToHost));
   for (int x = 0; x < kSzCount; ++x) sizes[x] = sz[x];
   API_END

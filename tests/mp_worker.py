@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--train-end", type=int, default=90)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--direct", action="store_true", help="single-stream path instead of CUDA graphs")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -35,7 +36,7 @@ def main():
                        num_nodes=20, max_t=float(s.t[-1]))
     tc = T.TrainConfig(i=a.i, j=a.j, k=a.k, local_batch=a.local_batch, epochs=a.epochs, seed=3,
                        lr_base=a.lr)
-    run = T.Run(ctx, g, mc, tc, 0, a.train_end, rank=rank, nranks=world, oplog=True)
+    run = T.Run(ctx, g, mc, tc, 0, a.train_end, rank=rank, nranks=world, oplog=True, use_graphs=not a.direct)
     uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
     if rank == 0:
         uid.copy_(torch.frombuffer(bytearray(T.comm_unique_id()), dtype=torch.uint8))

@@ -63,3 +63,23 @@ def test_parallel_run_matches_reference(i, j, k, epochs, tmp_path):
         want = (tmp_path / f"ref.{grp}.oplog").read_text()
         assert ours.read_text() == want, grp
         assert ref.validate_oplog(str(ours), i, j)[0]
+
+
+@pytest.mark.parametrize("i,j,k,epochs", [(1, 2, 1, 2), (2, 2, 1, 2)])
+def test_stint_graphs_bitwise_equal_direct(i, j, k, epochs, tmp_path):
+    """j > 1: the per-position stint graphs reproduce the direct path bitwise."""
+    T_ = i * j * k
+    if ngpus() < T_:
+        pytest.skip(f"needs {T_} GPUs")
+    res = {}
+    for mode in ("graph", "direct"):
+        out = tmp_path / f"{mode}.npz"
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={T_}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29600 + 7 * i + 3 * j + k + (mode == "direct")),
+               os.path.join(ROOT, "tests", "mp_worker.py"), "--i", str(i), "--j", str(j), "--k", str(k),
+               "--epochs", str(epochs), "--out", str(out)] + (["--direct"] if mode == "direct" else [])
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        res[mode] = np.load(out)
+    for key in ("losses", "params", "oplog"):
+        assert np.array_equal(res["graph"][key], res["direct"][key]), key
