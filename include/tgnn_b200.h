@@ -192,6 +192,9 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count);
  * over active trainers, ref trainer.hpp:713-722; valid on every rank). */
 int tgnn_run_losses(tgnn_run* r, int64_t first, int64_t count, double* out);
 int tgnn_run_params(tgnn_run* r, double* flat);
+/* Enqueue (no sync) the D2H copy of this rank's loss of barrier b into dst
+ * (pinned host memory); valid after the next synchronisation. */
+int tgnn_run_loss_async(tgnn_run* r, int64_t b, double* dst);
 /* MetricsRow list (ref trainer.hpp:562-570, one row per eval barrier reached
  * so far, rank 0 evaluates with its device weights as run_training does,
  * trainer.hpp:725-743). rows[count x 5] = iter, traversed, loss (mean barrier

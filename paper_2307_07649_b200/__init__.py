@@ -434,6 +434,11 @@ class TrainerCore:
         flat = np.ascontiguousarray(flat, np.float64)
         check(lib().tgnn_trainer_set_params(self.h, _p(flat, f64p)))
 
+    def loss_async(self, b, dst):
+        """Enqueues the D2H copy of this rank's barrier-b loss into dst (a pinned
+        float64 array view of length >= 1); valid after the next synchronisation."""
+        check(lib().tgnn_run_loss_async(self.h, b, _p(dst, f64p)))
+
     def params(self):
         out = np.empty(self.nparam)
         check(lib().tgnn_trainer_get_params(self.h, _p(out, f64p)))
@@ -592,6 +597,11 @@ class Run:
         out = np.empty(count)
         check(lib().tgnn_run_losses(self.h, first, count, _p(out, f64p)))
         return out
+
+    def loss_async(self, b, dst):
+        """Enqueues the D2H copy of this rank's barrier-b loss into dst (a pinned
+        float64 array view of length >= 1); valid after the next synchronisation."""
+        check(lib().tgnn_run_loss_async(self.h, b, _p(dst, f64p)))
 
     def params(self):
         out = np.empty(self.nparam)

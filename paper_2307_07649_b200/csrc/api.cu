@@ -2446,4 +2446,13 @@ int tgnn_run_oplog(tgnn_run* r, int64_t* count, int64_t* rows) {
   API_END
 }
 
+
+int tgnn_run_loss_async(tgnn_run* r, int64_t b, double* dst) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(b >= 0 && b < r->next_barrier, kConfig, "run: loss of a barrier not yet enqueued");
+  TGB_CUDA(cudaMemcpyAsync(dst, r->d_losses + b, sizeof(double), cudaMemcpyDeviceToHost, r->ctx->stream));
+  API_END
+}
+
 }  // extern "C"

@@ -83,3 +83,27 @@ def test_stint_graphs_bitwise_equal_direct(i, j, k, epochs, tmp_path):
         res[mode] = np.load(out)
     for key in ("losses", "params", "oplog"):
         assert np.array_equal(res["graph"][key], res["direct"][key]), key
+
+
+# acceptance criterion 8 (ref/tests/acceptance.cpp:435-458): final val
+# MRR at 525,000 traversed events; reference anchors and tolerances
+ANCHORS = {(1, 1, 1): (0.8767, 0.02), (1, 1, 4): (0.8824, 0.02), (1, 4, 1): (0.8368, 0.05)}
+
+
+@pytest.mark.parametrize("i,j,k", [(1, 1, 4), (1, 4, 1)])
+def test_convergence_matches_reference_anchors(i, j, k, tmp_path):
+    T_ = i * j * k
+    if ngpus() < T_:
+        pytest.skip(f"needs {T_} GPUs")
+    out = tmp_path / "c.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={T_}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + 7 * i + 3 * j + k),
+           os.path.join(ROOT, "tests", "mp_convergence.py"), "--i", str(i), "--j", str(j), "--k", str(k),
+           "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = np.load(out)
+    assert int(res["traversed"]) == 525000
+    want, tol = ANCHORS[(i, j, k)]
+    print(f"\n({i},{j},{k}) device MRR {float(res['mrr']):.4f} vs reference {want}")
+    assert abs(float(res["mrr"]) - want) <= tol
