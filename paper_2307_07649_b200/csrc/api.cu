@@ -503,6 +503,10 @@ struct tgnn_run {
   int* d_ctr = nullptr;
   cudaGraph_t graph[2] = {nullptr, nullptr};
   cudaGraphExec_t exec[2] = {nullptr, nullptr};  // barrier b runs exec[b % 2]
+  // kMultiBarrier consecutive barriers (from an even b) captured as one graph:
+  // fewer graph launches, so the device starts each barrier's first kernel sooner
+  cudaGraph_t mgraph = nullptr;
+  cudaGraphExec_t mexec = nullptr;
   // j > 1: one graph per sub-iteration position s = b % j (a whole stint is
   // j consecutive launches); per-stint plan args and team resets in d_stint
   std::vector<cudaGraph_t> sgraph;
@@ -541,6 +545,8 @@ struct tgnn_run {
       if (exec[p]) cudaGraphExecDestroy(exec[p]);
       if (graph[p]) cudaGraphDestroy(graph[p]);
     }
+    if (mexec) cudaGraphExecDestroy(mexec);
+    if (mgraph) cudaGraphDestroy(mgraph);
     for (auto e : sexec)
       if (e) cudaGraphExecDestroy(e);
     for (auto g : sgraph)
@@ -990,6 +996,8 @@ void build_stint_graphs(tgnn_run* r) {
   r->launches = kernels;
 }
 
+constexpr int kMultiBarrier = 4;
+
 void build_graph(tgnn_run* r) {
   cudaStream_t s = r->ctx->stream;
   gemm_kernels_prepare();
@@ -1017,6 +1025,17 @@ void build_graph(tgnn_run* r) {
     TGB_CUDA(cudaStreamEndCapture(s, &r->graph[p]));
     TGB_CUDA(cudaGraphInstantiate(&r->exec[p], r->graph[p], 0));
   }
+  TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int x = 0; x < kMultiBarrier; ++x) barrier_body_dev(r, x & 1);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  TGB_CUDA(cudaStreamEndCapture(s, &r->mgraph));
+  TGB_CUDA(cudaGraphInstantiate(&r->mexec, r->mgraph, 0));
   size_t n = 0;
   TGB_CUDA(cudaGraphGetNodes(r->graph[0], nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
@@ -1930,7 +1949,15 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
     } else if (r->use_graphs) {
       if (!r->exec[0]) build_graph(r);
       if (r->prepared != b) prepare_barrier(r, b);
-      for (int64_t x = b; x < seg_end; ++x) TGB_CUDA(cudaGraphLaunch(r->exec[x & 1], r->ctx->stream));
+      for (int64_t x = b; x < seg_end;) {
+        if ((x & 1) == 0 && x + kMultiBarrier <= seg_end) {
+          TGB_CUDA(cudaGraphLaunch(r->mexec, r->ctx->stream));
+          x += kMultiBarrier;
+        } else {
+          TGB_CUDA(cudaGraphLaunch(r->exec[x & 1], r->ctx->stream));
+          ++x;
+        }
+      }
       r->prepared = seg_end;
       r->tr->adam_t = seg_end;
     } else {
