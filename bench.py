@@ -322,7 +322,7 @@ def main():
     for _ in range(args.profile_steps):
         ph, sz = run.profile_barrier(direct=True)
         prof.append((ph, sz))
-    gprof = [run.profile_barrier(direct=False)[0] for _ in range(args.profile_steps)] if world == 1 else []
+    gprof = [run.profile_barrier(direct=False)[0] for _ in range(args.profile_steps)]
     ph_graph = {k: float(np.mean([p[k] for p in gprof])) for k in gprof[0]} if gprof else None
     ph_mean = {k: float(np.mean([p[0][k] for p in prof])) for k in prof[0][0]}
     sz_mean = {k: float(np.mean([p[1][k] for p in prof])) for k in prof[0][1]}

@@ -107,3 +107,24 @@ def test_convergence_matches_reference_anchors(i, j, k, tmp_path):
     want, tol = ANCHORS[(i, j, k)]
     print(f"\n({i},{j},{k}) device MRR {float(res['mrr']):.4f} vs reference {want}")
     assert abs(float(res["mrr"]) - want) <= tol
+
+
+def test_peer_allreduce_matches_nccl(tmp_path):
+    """TGNN_ALLREDUCE=peer (NVLink peer-memory all-reduce, peer.cu): the same
+    run as NCCL up to the summation order -- losses within 1e-6, replicas
+    bitwise identical, op-log identical."""
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = {}
+    for mode in ("peer", "nccl"):
+        out = tmp_path / f"{mode}.npz"
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr", "127.0.0.1", "--master-port", str(29650 + (mode == "nccl")),
+               os.path.join(ROOT, "tests", "mp_worker.py"), "--k", "2", "--epochs", "2", "--out", str(out)]
+        env = dict(os.environ, TGNN_ALLREDUCE=mode)
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        res[mode] = np.load(out)
+        assert bool(res[mode]["replicas_identical"])
+    assert np.abs(res["peer"]["losses"] - res["nccl"]["losses"]).max() <= 1e-6
+    assert np.array_equal(res["peer"]["oplog"], res["nccl"]["oplog"])
