@@ -206,6 +206,11 @@ int tgnn_run_metrics(tgnn_run* r, int64_t* count, double* rows);
  * (ref OpRecord, oplog.hpp:15-24). A memory copy's op-log is the union of its
  * ranks' rows ordered by (iter, kind, rank). rows == NULL returns the count. */
 int tgnn_run_oplog(tgnn_run* r, int64_t* count, int64_t* rows);
+/* Replica invariant (ref SPEC.md:397): collective over all ranks; fails with
+ * TGNN_PROTOCOL if any rank's parameters differ bitwise; hash_out receives the
+ * order-independent 64-bit parameter fingerprint. Also checked automatically at
+ * every eval point of a multi-rank run. */
+int tgnn_run_check_replicas(tgnn_run* r, uint64_t* hash_out);
 /* evaluate_mrr of the run's current weights (rank-local, no collective). */
 int tgnn_run_evaluate_mrr(tgnn_run* r, int64_t eval_begin, int64_t eval_end, int64_t batch_size,
                           int32_t n_negatives, uint64_t seed, double* mrr, int64_t* queries);

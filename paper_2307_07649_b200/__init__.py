@@ -623,6 +623,13 @@ class Run:
             check(lib().tgnn_run_metrics(self.h, C.byref(n), _p(out, f64p)))
         return out
 
+    def check_replicas(self) -> int:
+        """Collective: raises ProtocolError unless every rank holds bitwise the
+        same parameters; returns the 64-bit fingerprint."""
+        h = C.c_uint64()
+        check(lib().tgnn_run_check_replicas(self.h, C.byref(h)))
+        return h.value
+
     def oplog(self):
         """This rank's daemon op-log rows [n x 6]: epoch, iter, kind (0 R / 1 W),
         rank within the memory copy, first, len (OpRecord, oplog.hpp:15-24)."""

@@ -136,6 +136,7 @@ SIGNATURES = {
     "tgnn_run_traversed": [vp, i64, i64, i64p],
     "tgnn_run_metrics": [vp, i64p, f64p],
     "tgnn_run_oplog": [vp, i64p, i64p],
+    "tgnn_run_check_replicas": [vp, C.POINTER(C.c_uint64)],
     "tgnn_run_evaluate_mrr": [vp, i64, i64, i64, i32, u64, f64p, i64p],
     "tgnn_evaluator_create": [vp, vp, C.POINTER(ModelConfigC), i64, i32, C.POINTER(vp)],
     "tgnn_evaluator_destroy": [vp],

@@ -1114,9 +1114,33 @@ void tgnn_evaluator::init(tgnn_ctx* cx, tgnn_graph* gr, const ModelDims& md, int
 namespace {
 
 // One metrics row at eval barrier b (rank 0 evaluates with its own weights).
+// Replica invariant: every rank holds bitwise the same
+// parameters. Collective: the parameter fingerprint's min and max over ranks
+// must agree. Returns the fingerprint.
+uint64_t check_replicas(tgnn_run* r) {
+  cudaStream_t s = r->ctx->stream;
+  unsigned long long* d = dalloc<unsigned long long>(3);
+  params_hash_launch(r->tr->params, r->tr->L.total, d, s);
+  if (r->nranks > 1) {
+    NCCL_CHECK(nccl::api().AllReduce(d, d + 1, 1, ncclUint64, ncclMin, r->comm, s));
+    NCCL_CHECK(nccl::api().AllReduce(d, d + 2, 1, ncclUint64, ncclMax, r->comm, s));
+  } else {
+    TGB_CUDA(cudaMemcpyAsync(d + 1, d, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    TGB_CUDA(cudaMemcpyAsync(d + 2, d, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+  }
+  unsigned long long h[3];
+  TGB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TGB_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d);
+  if (h[1] != h[2])
+    throw Error(kProtocol, "run: replica parameters diverged by barrier " + std::to_string(r->next_barrier));
+  return h[0];
+}
+
 void run_eval_point(tgnn_run* r, int64_t b) {
   tgnn_run::Row row;
   row.barrier = b;
+  if (r->nranks > 1) check_replicas(r);  // once per eval point (epoch-equivalent)
   if (r->rank == 0 && r->val_end > r->val_begin) {
     const int64_t batch = r->eval_batch > 0 ? r->eval_batch : r->tc.local_batch;
     if (!r->ev || r->ev->cap_B != batch || r->ev->n_neg != r->eval_negatives) {
@@ -2577,6 +2601,15 @@ int tgnn_run_loss_async(tgnn_run* r, int64_t b, double* dst) {
   r->ctx->use();
   TGB_REQUIRE(b >= 0 && b < r->next_barrier, kConfig, "run: loss of a barrier not yet enqueued");
   TGB_CUDA(cudaMemcpyAsync(dst, r->d_losses + b, sizeof(double), cudaMemcpyDeviceToHost, r->ctx->stream));
+  API_END
+}
+
+
+int tgnn_run_check_replicas(tgnn_run* r, uint64_t* hash_out) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
+  *hash_out = check_replicas(r);
   API_END
 }
 

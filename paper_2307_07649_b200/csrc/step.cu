@@ -2135,12 +2135,29 @@ void adam_launch(float* params, const float* grads, float* m, float* v, int64_t 
 }
 
 namespace {
+// Order-independent 64-bit fingerprint of a parameter vector: XOR over x of
+// splitmix64(bits(p[x]) ^ x * golden) -- identical bit patterns give identical
+// hashes whatever the thread schedule.
+__global__ void params_hash_kernel(const float* __restrict__ p, int64_t n, unsigned long long* out) {
+  unsigned long long h = 0;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    h ^= splitmix64(static_cast<uint64_t>(__float_as_uint(p[x])) ^ (static_cast<uint64_t>(x) * kGamma));
+  for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicXor(out, h);
+}
+
 __global__ void stamp_kernel(unsigned long long* dst) {
   unsigned long long v;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
   *dst = v;
 }
 }  // namespace
+
+void params_hash_launch(const float* p, int64_t n, unsigned long long* out, cudaStream_t s) {
+  TGB_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
+  params_hash_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 4 * kSMs)), 256, 0, s>>>(p, n, out);
+  TGB_CUDA(cudaGetLastError());
+}
 
 void stamp_launch(unsigned long long* dst, cudaStream_t s) {
   stamp_kernel<<<1, 1, 0, s>>>(dst);

@@ -209,6 +209,8 @@ void adam_pack_launch(const StepCtx& c, float* m, float* v, cudaStream_t s, cons
                       const int* ctr, int64_t r_lo = 0, int64_t r_hi = -1);
 // Packs the TMA engine's weight operands from the fp32 parameters.
 void pack_weights(const StepCtx& c, cudaStream_t s);
+// Order-independent 64-bit fingerprint of n floats into *out (device).
+void params_hash_launch(const float* p, int64_t n, unsigned long long* out, cudaStream_t s);
 // Graph mode helpers: reset the memory copy if desc[*ctr].reset; ++*ctr.
 void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s, int offset = 0);
 void incr_launch(int* ctr, cudaStream_t s);

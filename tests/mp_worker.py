@@ -48,6 +48,7 @@ def main():
     allp = [torch.zeros(len(params), dtype=torch.float64, device="cuda") for _ in range(world)]
     dist.all_gather(allp, torch.tensor(params, device="cuda"))
     same = all(torch.equal(allp[0], x) for x in allp)
+    run.check_replicas()  # the device-side invariant (raises ProtocolError on divergence)
     logs = [None] * world
     dist.all_gather_object(logs, (rank // (a.i * a.j), run.oplog().tolist()))
     if rank == 0:
