@@ -69,8 +69,13 @@ struct TcGroup {
 // [K rows x M cols]. B K-major: stored [N rows x K cols]; MN-major: [K x N].
 // (col0 % 8 == 0 so the view base is 16-byte aligned.)
 TmaOp tma_view(const BfMat& m, int64_t col0, int64_t cols, int64_t rows, bool kmajor, int box_rows);
+// UMMA N per tile: the fewest tiles of width <= cap, balanced (a 272-wide
+// problem runs as 2 x 144, not 256 + 16, so no CTA streams a full A tile for
+// a sliver of outputs).
 inline int tc_ntile(int N, int cap = 256) {
-  return static_cast<int>(std::min<int64_t>(cap, (N + 15) / 16 * 16));
+  const int tiles = (N + cap - 1) / cap;
+  const int w = (N + tiles - 1) / tiles;
+  return static_cast<int>(std::min<int64_t>(cap, (w + 15) / 16 * 16));
 }
 
 // reduce_stream / ev (optional): the split-K reduction of the group's split
