@@ -2340,7 +2340,7 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
   API_BEGIN
   TGB_REQUIRE(M > 0 && N > 0 && K > 0 && splits >= 1, kConfig, "debug_gemm: bad sizes");
   float *dA = dalloc<float>(M * K), *dB = dalloc<float>(K * N), *dC = dalloc<float>(M * N);
-  float* ws = splits > 1 ? dalloc<float>(static_cast<size_t>(splits) * M * N) : nullptr;
+  float* ws = splits > 1 ? dalloc<float>(static_cast<size_t>(splits) * M * ((N + 3) / 4 * 4)) : nullptr;
   TGB_CUDA(cudaMemcpy(dA, A, sizeof(float) * M * K, cudaMemcpyHostToDevice));
   TGB_CUDA(cudaMemcpy(dB, B, sizeof(float) * K * N, cudaMemcpyHostToDevice));
   GemmGroup gg;
@@ -2373,6 +2373,7 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
     T.ldc = N;
     T.splits = splits;
     T.ws = ws;
+    T.ldw = static_cast<int>((N + 3) / 4 * 4);
     tc_group_launch(tg, nullptr);
     TGB_CUDA(cudaDeviceSynchronize());
     bf_free(ba);

@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include <mutex>
@@ -28,8 +29,8 @@ constexpr int kBM = 128, kBK = 64, kStMax = 6;
 constexpr int kEpiWarps = 8;                      // two warps per TMEM lane quarter
 constexpr int kThreads = 64 + 32 * kEpiWarps;     // producer, MMA, epilogue
 constexpr int kATileB = kBM * kBK * 2;   // 16 KB (one of hi / lo)
-constexpr int kEpiStageB = kEpiWarps * 32 * 33 * 4;  // static epilogue transpose buffers
-constexpr int kSmemMax = 232448 - kEpiStageB;  // opt-in dynamic maximum per CTA
+constexpr int kEpiStageB = kEpiWarps * 32 * 32 * 4;  // static epilogue staging tiles
+constexpr int kSmemMax = 232448 - kEpiStageB - 1024;  // opt-in dynamic maximum per CTA (static tile is 1 KB aligned)
 
 // Shared-memory / TMEM geometry is sized by the group's widest N tile, so
 // narrow-tile groups fit several CTAs per SM.
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint64_t* tfull = empty + kSt;   // [2] accumulator ready for the epilogue
   uint64_t* tempty = tfull + 2;    // [2] accumulator drained by the epilogue
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ float epi_stage[kEpiWarps * 32 * 33];  // epilogue transposes (static: LDS / STS, not generic)
+  __shared__ __align__(1024) float epi_stage[kEpiWarps * 32 * 32];  // epilogue staging (128 B swizzle)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = gp.tile_base[gp.count];
 
@@ -287,6 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     const int quarter = warp & 3;
     const int ehalf = (warp - 2) >> 2;  // the two warps of a quarter take alternate 32-column chunks
     const int epi_mode = g_tc_epi_mode;
+    float* stg = epi_stage + (warp - 2) * (32 * 32);
+    const uint32_t stg_s = su32(stg);
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       TileInfo ti;
@@ -308,54 +311,102 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       float* const C2p = P.C2;
       float* const wsp = P.ws;
       const int64_t ldcp = P.ldc;
-      // TMEM -> registers (thread = row) -> shared-memory transpose -> global
-      // stores with lane = column (or float4 per lane, four rows per instruction)
-      float* stg = epi_stage + (warp - 2) * (32 * 33);
+      const int ldw = P.ldw > 0 ? P.ldw : N;
+      const int cmode = epi_mode == 0 ? P.c_mode : 0;
+      const CUtensorMap* cmap = &P.cmap;
+      // TMEM -> registers (thread = row) -> 128 B-swizzled shared tile (alpha
+      // applied, rows past the runtime count zeroed) -> one TMA tensor store
+      // (or reduce-add for beta = 1) per 32 x 32 chunk; a per-lane store path
+      // remains for unaligned outputs and partial row quarters.
       const int mb = ti.m0 + quarter * 32;  // first row of this warp
-      const int npart = splits > 1 ? N : static_cast<int>(ldcp);
-      float* const vbase = splits > 1 ? wsp + static_cast<int64_t>(ti.split) * PM * N : Cp;
+      const int row = mb + lane;
+      const bool live = row < ti.M;
+      const int npart = splits > 1 ? ldw : static_cast<int>(ldcp);
+      float* const vbase = splits > 1 ? wsp + static_cast<int64_t>(ti.split) * PM * ldw : Cp;
       const int rmax = splits > 1 ? PM : ti.M;  // rows to write (zeros past ti.M for partials)
-      const bool vec_ok = epi_mode == 0 && (npart & 3) == 0 && (reinterpret_cast<uintptr_t>(vbase) & 15) == 0 &&
+      const int ncols = (C2p && splits == 1) ? N - 1 : N;  // columns of C (map extent)
+      const bool rows_tma = mb + 32 <= ti.M || ti.M >= PM;  // else partial quarter: per-lane path
+      const bool vec_ok = epi_mode != 1 && (npart & 3) == 0 && (reinterpret_cast<uintptr_t>(vbase) & 15) == 0 &&
                           beta == 0.0f;
       for (int c0 = 32 * ehalf; c0 < ntile; c0 += 64) {
         const int halves = min(2, (ntile - c0) / 16);
-        for (int h = 0; h < halves; ++h) {
-          uint32_t v[16];
-          if (ti.nk > 0 && epi_mode != 2) {
-            const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                acc * static_cast<uint32_t>(acc_cols) + static_cast<uint32_t>(c0 + 16 * h);
+        uint32_t v[32];
+        if (ti.nk > 0 && epi_mode != 2) {
+          const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                              acc * static_cast<uint32_t>(acc_cols) + static_cast<uint32_t>(c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                "=r"(v[14]), "=r"(v[15])
+              : "r"(ta));
+          if (halves == 2) {
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                  "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                  "=r"(v[14]), "=r"(v[15])
-                : "r"(ta));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                : "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+                  "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                  "=r"(v[30]), "=r"(v[31])
+                : "r"(ta + 16u));
           } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = 0u;
+            for (int q = 16; q < 32; ++q) v[q] = 0u;
           }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        } else {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) stg[lane * 33 + 16 * h + q] = __uint_as_float(v[q]);
+          for (int q = 0; q < 32; ++q) v[q] = 0u;
+        }
+        // the previous chunk's bulk store must have read the staging tile
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 o;
+          o.x = live ? alpha * __uint_as_float(v[4 * j + 0]) : 0.0f;
+          o.y = live ? alpha * __uint_as_float(v[4 * j + 1]) : 0.0f;
+          o.z = live ? alpha * __uint_as_float(v[4 * j + 2]) : 0.0f;
+          o.w = live ? alpha * __uint_as_float(v[4 * j + 3]) : 0.0f;
+          *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) << 2)) = o;
         }
         __syncwarp();
         if (warp == 2 && lane == 0 && c0 < 96) trace(8 + 2 * (c0 / 32));
+        // a 16-wide last chunk may only use the bulk store if nothing of a
+        // neighbouring tile lies in its upper 16 columns (the map clips at ncols)
+        if (cmode != 0 && rows_tma && (halves == 2 || n0 + c0 + 16 >= ncols)) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int cx = n0 + c0, cy = mb, cz = splits > 1 ? ti.split : 0;
+            if (cmode == 2)
+              asm volatile(
+                  "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                      reinterpret_cast<uint64_t>(cmap)),
+                  "r"(stg_s), "r"(cx), "r"(cy), "r"(cz)
+                  : "memory");
+            else
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                      reinterpret_cast<uint64_t>(cmap)),
+                  "r"(stg_s), "r"(cx), "r"(cy), "r"(cz)
+                  : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          if (C2p && splits == 1 && n0 + c0 <= N - 1 && N - 1 < n0 + c0 + 16 * halves && live) {
+            const int cc = N - 1 - n0 - c0;  // the bias column goes to C2 (beta == 0 here)
+            C2p[row] = stg[lane * 32 + (((cc >> 2) ^ (lane & 7)) << 2) + (cc & 3)];
+          }
+          if (warp == 2 && lane == 0 && c0 < 96) trace(9 + 2 * (c0 / 32));
+          continue;
+        }
         if (vec_ok && halves == 2 && c0 + 32 <= nvalid && ((n0 + c0) & 3) == 0 && !(C2p && n0 + c0 + 32 > N - 1)) {
-          const int rr = lane >> 3, cc = (lane & 7) * 4;
+          const int rr = lane >> 3, ch = lane & 7, cc = ch * 4;
           float* dst0 = vbase + static_cast<int64_t>(mb + rr) * npart + n0 + c0 + cc;
-          float4 o[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            const float* src = stg + (4 * k + rr) * 33 + cc;
-            const bool live = mb + 4 * k + rr < ti.M;
-            o[k].x = live ? alpha * src[0] : 0.0f;
-            o[k].y = live ? alpha * src[1] : 0.0f;
-            o[k].z = live ? alpha * src[2] : 0.0f;
-            o[k].w = live ? alpha * src[3] : 0.0f;
+            const int r = 4 * k + rr;
+            const float4 o = *reinterpret_cast<const float4*>(stg + r * 32 + ((ch ^ (r & 7)) << 2));
+            if (mb + r < rmax) *reinterpret_cast<float4*>(dst0 + static_cast<int64_t>(4 * k) * npart) = o;
           }
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (mb + 4 * k + rr < rmax) *reinterpret_cast<float4*>(dst0 + static_cast<int64_t>(4 * k) * npart) = o[k];
           if (warp == 2 && lane == 0 && c0 < 96) trace(9 + 2 * (c0 / 32));
           __syncwarp();
           continue;
@@ -363,16 +414,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const int col = c0 + lane;                 // this lane's column in the tile
         const bool col_ok = lane < 16 * halves && col < nvalid && epi_mode != 1;
         const int n = n0 + col;
+        const int sw = lane >> 2, sl = lane & 3;   // swizzled column read: conflict-free per row
         if (splits > 1) {
           const int rows = min(32, PM - mb);
-          float* wrow = wsp + (static_cast<int64_t>(ti.split) * PM + mb) * N + n;
+          float* wrow = wsp + (static_cast<int64_t>(ti.split) * PM + mb) * ldw + n;
           for (int r0 = 0; r0 < rows; r0 += 8) {
             float val[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) val[k] = stg[(r0 + k) * 33 + lane];
+            for (int k = 0; k < 8; ++k) {
+              const int r = r0 + k;
+              val[k] = stg[r * 32 + ((sw ^ (r & 7)) << 2) + sl];
+            }
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-              if (r0 + k < rows && col_ok) wrow[static_cast<int64_t>(r0 + k) * N] = mb + r0 + k < ti.M ? val[k] : 0.0f;
+              if (r0 + k < rows && col_ok) wrow[static_cast<int64_t>(r0 + k) * ldw] = val[k];
           }
         } else {
           const bool to_c2 = C2p && n == N - 1;
@@ -383,7 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
             float val[8], prev[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-              val[k] = stg[(r0 + k) * 33 + lane];
+              const int r = r0 + k;
+              val[k] = stg[r * 32 + ((sw ^ (r & 7)) << 2) + sl];
               prev[k] = 0.0f;
             }
             if (beta != 0.0f) {
@@ -394,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               if (r0 + k < rows && col_ok) {
-                const float x = alpha * val[k] + beta * prev[k];
+                const float x = val[k] + beta * prev[k];
                 if (to_c2) C2p[mb + r0 + k] = x;
                 else crow[(r0 + k) * ldc] = x;
               }
@@ -410,6 +466,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       if (warp == 2 && lane == 0) trace(5);
       ++lt;
     }
+    // bulk stores must finish reading shared memory before the CTA exits
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -424,10 +483,11 @@ __global__ void tc_splitk_reduce_kernel(const __grid_constant__ TcParams gp) {
   const TcProblem& P = gp.p[blockIdx.y];
   if (P.splits <= 1) return;
   const int64_t total = static_cast<int64_t>(P.M) * P.N;
+  const int64_t ldw = P.ldw > 0 ? P.ldw : P.N, pstride = static_cast<int64_t>(P.M) * ldw;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float s = 0.0f;
-    for (int sp = 0; sp < P.splits; ++sp) s += P.ws[sp * total + x];
     const int64_t m = x / P.N, n = x % P.N;
+    float s = 0.0f;
+    for (int sp = 0; sp < P.splits; ++sp) s += P.ws[sp * pstride + m * ldw + n];
     const float v = P.alpha * s;
     if (P.C2 && n == P.N - 1) {
       P.C2[m] = P.beta != 0.0f ? v + P.beta * P.C2[m] : v;
@@ -475,6 +535,42 @@ CUtensorMap encode(void* base, int64_t inner, int64_t outer, int64_t ld_bytes, i
   return m;
 }
 
+// fp32 output map [depth][rows][cols] (row stride ld_bytes, plane stride
+// rows * ld_bytes), 32 x 32 x 1 boxes with 128 B swizzle (the epilogue's
+// staging layout). Cached: the step's outputs are fixed buffers.
+bool encode_out(float* base, int64_t cols, int64_t rows, int64_t depth, int64_t ld_bytes, CUtensorMap* out) {
+  using Key = std::tuple<const void*, int64_t, int64_t, int64_t, int64_t>;
+  struct H {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(std::get<0>(k)) ^ (std::get<1>(k) * 0x9e3779b97f4a7c15ull) ^
+             (std::get<2>(k) * 0xbf58476d1ce4e5b9ull) ^ (std::get<3>(k) << 7) ^ (std::get<4>(k) * 31);
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, CUtensorMap, H> cache;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld_bytes & 15) != 0 || cols <= 0 || rows <= 0) return false;
+  const Key key = std::make_tuple(static_cast<const void*>(base), cols, rows, depth, ld_bytes);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(depth)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld_bytes), static_cast<cuuint64_t>(ld_bytes * rows)};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  cache.emplace(key, m);
+  *out = m;
+  return true;
+}
+
 using MapKey = std::tuple<const void*, const void*, int64_t, int64_t, int64_t, int, int>;
 
 struct KeyHash {
@@ -489,6 +585,12 @@ struct KeyHash {
 };
 
 }  // namespace
+
+// TGNN_TC_BULK=0 forces the per-lane epilogue stores (A/B measurements)
+int g_tc_bulk_store = [] {
+  const char* e = std::getenv("TGNN_TC_BULK");
+  return e ? std::atoi(e) : 1;
+}();
 
 BfMat bf_alloc(int64_t rows, int64_t cols) {
   BfMat m;
@@ -553,6 +655,18 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_strea
   bool any_split = false;
   for (int i = 0; i < g.count; ++i) {
     gp.p[i] = g.p[i];
+    TcProblem& Q = gp.p[i];
+    // epilogue: bulk tensor stores where the output layout allows them
+    Q.c_mode = 0;
+    if (g_tc_bulk_store) {
+      if (Q.splits > 1) {
+        const int ldw = Q.ldw > 0 ? Q.ldw : Q.N;
+        if (encode_out(Q.ws, Q.N, Q.M, Q.splits, 4ll * ldw, &Q.cmap)) Q.c_mode = 1;
+      } else if (Q.beta == 0.0f || (Q.beta == 1.0f && !Q.C2)) {
+        const int cols = Q.C2 ? Q.N - 1 : Q.N;
+        if (encode_out(Q.C, cols, Q.M, 1, 4 * Q.ldc, &Q.cmap)) Q.c_mode = Q.beta == 0.0f ? 1 : 2;
+      }
+    }
     TGB_REQUIRE(g.p[i].ntile % 16 == 0 && g.p[i].ntile >= 16 && g.p[i].ntile <= 256, kConfig,
                 "tc gemm: ntile must be a multiple of 16 in [16, 256]");
     gp.tiles_m[i] = static_cast<int>(ceil_div(g.p[i].M, kBM));

@@ -55,8 +55,14 @@ struct TcProblem {
   float* C2 = nullptr;         // when set, output column N-1 goes to C2[m]
   float alpha = 1.0f, beta = 0.0f;
   int splits = 1;
-  float* ws = nullptr;         // split-K partials [splits][M][N]
+  float* ws = nullptr;         // split-K partials [splits][M][ldw]
+  int ldw = 0;                 // partial row stride (0: N); a multiple of 4 enables bulk stores
   int ntile = 0;               // UMMA N per tile (multiple of 16, <= 256)
+  // set by tc_group_launch: output tensor map (fp32 [splits][rows][cols], 32 x 32
+  // boxes, 128 B swizzle) and the epilogue mode (0 per-lane stores, 1 TMA
+  // store, 2 TMA reduce-add for beta = 1)
+  CUtensorMap cmap;
+  int c_mode = 0;
 };
 
 constexpr int kMaxTc = 8;
@@ -77,6 +83,8 @@ inline int tc_ntile(int N, int cap = 256) {
   const int w = (N + tiles - 1) / tiles;
   return static_cast<int>(std::min<int64_t>(cap, (w + 15) / 16 * 16));
 }
+
+extern int g_tc_bulk_store;  // 0: per-lane epilogue stores only (A/B switch)
 
 // reduce_stream / ev (optional): the split-K reduction of the group's split
 // problems runs on reduce_stream after ev (recorded on s past the GEMM).

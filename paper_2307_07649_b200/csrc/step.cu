@@ -1301,6 +1301,7 @@ struct WsCarver {
   float* base;
   size_t used = 0, cap;
   float* take(size_t n) {
+    n = (n + 3) / 4 * 4;  // 16-byte aligned partial planes (bulk tensor stores)
     if (used + n > cap) throw Error(kConfig, "split-K workspace exhausted");
     float* p = base + used;
     used += n;
@@ -1405,7 +1406,8 @@ void tc_tn(TcGroup& g, WsCarver& wc, int M, int N, int Kcap, const int* K_dev, c
   P.ldc = ldc;
   P.C2 = C2;
   P.splits = choose_splits_tma(M, N, Kcap);
-  if (P.splits > 1) P.ws = wc.take(static_cast<size_t>(P.splits) * M * N);
+  P.ldw = (N + 3) / 4 * 4;
+  if (P.splits > 1) P.ws = wc.take(static_cast<size_t>(P.splits) * M * P.ldw);
 }
 
 int max_splits(int M, int N, int64_t K) {
@@ -1505,7 +1507,9 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   w.cq = dalloc<float>(da);
   // split-K arena (max over the engines) + routing partials in its tail
   size_t ws = 0;
-  auto acc = [&](int M, int N, int64_t K) { ws += static_cast<size_t>(max_splits(M, N + 1, K)) * M * (N + 1); };
+  auto acc = [&](int M, int N, int64_t K) {
+    ws += static_cast<size_t>(max_splits(M, N + 1, K)) * M * ((N + 1 + 3) / 4 * 4) + 4;
+  };
   // decoder bwd
   acc(static_cast<int>(dh), static_cast<int>(2 * da), B2);
   acc(1, static_cast<int>(dh), B2);
