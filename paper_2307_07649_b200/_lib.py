@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtgnn_b200.so")
+LIB_PATH = os.environ.get("TGNN_LIB") or os.path.join(HERE, "libtgnn_b200.so")
 
 
 class TgnnError(RuntimeError):
