@@ -767,6 +767,7 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
   // 16-byte aligned split: the few Wq entries below it join the head bucket
   const int64_t split = (tr->L.off[tWq] + 3) / 4 * 4;
   TGB_CUDA(cudaStreamWaitEvent(c, r->ev_tail, 0));
+  if (c != r->ctx->br) TGB_CUDA(cudaStreamWaitEvent(c, r->ev_brjoin, 0));  // the branch's tail gradients
   if (r->nranks > 1) {
     if (r->peer_ok) peer_allreduce_launch(r->peer, split, tr->L.total - split, r->d_ctr, 0, c);
     else NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),

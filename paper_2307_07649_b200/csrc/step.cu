@@ -1994,10 +1994,10 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     launch_pdl(qtime_grad_kernel, dim3(ceil_div(static_cast<int64_t>(da) * dt, 256)), dim3(256), 0,
                c.br ? c.br : s, D, G + L.off[tWq], G + L.off[tBq]);
   }
-  if (c.br) {  // the branch's loss, W2 / b2 gradient and split-K reductions so far
-    TGB_CUDA(cudaEventRecord(c.ev_br_join, c.br));
-    TGB_CUDA(cudaStreamWaitEvent(s, c.ev_br_join, 0));
-  }
+  // the branch's loss, W2 / b2 gradient, split-K reductions and omega part 1:
+  // the tail-range update waits for it (update_split), the main stream only
+  // before the omega gradient's second part
+  if (c.br) TGB_CUDA(cudaEventRecord(c.ev_br_join, c.br));
   if (c.ev_tail_grads) TGB_CUDA(cudaEventRecord(c.ev_tail_grads, s));
   if (tma) {
     TcGroup tg;
@@ -2028,6 +2028,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     add_tn(gg, wc, 3 * d, dt, U, szU, A_trans(w.Dg, 3 * d, U), B_w(w.GU, dt, U), w.DMT, dt);
     gemm_group_launch(gg, s);
   }
+  if (c.br) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_br_join, 0));
   if (dt > 0)
     launch_pdl(omega_final_kernel, dim3(dt), dim3(256), 0, s, D, P, L.off[tWk], L.off[tWv], L.off[tWz], w.Mom, w.DMT,
                G + L.off[tOmega], tma ? B.d8a : da, tma ? B.d8d : d, 2 * da, 2 * da + 3 * d,
