@@ -824,7 +824,8 @@ void barrier_body_dev(tgnn_run* r, int p) {
   sc.ev_br_join = r->ev_brjoin;
   sc.ev_red = r->ev_red;
   // edge branch: the plan-only half of the attention projection runs beside the GRU
-  if (gemm_impl() == kGemmTma) {
+  static const bool no_edge = std::getenv("TGNN_NOEDGE") != nullptr;  // A/B: edge part inline
+  if (gemm_impl() == kGemmTma && !no_edge) {
     TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_fork, 0));
     StepCtx se = sc;
     se.marks = nullptr;  // phase markers live on the main stream

@@ -128,6 +128,16 @@ Dims make_dims(const ModelDims& m, const DGraph& g) {
   return D;
 }
 
+// cos / sin of the time-encoding argument dt * w (dt an f64 time delta): the
+// product and the reduction by 2 pi in f64, then f32 sincos on |r| <= pi --
+// accurate for the large deltas of long-lived neighbours and never on
+// sincosf's slow (Payne-Hanek) path.
+__device__ __forceinline__ void time_sincos(double dt, float w, float* sn, float* cs) {
+  const double a = dt * static_cast<double>(w);
+  const double k = rint(a * 0.15915494309189535);
+  sincosf(static_cast<float>(fma(-k, 6.283185307179586, a)), sn, cs);
+}
+
 // ---------------------------------------------------------------- forward
 // GRU input rows {mail_mem | cos(dt w) | e(mail event) | s | 1} (make_mail,
 // model.hpp:153-166) and GU = -dt sin(dt w) (time_encode_backward factor),
@@ -148,10 +158,8 @@ __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const 
     const double dt = vw.mail_dt[u];
     for (int x = lane; x < 2 * D.d; x += 32) row[x] = vw.mail_mem[u * 2 * D.d + x];
     for (int i = lane; i < D.dt; i += 32) {
-      // product in f64 (dt is an f64 time delta), cos/sin in f32: |arg| = O(1)
-      const float arg = static_cast<float>(dt * static_cast<double>(omega[i]));
       float sn, cs;
-      sincosf(arg, &sn, &cs);
+      time_sincos(dt, omega[i], &sn, &cs);
       row[2 * D.d + i] = cs;
       gu[i] = has ? static_cast<float>(-dt) * sn : 0.0f;
     }
@@ -247,9 +255,8 @@ __global__ void assemble_edge_kernel(Dims D, DPlan pl, DGraph g, const float* __
     const float* ef = g.efeat + ev * D.de_pad;
     for (int x = lane; x < D.de; x += 32) row[x] = ef[x];
     for (int i = lane; i < D.dt; i += 32) {
-      const float arg = static_cast<float>(dt * static_cast<double>(omega[i]));
       float sn, cs;
-      sincosf(arg, &sn, &cs);
+      time_sincos(dt, omega[i], &sn, &cs);
       row[D.de + i] = cs;
       gt[i] = static_cast<float>(-dt) * sn;
     }
@@ -270,10 +277,12 @@ __global__ void query_const_kernel(Dims D, const float* __restrict__ Wq, const f
   pdl_wait();
   pdl_trigger();
   const int nd = D.d + D.ds;
-  for (int i = threadIdx.x; i < D.da; i += blockDim.x) {
-    float s = bq[i];
-    for (int j = 0; j < D.dt; ++j) s += Wq[static_cast<int64_t>(i) * D.q_in + nd + j];
-    cq[i] = s;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = gwarp(); i < D.da; i += nwarp()) {  // one warp per output, fixed order
+    float s = 0.0f;
+    for (int j = lane; j < D.dt; j += 32) s += Wq[i * D.q_in + nd + j];
+    s = warp_sum(s);
+    if (lane == 0) cq[i] = bq[i] + s;
   }
 }
 
@@ -312,9 +321,8 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
       const float* ef = g.efeat + ev * D.de_pad;
       for (int x = lane; x < D.de; x += 32) row[D.d + D.ds + x] = ef[x];
       for (int i = lane; i < D.dt; i += 32) {
-        const float arg = static_cast<float>(dt * static_cast<double>(omega[i]));
         float sn, cs;
-        sincosf(arg, &sn, &cs);
+        time_sincos(dt, omega[i], &sn, &cs);
         row[D.d + D.ds + D.de + i] = cs;
         gt[i] = static_cast<float>(-dt) * sn;
       }
@@ -1768,7 +1776,7 @@ void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   const int stage = (ke + D.dt + 7) / 8 * 8;
   launch_pdl(assemble_edge_kernel, dim3(row_blocks(Pc)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, D,
              pl, g, P + L.off[tOmega], w.bf, Pc, stage);
-  launch_pdl(query_const_kernel, dim3(1), dim3(128), 0, s, D, P + L.off[tWq], P + L.off[tBq], w.cq);
+  launch_pdl(query_const_kernel, dim3(row_blocks(D.da)), dim3(32 * kWarps), 0, s, D, P + L.off[tWq], P + L.off[tBq], w.cq);
   c.mark(phAttnProj, s);
   TcGroup tg;
   g_wide = 1;  // per-pair K and V edge parts in one pass: [Wk_e Wk_t bk ; Wv_e Wv_t bv]
