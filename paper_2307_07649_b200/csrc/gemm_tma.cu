@@ -548,7 +548,12 @@ bool encode_out(float* base, int64_t cols, int64_t rows, int64_t depth, int64_t 
   };
   static std::mutex mu;
   static std::unordered_map<Key, CUtensorMap, H> cache;
-  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld_bytes & 15) != 0 || cols <= 0 || rows <= 0) return false;
+  // every row segment must start and end on a 16-byte boundary: a clipped
+  // box edge inside a 16-byte granule races with the neighbouring columns'
+  // writers (measured: graph-mode runs diverged with a 2-column output)
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld_bytes & 15) != 0 || (cols & 3) != 0 || cols <= 0 ||
+      rows <= 0)
+    return false;
   const Key key = std::make_tuple(static_cast<const void*>(base), cols, rows, depth, ld_bytes);
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
@@ -586,10 +591,11 @@ struct KeyHash {
 
 }  // namespace
 
-// TGNN_TC_BULK=0 forces the per-lane epilogue stores (A/B measurements)
+// TGNN_TC_BULK (bit mask, default 7): 1 plain stores, 2 split-K partials, 4 reduce-add;
+// 0 forces the per-lane epilogue stores (A/B measurements)
 int g_tc_bulk_store = [] {
   const char* e = std::getenv("TGNN_TC_BULK");
-  return e ? std::atoi(e) : 1;
+  return e ? std::atoi(e) : 7;
 }();
 
 BfMat bf_alloc(int64_t rows, int64_t cols) {
@@ -661,8 +667,8 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_strea
     if (g_tc_bulk_store) {
       if (Q.splits > 1) {
         const int ldw = Q.ldw > 0 ? Q.ldw : Q.N;
-        if (encode_out(Q.ws, Q.N, Q.M, Q.splits, 4ll * ldw, &Q.cmap)) Q.c_mode = 1;
-      } else if (Q.beta == 0.0f || (Q.beta == 1.0f && !Q.C2)) {
+        if ((g_tc_bulk_store & 2) && encode_out(Q.ws, Q.N, Q.M, Q.splits, 4ll * ldw, &Q.cmap)) Q.c_mode = 1;
+      } else if (((g_tc_bulk_store & 1) && Q.beta == 0.0f) || ((g_tc_bulk_store & 4) && Q.beta == 1.0f && !Q.C2)) {
         const int cols = Q.C2 ? Q.N - 1 : Q.N;
         if (encode_out(Q.C, cols, Q.M, 1, 4 * Q.ldc, &Q.cmap)) Q.c_mode = Q.beta == 0.0f ? 1 : 2;
       }

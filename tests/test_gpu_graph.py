@@ -34,6 +34,27 @@ def test_graph_barriers_bitwise_equal_direct(ctx, cfg):
     assert np.array_equal(res[True][1], res[False][1])
 
 
+def test_graph_bitwise_tiny_dims(ctx):
+    """Tiny widths (2-column decoder halves, 3-wide attention) put GEMM outputs
+    next to other writers inside one 16-byte granule: the epilogue's bulk
+    tensor stores must not touch them (a graph-mode divergence caught in r01)."""
+    g = T.TemporalGraph.synthetic(ctx, T.SynthParams(nodes=20, events=120, d_e=2, seed=21))
+    _, _, t = g.events()
+    mc = T.ModelConfig(d_mem=3, d_time=2, d_static=2, d_attn=3, d_hidden=2, d_e=2, n_neighbors=2, num_nodes=20,
+                       max_t=float(t[-1]))
+    tc = T.TrainConfig(local_batch=15, lr_base=1e-3, seed=3, epochs=6)
+    res = {}
+    for graphs in (True, False):
+        for rep in range(3 if graphs else 1):
+            run = T.Run(ctx, g, mc, tc, 0, 90, use_graphs=graphs)
+            run.step(run.barriers)
+            res[(graphs, rep)] = (run.losses(), run.params())
+            run.close()
+    for rep in range(3):
+        assert np.array_equal(res[(True, rep)][0], res[(False, 0)][0])
+        assert np.array_equal(res[(True, rep)][1], res[(False, 0)][1])
+
+
 def test_oplog_matches_reference(ctx, tmp_path):
     """(1,1,1) graph-mode run: the daemon op-log (oplog.hpp) equals the reference
     run_training's, byte for byte, and passes validate_oplog."""
