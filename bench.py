@@ -372,15 +372,23 @@ def main():
     ctx.synchronize()
     tw0 = time.perf_counter()
     first_e2e = run.next
+    def ingest(x):
+        nonlocal_h2d = 0
+        if x < args.e2e_steps and sched["active"][x]:
+            b0, b1 = int(sched["slice_begin"][x]), int(sched["slice_end"][x])
+            n = b1 - b0
+            if n > 0:
+                o = b0 - w_lo
+                g.ingest(b0, p_src[o:o + n], p_dst[o:o + n], p_t[o:o + n], p_f[o:o + n])
+                nonlocal_h2d = n * (4 + 4 + 8 + 4 * d_e)
+        return nonlocal_h2d
+
+    # per step: H2D of the step's events (copy stream, one step ahead: barrier
+    # x plans barrier x + 1, so x + 1's events must be resident before it),
+    # the barrier, the D2H of its loss; the host runs ahead, one sync at the end
+    h2d += ingest(0)
     for x in range(args.e2e_steps):
-        # per step: H2D of the step's events (async, stream-ordered), the
-        # barrier, the D2H of its loss; the host runs ahead, one sync at the end
-        b0, b1 = int(sched["slice_begin"][x]), int(sched["slice_end"][x])
-        n = b1 - b0
-        if sched["active"][x] and n > 0:
-            o = b0 - w_lo
-            g.ingest(b0, p_src[o:o + n], p_dst[o:o + n], p_t[o:o + n], p_f[o:o + n])
-            h2d += n * (4 + 4 + 8 + 4 * d_e)
+        h2d += ingest(x + 1)
         run.step(1)
         run.loss_async(run.next - 1, p_loss[x:x + 1])
     ctx.synchronize()

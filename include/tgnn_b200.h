@@ -193,7 +193,8 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count);
 int tgnn_run_losses(tgnn_run* r, int64_t first, int64_t count, double* out);
 int tgnn_run_params(tgnn_run* r, double* flat);
 /* Enqueue (no sync) the D2H copy of this rank's loss of barrier b into dst
- * (pinned host memory); valid after the next synchronisation. */
+ * (pinned host memory) on the context's read-back stream, after the barrier's
+ * loss is written; valid after the next tgnn_ctx_synchronize. */
 int tgnn_run_loss_async(tgnn_run* r, int64_t b, double* dst);
 /* MetricsRow list (ref trainer.hpp:562-570, one row per eval barrier reached
  * so far, rank 0 evaluates with its device weights as run_training does,
@@ -248,7 +249,10 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
  * Streaming ingestion: (re)writes events [first, first+count) of a device
  * graph from host buffers (src/dst/t must match the finalized order; edge
  * features float32 [count x d_e]). Used to stream feature windows and by the
- * end-to-end measurement. Pinned buffers make the copies asynchronous. */
+ * end-to-end measurement. Pinned buffers make the copies asynchronous: they
+ * run on the context's copy stream, overlap work enqueued before the call
+ * (which never reads events past its own barrier) and are ordered before any
+ * work enqueued after it. */
 int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t* src,
                       const int32_t* dst, const double* t, const float* efeat);
 /* Debug: timing (us per launch) of the tcgen05 engine on an M x N x K

@@ -150,6 +150,10 @@ struct tgnn_ctx {
   cudaStream_t aux = nullptr;   // next barrier's plan / read, overlapped with this barrier's step
   cudaStream_t br = nullptr;    // leaves of the step (gradient zeroing, root writes, loss)
   cudaStream_t edge = nullptr;  // per-pair edge projection, overlapped with the GRU
+  cudaStream_t h2d = nullptr;   // event ingestion (copy engine), overlapped with earlier work
+  cudaEvent_t ev_h2d = nullptr;
+  cudaStream_t d2h = nullptr;   // asynchronous result reads, off the compute stream
+  cudaEvent_t ev_d2h = nullptr;
   int* d_flag = nullptr;
 
   void check_numeric() {
@@ -1275,6 +1279,10 @@ int tgnn_ctx_create(int device, tgnn_ctx** out) {
   TGB_CUDA(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo_prio));
   TGB_CUDA(cudaStreamCreateWithPriority(&c->br, cudaStreamNonBlocking, lo_prio));
   TGB_CUDA(cudaStreamCreateWithPriority(&c->edge, cudaStreamNonBlocking, lo_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->h2d, cudaStreamNonBlocking, hi_prio));
+  TGB_CUDA(cudaEventCreateWithFlags(&c->ev_h2d, cudaEventDisableTiming));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->d2h, cudaStreamNonBlocking, lo_prio));
+  TGB_CUDA(cudaEventCreateWithFlags(&c->ev_d2h, cudaEventDisableTiming));
   c->d_flag = dalloc<int>(1);
   TGB_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
   *out = c;
@@ -1291,6 +1299,12 @@ int tgnn_ctx_destroy(tgnn_ctx* ctx) {
   cudaStreamSynchronize(ctx->aux);
   cudaStreamSynchronize(ctx->br);
   cudaStreamSynchronize(ctx->edge);
+  cudaStreamSynchronize(ctx->h2d);
+  cudaStreamSynchronize(ctx->d2h);
+  cudaEventDestroy(ctx->ev_h2d);
+  cudaEventDestroy(ctx->ev_d2h);
+  cudaStreamDestroy(ctx->h2d);
+  cudaStreamDestroy(ctx->d2h);
   cudaStreamDestroy(ctx->aux);
   cudaStreamDestroy(ctx->br);
   cudaStreamDestroy(ctx->edge);
@@ -1304,6 +1318,7 @@ int tgnn_ctx_destroy(tgnn_ctx* ctx) {
 int tgnn_ctx_synchronize(tgnn_ctx* ctx) {
   API_BEGIN
   TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->d2h));  // asynchronous result reads
   API_END
 }
 
@@ -2307,7 +2322,10 @@ int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t
   tgnn_ctx* ctx = g->ctx;
   ctx->use();
   TGB_REQUIRE(first >= 0 && count >= 0 && first + count <= g->d.E, kConfig, "ingest: range out of bounds");
-  cudaStream_t s = ctx->stream;
+  // copies on the ingestion stream: they overlap work enqueued earlier (which
+  // never reads events past its own barrier) and are ordered before any work
+  // enqueued after this call
+  cudaStream_t s = ctx->h2d;
   h2d(g->d.src + first, src, static_cast<size_t>(count), s);
   h2d(g->d.dst + first, dst, static_cast<size_t>(count), s);
   h2d(g->d.t + first, t, static_cast<size_t>(count), s);
@@ -2320,6 +2338,8 @@ int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t
                                  cudaMemcpyHostToDevice, s));
     }
   }
+  TGB_CUDA(cudaEventRecord(ctx->ev_h2d, s));
+  TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_h2d, 0));
   API_END
 }
 
@@ -2603,7 +2623,11 @@ int tgnn_run_loss_async(tgnn_run* r, int64_t b, double* dst) {
   API_BEGIN
   r->ctx->use();
   TGB_REQUIRE(b >= 0 && b < r->next_barrier, kConfig, "run: loss of a barrier not yet enqueued");
-  TGB_CUDA(cudaMemcpyAsync(dst, r->d_losses + b, sizeof(double), cudaMemcpyDeviceToHost, r->ctx->stream));
+  // on the read-back stream once the barrier's loss is written: the compute
+  // stream never waits for the copy (tgnn_ctx_synchronize joins it)
+  TGB_CUDA(cudaEventRecord(r->ctx->ev_d2h, r->ctx->stream));
+  TGB_CUDA(cudaStreamWaitEvent(r->ctx->d2h, r->ctx->ev_d2h, 0));
+  TGB_CUDA(cudaMemcpyAsync(dst, r->d_losses + b, sizeof(double), cudaMemcpyDeviceToHost, r->ctx->d2h));
   API_END
 }
 
