@@ -236,6 +236,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--e2e-chunk", type=int, default=4, help="barriers per run.step call in the e2e loop")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--cpu-baseline-steps", type=int, default=3)
     ap.add_argument("--ref-max-steps", type=int, default=12)
@@ -385,12 +386,19 @@ def main():
 
     # per step: H2D of the step's events (copy stream, one step ahead: barrier
     # x plans barrier x + 1, so x + 1's events must be resident before it),
-    # the barrier, the D2H of its loss; the host runs ahead, one sync at the end
+    # the barrier, the D2H of its loss; the host runs ahead, one sync at the
+    # end. Barriers are enqueued --e2e-chunk at a time (one graph launch), each
+    # with its own ingestion call before and its own loss read after.
     h2d += ingest(0)
-    for x in range(args.e2e_steps):
-        h2d += ingest(x + 1)
-        run.step(1)
-        run.loss_async(run.next - 1, p_loss[x:x + 1])
+    x = 0
+    while x < args.e2e_steps:
+        c = min(args.e2e_chunk, args.e2e_steps - x)
+        for y in range(x + 1, x + c + 1):
+            h2d += ingest(y)
+        run.step(c)
+        for y in range(x, x + c):
+            run.loss_async(run.next - c + (y - x), p_loss[y:y + 1])
+        x += c
     ctx.synchronize()
     assert np.all(np.isfinite(p_loss))
     e2e_s = time.perf_counter() - tw0
