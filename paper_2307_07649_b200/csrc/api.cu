@@ -527,7 +527,7 @@ struct tgnn_run {
   int64_t prepared = -1;  // barrier whose plan + read view are ready in plans/views[b % 2]
   cudaEvent_t ev_fork = nullptr, ev_written = nullptr, ev_next = nullptr;
   cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
-  cudaEvent_t ev_red = nullptr;
+  cudaEvent_t ev_red = nullptr, ev_artail = nullptr, ev_upd = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
   // daemon op-log records [barriers x 4] (R first, R len, W first, W len)
   bool oplog = false;
@@ -567,7 +567,7 @@ struct tgnn_run {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_written) cudaEventDestroy(ev_written);
     if (ev_next) cudaEventDestroy(ev_next);
-    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin, ev_edge, ev_red};
+    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin, ev_edge, ev_red, ev_artail, ev_upd};
     for (cudaEvent_t e : more)
       if (e) cudaEventDestroy(e);
     if (d_desc) cudaFree(d_desc);
@@ -772,13 +772,20 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
   const int64_t split = (tr->L.off[tWq] + 3) / 4 * 4;
   TGB_CUDA(cudaStreamWaitEvent(c, r->ev_tail, 0));
   if (c != r->ctx->br) TGB_CUDA(cudaStreamWaitEvent(c, r->ev_brjoin, 0));  // the branch's tail gradients
+  cudaStream_t u = c;  // the tail update
   if (r->nranks > 1) {
     if (r->peer_ok) peer_allreduce_launch(r->peer, split, tr->L.total - split, r->d_ctr, 0, c);
     else NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),
                                           ncclFloat, ncclSum, r->comm, c));
+    // the tail Adam on the (idle by now) branch stream, so the head bucket's
+    // all-reduce does not queue behind it on the comm stream
+    TGB_CUDA(cudaEventRecord(r->ev_artail, c));
+    TGB_CUDA(cudaStreamWaitEvent(r->ctx->br, r->ev_artail, 0));
+    u = r->ctx->br;
   }
-  adam_pack_launch(sc, tr->am, tr->av, c, r->d_desc, r->d_ctr, split, tr->L.total);
+  adam_pack_launch(sc, tr->am, tr->av, u, r->d_desc, r->d_ctr, split, tr->L.total);
   if (r->nranks > 1) {
+    TGB_CUDA(cudaEventRecord(r->ev_upd, u));
     TGB_CUDA(cudaEventRecord(r->ev_head, s));
     TGB_CUDA(cudaStreamWaitEvent(c, r->ev_head, 0));
     if (r->peer_ok) peer_allreduce_launch(r->peer, 0, split, r->d_ctr, 1, c);
@@ -786,6 +793,7 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
     adam_pack_launch(sc, tr->am, tr->av, c, r->d_desc, r->d_ctr, 0, split);
     TGB_CUDA(cudaEventRecord(r->ev_comm, c));
     TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
+    TGB_CUDA(cudaStreamWaitEvent(s, r->ev_upd, 0));
   } else {
     adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr, 0, split);
     TGB_CUDA(cudaEventRecord(r->ev_comm, c));
@@ -1027,7 +1035,8 @@ void build_graph(tgnn_run* r) {
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming));
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_written, cudaEventDisableTiming));
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
-    cudaEvent_t* more[] = {&r->ev_gru, &r->ev_gzero, &r->ev_dec, &r->ev_brjoin, &r->ev_edge, &r->ev_red};
+    cudaEvent_t* more[] = {&r->ev_gru,  &r->ev_gzero, &r->ev_dec,    &r->ev_brjoin,
+                           &r->ev_edge, &r->ev_red,   &r->ev_artail, &r->ev_upd};
     for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     cudaEvent_t* upd[] = {&r->ev_tail, &r->ev_head, &r->ev_comm};
     for (cudaEvent_t* e : upd)
