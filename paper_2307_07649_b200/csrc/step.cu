@@ -351,12 +351,31 @@ constexpr int kNbGroup = 4;     // neighbour rows loaded ahead of their use
 template <int LANES>
 __global__ void attn_fwd_kernel(Dims D, DPlan pl, float* Q, const float* __restrict__ KV, float* __restrict__ attn_a,
                                 float* __restrict__ H, int* flag, StepBf bf,
-                                const float* __restrict__ QKVn, const float* __restrict__ cq) {
+                                const float* __restrict__ QKVn, const float* __restrict__ cq, int cap_B2) {
   pdl_wait();
   pdl_trigger();
   const int R = pl.sizes[kSzR];
+  const int B = pl.sizes[kSzB];
   const int lane = threadIdx.x & 31;
   const int da = D.da;
+  // the decoder's pre-split input rows [h_src | h_other | 1] (positive row e,
+  // negative row B + e) are written here, as each root's h is produced
+  const bool hin = pl.rpe == 3 && bf.Hin.hi != nullptr;  // training plans only
+  auto put_hin = [&](int64_t r, int i, float v) {
+    if (!hin) return;
+    const int64_t e = r / 3;
+    const int side = static_cast<int>(r % 3);
+    if (side == 0) {
+      bf_put(bf.Hin, e, i, v);
+      bf_put(bf.Hin, B + e, i, v);
+      if (i == 0) {
+        bf_put(bf.Hin, e, 2 * da, 1.0f);
+        bf_put(bf.Hin, B + e, 2 * da, 1.0f);
+      }
+    } else {
+      bf_put(bf.Hin, side == 1 ? e : B + e, da + i, v);
+    }
+  };
   for (int64_t r = gwarp(); r < R; r += nwarp()) {
     const int n = pl.nbr_cnt[r];
     float* h = H + r * da;
@@ -364,6 +383,7 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, float* Q, const float* __restr
       for (int i = lane; i < da; i += 32) {
         h[i] = 0.0f;
         bf_put(bf.H, r, i, 0.0f);
+        put_hin(r, i, 0.0f);
       }
       continue;
     }
@@ -446,10 +466,12 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, float* Q, const float* __restr
       if (i < da) {
         h[i] = hv[c];
         bf_put(bf.H, r, i, hv[c]);
+        put_hin(r, i, hv[c]);
         flag_if_nonfinite(hv[c], flag);
       }
     }
   }
+  if (hin) bf_zero_tail(bf.Hin, 2 * B, cap_B2, 2 * da + 1);
 }
 
 __device__ __forceinline__ double softplus_d(double x) {
@@ -504,21 +526,15 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
     const float* hs = H + (3 * e) * da;
     const float* hd = H + (3 * e + 1) * da;
     const float* hn = H + (3 * e + 2) * da;
-    for (int i = lane; i < da; i += 32) {
-      if (Hin) {
+    // (the pre-split rows bf.Hin come from attn_fwd_kernel; the fp32 copy
+    // feeds the fp32-operand engines)
+    if (Hin) {
+      for (int i = lane; i < da; i += 32) {
         Hin[e * 2 * da + i] = hs[i];
         Hin[e * 2 * da + da + i] = hd[i];
         Hin[(B + e) * 2 * da + i] = hs[i];
         Hin[(B + e) * 2 * da + da + i] = hn[i];
       }
-      bf_put(bf.Hin, e, i, hs[i]);
-      bf_put(bf.Hin, e, da + i, hd[i]);
-      bf_put(bf.Hin, B + e, i, hs[i]);
-      bf_put(bf.Hin, B + e, da + i, hn[i]);
-    }
-    if (lane == 0) {
-      bf_put(bf.Hin, e, 2 * da, 1.0f);
-      bf_put(bf.Hin, B + e, 2 * da, 1.0f);
     }
     if (lane == 0) {
       dlogit[e] = dpos;
@@ -532,7 +548,6 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
     }
   }
   bf_zero_tail(bf.Dhid, 2 * B, cap_B2, dh);
-  bf_zero_tail(bf.Hin, 2 * B, cap_B2, 2 * da + 1);
 }
 
 // bce_loss: mean softplus(-pos) + mean softplus(neg), fixed-order f64 reduction.
@@ -1838,7 +1853,7 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
     auto fwd = lanes <= 1 ? attn_fwd_kernel<1> : lanes <= 2 ? attn_fwd_kernel<2>
              : lanes <= 4 ? attn_fwd_kernel<4> : attn_fwd_kernel<8>;
     launch_pdl(fwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag,
-               bfx, tma ? w.QKVn : nullptr, w.cq);
+               bfx, tma ? w.QKVn : nullptr, w.cq, 2 * w.cap_B);
   }
 }
 
