@@ -801,6 +801,8 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
   }
 }
 
+void barrier_body_slot(tgnn_run* r, int p, bool xg_split);
+
 // Graph body (j == 1): the same launch sequence for every barrier; all
 // per-barrier values come from d_desc[*d_ctr]. Barrier b runs on slot p =
 // b % 2 (plan + read view prepared by the previous barrier) and prepares
@@ -810,8 +812,25 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
 void barrier_body_dev(tgnn_run* r, int p) {
   tgnn_ctx* ctx = r->ctx;
   tgnn_trainer* tr = r->tr.get();
+  // slot p's GRU input operand is w.bf.Xg while this body is enqueued (the
+  // other slot's, w.xg_alt, is pre-assembled for the next barrier on aux)
+  const bool xg_split = gemm_impl() == kGemmTma && tr->w.xg_alt.valid();
+  if (xg_split && p == 1) std::swap(tr->w.bf.Xg, tr->w.xg_alt);
+  try {
+    barrier_body_slot(r, p, xg_split);
+  } catch (...) {
+    if (xg_split && p == 1) std::swap(tr->w.bf.Xg, tr->w.xg_alt);
+    throw;
+  }
+  if (xg_split && p == 1) std::swap(tr->w.bf.Xg, tr->w.xg_alt);
+}
+
+void barrier_body_slot(tgnn_run* r, int p, bool xg_split) {
+  tgnn_ctx* ctx = r->ctx;
+  tgnn_trainer* tr = r->tr.get();
   cudaStream_t s = ctx->stream, aux = ctx->aux;
   StepCtx sc = tr->sc();
+  sc.xg_pre = xg_split;
   sc.d_ctr = r->d_ctr;
   sc.packed = true;  // by the previous barrier's Adam (or the prologue)
   sc.marks = r->marks.on ? &r->marks : nullptr;  // profiling graph only
@@ -882,6 +901,7 @@ void barrier_body_dev(tgnn_run* r, int p) {
     TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_written, 0));
     reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, aux, 1);
     gather_view_launch(nx, r->mem->d, nv, aux);
+    if (xg_split) assemble_gru_view_launch(sc, nx, nv, tr->w.xg_alt, aux);
     TGB_CUDA(cudaStreamWaitEvent(aux, nx.ev_sorted, 0));
     TGB_CUDA(cudaEventRecord(r->ev_next, aux));
     sc.ev_tail_grads = r->ev_tail;
@@ -1092,6 +1112,9 @@ void prepare_barrier(tgnn_run* r, int64_t b) {
   select_plan_args_launch(pl.args, r->d_desc, r->d_ctr, s, 0);
   plan_launch(r->g->d, pl, s, ctx->side);
   gather_view_launch(pl, r->mem->d, tr->views[static_cast<size_t>(b & 1)], s);
+  if (gemm_impl() == kGemmTma && tr->w.xg_alt.valid())  // the graph body assembles only the time columns
+    assemble_gru_view_launch(tr->sc(), pl, tr->views[static_cast<size_t>(b & 1)],
+                             (b & 1) ? tr->w.xg_alt : tr->w.bf.Xg, s);
   TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));
   pack_weights(tr->sc(), s);
   r->prepared = b;

@@ -180,6 +180,51 @@ __global__ void assemble_gru_kernel(Dims D, DPlan pl, DView vw, DGraph g, const 
   bf_zero_tail(bf.GU, U, cap_U, D.dt);
 }
 
+// Split form of assemble_gru_kernel for the graph pipeline: the view columns
+// (here, on the aux stream, ahead of the barrier) ...
+__global__ void assemble_gru_view_kernel(Dims D, DPlan pl, DView vw, DGraph g, BfMat xg, int cap_U, int stage) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float sbuf[];
+  const int U = pl.sizes[kSzU];
+  const int lane = threadIdx.x & 31;
+  float* row = sbuf + (threadIdx.x >> 5) * stage;
+  for (int64_t u = gwarp(); u < U; u += nwarp()) {
+    const int32_t ev = vw.mail_ev[u];
+    const bool has = ev >= 0;
+    for (int x = lane; x < 2 * D.d; x += 32) row[x] = vw.mail_mem[u * 2 * D.d + x];
+    for (int i = lane; i < D.dt; i += 32) row[2 * D.d + i] = 0.0f;  // time columns: written in the step
+    const float* ef = has ? g.efeat + static_cast<int64_t>(ev) * D.de_pad : nullptr;
+    for (int x = lane; x < D.de; x += 32) row[2 * D.d + D.dt + x] = has ? ef[x] : 0.0f;
+    for (int x = lane; x < D.d; x += 32) row[D.md + x] = vw.mem[u * D.d + x];
+    if (lane == 0) row[D.gin] = 1.0f;
+    __syncwarp();
+    warp_store_row(xg, u, row, D.gin + 1, nullptr, 0);
+    __syncwarp();
+  }
+  bf_zero_tail(xg, U, cap_U, D.gin + 1);
+}
+
+// ... and the time-encoding columns cos(dt w) and GU = -dt sin(dt w) in the
+// step (they depend on omega, updated by the previous barrier's Adam).
+__global__ void assemble_gru_time_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ omega, StepBf bf,
+                                         int cap_U) {
+  pdl_wait();
+  pdl_trigger();
+  const int U = pl.sizes[kSzU];
+  const int64_t total = static_cast<int64_t>(U) * D.dt;
+  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t u = x / D.dt;
+    const int i = static_cast<int>(x % D.dt);
+    const double dt = vw.mail_dt[u];
+    float sn, cs;
+    time_sincos(dt, omega[i], &sn, &cs);
+    bf_put(bf.Xg, u, 2 * D.d + i, cs);
+    bf_put(bf.GU, u, i, vw.mail_ev[u] >= 0 ? static_cast<float>(-dt) * sn : 0.0f);
+  }
+  bf_zero_tail(bf.GU, U, cap_U, D.dt);
+}
+
 // z, r = sigmoid(gates + b) (bias already added by the GEMM); RS = r * s.
 __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
                                float* __restrict__ RS, StepBf bf, int cap_U) {
@@ -1499,6 +1544,7 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
     b.d8d = static_cast<int>((d + 7) / 8 * 8);
     const int64_t md = m.mail_dim(), ds = m.d_static;
     b.Xg = bf_alloc(U, gin + 1);
+    if (!fwd_only) w.xg_alt = bf_alloc(U, gin + 1);
     b.GU = bf_alloc(U, std::max<int64_t>(dt, 1));
     b.RS = bf_alloc(U, d + 1);
     b.Qin = bf_alloc(R, q + 1);
@@ -1596,7 +1642,7 @@ void step_free(StepWork& w) {
   BfMat* bfs[] = {&w.bf.Xg, &w.bf.GU, &w.bf.RS, &w.bf.Qin, &w.bf.KVin, &w.bf.Gt, &w.bf.H, &w.bf.Hin,
                   &w.bf.Dhid, &w.bf.dQ, &w.bf.dKV, &w.bf.dNA, &w.bf.Dg, &w.bf.Wzr, &w.bf.Whm, &w.bf.Whs,
                   &w.bf.Wq, &w.bf.Wkv, &w.bf.W1a, &w.bf.W1b, &w.bf.W1, &w.bf.Wst, &w.bf.NF,
-                  &w.bf.EF, &w.bf.Wkve};
+                  &w.bf.EF, &w.bf.Wkve, &w.xg_alt};
   for (BfMat* b : bfs) bf_free(*b);
   w = StepWork{};
 }
@@ -1744,7 +1790,9 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   // ---- GRU freshen (K5)
   c.mark(phGruFwd, s);
   if (tma && !c.packed) pack_weights_launch(c, s);
-  {
+  if (tma && c.xg_pre) {
+    launch_pdl(assemble_gru_time_kernel, dim3(4 * kSMs), dim3(256), 0, s, D, pl, vw, P + L.off[tOmega], bfx, U);
+  } else {
     const int stage = (D.gin + 1 + D.dt + 7) / 8 * 8;
     launch_pdl(assemble_gru_kernel, dim3(row_blocks(U)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, 
         D, pl, vw, g, P + L.off[tOmega], tma ? nullptr : w.Xg, w.ldx, w.GU, bfx, U, stage);
@@ -1776,6 +1824,15 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   }
   launch_pdl(gru_out_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, w.s_hat, c.d_numeric_flag,
              P + L.off[tStatic], bfx, U);
+  TGB_CUDA(cudaGetLastError());
+}
+
+void assemble_gru_view_launch(const StepCtx& c, const DPlan& pl, const DView& vw, const BfMat& xg,
+                              cudaStream_t s) {
+  const Dims D = make_dims(c.m, *c.g);
+  const int stage = (D.gin + 1 + 7) / 8 * 8;
+  launch_pdl(assemble_gru_view_kernel, dim3(row_blocks(c.w->cap_U)), dim3(32 * kWarps), sizeof(float) * stage * kWarps,
+             s, D, pl, vw, *c.g, xg, c.w->cap_U, stage);
   TGB_CUDA(cudaGetLastError());
 }
 

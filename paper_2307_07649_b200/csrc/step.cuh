@@ -68,6 +68,7 @@ struct StepWork {
   float *dKV = nullptr, *dNodeAcc = nullptr, *dNode = nullptr, *Dg = nullptr, *T1 = nullptr;
   float *DMT = nullptr, *Mom = nullptr, *omega_part = nullptr, *ones = nullptr;
   float *QKVn = nullptr, *cq = nullptr;
+  BfMat xg_alt;  // second GRU-input operand: graph slots alternate (bf.Xg is the current one)
   float* omega_att = nullptr;  // attention part of the omega gradient [d_t]  // node parts [U, 3 d8a]; query constant W_q,t 1 + b_q [d_a]
   double* loss_terms = nullptr;
   float* splitk_ws = nullptr;
@@ -128,6 +129,9 @@ struct StepCtx {
   // gradient there (ev_br_dec -> ev_br_join), off the critical path.
   cudaStream_t br = nullptr;
   bool packed = false;  // the TMA weight operands are current (packed by the fused Adam)
+  // the GRU input operand's view-only columns were assembled ahead (on the aux
+  // stream, assemble_gru_view_launch): only the time-encoding columns remain
+  bool xg_pre = false;
   // Graph mode: the per-pair edge half of the attention projection was
   // enqueued on another stream (attn_edge_launch); wait for ev_edge first.
   cudaEvent_t ev_edge = nullptr;
@@ -143,6 +147,11 @@ struct StepCtx {
 void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t num_nodes, int rpe = 3,
                 bool fwd_only = false);
 void step_free(StepWork& w);
+// The view-dependent columns {mail_mem | . | e(mail event) | s | 1} of the GRU
+// input operand xg for a prepared plan and read view (everything but the
+// time encoding, which depends on omega and is written in the step).
+void assemble_gru_view_launch(const StepCtx& c, const DPlan& pl, const DView& vw, const BfMat& xg,
+                              cudaStream_t s);
 
 // Forward + backward of one sub-iteration on (plan, view). Writes the loss to
 // *loss_out (device double) and the flat gradient (grads zeroed first).
