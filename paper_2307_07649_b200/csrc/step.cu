@@ -1409,13 +1409,17 @@ void add_nn(GemmGroup& gg, int Mcap, const int* M_dev, int N, int K, Operand a, 
 
 Operand ones_op(const float* ones, int K) { return op_dense(ones, 0, 0, K); }
 
-// ~32 CTAs per weight-gradient problem (a group runs 4-5 of them at once) and
-// >= 512 reduction rows of capacity per split, which keeps the fp32 partial
-// traffic of the deterministic split-K reduction small next to the MMA work.
+// ~48 CTAs per weight-gradient problem (a group runs 3-5 of them at once)
+// and >= 128 reduction rows of capacity per split: the per-CTA k-chain, not
+// the fp32 partial traffic, bounds these latency-bound groups (A/B sweep on
+// B200 at C2: 32 / 512 -> 48 / 128 is +3.6 %). TGNN_SK_T / _R / _C override.
 int choose_splits_tma(int M, int N, int64_t Kcap) {
+  static const int target = [] { const char* e = std::getenv("TGNN_SK_T"); return e ? std::atoi(e) : 48; }();
+  static const int rows = [] { const char* e = std::getenv("TGNN_SK_R"); return e ? std::atoi(e) : 128; }();
   const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
-  int64_t s = std::min<int64_t>(ceil_div(32, tiles), ceil_div(Kcap, 512));
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 32)));
+  int64_t s = std::min<int64_t>(ceil_div(target, tiles), ceil_div(Kcap, rows));
+  static const int cap = [] { const char* e = std::getenv("TGNN_SK_C"); return e ? std::atoi(e) : 32; }();
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, cap)));
 }
 
 // Forward-style problem: A K-major [M x K] (runtime rows M_dev), B K-major [N x K].
