@@ -44,7 +44,7 @@ ParamLayout ParamLayout::make(const ModelDims& m) {
 
 namespace {
 
-constexpr int kWarps = 8;  // warps per block for row kernels
+static const int kWarps = [] { const char* e = std::getenv("TGNN_KW"); return e ? std::atoi(e) : 4; }();  // warps per block for row kernels (TGNN_KW; A/B: 4 > 8 > 2)
 constexpr int kChunk = 32; // routing chunk (items)
 constexpr int kOmegaRows = 256;
 
@@ -1814,7 +1814,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
            3 * d, P + L.off[tBh]);
     gemm_group_launch(gg, s);
   }
-  const int eblocks = 4 * kSMs;
+  static const int eblocks = [] { const char* e = std::getenv("TGNN_EB"); return e ? std::atoi(e) : 4; }() * kSMs;  // elementwise grid (TGNN_EB x SMs)
   launch_pdl(gru_mid_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, tma ? nullptr : w.RS, bfx, U);
   if (tma) {
     TcGroup tg;  // Gh += [r*s | 1] [Wh_s | bh]^T  (the bias rides the ones column)
@@ -1941,7 +1941,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   const StepBf& B = w.bf;
 
   if (!c.br) TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));  // else zeroed on the branch
-  const int eblocks = 4 * kSMs;
+  static const int eblocks = [] { const char* e = std::getenv("TGNN_EB"); return e ? std::atoi(e) : 4; }() * kSMs;  // elementwise grid (TGNN_EB x SMs)
 
   attn_forward_launch(c, pl, s);
 
