@@ -527,7 +527,7 @@ struct tgnn_run {
   int64_t prepared = -1;  // barrier whose plan + read view are ready in plans/views[b % 2]
   cudaEvent_t ev_fork = nullptr, ev_written = nullptr, ev_next = nullptr;
   cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
-  cudaEvent_t ev_red = nullptr, ev_artail = nullptr, ev_upd = nullptr;
+  cudaEvent_t ev_red = nullptr, ev_artail = nullptr, ev_upd = nullptr, ev_mid = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
   // daemon op-log records [barriers x 4] (R first, R len, W first, W len)
   bool oplog = false;
@@ -567,7 +567,7 @@ struct tgnn_run {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_written) cudaEventDestroy(ev_written);
     if (ev_next) cudaEventDestroy(ev_next);
-    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin, ev_edge, ev_red, ev_artail, ev_upd};
+    cudaEvent_t more[] = {ev_gru, ev_gzero, ev_dec, ev_brjoin, ev_edge, ev_red, ev_artail, ev_upd, ev_mid};
     for (cudaEvent_t e : more)
       if (e) cudaEventDestroy(e);
     if (d_desc) cudaFree(d_desc);
@@ -898,14 +898,24 @@ void barrier_body_slot(tgnn_run* r, int p, bool xg_split) {
     }
     // join: the next barrier reads the memory copy once this barrier's writes landed
     TGB_CUDA(cudaEventRecord(r->ev_written, ws));
-    TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_written, 0));
-    reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, aux, 1);
-    gather_view_launch(nx, r->mem->d, nv, aux);
-    if (xg_split) assemble_gru_view_launch(sc, nx, nv, tr->w.xg_alt, aux);
-    TGB_CUDA(cudaStreamWaitEvent(aux, nx.ev_sorted, 0));
-    TGB_CUDA(cudaEventRecord(r->ev_next, aux));
+    // the next read (reset, gather, GRU-input view columns) starts after this
+    // barrier's decoder, not beside its projections (TGNN_AUXMID; A/B: 1 best)
+    static const int mid_at = [] { const char* e = std::getenv("TGNN_AUXMID"); return e ? std::atoi(e) : 1; }();
+    auto next_read = [&] {
+      TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_written, 0));
+      if (mid_at > 0) TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_mid, 0));
+      reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, aux, 1);
+      gather_view_launch(nx, r->mem->d, nv, aux);
+      if (xg_split) assemble_gru_view_launch(sc, nx, nv, tr->w.xg_alt, aux);
+      TGB_CUDA(cudaStreamWaitEvent(aux, nx.ev_sorted, 0));
+      TGB_CUDA(cudaEventRecord(r->ev_next, aux));
+    };
+    if (mid_at == 0) next_read();
     sc.ev_tail_grads = r->ev_tail;
+    sc.ev_mid = mid_at > 0 ? r->ev_mid : nullptr;
+    sc.mid_at = mid_at;
     substep_rest_launch(sc, pl, vw, r->d_losses, s);
+    if (mid_at > 0) next_read();
     sc.mark(phAdam, s);
     update_split(r, sc, s);
     TGB_CUDA(cudaStreamWaitEvent(s, r->ev_next, 0));
@@ -1056,7 +1066,7 @@ void build_graph(tgnn_run* r) {
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_written, cudaEventDisableTiming));
     TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
     cudaEvent_t* more[] = {&r->ev_gru,  &r->ev_gzero, &r->ev_dec,    &r->ev_brjoin,
-                           &r->ev_edge, &r->ev_red,   &r->ev_artail, &r->ev_upd};
+                           &r->ev_edge, &r->ev_red,   &r->ev_artail, &r->ev_upd, &r->ev_mid};
     for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     cudaEvent_t* upd[] = {&r->ev_tail, &r->ev_head, &r->ev_comm};
     for (cudaEvent_t* e : upd)

@@ -1962,6 +1962,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   launch_pdl(decoder_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s, 
       D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, tma ? nullptr : w.Dhid,
       tma ? nullptr : w.Hin, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
+  if (c.ev_mid && c.mid_at == 1) TGB_CUDA(cudaEventRecord(c.ev_mid, s));
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
   c.mark(phDecoderBwd, s);
   {
@@ -2006,6 +2007,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     launch_pdl(bwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV, bfx, R, Pc,
                tma ? w.QKVn : nullptr);
   }
+  if (c.ev_mid && c.mid_at == 2) TGB_CUDA(cudaEventRecord(c.ev_mid, s));
   if (pl.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));  // routing CSR ready
   const int64_t nchunks = ceil_div(R + Pc, kChunk) + 1;
   float* part_first = wc.take(static_cast<size_t>(nchunks) * 3 * da);
@@ -2037,6 +2039,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     }
     if (dt > 0) tc_tn(tg, wc, B.d8a + da, dt, Pc, szP, B.dKV, 0, B.Gt, 0, w.Mom, dt);
     tc_group_launch(tg, s, c.br, c.ev_red);
+    if (c.ev_mid && c.mid_at == 3) TGB_CUDA(cudaEventRecord(c.ev_mid, s));
   } else {
     GemmGroup gg;
     Operand bs;

@@ -132,6 +132,11 @@ struct StepCtx {
   // the GRU input operand's view-only columns were assembled ahead (on the aux
   // stream, assemble_gru_view_launch): only the time-encoding columns remain
   bool xg_pre = false;
+  // graph pipeline: ev_mid is recorded on the main stream at point mid_at (1
+  // after the decoder, 2 after the attention backward kernel, 3 after the
+  // attention backward GEMMs); the next barrier's read starts after it
+  cudaEvent_t ev_mid = nullptr;
+  int mid_at = 0;
   // Graph mode: the per-pair edge half of the attention projection was
   // enqueued on another stream (attn_edge_launch); wait for ev_edge first.
   cudaEvent_t ev_edge = nullptr;
