@@ -85,7 +85,7 @@ def step_model_flops(sz, cfg):
 def roofline_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of the roofline kernel from
     the committed ncu --set full capture (profiles/), per launch."""
-    p = os.path.join(ROOT, "profiles", "r01c_roofline_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r01f_roofline_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
