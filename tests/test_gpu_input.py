@@ -94,3 +94,40 @@ def test_load_dataset_matches_reference(ctx, tmp_path):
         assert np.array_equal(a[x], b[x])
     assert np.array_equal(g.edge_feats(), b[3].astype(np.float32))
     _sampler_equal(g, back, np.random.default_rng(2))
+
+
+def test_ingest_is_ordered_before_later_work(ctx):
+    """tgnn_graph_ingest copies on the context's copy stream: work enqueued
+    after the call must see the new rows. Overwriting a window of edge
+    features and training gives bitwise the run of a graph built with them."""
+    kw = dict(nodes=300, events=6000, d_e=5, seed=11)
+    g1 = T.TemporalGraph.synthetic(ctx, T.SynthParams(**kw))
+    src, dst, t = g1.events()
+    ef = g1.edge_feats().astype(np.float64)
+    a, b = 1500, 3900
+    ef2 = ef.copy()
+    ef2[a:b] = -0.5 * ef2[a:b] + 0.25
+    g2 = T.TemporalGraph(ctx, g1.num_nodes, g1.boundary, src, dst, t, ef2)
+    n = b - a
+    p_src = T.pinned_empty((n,), np.int32)
+    p_dst = T.pinned_empty((n,), np.int32)
+    p_t = T.pinned_empty((n,), np.float64)
+    p_f = T.pinned_empty((n, 5), np.float32)
+    p_src[:] = src[a:b]
+    p_dst[:] = dst[a:b]
+    p_t[:] = t[a:b]
+    p_f[:] = ef2[a:b].astype(np.float32)
+    mc = T.ModelConfig(d_mem=16, d_time=8, d_static=4, d_attn=16, d_hidden=8, d_e=5, n_neighbors=5,
+                       num_nodes=g1.num_nodes, max_t=float(t[-1]))
+    tc = T.TrainConfig(local_batch=200, lr_base=1e-3, seed=2, epochs=1)
+    res = []
+    for g, ingest in ((g1, True), (g2, False)):
+        if ingest:
+            g.ingest(a, p_src, p_dst, p_t, p_f)  # no sync: the run below is ordered after it
+        run = T.Run(ctx, g, mc, tc, 0, 4200)
+        run.step(run.barriers)
+        res.append((run.losses(), run.params()))
+        run.close()
+    assert np.array_equal(g1.edge_feats(), ef2.astype(np.float32))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
