@@ -384,7 +384,7 @@ __global__ void assemble_attn_kernel(Dims D, DPlan pl, DGraph g, const float* __
 }
 
 constexpr int kMaxDaLanes = 8;  // d_attn <= 256
-constexpr int kNbGroup = 4;     // neighbour rows loaded ahead of their use
+constexpr int kNbGroup = 8;     // neighbour rows loaded ahead of their use
 
 // attention_forward (attention.hpp:36-91): scores q.K / sqrt(n), stable
 // softmax, h = sum a V; n = 0 gives h = 0. One warp per root; LANES = ceil(d_a
