@@ -794,7 +794,7 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
   const int nchunks = (items + kChunk - 1) / kChunk;
   const int lane = threadIdx.x & 31;
   const int da = D.da, w3 = 3 * D.da;
-  constexpr int kAhead = 16;
+  constexpr int kAhead = 4;  // item rows in flight per round (A/B: 4 > 8 > 16 > 24: registers buy residency)
   static_assert(kChunk == 32, "one sorted item per lane");
   for (int64_t gw = gwarp(); gw < 3ll * nchunks; gw += nwarp()) {
     const int64_t c = gw / 3;
