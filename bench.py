@@ -195,19 +195,34 @@ def reference_arm(args, world, rank, emit):
     # bound the sample: each reference barrier is several seconds of CPU work
     steps = min(args.steps, args.ref_max_steps)
     warm = min(args.warmup, 1)
-    value, secs, ev, threads = reference_time(cfg, world, steps, warm, log=lambda *a: print(*a, file=sys.stderr))
+    log = lambda *a: print(*a, file=sys.stderr)  # noqa: E731
+    # all the host cores: the reference's threaded trainer with one memory
+    # group (trainer + daemon thread) per two cores, at least one per GPU of
+    # the B200 arm, and no more than the mid-stream event window holds
+    n_ev = min(cfg["events"], REF_MAX_EVENTS)
+    room = (n_ev - int(n_ev * TRAIN_FRAC) // 2) // ((warm + steps) * LOCAL_BATCH)
+    groups = args.ref_groups or max(world, min(16, (os.cpu_count() or 2) // 2, room))
+    value, secs, ev, threads = reference_time(cfg, groups, steps, warm, log=log)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s",
         "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * secs / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference gen_synthetic, seed 1)",
-        "config": {"workload": cfg["workload"], "parallelism": f"(i,j,k)=(1,1,{world}) host threads",
-                   "global_batch": LOCAL_BATCH * world},
+        "config": {"workload": cfg["workload"],
+                   "parallelism": f"(i,j,k)=(1,1,{groups}) host threads (the B200 arm: (1,1,{world}), "
+                                  f"one trainer per GPU)",
+                   "global_batch": LOCAL_BATCH * groups, "host_cpus": os.cpu_count()},
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
-                         "sample": f"{steps} barriers x {world} x 600 events mid-stream, "
-                                   f"run_{'training' if world > 1 else 'sequential'} (oracle/_ref)"},
+                         "sample": f"{steps} barriers x {groups} x 600 events mid-stream, "
+                                   f"run_{'training' if groups > 1 else 'sequential'} (oracle/_ref)"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if groups != world:
+        # the reference at the B200 arm's own parallelism, for context
+        s1 = min(steps, 4)
+        v1, secs1, _, thr1 = reference_time(cfg, world, s1, warm, log=log)
+        line["same_parallelism"] = {"value": v1, "unit": "events/s", "cores": thr1,
+                                    "parallelism": f"(i,j,k)=(1,1,{world})", "steps": s1}
     emit(line)
     return 0
 
@@ -240,6 +255,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--cpu-baseline-steps", type=int, default=3)
     ap.add_argument("--ref-max-steps", type=int, default=12)
+    ap.add_argument("--ref-groups", type=int, default=0,
+                    help="reference arm memory groups (0: one per two host cores, >= n_gpus)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
