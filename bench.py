@@ -150,6 +150,9 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- reference (CPU) arm
+_REF_GRAPHS: dict = {}
+
+
 def reference_time(cfg, n_groups, barriers, warmup, log=print):
     """Times the unmodified reference (oracle/_ref, compiled from
     /root/reference/proj/include by oracle/Makefile) on this host's cores:
@@ -162,9 +165,12 @@ def reference_time(cfg, n_groups, barriers, warmup, log=print):
     # the generator is sequential, so a prefix of the stream is the full
     # stream's prefix: the f64 reference holds at most REF_MAX_EVENTS of it
     n_ev = min(cfg["events"], REF_MAX_EVENTS)
-    g = ref.RefGraph.synthetic(cfg["nodes"], n_ev, d_e=cfg["d_e"], seed=1)
-    _, _, t, _ = g.export(feats=False)
-    log(f"[ref] graph ready in {time.time() - t0:.1f}s")
+    key = (cfg["nodes"], n_ev, cfg["d_e"])
+    if key not in _REF_GRAPHS:  # one generated graph per workload and process
+        g = ref.RefGraph.synthetic(cfg["nodes"], n_ev, d_e=cfg["d_e"], seed=1)
+        _REF_GRAPHS[key] = (g, g.export(feats=False)[2])
+        log(f"[ref] graph ready in {time.time() - t0:.1f}s")
+    g, t = _REF_GRAPHS[key]
     mc = O.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(t[-1]), **model_dims(cfg))
     gb = LOCAL_BATCH
     mid = int(n_ev * TRAIN_FRAC) // 2
