@@ -1,7 +1,8 @@
 #!/bin/bash
 # A/B sweep of NCCL channel / protocol settings for the gradient all-reduce at
 # N GPUs (C2 bench, one line per setting). Usage: scripts/nccl_sweep.sh N OUTDIR
-N=${1:-2}; OUT=${2:-gpurun_out}
+# [tag:VAR=value ...] (no settings: the NCCL sweep below)
+N=${1:-2}; OUT=${2:-gpurun_out}; shift 2 2>/dev/null
 run() {
   local tag=$1; shift
   env "$@" timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$N" \
@@ -16,6 +17,10 @@ except Exception as e:
     print(sys.argv[2], "failed", e)
 PY
 }
+if [ $# -gt 0 ]; then
+  for kv in "$@"; do run "${kv%%:*}" "${kv#*:}"; done
+  exit 0
+fi
 run default X=1
 run minch16 NCCL_MIN_NCHANNELS=16
 run minch32 NCCL_MIN_NCHANNELS=32
