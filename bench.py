@@ -7,6 +7,9 @@ freshen -> attention -> decoder/BCE -> backward -> root writes -> gradient
 all-reduce -> Adam). N=1 runs BASELINE configs[1] (Reddit shape, TGN + static
 memory); N>1 runs the same workload with memory parallelism k=N, one GPU per
 trainer, weak scaling (epochs=N so every memory copy sweeps a full epoch).
+`--impl reference` (rank 0 only) times the unmodified reference trainer
+(oracle/_ref) on all the host cores: (1,1,G) with G = one memory group per two
+CPUs (>= N), plus its (1,1,N) number as `same_parallelism`.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 """
