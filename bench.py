@@ -7,9 +7,15 @@ freshen -> attention -> decoder/BCE -> backward -> root writes -> gradient
 all-reduce -> Adam). N=1 runs BASELINE configs[1] (Reddit shape, TGN + static
 memory); N>1 runs the same workload with memory parallelism k=N, one GPU per
 trainer, weak scaling (epochs=N so every memory copy sweeps a full epoch).
+--config c3 / c4 run BASELINE configs[2] / [3] with mini-batch (i=N) / epoch
+(j=N) parallelism instead; c5p / c5 the GDELT shape (5M prefix / full stream).
+The timed window is mid-stream: the run is fast-forwarded so the K timed
+barriers are centred on the middle of the schedule, where the CPU reference
+legs are timed as well; the line reports both windows.
 `--impl reference` (rank 0 only) times the unmodified reference trainer
-(oracle/_ref) on all the host cores: (1,1,G) with G = one memory group per two
-CPUs (>= N), plus its (1,1,N) number as `same_parallelism`.
+(oracle/_ref) on all the host cores: for k-parallel configs (1,1,G) with G =
+one memory group per two CPUs (>= N), plus its (1,1,N) number as
+`same_parallelism`; for c3 / c4 the B200 arm's own (i,j,k).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 """
@@ -40,6 +46,14 @@ CONFIGS = {
     "c5p": dict(workload="synthetic GDELT-shape CTDG (C5, 5M-event prefix): 16,682 nodes, "
                          "186-d edge feats, TGN + static memory, batch 600",
                 nodes=16682, events=5_000_000, d_e=186, d_static=100),
+    # BASELINE.json configs[2]: LastFM shape, high-degree, mini-batch parallelism i = N
+    "c3": dict(workload="synthetic LastFM-shape CTDG (C3): 1,980 nodes, 1,293,103 events, no edge feats, "
+                        "TGN + static memory, 10 recent nbrs, mem 100, local batch 600, mini-batch parallelism i=N",
+               nodes=1980, events=1_293_103, d_e=0, d_static=100, axis="i"),
+    # BASELINE.json configs[3]: MOOC shape, epoch parallelism j = N
+    "c4": dict(workload="synthetic MOOC-shape CTDG (C4): 7,144 nodes, 411,749 events, no edge feats, "
+                        "TGN + static memory, 10 recent nbrs, mem 100, local batch 600, epoch parallelism j=N",
+               nodes=7144, events=411_749, d_e=0, d_static=100, axis="j"),
     # BASELINE.json configs[4] at full size: 191M events x 186 fp32 features
     # (143 GB) streamed into HBM by the chunked generator
     "c5": dict(workload="synthetic GDELT-shape CTDG (C5): 16,682 nodes, 191,290,882 events, "
@@ -85,10 +99,43 @@ def step_model_flops(sz, cfg):
     return 6.0 * macs
 
 
+def ijk_of(cfg, world):
+    """The B200 arm's (i, j, k): the config's parallelism axis carries the N ranks."""
+    ax = cfg.get("axis", "k")
+    return (world, 1, 1) if ax == "i" else (1, world, 1) if ax == "j" else (1, 1, world)
+
+
+def step_compulsory_bytes(sz, cfg, nparam):
+    """SURVEY.md 8(d) compulsory fp32 traffic of one sub-iteration: sampler
+    probes R n (t f64 + event + neighbour), memory + mail rows of the U
+    supports (1,220 B each), their static rows, edge-feature rows of the P
+    pairs and U mails, the W root-write rows, and dense Adam (28 B/param) plus
+    gradient zeroing (4 B/param)."""
+    d_s, d_e = cfg["d_static"], cfg["d_e"]
+    return (sz["R"] * 10 * 16 + sz["U"] * 1220 + sz["U"] * d_s * 4 + (sz["P"] + sz["U"]) * d_e * 4
+            + sz["W"] * 1220 + 32 * nparam)
+
+
+def step_roofline(sz, cfg, nparam, events_s_per_gpu, peaks):
+    """Step-level roofline: t_roof per training event =
+    max(model FLOPs / bf16 peak, compulsory bytes / HBM peak), from the
+    mid-stream plan sizes measured in this run."""
+    B = max(sz["B"], 1)
+    f_ev = step_model_flops(sz, cfg) / B
+    b_ev = step_compulsory_bytes(sz, cfg, nparam) / B
+    t_t = f_ev / (peaks["bf16_tflops"] * 1e12)
+    t_h = b_ev / (peaks["hbm_gbs"] * 1e9)
+    t_roof = max(t_t, t_h)
+    return {"bound": "tensor" if t_t >= t_h else "hbm", "mflop_per_event": f_ev / 1e6,
+            "kb_per_event": b_ev / 1e3, "t_roof_ns_per_event": t_roof * 1e9,
+            "roofline_events_s_per_gpu": 1.0 / t_roof, "achieved_events_s_per_gpu": events_s_per_gpu,
+            "frac": events_s_per_gpu * t_roof}
+
+
 def roofline_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of the roofline kernel from
     the committed ncu --set full capture (profiles/), per launch."""
-    p = os.path.join(ROOT, "profiles", "r01f_roofline_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
@@ -156,14 +203,17 @@ class ClockSampler:
 _REF_GRAPHS: dict = {}
 
 
-def reference_time(cfg, n_groups, barriers, warmup, log=print):
+def reference_time(cfg, ijk, barriers, warmup, log=print):
     """Times the unmodified reference (oracle/_ref, compiled from
     /root/reference/proj/include by oracle/Makefile) on this host's cores:
-    run_sequential at (1,1,1), run_training (threaded) at (1,1,k). Returns
-    (events/s, seconds, events, threads)."""
+    run_sequential at (1,1,1), run_training (threaded: one thread per trainer
+    plus one daemon per memory copy) otherwise, on the mid-stream window that
+    starts at the middle of the training range (the B200 arm's timed window is
+    centred there too). Returns (events/s, seconds, events, threads, window)."""
     from oracle import ref
     from oracle import tgnn_oracle as O
 
+    i, j, k = ijk
     t0 = time.time()
     # the generator is sequential, so a prefix of the stream is the full
     # stream's prefix: the f64 reference holds at most REF_MAX_EVENTS of it
@@ -175,20 +225,19 @@ def reference_time(cfg, n_groups, barriers, warmup, log=print):
         log(f"[ref] graph ready in {time.time() - t0:.1f}s")
     g, t = _REF_GRAPHS[key]
     mc = O.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(t[-1]), **model_dims(cfg))
-    gb = LOCAL_BATCH
     mid = int(n_ev * TRAIN_FRAC) // 2
     out = None
     for phase, nbar in (("warmup", warmup), ("timed", barriers)):
         if nbar <= 0:
             continue
         lo = mid
-        hi = lo + nbar * gb * n_groups
-        tc = ref.train_cfg(k=n_groups, local_batch=gb, seed=1, epochs=1, lr_base=1e-3)
+        hi = lo + nbar * LOCAL_BATCH * i * k
+        tc = ref.train_cfg(i=i, j=j, k=k, local_batch=LOCAL_BATCH, seed=1, epochs=j, lr_base=1e-3)
         r = g.run(mc, tc, lo, hi, want_params=False)
-        assert r["barriers"] == nbar
         if phase == "timed":
-            ev = nbar * gb * n_groups
-            out = (ev / r["elapsed_s"], r["elapsed_s"], ev, 2 * n_groups if n_groups > 1 else 1)
+            ev = int(ref.assignment(tc, lo, hi)["traversed_after"][-1])
+            threads = i * j * k + (k if i * j * k > 1 else 0)
+            out = (ev / r["elapsed_s"], r["elapsed_s"], ev, threads, [lo, hi])
         mid = hi
     return out
 
@@ -205,33 +254,42 @@ def reference_arm(args, world, rank, emit):
     steps = min(args.steps, args.ref_max_steps)
     warm = min(args.warmup, 1)
     log = lambda *a: print(*a, file=sys.stderr)  # noqa: E731
-    # all the host cores: the reference's threaded trainer with one memory
-    # group (trainer + daemon thread) per two cores, at least one per GPU of
-    # the B200 arm, and no more than the mid-stream event window holds
-    n_ev = min(cfg["events"], REF_MAX_EVENTS)
-    room = (n_ev - int(n_ev * TRAIN_FRAC) // 2) // ((warm + steps) * LOCAL_BATCH)
-    groups = args.ref_groups or max(world, min(16, (os.cpu_count() or 2) // 2, room))
-    value, secs, ev, threads = reference_time(cfg, groups, steps, warm, log=log)
+    ours = ijk_of(cfg, world)
+    if cfg.get("axis", "k") == "k":
+        # all the host cores: the reference's threaded trainer with one memory
+        # group (trainer + daemon thread) per two cores, at least one per GPU of
+        # the B200 arm, and no more than the mid-stream event window holds
+        n_ev = min(cfg["events"], REF_MAX_EVENTS)
+        room = (n_ev - int(n_ev * TRAIN_FRAC) // 2) // ((warm + steps) * LOCAL_BATCH)
+        groups = args.ref_groups or max(world, min(16, (os.cpu_count() or 2) // 2, room))
+        shape = (1, 1, groups)
+    else:  # i- and j-parallel configs: the reference at the B200 arm's own (i, j, k)
+        shape = ours
+    value, secs, ev, threads, window = reference_time(cfg, shape, steps, warm, log=log)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s",
         "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * secs / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference gen_synthetic, seed 1)",
         "config": {"workload": cfg["workload"],
-                   "parallelism": f"(i,j,k)=(1,1,{groups}) host threads (the B200 arm: (1,1,{world}), "
+                   "parallelism": f"(i,j,k)={shape} host threads (the B200 arm: (i,j,k)={ours}, "
                                   f"one trainer per GPU)",
-                   "global_batch": LOCAL_BATCH * groups, "host_cpus": os.cpu_count()},
+                   "same_parallelism_as_b200_arm": shape == ours,
+                   "global_batch": LOCAL_BATCH * shape[0] * shape[2], "host_cpus": os.cpu_count(),
+                   "window": {"first_event": window[0], "last_event": window[1]}},
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
-                         "sample": f"{steps} barriers x {groups} x 600 events mid-stream, "
-                                   f"run_{'training' if groups > 1 else 'sequential'} (oracle/_ref)"},
+                         "sample": f"{steps} barriers at (i,j,k)={shape} x 600 events, mid-stream window "
+                                   f"[{window[0]}, {window[1]}), run_{'training' if threads > 1 else 'sequential'} "
+                                   f"(oracle/_ref)"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    if groups != world:
+    if shape != ours:
         # the reference at the B200 arm's own parallelism, for context
         s1 = min(steps, 4)
-        v1, secs1, _, thr1 = reference_time(cfg, world, s1, warm, log=log)
+        v1, secs1, _, thr1, w1 = reference_time(cfg, ours, s1, warm, log=log)
         line["same_parallelism"] = {"value": v1, "unit": "events/s", "cores": thr1,
-                                    "parallelism": f"(i,j,k)=(1,1,{world})", "steps": s1}
+                                    "parallelism": f"(i,j,k)={ours}", "steps": s1,
+                                    "window": {"first_event": w1[0], "last_event": w1[1]}}
     emit(line)
     return 0
 
@@ -302,9 +360,12 @@ def main():
     log(f"stream generated into HBM in {time.time() - t0:.1f}s")
     mc = T.ModelConfig(d_e=cfg["d_e"], num_nodes=cfg["nodes"], max_t=float(ev_t[-1]), **model_dims(cfg))
     train_end = int(round(cfg["events"] * TRAIN_FRAC))
-    tc = T.TrainConfig(i=1, j=1, k=world, local_batch=LOCAL_BATCH, lr_base=1e-3, seed=1, epochs=world)
+    ijk = ijk_of(cfg, world)
+    # weak scaling: every memory copy / team sweeps the training range once per
+    # rank along the parallel axis, so the barrier count stays ~ constant in N
+    tc = T.TrainConfig(i=ijk[0], j=ijk[1], k=ijk[2], local_batch=LOCAL_BATCH, lr_base=1e-3, seed=1, epochs=world)
     run = T.Run(ctx, g, mc, tc, 0, train_end, rank=rank, nranks=world)
-    need = args.warmup + args.steps + 2 * args.profile_steps + args.e2e_steps + 1
+    need = args.warmup + args.steps + 3 * args.profile_steps + args.e2e_steps + 1
     if run.barriers < need:
         raise SystemExit(f"schedule has {run.barriers} barriers, need {need}")
     if world > 1:
@@ -313,9 +374,15 @@ def main():
             uid.copy_(torch.frombuffer(bytearray(T.comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         run.comm_init(bytes(uid.cpu().numpy().tobytes()))
-    log(f"setup {time.time() - t0:.1f}s; {run.barriers} barriers, {run.nparam} params")
+    log(f"setup {time.time() - t0:.1f}s; {run.barriers} barriers, {run.nparam} params, (i,j,k)={ijk}")
 
-    launches = run.launches_per_barrier() if world == 1 else None
+    launches = run.launches_per_barrier()
+    # mid-stream window: fast-forward so the timed barriers are
+    # centred on the middle of the schedule, where the CPU reference is timed too
+    first_timed = run.barriers // 2 - args.steps // 2
+    start = max(0, min(first_timed - args.warmup, run.barriers - need))
+    if start > 0:
+        run.step(start)
     run.step(args.warmup)
     ctx.synchronize()
 
@@ -341,39 +408,56 @@ def main():
     ms_max = float(ms_t.item())
     events = run.traversed(first, args.steps)
     value = events / (ms_max / 1e3)
-    log(f"timed {args.steps} barriers: {ms_max:.2f} ms, {events} events, {value:,.0f} events/s, "
-        f"loss {losses[0]:.4f} -> {losses[-1]:.4f}")
+    _, tsched = T.schedule_query(tc, 0, train_end, rank, first, args.steps)
+    act = [x for x in range(args.steps) if tsched["active"][x]]
+    window = {"first_event": int(min(tsched["slice_begin"][x] for x in act)) if act else None,
+              "last_event": int(max(tsched["slice_end"][x] for x in act)) if act else None,
+              "barriers": [first, first + args.steps], "of_rank": rank, "schedule_barriers": run.barriers}
+    log(f"timed {args.steps} barriers [{first}, {first + args.steps}): {ms_max:.2f} ms, {events} events, "
+        f"{value:,.0f} events/s, loss {losses[0]:.4f} -> {losses[-1]:.4f}")
 
-    # ---- phase profile (dominant kernel for the roofline)
+    # ---- phase profile and the per-launch GEMM profile (the kernel roofline)
     prof = []
     for _ in range(args.profile_steps):
         ph, sz = run.profile_barrier(direct=True)
         prof.append((ph, sz))
-    gprof = [run.profile_barrier(direct=False)[0] for _ in range(args.profile_steps)]
+    gprof = [run.profile_barrier(direct=False)[0] for _ in range(args.profile_steps)] if ijk[1] == 1 else []
     ph_graph = {k: float(np.mean([p[k] for p in gprof])) for k in gprof[0]} if gprof else None
     ph_mean = {k: float(np.mean([p[0][k] for p in prof])) for k in prof[0][0]}
     sz_mean = {k: float(np.mean([p[1][k] for p in prof])) for k in prof[0][1]}
-    proj_ms = ph_mean["attn_proj"]
-    flops = attn_proj_flops(sz_mean, cfg)
-    hbm_bytes = attn_proj_bytes(sz_mean, cfg)
+    gemm = [run.gemm_profile() for _ in range(args.profile_steps)]
+    g_ms = float(np.mean([x[:, 0].sum() for x in gemm]))
+    g_flops = float(np.mean([x[:, 1].sum() for x in gemm]))
+    g_bytes = float(np.mean([x[:, 2].sum() for x in gemm]))
+    g_launches = int(np.mean([len(x) for x in gemm]))
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
-    src = "MEASURED_PEAKS.json" if "when" in peaks else "B200_PROFILING.md fallback"
-    t_tensor = flops / (peaks["bf16_tflops"] * 1e12)
-    t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
-    secs = proj_ms / 1e3
-    tensor_view = {"achieved": flops / secs / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s"}
-    hbm_view = {"achieved": hbm_bytes / secs / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    src = "MEASURED_PEAKS.json (burst)" if "when" in peaks else "B200_PROFILING.md fallback"
+    secs = g_ms / 1e3
+    t_tensor = g_flops / (peaks["bf16_tflops"] * 1e12)
+    t_hbm = g_bytes / (peaks["hbm_gbs"] * 1e9)
+    tensor_view = {"achieved": g_flops / secs / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                   "executed_bf16x3": 3 * g_flops / secs / 1e12}
+    hbm_view = {"achieved": g_bytes / secs / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
     bound = "hbm" if t_hbm >= t_tensor else "tensor"
-    main = hbm_view if bound == "hbm" else tensor_view
-    roofline = {"kernel": "attention projection GEMMs (tcgen05 bf16x3, TMA): per-pair edge K|V + per-support node Q|K|V",
-                "bound": bound, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
-                "frac": main["achieved"] / main["peak"], "traffic": roofline_traffic(), "peak_source": src,
-                "flops_per_launch": flops, "algorithmic_bytes_per_launch": hbm_bytes,
-                "launch_ms": proj_ms, "tensor_view": tensor_view, "hbm_view": hbm_view,
-                "share_of_step": proj_ms / max(sum(ph_mean.values()), 1e-9)}
+    main_v = hbm_view if bound == "hbm" else tensor_view
+    step_direct_ms = max(sum(ph_mean.values()), 1e-9)
+    roofline = {"kernel": "tc_gemm_kernel group: every tcgen05 GEMM launch of a barrier (bf16x3, TMA, TMEM), "
+                          "the largest share of the barrier's launch list",
+                "bound": bound, "achieved": main_v["achieved"], "peak": main_v["peak"], "unit": main_v["unit"],
+                "frac": main_v["achieved"] / main_v["peak"], "traffic": roofline_traffic(), "peak_source": src,
+                "launches_per_step": g_launches, "flops_per_step": g_flops, "algorithmic_bytes_per_step": g_bytes,
+                "flops_per_launch": g_flops / max(g_launches, 1),
+                "algorithmic_bytes_per_launch": g_bytes / max(g_launches, 1),
+                "launch_ms_avg": g_ms / max(g_launches, 1), "gemm_ms_per_step": g_ms,
+                "tensor_view": tensor_view, "hbm_view": hbm_view,
+                "share_of_step_direct": g_ms / step_direct_ms,
+                "per_launch": [[round(float(v), 6) for v in row] for row in gemm[-1]],
+                "per_launch_cols": ["ms", "flops", "bytes", "problems", "max_M", "max_splits"]}
     log("phases (ms): " + ", ".join(f"{k}={v:.3f}" for k, v in ph_mean.items()))
-    log(f"plan sizes: {sz_mean}")
+    log(f"plan sizes: {sz_mean}; GEMMs {g_launches} launches {g_ms * 1e3:.1f} us/step "
+        f"{tensor_view['achieved']:.1f} TFLOP/s {hbm_view['achieved']:.0f} GB/s")
+    rstep = step_roofline(sz_mean, cfg, run.nparam, value / world, peaks)
 
     # ---- end-to-end through the public API: per step H2D of the step's events
     # (src/dst/t/edge features from pinned host memory) + barrier + D2H loss read
@@ -388,11 +472,12 @@ def main():
     p_src = T.pinned_empty((nw,), np.int32)
     p_dst = T.pinned_empty((nw,), np.int32)
     p_t = T.pinned_empty((nw,), np.float64)
-    p_f = T.pinned_empty((nw, d_e), np.float32)
+    p_f = T.pinned_empty((nw, max(d_e, 1)), np.float32)[:, :d_e]
     p_src[:w_hi - w_lo] = ev_src[w_lo:w_hi]
     p_dst[:w_hi - w_lo] = ev_dst[w_lo:w_hi]
     p_t[:w_hi - w_lo] = ev_t[w_lo:w_hi]
-    p_f[:w_hi - w_lo] = g.edge_feats(w_lo, w_hi - w_lo)
+    if d_e:
+        p_f[:w_hi - w_lo] = g.edge_feats(w_lo, w_hi - w_lo)
     p_loss = T.pinned_empty((args.e2e_steps,), np.float64)
     if world > 1:
         dist.barrier()
@@ -453,10 +538,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import ref
         if ref.available():
-            v, secs, ev, thr = reference_time(cfg, 1, args.cpu_baseline_steps, 0, log=log)
+            v, secs, ev, thr, cw = reference_time(cfg, (1, 1, 1), args.cpu_baseline_steps, 0, log=log)
             cpu = {"value": v, "unit": "events/s", "cores": thr, "kind": "reference",
-                   "sample": f"{args.cpu_baseline_steps} barriers x 600 events mid-stream, "
-                             f"run_sequential of the unmodified reference (oracle/_ref), {secs:.1f}s"}
+                   "sample": f"{args.cpu_baseline_steps} barriers x 600 events, mid-stream window "
+                             f"[{cw[0]}, {cw[1]}), run_sequential of the unmodified reference "
+                             f"(oracle/_ref), {secs:.1f}s",
+                   "window": {"first_event": cw[0], "last_event": cw[1]}}
 
     if rank == 0:
         line = {
@@ -465,8 +552,9 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (tcgen05 bf16x3 GEMMs, fp32 accumulate; f64 times)",
             "data": "synthetic (bit-identical gen_synthetic, seed 1)",
             "config": {"workload": cfg["workload"],
-                       "parallelism": f"(i,j,k)=(1,1,{world}), one trainer per GPU",
-                       "global_batch": LOCAL_BATCH * world, "local_batch": LOCAL_BATCH,
+                       "parallelism": f"(i,j,k)={ijk}, one trainer per GPU",
+                       "global_batch": LOCAL_BATCH * ijk[0], "local_batch": LOCAL_BATCH,
+                       "window": window,
                        "l2": "inputs larger than L2 (edge features "
                              f"{cfg['events'] * cfg['d_e'] * 4 / 1e6:.0f} MB; each step reads a new "
                              "event window); no explicit flush"},
@@ -476,6 +564,7 @@ def main():
             "gpu_launches": (launches * args.steps) if launches is not None else None,
             "gpu_launches_per_step": launches,
             "roofline": roofline,
+            "roofline_step": rstep,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "phases_ms": ph_mean,

@@ -170,7 +170,13 @@ typedef struct tgnn_run_options {
   int64_t eval_batch;
   /* record the daemon op-log of this rank's reads and writes (ref
    * memory_daemon.hpp:73,90, oplog.hpp:15-45); read with tgnn_run_oplog */
-  int32_t oplog, pad1;
+  int32_t oplog;
+  /* RunOptions.segment_snapshots (ref trainer.hpp:581, parallel.hpp:288-290):
+   * copy this rank's memory replica (memory + last_update) after the write
+   * bracket of every pair that ends a segment (DaemonOp::Snapshot,
+   * memory_daemon.hpp:94-105); read with tgnn_run_snapshots. An oracle
+   * feature: the run uses the direct (uncaptured) barrier path. */
+  int32_t segment_snapshots;
 } tgnn_run_options;
 
 /* build_assignment + Assignment::task (ref parallel.hpp:150-331), host only.
@@ -183,7 +189,20 @@ int tgnn_schedule_query(const tgnn_train_config* tc, int64_t train_begin, int64_
 
 int tgnn_comm_unique_id(char* out128);
 int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, tgnn_run** out);
+/* One process per GPU: NCCL communicator over all ranks (+ ncclCommSplit per
+ * memory group), from a unique id every rank received out of band. */
 int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128);
+/* In-process alternative (the reference's threading model: run_training's
+ * trainer threads share host arrays, trainer.hpp:671-674): the ranks are host
+ * threads of one process, on one device or several. Each rank's thread
+ * attaches its run to one shared hub; every collective then becomes a host
+ * rendezvous plus cross-stream events and an ascending-rank device reduction
+ * (the reference's summation order). Barriers run on the direct path (no
+ * CUDA-graph capture). Destroy the hub after every attached run. */
+typedef struct tgnn_local_hub tgnn_local_hub;
+int tgnn_local_hub_create(int32_t nranks, tgnn_local_hub** out);
+int tgnn_local_hub_destroy(tgnn_local_hub* hub);
+int tgnn_run_local_init(tgnn_run* r, tgnn_local_hub* hub);
 int tgnn_run_destroy(tgnn_run* r);
 int tgnn_run_info(tgnn_run* r, int64_t* barriers, int64_t* param_count);
 /* Enqueue barriers [first, first + count) on the context stream (no host sync). */
@@ -207,6 +226,11 @@ int tgnn_run_metrics(tgnn_run* r, int64_t* count, double* rows);
  * (ref OpRecord, oplog.hpp:15-24). A memory copy's op-log is the union of its
  * ranks' rows ordered by (iter, kind, rank). rows == NULL returns the count. */
 int tgnn_run_oplog(tgnn_run* r, int64_t* count, int64_t* rows);
+/* RunResult.snapshots of this rank's memory copy (ref trainer.hpp:593,
+ * MemorySnapshot memory_daemon.hpp:12-17), in plan order: meta[count x 2] =
+ * sweep, segment; memory[count x N x d_mem]; last_update[count x N]. Any
+ * output may be NULL; count receives the number of snapshots taken so far. */
+int tgnn_run_snapshots(tgnn_run* r, int64_t* count, int64_t* meta, double* memory, double* last_update);
 /* Replica invariant (ref SPEC.md:397): collective over all ranks; fails with
  * TGNN_PROTOCOL if any rank's parameters differ bitwise; hash_out receives the
  * order-independent 64-bit parameter fingerprint. Also checked automatically at
@@ -223,11 +247,18 @@ int tgnn_run_launches_per_barrier(tgnn_run* r, int64_t* out);
 /* Runs the next barrier with CUDA-event phase markers and returns per-phase
  * device milliseconds [TGNN_PHASES] (plan, gru_fwd, attn_assemble, attn_proj,
  * attn_softmax, decoder, decoder_bwd, attn_bwd, attn_bwd_gemm, gru_bwd,
- * writes, allreduce, adam) and the plan sizes [8] (B, R, P, U, -, items, 2B, -).
+ * writes, allreduce, adam) and the plan sizes [8] (B, R, P, U, -, items, 2B, W).
  * direct != 0: the single-stream path (each phase alone); 0: the production
  * CUDA-graph schedule (markers on the critical-path stream). */
 #define TGNN_PHASES 13
 int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes, int32_t direct);
+/* Runs the next barrier on the direct path with every tcgen05 GEMM launch
+ * bracketed by CUDA events (the kernel roofline of bench.py). rows[cap x 6]
+ * per launch, in launch order: device ms, algorithmic FLOPs (sum of 2 M N K
+ * over the launch's problems at their runtime row counts), algorithmic bytes
+ * (bf16 hi/lo operands 4 B per element in, fp32 out), problems, largest M,
+ * largest split count. *count receives the number of launches. */
+int tgnn_run_gemm_profile(tgnn_run* r, int64_t cap, int64_t* count, double* rows);
 
 /* ------------------------------------------------------------------ GEMM engine
  * Process-wide choice for the step's dense contractions:
@@ -246,13 +277,17 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
                     const float* B, int b_trans, float* C, int splits);
 
 /* ------------------------------------------------------------------ host I/O
- * Streaming ingestion: (re)writes events [first, first+count) of a device
- * graph from host buffers (src/dst/t must match the finalized order; edge
- * features float32 [count x d_e]). Used to stream feature windows and by the
- * end-to-end measurement. Pinned buffers make the copies asynchronous: they
- * run on the context's copy stream, overlap work enqueued before the call
- * (which never reads events past its own barrier) and are ordered before any
- * work enqueued after it. */
+ * Streaming ingestion of events [first, first+count) from host buffers: the
+ * edge features (float32 [count x d_e]) overwrite the device rows; src / dst /
+ * t are uploaded and verified bitwise against the finalized (T-CSR indexed)
+ * events -- they are never rewritten, and a mismatch fails the next
+ * synchronising call with TGNN_PROTOCOL. Used to stream feature windows and
+ * by the end-to-end measurement. Pinned buffers make the copies asynchronous:
+ * they run on the context's copy stream, overlap work enqueued before the call
+ * and are ordered before any work enqueued after it. Ordering contract: in
+ * CUDA-graph runs barrier b plans barrier b + 1 (reads its events) while b
+ * runs, so the rows of barrier b + 1 must be ingested BEFORE the
+ * tgnn_run_barriers call that runs barrier b. */
 int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t* src,
                       const int32_t* dst, const double* t, const float* efeat);
 /* Debug: timing (us per launch) of the tcgen05 engine on an M x N x K

@@ -278,6 +278,22 @@ class RefGraph:
                     metrics=metrics[:nm.value].copy(), elapsed_s=el.value, barriers=nb.value)
 
 
+def run_snapshots(graph, mcfg, tcfg, train_begin, train_end, cap=64):
+    """run_training with segment_snapshots: (meta [n x 3] = copy, sweep, segment,
+    memory [n, N, d_mem], last_update [n, N]) over every memory copy."""
+    mc = model_cfg(mcfg)
+    N, d = int(mcfg.num_nodes), int(mcfg.d_mem)
+    meta = np.zeros((cap, 3), np.int64)
+    mem = np.zeros((cap, N, d))
+    lu = np.zeros((cap, N))
+    n = C.c_int64()
+    _check(lib().ref_run_snapshots(graph.h, C.byref(mc), C.byref(tcfg), C.c_int64(train_begin),
+                                   C.c_int64(train_end), C.c_int64(cap), C.byref(n), _p(meta, i64p),
+                                   _p(mem, f64p), _p(lu, f64p)))
+    assert n.value <= cap, "raise cap"
+    return meta[:n.value], mem[:n.value], lu[:n.value]
+
+
 def validate_oplog(path, i, j):
     """validate_oplog_file (oplog.hpp:105-160) -> (ok, line, message)."""
     line = C.c_int64()

@@ -558,6 +558,40 @@ int ref_run_oplog(void* gp, const ref_model_cfg* c, const ref_train_cfg* tc, int
   })
 }
 
+// run_training with segment_snapshots (trainer.hpp:581,593; parallel.hpp:288-290):
+// every memory copy's snapshots in plan order, meta[cap x 3] = copy, sweep,
+// segment; memory[cap x N x d_mem]; last_update[cap x N].
+int ref_run_snapshots(void* gp, const ref_model_cfg* c, const ref_train_cfg* tc, int64_t train_begin,
+                      int64_t train_end, int64_t cap, int64_t* count_out, int64_t* meta, double* memory,
+                      double* last_update) {
+  REF_GUARD({
+    auto* g = static_cast<TemporalGraph*>(gp);
+    RunOptions opt;
+    opt.model = to_mcfg(c);
+    opt.train = to_tcfg(tc);
+    opt.train_begin = train_begin;
+    opt.train_end = train_end;
+    opt.segment_snapshots = true;
+    RunResult res = run_training(*g, opt);
+    int64_t n = 0;
+    for (std::size_t grp = 0; grp < res.snapshots.size(); ++grp) {
+      for (const MemorySnapshot& sn : res.snapshots[grp]) {
+        if (n < cap) {
+          meta[n * 3 + 0] = static_cast<int64_t>(grp);
+          meta[n * 3 + 1] = sn.sweep;
+          meta[n * 3 + 2] = sn.segment;
+          const auto f = sn.memory.flat();
+          std::copy(f.begin(), f.end(), memory + n * static_cast<int64_t>(f.size()));
+          std::copy(sn.last_update.begin(), sn.last_update.end(),
+                    last_update + n * static_cast<int64_t>(sn.last_update.size()));
+        }
+        ++n;
+      }
+    }
+    *count_out = n;
+  })
+}
+
 int ref_validate_oplog(const char* path, int32_t i, int32_t j, int64_t* bad_line, char* msg, int64_t msg_cap) {
   REF_GUARD({
     OplogVerdict v = validate_oplog_file(path, i, j);

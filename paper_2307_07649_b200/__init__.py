@@ -35,7 +35,7 @@ __all__ = [
     "gen_synthetic", "Context", "TemporalGraph", "NodeMemoryStore", "ReadView", "TrainerCore",
     "Run", "run_sequential", "param_count", "init_params", "lr_eff", "Evaluator",
     "write_metrics_csv", "save_checkpoint", "load_checkpoint", "write_dataset", "chronological_split",
-    "write_oplog",
+    "write_oplog", "LocalHub", "run_ranks",
 ]
 
 lib()  # fail loudly at import if the native library is absent
@@ -563,20 +563,71 @@ def comm_unique_id() -> bytes:
     return buf.raw
 
 
+class LocalHub:
+    """In-process exchange for the ranks of one job run as threads of this
+    process (tgnn_local_hub): collectives are host rendezvous + cross-stream
+    events + ascending-rank device reductions, on one GPU or several."""
+
+    def __init__(self, nranks: int):
+        self.h = C.c_void_p()
+        check(lib().tgnn_local_hub_create(nranks, C.byref(self.h)))
+        self.nranks = nranks
+
+    def close(self):
+        if self.h:
+            lib().tgnn_local_hub_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_ranks(fn, nranks: int, timeout: float = 900.0):
+    """Runs fn(rank, hub) on nranks threads sharing one LocalHub; returns the
+    per-rank results (re-raises the first failure)."""
+    import threading
+
+    hub = LocalHub(nranks)
+    out, err = [None] * nranks, [None] * nranks
+
+    def body(r):
+        try:
+            out[r] = fn(r, hub)
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+    if any(t.is_alive() for t in th):
+        raise TimeoutError("run_ranks: a rank did not finish")
+    first = next((e for e in err if e is not None), None)
+    if first is not None:
+        raise first
+    hub.close()
+    return out
+
+
 class Run:
     """One rank of run_training (trainer.hpp:630-772); nranks == i*j*k, one GPU each."""
 
     def __init__(self, ctx: Context, g: TemporalGraph, model: ModelConfig, train: TrainConfig,
                  train_begin: int, train_end: int, rank: int = 0, nranks: int = 1,
                  use_graphs: bool = True, val_begin: int = 0, val_end: int = 0,
-                 eval_negatives: int = 49, eval_batch: int = 0, oplog: bool = False):
+                 eval_negatives: int = 49, eval_batch: int = 0, oplog: bool = False,
+                 segment_snapshots: bool = False):
         self.ctx, self.g, self.model, self.train = ctx, g, model, train
         ctx._adopt(self)
         if model.num_nodes == 0:
             model.num_nodes = g.num_nodes
         opt = RunOptionsC(model.c(), train.c(), train_begin, train_end, rank, nranks,
                           1 if use_graphs else 0, val_begin, val_end, eval_negatives, 0, eval_batch,
-                          1 if oplog else 0, 0)
+                          1 if oplog else 0, 1 if segment_snapshots else 0)
         self.h = C.c_void_p()
         check(lib().tgnn_run_create(ctx.h, g.h, C.byref(opt), C.byref(self.h)))
         b, n = C.c_int64(), C.c_int64()
@@ -587,6 +638,12 @@ class Run:
 
     def comm_init(self, uid: bytes):
         check(lib().tgnn_run_comm_init(self.h, uid))
+
+    def local_init(self, hub: "LocalHub"):
+        """Joins the in-process hub (every rank a thread of this process); call
+        from each rank's own thread -- it returns once all ranks attached."""
+        check(lib().tgnn_run_local_init(self.h, hub.h))
+        self.hub = hub
 
     def step(self, count: int = 1):
         check(lib().tgnn_run_barriers(self.h, self.next, count))
@@ -640,6 +697,19 @@ class Run:
             check(lib().tgnn_run_oplog(self.h, C.byref(n), _p(out, i64p)))
         return out
 
+    def snapshots(self):
+        """RunResult.snapshots of this rank's memory copy (trainer.hpp:593):
+        dict(meta [n x 2] = sweep, segment; memory [n, N, d_mem]; last_update [n, N])."""
+        n = C.c_int64()
+        check(lib().tgnn_run_snapshots(self.h, C.byref(n), None, None, None))
+        N, d = self.g.num_nodes, self.model.d_mem
+        meta = np.zeros((n.value, 2), np.int64)
+        mem = np.zeros((n.value, N, d))
+        lu = np.zeros((n.value, N))
+        if n.value:
+            check(lib().tgnn_run_snapshots(self.h, C.byref(n), _p(meta, i64p), _p(mem, f64p), _p(lu, f64p)))
+        return dict(meta=meta, memory=mem, last_update=lu)
+
     def save_checkpoint(self, path):
         """model.ckpt of this rank's current weights (all replicas are identical)."""
         save_checkpoint(self.model, self.params(), path)
@@ -669,7 +739,17 @@ class Run:
                                              1 if direct else 0))
         self.next += 1
         return dict(zip(self.PHASES, ms.tolist())), dict(B=int(sz[0]), R=int(sz[1]), P=int(sz[2]),
-                                                         U=int(sz[3]))
+                                                         U=int(sz[3]), W=int(sz[7]))
+
+    def gemm_profile(self):
+        """Runs the next barrier (direct path) with every tcgen05 GEMM launch
+        event-timed: array [launches x 6] = ms, algorithmic FLOPs, algorithmic
+        bytes, problems, max M, max splits."""
+        rows = np.zeros((64, 6))
+        n = C.c_int64()
+        check(lib().tgnn_run_gemm_profile(self.h, 64, C.byref(n), _p(rows, f64p)))
+        self.next += 1
+        return rows[:min(n.value, 64)].copy()
 
     def launches_per_barrier(self):
         out = C.c_int64()

@@ -81,7 +81,7 @@ class RunOptionsC(C.Structure):
     _fields_ = [("model", ModelConfigC), ("train", TrainConfigC), ("train_begin", i64),
                 ("train_end", i64), ("rank", i32), ("nranks", i32), ("use_graphs", i32),
                 ("val_begin", i64), ("val_end", i64), ("eval_negatives", i32), ("pad0", i32),
-                ("eval_batch", i64), ("oplog", i32), ("pad1", i32)]
+                ("eval_batch", i64), ("oplog", i32), ("segment_snapshots", i32)]
 
 
 _lib = None
@@ -127,6 +127,9 @@ SIGNATURES = {
     "tgnn_comm_unique_id": [C.c_char_p],
     "tgnn_run_create": [vp, vp, C.POINTER(RunOptionsC), C.POINTER(vp)],
     "tgnn_run_comm_init": [vp, C.c_char_p],
+    "tgnn_local_hub_create": [i32, C.POINTER(vp)],
+    "tgnn_local_hub_destroy": [vp],
+    "tgnn_run_local_init": [vp, vp],
     "tgnn_run_destroy": [vp],
     "tgnn_run_info": [vp, i64p, i64p],
     "tgnn_run_barriers": [vp, i64, i64],
@@ -136,6 +139,7 @@ SIGNATURES = {
     "tgnn_run_traversed": [vp, i64, i64, i64p],
     "tgnn_run_metrics": [vp, i64p, f64p],
     "tgnn_run_oplog": [vp, i64p, i64p],
+    "tgnn_run_snapshots": [vp, i64p, i64p, f64p, f64p],
     "tgnn_run_check_replicas": [vp, C.POINTER(C.c_uint64)],
     "tgnn_run_evaluate_mrr": [vp, i64, i64, i64, i32, u64, f64p, i64p],
     "tgnn_evaluator_create": [vp, vp, C.POINTER(ModelConfigC), i64, i32, C.POINTER(vp)],
@@ -152,6 +156,7 @@ SIGNATURES = {
     "tgnn_checkpoint_load": [C.POINTER(ModelConfigC), C.c_char_p, f64p],
     "tgnn_run_launches_per_barrier": [vp, i64p],
     "tgnn_run_profile_barrier": [vp, f64p, C.POINTER(C.c_int32), i32],
+    "tgnn_run_gemm_profile": [vp, i64, i64p, f64p],
     "tgnn_graph_ingest": [vp, i64, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), f64p, f32p],
     "tgnn_pinned_alloc": [i64, C.POINTER(vp)],
     "tgnn_debug_gemm_bench": [i64, i64, i64, i32, i32, f64p, C.POINTER(C.c_uint64), C.POINTER(i32)],

@@ -6,7 +6,11 @@
 // every exchange is an NCCL collective on the same stream (NVLink/NVSwitch).
 
 #include <algorithm>
+#include <array>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -24,7 +28,6 @@
 #include "host/synth.hpp"
 #include "nccl_dyn.hpp"
 #include "graph.cuh"
-#include "peer.cuh"
 #include "plan.cuh"
 #include "step.cuh"
 #include "gemm_tma.cuh"
@@ -142,6 +145,19 @@ std::vector<double> host_init_params(const ModelDims& m, uint64_t seed) {
 }  // namespace
 
 // ----------------------------------------------------------------- handles
+constexpr int kFlagIngest = 2;  // d_flag bit: an ingested event differed from the indexed one
+
+__global__ void ingest_verify_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                     const double* __restrict__ t, const int32_t* __restrict__ g_src,
+                                     const int32_t* __restrict__ g_dst, const double* __restrict__ g_t,
+                                     int64_t count, int* flag) {
+  bool bad = false;
+  for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < count;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= src[x] != g_src[x] || dst[x] != g_dst[x] || __double_as_longlong(t[x]) != __double_as_longlong(g_t[x]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, kFlagIngest);
+}
+
 struct tgnn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -162,6 +178,9 @@ struct tgnn_ctx {
     TGB_CUDA(cudaStreamSynchronize(stream));
     if (f) {
       TGB_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
+      if (f & kFlagIngest)
+        throw Error(kProtocol, "ingest: events differ from the finalized graph (src, dst and t must match "
+                               "the indexed stream; only edge features may be rewritten)");
       throw Error(kNumeric, "non-finite value in the training step");
     }
   }
@@ -171,8 +190,14 @@ struct tgnn_ctx {
 struct tgnn_graph {
   tgnn_ctx* ctx = nullptr;
   DGraph d;
+  // tgnn_graph_ingest staging: incoming src / dst / t are verified against
+  // the finalized (indexed) events instead of overwriting them
+  int32_t* st_src = nullptr;
+  int32_t* st_dst = nullptr;
+  double* st_t = nullptr;
+  int64_t st_cap = 0;
   ~tgnn_graph() {
-    void* ptrs[] = {d.src, d.dst, d.t, d.inc_ptr, d.inc_t, d.inc_eid, d.inc_nbr, d.efeat};
+    void* ptrs[] = {d.src, d.dst, d.t, d.inc_ptr, d.inc_t, d.inc_eid, d.inc_nbr, d.efeat, st_src, st_dst, st_t};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -485,6 +510,57 @@ struct tgnn_evaluator {
   }
 };
 
+// In-process communicator (include/tgnn_b200.h, tgnn_local_hub): the ranks of
+// a job are host threads of ONE process -- the reference's own threading model
+// (trainer threads sharing host arrays, trainer.hpp:671-674) -- on one device
+// or several. A collective is a host rendezvous at enqueue time plus cross-
+// stream CUDA events: every rank publishes its buffer and a ready event, waits
+// for the others' events, reduces ALL ranks' buffers in ascending rank order
+// into private scratch (so every replica computes the identical sum, the
+// reference's average_active_grads order, trainer.hpp:473-483), then, after a
+// second rendezvous (nobody still reads its input), copies the result back.
+// Nothing spins on the device; a rank that never arrives times out the others.
+constexpr int kLocalMax = 16;
+struct tgnn_local_hub {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  std::vector<tgnn_run*> runs;
+  std::vector<const void*> src;
+
+  void rendezvous() {
+    static const int secs = [] {
+      const char* e = std::getenv("TGNN_LOCAL_TIMEOUT_S");
+      const int v = e ? std::atoi(e) : 0;
+      return v > 0 ? v : 300;
+    }();
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) throw Error(kProtocol, "local hub: another rank failed");
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    const bool ok = cv.wait_for(lk, std::chrono::seconds(secs), [&] { return gen != g || broken; });
+    if (!ok) {
+      broken = true;
+      cv.notify_all();
+      throw Error(kProtocol, "local hub: rendezvous timed out (a rank stopped issuing collectives)");
+    }
+    if (gen == g) throw Error(kProtocol, "local hub: another rank failed");
+  }
+  void fail() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
 struct tgnn_run {
   tgnn_ctx* ctx = nullptr;
   tgnn_graph* g = nullptr;
@@ -496,12 +572,11 @@ struct tgnn_run {
   int group = 0, team = 0, member = 0, group_size = 1;
   ncclComm_t comm = nullptr, gcomm = nullptr;
   bool comm_ready = false;
-  // gradient all-reduce over NVLink peer memory (peer.cuh); NCCL otherwise
-  bool peer_ok = false;
-  PeerAR peer;
-  std::vector<void*> peer_opened;  // IPC mappings to close
-  unsigned* peer_flags = nullptr;
-  float* peer_recv = nullptr;
+  // in-process exchange (tgnn_run_local_init) instead of NCCL
+  tgnn_local_hub* hub = nullptr;
+  cudaEvent_t ev_lready = nullptr, ev_ldone = nullptr;
+  void* lscratch = nullptr;
+  size_t lscratch_bytes = 0;
   double* d_losses = nullptr;
   void* gathered = nullptr;  // [i, wpack_bytes]
   int64_t next_barrier = 0;
@@ -529,6 +604,14 @@ struct tgnn_run {
   cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
   cudaEvent_t ev_red = nullptr, ev_artail = nullptr, ev_upd = nullptr, ev_mid = nullptr;
   cudaEvent_t ev_tail = nullptr, ev_head = nullptr, ev_comm = nullptr;
+  // segment snapshots (DaemonOp::Snapshot): slot per snapshot pair of this
+  // rank's memory copy, memory + last_update copied after the pair's writes
+  bool snaps = false;
+  std::vector<int64_t> snap_slot;            // per pair of the group (-1: none)
+  std::vector<std::array<int64_t, 2>> snap_meta;  // sweep, segment per slot
+  int64_t snap_taken = 0;
+  float* d_snap_mem = nullptr;
+  double* d_snap_lu = nullptr;
   // daemon op-log records [barriers x 4] (R first, R len, W first, W len)
   bool oplog = false;
   int64_t* d_oplog = nullptr;
@@ -547,6 +630,8 @@ struct tgnn_run {
 
   ~tgnn_run() {
     if (d_oplog) cudaFree(d_oplog);
+    if (d_snap_mem) cudaFree(d_snap_mem);
+    if (d_snap_lu) cudaFree(d_snap_lu);
     for (Row& row : rows)
       if (row.done) cudaEventDestroy(row.done);
     if (ev_t0) cudaEventDestroy(ev_t0);
@@ -572,9 +657,9 @@ struct tgnn_run {
       if (e) cudaEventDestroy(e);
     if (d_desc) cudaFree(d_desc);
     if (d_ctr) cudaFree(d_ctr);
-    for (void* q : peer_opened) cudaIpcCloseMemHandle(q);
-    if (peer_flags) cudaFree(peer_flags);
-    if (peer_recv) cudaFree(peer_recv);
+    if (ev_lready) cudaEventDestroy(ev_lready);
+    if (ev_ldone) cudaEventDestroy(ev_ldone);
+    if (lscratch) cudaFree(lscratch);
     if (gcomm) nccl::api().CommDestroy(gcomm);
     if (comm) nccl::api().CommDestroy(comm);
     if (d_losses) cudaFree(d_losses);
@@ -584,6 +669,141 @@ struct tgnn_run {
 
 // ----------------------------------------------------------------- runtime pieces
 namespace {
+
+// ----------------------------------------------------------------- exchange
+// Every collective of a run goes through comm_allreduce / comm_bcast_packs:
+// NCCL over NVLink (one process per GPU, tgnn_run_comm_init) or the in-process
+// hub (tgnn_run_local_init). Both backends see the same call sequence on
+// every rank, so the op-log, the schedule and the replicas are unchanged.
+enum class RedTy { F32, F64, U64 };
+enum class RedOp { Sum, Min, Max };
+
+struct LocalSrcs {
+  const void* p[kLocalMax];
+  int n;
+};
+
+template <typename T, int OP>
+__global__ void local_reduce_kernel(LocalSrcs src, int64_t count, T* __restrict__ out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < count; x += stride) {
+    T acc = static_cast<const T*>(src.p[0])[x];
+    for (int q = 1; q < src.n; ++q) {  // ascending rank order
+      const T v = static_cast<const T*>(src.p[q])[x];
+      acc = OP == 0 ? acc + v : OP == 1 ? (v < acc ? v : acc) : (v > acc ? v : acc);
+    }
+    out[x] = acc;
+  }
+}
+
+size_t red_size(RedTy t) { return t == RedTy::F32 ? 4 : 8; }
+
+template <typename T>
+void local_reduce_typed(RedOp op, const LocalSrcs& src, int64_t count, void* out, cudaStream_t s) {
+  const int grid = static_cast<int>(std::min<int64_t>((count + 255) / 256, 4 * num_sms()));
+  if (count <= 0) return;
+  if (op == RedOp::Sum) local_reduce_kernel<T, 0><<<grid, 256, 0, s>>>(src, count, static_cast<T*>(out));
+  else if (op == RedOp::Min) local_reduce_kernel<T, 1><<<grid, 256, 0, s>>>(src, count, static_cast<T*>(out));
+  else local_reduce_kernel<T, 2><<<grid, 256, 0, s>>>(src, count, static_cast<T*>(out));
+  TGB_CUDA(cudaGetLastError());
+}
+
+// Marks the hub broken when a collective-issuing call fails on one rank, so
+// the other ranks fail at their next rendezvous instead of timing out.
+struct HubGuard {
+  tgnn_run* r;
+  bool armed = true;
+  explicit HubGuard(tgnn_run* run) : r(run) {}
+  ~HubGuard() {
+    if (armed && r->hub) r->hub->fail();
+  }
+  void ok() { armed = false; }
+};
+
+void local_wait_all(tgnn_run* r, bool done, cudaStream_t s) {
+  tgnn_local_hub* h = r->hub;
+  for (int q = 0; q < h->n; ++q)
+    if (q != r->rank) TGB_CUDA(cudaStreamWaitEvent(s, done ? h->runs[q]->ev_ldone : h->runs[q]->ev_lready, 0));
+}
+
+void comm_allreduce(tgnn_run* r, void* buf, size_t count, RedTy ty, RedOp op, cudaStream_t s) {
+  if (r->nranks == 1 || count == 0) return;
+  if (r->hub) {
+    tgnn_local_hub* h = r->hub;
+    const size_t bytes = count * red_size(ty);
+    if (r->lscratch_bytes < bytes) {
+      if (r->lscratch) {
+        TGB_CUDA(cudaStreamSynchronize(s));
+        cudaFree(r->lscratch);
+      }
+      r->lscratch = dalloc<char>(bytes);
+      r->lscratch_bytes = bytes;
+    }
+    h->src[static_cast<size_t>(r->rank)] = buf;
+    TGB_CUDA(cudaEventRecord(r->ev_lready, s));
+    h->rendezvous();
+    local_wait_all(r, false, s);
+    LocalSrcs src{};
+    src.n = h->n;
+    for (int q = 0; q < h->n; ++q) src.p[q] = h->src[static_cast<size_t>(q)];
+    if (ty == RedTy::F32) local_reduce_typed<float>(op, src, static_cast<int64_t>(count), r->lscratch, s);
+    else if (ty == RedTy::F64) local_reduce_typed<double>(op, src, static_cast<int64_t>(count), r->lscratch, s);
+    else local_reduce_typed<unsigned long long>(op, src, static_cast<int64_t>(count), r->lscratch, s);
+    TGB_CUDA(cudaEventRecord(r->ev_ldone, s));
+    h->rendezvous();  // every rank has enqueued its reads of every input
+    local_wait_all(r, true, s);
+    TGB_CUDA(cudaMemcpyAsync(buf, r->lscratch, bytes, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  const ncclDataType_t dt = ty == RedTy::F32 ? ncclFloat : ty == RedTy::F64 ? ncclDouble : ncclUint64;
+  const ncclRedOp_t o = op == RedOp::Sum ? ncclSum : op == RedOp::Min ? ncclMin : ncclMax;
+  NCCL_CHECK(nccl::api().AllReduce(buf, buf, count, dt, o, r->comm, s));
+}
+
+// The write packs of team `team`'s i members into r->gathered[member]
+// (memory group exchange of the i-axis): grouped NCCL broadcasts
+// over the group communicator, or device copies from the members' packs.
+void comm_bcast_packs(tgnn_run* r, int team, cudaStream_t s) {
+  tgnn_trainer* tr = r->tr.get();
+  const size_t pb = tr->w.wpack_bytes;
+  const int i = r->tc.i;
+  char* dst = static_cast<char*>(r->gathered);
+  if (r->hub) {
+    tgnn_local_hub* h = r->hub;
+    h->src[static_cast<size_t>(r->rank)] = tr->w.wpack;
+    TGB_CUDA(cudaEventRecord(r->ev_lready, s));
+    h->rendezvous();
+    const int base = r->group * i * r->tc.j + team * i;
+    for (int mm = 0; mm < i; ++mm) {
+      const int q = base + mm;
+      if (q != r->rank) TGB_CUDA(cudaStreamWaitEvent(s, h->runs[static_cast<size_t>(q)]->ev_lready, 0));
+      TGB_CUDA(cudaMemcpyAsync(dst + static_cast<size_t>(mm) * pb, h->src[static_cast<size_t>(q)], pb,
+                               cudaMemcpyDefault, s));
+    }
+    TGB_CUDA(cudaEventRecord(r->ev_ldone, s));
+    h->rendezvous();  // every reader has enqueued its copy of every pack
+    local_wait_all(r, true, s);
+    return;
+  }
+  NCCL_CHECK(nccl::api().GroupStart());
+  for (int mm = 0; mm < i; ++mm)
+    NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, dst + static_cast<size_t>(mm) * pb, pb, ncclChar, team * i + mm,
+                                     r->gcomm, s));
+  NCCL_CHECK(nccl::api().GroupEnd());
+}
+
+// Applies the gathered packs in ascending member order (later members win on
+// equal nodes: memory_daemon.hpp:35-38).
+void apply_gathered(tgnn_run* r, cudaStream_t s) {
+  tgnn_trainer* tr = r->tr.get();
+  const size_t pb = tr->w.wpack_bytes;
+  std::vector<WriteSet> sets;
+  for (int mm = 0; mm < r->tc.i; ++mm)
+    sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, 2 * tr->cap_B,
+                             tr->m.d_mem));
+  apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+}
+
 
 tgnn_memstore* memstore_new(tgnn_ctx* ctx, int64_t N, int64_t d) {
   TGB_REQUIRE(N > 0 && d > 0, kConfig, "memstore: invalid shape");
@@ -657,6 +877,21 @@ void plan_explicit(tgnn_trainer* tr, int slot, int64_t begin, int64_t end, const
   TGB_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// DaemonOp::Snapshot (memory_daemon.hpp:94-105): the replica's memory and
+// last_update after the write bracket of `pair`, when the pair closes its
+// segment (parallel.hpp:288-290).
+void take_snapshot(tgnn_run* r, int64_t pair, cudaStream_t s) {
+  if (pair < 0 || pair >= static_cast<int64_t>(r->snap_slot.size())) return;
+  const int64_t slot = r->snap_slot[static_cast<size_t>(pair)];
+  if (slot < 0) return;
+  const DMem& st = r->mem->d;
+  TGB_CUDA(cudaMemcpyAsync(r->d_snap_mem + slot * st.N * st.d, st.memory, sizeof(float) * st.N * st.d,
+                           cudaMemcpyDeviceToDevice, s));
+  TGB_CUDA(cudaMemcpyAsync(r->d_snap_lu + slot * st.N, st.last_update, sizeof(double) * st.N,
+                           cudaMemcpyDeviceToDevice, s));
+  r->snap_taken = std::max(r->snap_taken, slot + 1);
+}
+
 // One barrier of a run on this rank (TrainerCore::iterate + the daemon's
 // read/write brackets + average_active_grads + Adam::step).
 void run_barrier(tgnn_run* r, int64_t b) {
@@ -710,22 +945,11 @@ void run_barrier(tgnn_run* r, int64_t b) {
           oplog_record_launch(sc, op, r->d_oplog, b, s);
         }
       }
-      const size_t pb = tr->w.wpack_bytes;
-      const int cap = 2 * tr->cap_B;
       if (r->group_size > 1) {
-        NCCL_CHECK(nccl::api().GroupStart());
-        for (int mm = 0; mm < i; ++mm) {
-          const int root = tt * i + mm;
-          char* dst = static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb;
-          NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, dst, pb, ncclChar, root, r->gcomm, s));
-        }
-        NCCL_CHECK(nccl::api().GroupEnd());
-        std::vector<WriteSet> sets;
-        for (int mm = 0; mm < i; ++mm)
-          sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap,
-                                   tr->m.d_mem));
-        apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+        comm_bcast_packs(r, tt, s);
+        apply_gathered(r, s);
       }
+      if (r->snaps) take_snapshot(r, (b / j) * j + tt, s);
     }
     if (t.active) {
       substep_rest_launch(sc, tr->plans[0], tr->views[0], loss_slot, s);
@@ -744,9 +968,7 @@ void run_barrier(tgnn_run* r, int64_t b) {
   }
   // average_active_grads (trainer.hpp:473-483): idle ranks contribute zeros.
   sc.mark(phAllreduce, s);
-  if (r->nranks > 1)
-    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
-                             r->comm, s));
+  comm_allreduce(r, tr->grads, static_cast<size_t>(tr->L.total), RedTy::F32, RedOp::Sum, s);
   const int64_t active = r->sched.active_trainers[static_cast<size_t>(b)];
   sc.mark(phAdam, s);
   tr->adam_t = b;  // Adam's step counter advances on every rank at every barrier
@@ -774,8 +996,7 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
   if (c != r->ctx->br) TGB_CUDA(cudaStreamWaitEvent(c, r->ev_brjoin, 0));  // the branch's tail gradients
   cudaStream_t u = c;  // the tail update
   if (r->nranks > 1) {
-    if (r->peer_ok) peer_allreduce_launch(r->peer, split, tr->L.total - split, r->d_ctr, 0, c);
-    else NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),
+    NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),
                                           ncclFloat, ncclSum, r->comm, c));
     // the tail Adam on the (idle by now) branch stream, so the head bucket's
     // all-reduce does not queue behind it on the comm stream
@@ -788,8 +1009,7 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
     TGB_CUDA(cudaEventRecord(r->ev_upd, u));
     TGB_CUDA(cudaEventRecord(r->ev_head, s));
     TGB_CUDA(cudaStreamWaitEvent(c, r->ev_head, 0));
-    if (r->peer_ok) peer_allreduce_launch(r->peer, 0, split, r->d_ctr, 1, c);
-    else NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(split), ncclFloat, ncclSum, r->comm, c));
+    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(split), ncclFloat, ncclSum, r->comm, c));
     adam_pack_launch(sc, tr->am, tr->av, c, r->d_desc, r->d_ctr, 0, split);
     TGB_CUDA(cudaEventRecord(r->ev_comm, c));
     TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
@@ -883,24 +1103,17 @@ void barrier_body_slot(tgnn_run* r, int p, bool xg_split) {
       op.supports[0] = pl.supports;
       oplog_record_launch(sc, op, r->d_oplog, 0, ws);
     }
-    const size_t pb = tr->w.wpack_bytes;
-    const int cap = 2 * tr->cap_B;
     if (r->group_size > 1) {
-      NCCL_CHECK(nccl::api().GroupStart());
-      for (int mm = 0; mm < r->tc.i; ++mm)
-        NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb,
-                                         pb, ncclChar, mm, r->gcomm, s));
-      NCCL_CHECK(nccl::api().GroupEnd());
-      std::vector<WriteSet> sets;
-      for (int mm = 0; mm < r->tc.i; ++mm)
-        sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, cap, tr->m.d_mem));
-      apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+      comm_bcast_packs(r, 0, s);
+      apply_gathered(r, s);
     }
     // join: the next barrier reads the memory copy once this barrier's writes landed
     TGB_CUDA(cudaEventRecord(r->ev_written, ws));
     // the next read (reset, gather, GRU-input view columns) starts after this
     // barrier's decoder, not beside its projections (TGNN_AUXMID; A/B: 1 best)
-    static const int mid_at = [] { const char* e = std::getenv("TGNN_AUXMID"); return e ? std::atoi(e) : 1; }();
+    // (0: beside the projections; 1 after the decoder, 2 after the attention
+    // backward kernel -- recorded on every GEMM engine)
+    static const int mid_at = env_knob("TGNN_AUXMID", 1, 0, 2);
     auto next_read = [&] {
       TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_written, 0));
       if (mid_at > 0) TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_mid, 0));
@@ -968,7 +1181,7 @@ void barrier_body_stint(tgnn_run* r, int sidx) {
   try {
     if (sidx == 0) {
       for (int tt = 0; tt < j; ++tt) {
-        reset_stint_kernel<<<4 * kSMs, 256, 0, s>>>(r->mem->d, r->d_stint, r->d_ctr, tt);
+        reset_stint_kernel<<<4 * num_sms(), 256, 0, s>>>(r->mem->d, r->d_stint, r->d_ctr, tt);
         TGB_CUDA(cudaGetLastError());
         if (tt == r->team) {
           for (int sub = 0; sub < j; ++sub) {
@@ -990,17 +1203,8 @@ void barrier_body_stint(tgnn_run* r, int sidx) {
             oplog_record_launch(sc, op, r->d_oplog, 0, s);
           }
         }
-        const size_t pb = tr->w.wpack_bytes;
-        NCCL_CHECK(nccl::api().GroupStart());
-        for (int mm = 0; mm < i; ++mm)
-          NCCL_CHECK(nccl::api().Broadcast(tr->w.wpack, static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, pb,
-                                           ncclChar, tt * i + mm, r->gcomm, s));
-        NCCL_CHECK(nccl::api().GroupEnd());
-        std::vector<WriteSet> sets;
-        for (int mm = 0; mm < i; ++mm)
-          sets.push_back(pack_view(static_cast<char*>(r->gathered) + static_cast<size_t>(mm) * pb, 2 * tr->cap_B,
-                                   tr->m.d_mem));
-        apply_writes_launch(sets, r->mem->d, r->mem->win, s);
+        comm_bcast_packs(r, tt, s);
+        apply_gathered(r, s);
       }
       substep_rest_launch(sc, tr->plans[0], tr->views[0], r->d_losses, s);
       // the later subs' routing sorts ran on the side stream: join them here
@@ -1010,9 +1214,7 @@ void barrier_body_stint(tgnn_run* r, int sidx) {
       pl.ev_sorted = nullptr;  // sorted inside the stint-start graph
       substep_launch(sc, pl, tr->views[static_cast<size_t>(sidx)], r->d_losses, s);
     }
-    if (r->nranks > 1)
-      NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(tr->L.total), ncclFloat, ncclSum,
-                                       r->comm, s));
+    comm_allreduce(r, tr->grads, static_cast<size_t>(tr->L.total), RedTy::F32, RedOp::Sum, s);
     adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr);
     incr_launch(r->d_ctr, s);
   } catch (...) {
@@ -1169,13 +1371,10 @@ uint64_t check_replicas(tgnn_run* r) {
   cudaStream_t s = r->ctx->stream;
   unsigned long long* d = dalloc<unsigned long long>(3);
   params_hash_launch(r->tr->params, r->tr->L.total, d, s);
-  if (r->nranks > 1) {
-    NCCL_CHECK(nccl::api().AllReduce(d, d + 1, 1, ncclUint64, ncclMin, r->comm, s));
-    NCCL_CHECK(nccl::api().AllReduce(d, d + 2, 1, ncclUint64, ncclMax, r->comm, s));
-  } else {
-    TGB_CUDA(cudaMemcpyAsync(d + 1, d, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-    TGB_CUDA(cudaMemcpyAsync(d + 2, d, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-  }
+  TGB_CUDA(cudaMemcpyAsync(d + 1, d, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+  TGB_CUDA(cudaMemcpyAsync(d + 2, d, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+  comm_allreduce(r, d + 1, 1, RedTy::U64, RedOp::Min, s);
+  comm_allreduce(r, d + 2, 1, RedTy::U64, RedOp::Max, s);
   unsigned long long h[3];
   TGB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
   TGB_CUDA(cudaStreamSynchronize(s));
@@ -1207,87 +1406,6 @@ void run_eval_point(tgnn_run* r, int64_t b) {
 
 }  // namespace
 
-namespace {
-
-// Maps every rank's gradient buffer and flag block into every rank (CUDA IPC,
-// handles exchanged with one NCCL reduction of a byte table). All ranks agree
-// (NCCL min) before the peer path is used; any failure keeps NCCL.
-// Opt-in with TGNN_ALLREDUCE=peer: measured at N = 2 / 4 it is 2-4 % slower
-// per barrier than NCCL's bucketed all-reduce here (its CTAs compete with the
-// overlapped GRU backward), so NCCL stays the default.
-void peer_setup(tgnn_run* r) {
-  const char* env = std::getenv("TGNN_ALLREDUCE");
-  int want = (env && std::string(env) == "peer") && r->nranks <= kPeerMax ? 1 : 0;
-  cudaStream_t s = r->ctx->stream;
-  constexpr int kH = static_cast<int>(sizeof(cudaIpcMemHandle_t));
-  const size_t table = static_cast<size_t>(r->nranks) * 3 * kH;
-  std::vector<uint8_t> h(table, 0);
-  int ok = want;
-  if (ok) {
-    r->peer_flags = dalloc<unsigned>(3 * kPeerMax + 2);
-    TGB_CUDA(cudaMemset(r->peer_flags, 0, sizeof(unsigned) * (3 * kPeerMax + 2)));
-    r->peer_recv = dalloc<float>(static_cast<size_t>(r->tr->L.total + 8 * kPeerMax));
-    cudaIpcMemHandle_t hg, hf, hr;
-    if (cudaIpcGetMemHandle(&hg, r->tr->grads) != cudaSuccess ||
-        cudaIpcGetMemHandle(&hf, r->peer_flags) != cudaSuccess ||
-        cudaIpcGetMemHandle(&hr, r->peer_recv) != cudaSuccess) {
-      cudaGetLastError();
-      ok = 0;
-    } else {
-      std::memcpy(h.data() + static_cast<size_t>(r->rank) * 3 * kH, &hg, kH);
-      std::memcpy(h.data() + static_cast<size_t>(r->rank) * 3 * kH + kH, &hf, kH);
-      std::memcpy(h.data() + static_cast<size_t>(r->rank) * 3 * kH + 2 * kH, &hr, kH);
-    }
-  }
-  uint8_t* d_h = dalloc<uint8_t>(table);
-  TGB_CUDA(cudaMemcpy(d_h, h.data(), table, cudaMemcpyHostToDevice));
-  NCCL_CHECK(nccl::api().AllReduce(d_h, d_h, table, ncclUint8, ncclSum, r->comm, s));
-  TGB_CUDA(cudaMemcpyAsync(h.data(), d_h, table, cudaMemcpyDeviceToHost, s));
-  TGB_CUDA(cudaStreamSynchronize(s));
-  cudaFree(d_h);
-  PeerAR& p = r->peer;
-  p.rank = r->rank;
-  p.n = r->nranks;
-  p.err = r->ctx->d_flag;
-  if (ok) {
-    for (int q = 0; q < r->nranks && ok; ++q) {
-      if (q == r->rank) {
-        p.buf[q] = r->tr->grads;
-        p.flags[q] = r->peer_flags;
-        p.recv[q] = r->peer_recv;
-        continue;
-      }
-      cudaIpcMemHandle_t hg, hf, hr;
-      std::memcpy(&hg, h.data() + static_cast<size_t>(q) * 3 * kH, kH);
-      std::memcpy(&hf, h.data() + static_cast<size_t>(q) * 3 * kH + kH, kH);
-      std::memcpy(&hr, h.data() + static_cast<size_t>(q) * 3 * kH + 2 * kH, kH);
-      void *pg = nullptr, *pf = nullptr, *pr = nullptr;
-      if (cudaIpcOpenMemHandle(&pg, hg, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-          cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-          cudaIpcOpenMemHandle(&pr, hr, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        cudaGetLastError();
-        ok = 0;
-        break;
-      }
-      r->peer_opened.push_back(pg);
-      r->peer_opened.push_back(pf);
-      r->peer_opened.push_back(pr);
-      p.buf[q] = static_cast<float*>(pg);
-      p.flags[q] = static_cast<unsigned*>(pf);
-      p.recv[q] = static_cast<float*>(pr);
-    }
-    p.cnt = r->peer_flags + 3 * kPeerMax;
-  }
-  int* d_ok = dalloc<int>(1);
-  TGB_CUDA(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
-  NCCL_CHECK(nccl::api().AllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, r->comm, s));
-  TGB_CUDA(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, s));
-  TGB_CUDA(cudaStreamSynchronize(s));
-  cudaFree(d_ok);
-  r->peer_ok = ok != 0;
-}
-
-}  // namespace
 
 // ----------------------------------------------------------------- C ABI
 extern "C" {
@@ -1999,6 +2117,19 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
     r->d_oplog = dalloc<int64_t>(static_cast<size_t>(4 * nb));
     TGB_CUDA(cudaMemset(r->d_oplog, 0, sizeof(int64_t) * 4 * nb));
   }
+  r->snaps = opt->segment_snapshots != 0;
+  if (r->snaps) {
+    const auto& ps = r->sched.groups[static_cast<size_t>(r->group)];
+    r->snap_slot.assign(ps.size(), -1);
+    for (size_t x = 0; x < ps.size(); ++x) {
+      if (!r->sched.snapshot_after(ps[x])) continue;
+      r->snap_slot[x] = static_cast<int64_t>(r->snap_meta.size());
+      r->snap_meta.push_back({static_cast<int64_t>(ps[x].sweep), static_cast<int64_t>(ps[x].segment)});
+    }
+    const size_t n = std::max<size_t>(r->snap_meta.size(), 1);
+    r->d_snap_mem = dalloc<float>(n * static_cast<size_t>(g->d.N * m.d_mem));
+    r->d_snap_lu = dalloc<double>(n * static_cast<size_t>(g->d.N));
+  }
   r->val_begin = opt->val_begin;
   r->val_end = opt->val_end;
   r->eval_batch = opt->eval_batch;
@@ -2007,7 +2138,7 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
               "run: validation range out of bounds");
   TGB_REQUIRE(r->eval_negatives >= 0 && r->eval_batch >= 0, kConfig, "run: invalid evaluation options");
   TGB_CUDA(cudaEventCreate(&r->ev_t0));
-  r->use_graphs = opt->use_graphs != 0 && r->tc.j <= kMaxStintJ;
+  r->use_graphs = opt->use_graphs != 0 && r->tc.j <= kMaxStintJ && !r->snaps;
   if (r->use_graphs && r->tc.j > 1) {
     std::vector<StintDesc> sd(static_cast<size_t>(r->sched.barriers + 1));
     for (int64_t b = 0; b < r->sched.barriers; b += r->tc.j) {
@@ -2070,6 +2201,7 @@ int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128) {
   API_BEGIN
   r->ctx->use();
   if (r->nranks == 1) return 0;
+  TGB_REQUIRE(!r->comm_ready, kProtocol, "run: communicator already initialised");
   ncclUniqueId id;
   std::memcpy(&id, unique_id128, 128);
   NCCL_CHECK(nccl::api().CommInitRank(&r->comm, r->nranks, id, r->rank));
@@ -2079,7 +2211,52 @@ int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128) {
   TGB_CUDA(cudaEventCreateWithFlags(&r->ev_tail, cudaEventDisableTiming));
   TGB_CUDA(cudaEventCreateWithFlags(&r->ev_head, cudaEventDisableTiming));
   TGB_CUDA(cudaEventCreateWithFlags(&r->ev_comm, cudaEventDisableTiming));
-  peer_setup(r);
+  r->comm_ready = true;
+  API_END
+}
+
+int tgnn_local_hub_create(int32_t nranks, tgnn_local_hub** out) {
+  API_BEGIN
+  TGB_REQUIRE(nranks >= 1 && nranks <= kLocalMax, kConfig, "local hub: rank count must lie in [1, 16]");
+  auto* h = new tgnn_local_hub();
+  h->n = nranks;
+  h->runs.assign(static_cast<size_t>(nranks), nullptr);
+  h->src.assign(static_cast<size_t>(nranks), nullptr);
+  *out = h;
+  API_END
+}
+
+int tgnn_local_hub_destroy(tgnn_local_hub* h) {
+  API_BEGIN
+  delete h;
+  API_END
+}
+
+int tgnn_run_local_init(tgnn_run* r, tgnn_local_hub* h) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(h != nullptr && h->n == r->nranks, kConfig, "local hub: rank count differs from the run's");
+  TGB_REQUIRE(!r->comm_ready, kProtocol, "run: communicator already initialised");
+  if (r->nranks == 1) return 0;
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_lready, cudaEventDisableTiming));
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_ldone, cudaEventDisableTiming));
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    TGB_REQUIRE(h->runs[static_cast<size_t>(r->rank)] == nullptr, kProtocol, "local hub: rank attached twice");
+    h->runs[static_cast<size_t>(r->rank)] = r;
+  }
+  r->hub = h;
+  // collectives are host rendezvous at enqueue time: barriers run on the
+  // direct (stream-ordered) path, not from captured graphs
+  r->use_graphs = false;
+  h->rendezvous();  // every rank attached
+  for (int q = 0; q < h->n; ++q) {
+    const int dev = h->runs[static_cast<size_t>(q)]->ctx->device;
+    if (dev == r->ctx->device) continue;
+    const cudaError_t e = cudaDeviceEnablePeerAccess(dev, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) TGB_CUDA(e);
+    cudaGetLastError();
+  }
   r->comm_ready = true;
   API_END
 }
@@ -2104,6 +2281,7 @@ int tgnn_run_info(tgnn_run* r, int64_t* barriers, int64_t* param_count) {
 int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
   API_BEGIN
   r->ctx->use();
+  HubGuard guard(r);
   TGB_REQUIRE(first == r->next_barrier, kProtocol, "run: barriers must be issued in order");
   TGB_REQUIRE(first + count <= r->sched.barriers, kConfig, "run: barrier range past the schedule");
   TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
@@ -2151,6 +2329,7 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
     b = seg_end;
   }
   r->next_barrier = stop;
+  guard.ok();
   API_END
 }
 
@@ -2158,14 +2337,15 @@ int tgnn_run_losses(tgnn_run* r, int64_t first, int64_t count, double* out) {
   API_BEGIN
   r->ctx->use();
   TGB_REQUIRE(first >= 0 && first + count <= r->next_barrier, kConfig, "run: loss range not yet run");
+  HubGuard guard(r);
   cudaStream_t s = r->ctx->stream;
   double* tmp = dalloc<double>(static_cast<size_t>(std::max<int64_t>(count, 1)));
   TGB_CUDA(cudaMemcpyAsync(tmp, r->d_losses + first, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
-  if (r->nranks > 1)
-    NCCL_CHECK(nccl::api().AllReduce(tmp, tmp, static_cast<size_t>(count), ncclDouble, ncclSum, r->comm, s));
+  comm_allreduce(r, tmp, static_cast<size_t>(count), RedTy::F64, RedOp::Sum, s);
   d2h(out, tmp, static_cast<size_t>(count), s);
   r->ctx->check_numeric();
   cudaFree(tmp);
+  guard.ok();
   for (int64_t b = 0; b < count; ++b) {
     const int64_t a = r->sched.active_trainers[static_cast<size_t>(first + b)];
     out[b] = a > 0 ? out[b] / static_cast<double>(a) : 0.0;
@@ -2354,7 +2534,71 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes, int3
   int32_t sz[kSzCount];
   TGB_CUDA(cudaMemcpy(sz, r->tr->plans[r->use_graphs && r->tc.j == 1 && !direct ? static_cast<size_t>(b & 1) : 0].sizes, sizeof(sz),
                       cudaMemcpyDeviceToHost));
+  TGB_CUDA(cudaMemcpy(&sz[7], r->tr->w.w_count, sizeof(int32_t), cudaMemcpyDeviceToHost));  // W root writes
   for (int x = 0; x < kSzCount; ++x) sizes[x] = sz[x];
+  API_END
+}
+
+int tgnn_run_gemm_profile(tgnn_run* r, int64_t cap, int64_t* count, double* rows) {
+  API_BEGIN
+  r->ctx->use();
+  TGB_REQUIRE(r->next_barrier < r->sched.barriers, kConfig, "run: no barrier left to profile");
+  TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
+  TGB_REQUIRE(gemm_impl() == kGemmTma, kConfig, "run: the GEMM profile covers the tcgen05 TMA engine");
+  HubGuard guard(r);
+  const int64_t b = r->next_barrier;
+  tc_trace_begin();
+  try {
+    run_barrier(r, b);
+  } catch (...) {
+    for (auto& e : tc_trace_end()) {
+      cudaEventDestroy(e.e0);
+      cudaEventDestroy(e.e1);
+    }
+    throw;
+  }
+  std::vector<TcTraceEntry> tr = tc_trace_end();
+  ++r->next_barrier;
+  r->prepared = -1;
+  TGB_CUDA(cudaStreamSynchronize(r->ctx->stream));
+  r->ctx->check_numeric();
+  *count = static_cast<int64_t>(tr.size());
+  for (size_t x = 0; x < tr.size(); ++x) {
+    const TcTraceEntry& e = tr[x];
+    float ms = 0.0f;
+    TGB_CUDA(cudaEventElapsedTime(&ms, e.e0, e.e1));
+    double flops = 0.0, bytes = 0.0;
+    int maxm = 0, maxs = 1;
+    for (int q = 0; q < e.count; ++q) {
+      int64_t M = e.M[q], K = e.K[q];
+      const int64_t N = e.N[q];
+      int v = 0;
+      if (e.M_dev[q]) {
+        TGB_CUDA(cudaMemcpy(&v, e.M_dev[q], sizeof(int), cudaMemcpyDeviceToHost));
+        M = std::min<int64_t>(M, v);
+      }
+      if (e.K_dev[q]) {
+        TGB_CUDA(cudaMemcpy(&v, e.K_dev[q], sizeof(int), cudaMemcpyDeviceToHost));
+        K = std::min<int64_t>(K, v);
+      }
+      flops += 2.0 * static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K);
+      bytes += 4.0 * static_cast<double>(M * K + N * K + M * N);
+      maxm = std::max<int>(maxm, static_cast<int>(M));
+      maxs = std::max(maxs, e.splits[q]);
+    }
+    if (static_cast<int64_t>(x) < cap) {
+      double* o = rows + 6 * x;
+      o[0] = ms;
+      o[1] = flops;
+      o[2] = bytes;
+      o[3] = e.count;
+      o[4] = maxm;
+      o[5] = maxs;
+    }
+    cudaEventDestroy(e.e0);
+    cudaEventDestroy(e.e1);
+  }
+  guard.ok();
   API_END
 }
 
@@ -2364,13 +2608,30 @@ int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t
   tgnn_ctx* ctx = g->ctx;
   ctx->use();
   TGB_REQUIRE(first >= 0 && count >= 0 && first + count <= g->d.E, kConfig, "ingest: range out of bounds");
-  // copies on the ingestion stream: they overlap work enqueued earlier (which
-  // never reads events past its own barrier) and are ordered before any work
-  // enqueued after this call
+  // copies on the ingestion stream: they overlap work enqueued earlier and
+  // are ordered before any work enqueued after this call
   cudaStream_t s = ctx->h2d;
-  h2d(g->d.src + first, src, static_cast<size_t>(count), s);
-  h2d(g->d.dst + first, dst, static_cast<size_t>(count), s);
-  h2d(g->d.t + first, t, static_cast<size_t>(count), s);
+  if (count > g->st_cap) {
+    TGB_CUDA(cudaStreamSynchronize(s));
+    for (void* p : {static_cast<void*>(g->st_src), static_cast<void*>(g->st_dst), static_cast<void*>(g->st_t)})
+      if (p) cudaFree(p);
+    g->st_src = dalloc<int32_t>(static_cast<size_t>(count));
+    g->st_dst = dalloc<int32_t>(static_cast<size_t>(count));
+    g->st_t = dalloc<double>(static_cast<size_t>(count));
+    g->st_cap = count;
+  }
+  // the index data lands in staging and is checked against the T-CSR's
+  // events (bitwise; a mismatch fails the next synchronising call with
+  // TGNN_PROTOCOL); the indexed arrays themselves are never rewritten, so
+  // planning work already enqueued cannot race with this copy
+  h2d(g->st_src, src, static_cast<size_t>(count), s);
+  h2d(g->st_dst, dst, static_cast<size_t>(count), s);
+  h2d(g->st_t, t, static_cast<size_t>(count), s);
+  if (count > 0) {
+    ingest_verify_kernel<<<static_cast<int>(std::min<int64_t>((count + 255) / 256, 2 * num_sms())), 256, 0, s>>>(
+        g->st_src, g->st_dst, g->st_t, g->d.src + first, g->d.dst + first, g->d.t + first, count, ctx->d_flag);
+    TGB_CUDA(cudaGetLastError());
+  }
   if (g->d.d_e > 0 && efeat) {
     if (g->d.d_e == g->d.d_e_pad) {
       h2d(g->d.efeat + first * g->d.d_e_pad, efeat, static_cast<size_t>(count * g->d.d_e), s);
@@ -2674,11 +2935,36 @@ int tgnn_run_loss_async(tgnn_run* r, int64_t b, double* dst) {
 }
 
 
+int tgnn_run_snapshots(tgnn_run* r, int64_t* count, int64_t* meta, double* memory, double* last_update) {
+  API_BEGIN
+  r->ctx->use();
+  *count = r->snap_taken;
+  if (!meta && !memory && !last_update) return 0;
+  TGB_CUDA(cudaStreamSynchronize(r->ctx->stream));
+  const int64_t N = r->mem->d.N, d = r->mem->d.d;
+  std::vector<float> mf(static_cast<size_t>(N * d));
+  for (int64_t x = 0; x < r->snap_taken; ++x) {
+    if (meta) {
+      meta[2 * x] = r->snap_meta[static_cast<size_t>(x)][0];
+      meta[2 * x + 1] = r->snap_meta[static_cast<size_t>(x)][1];
+    }
+    if (memory) {
+      TGB_CUDA(cudaMemcpy(mf.data(), r->d_snap_mem + x * N * d, sizeof(float) * mf.size(), cudaMemcpyDeviceToHost));
+      for (int64_t q = 0; q < N * d; ++q) memory[x * N * d + q] = mf[static_cast<size_t>(q)];
+    }
+    if (last_update)
+      TGB_CUDA(cudaMemcpy(last_update + x * N, r->d_snap_lu + x * N, sizeof(double) * N, cudaMemcpyDeviceToHost));
+  }
+  API_END
+}
+
 int tgnn_run_check_replicas(tgnn_run* r, uint64_t* hash_out) {
   API_BEGIN
   r->ctx->use();
   TGB_REQUIRE(r->nranks == 1 || r->comm_ready, kProtocol, "run: communicator not initialised");
+  HubGuard guard(r);
   *hash_out = check_replicas(r);
+  guard.ok();
   API_END
 }
 

@@ -1,6 +1,7 @@
 // Shared device/host helpers for the B200 DistTGL training step.
 #pragma once
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -100,7 +101,32 @@ __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf
 
 #endif  // __CUDACC__
 
-constexpr int kSMs = 148;
+// SM count of the current device (cudaDevAttrMultiProcessorCount; 148 on
+// B200), cached per device: every grid size, split-K policy and CTA budget
+// scales with it.
+inline int num_sms() {
+  static int cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  int& c = cache[dev & 63];
+  if (c == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    c = v;
+  }
+  return c;
+}
+
+// Validated integer knob from the environment (A/B switches): the default
+// unless the variable parses completely as an integer in [lo, hi].
+inline int env_knob(const char* name, int def, int lo, int hi) {
+  const char* e = std::getenv(name);
+  if (!e || !*e) return def;
+  char* end = nullptr;
+  const long v = std::strtol(e, &end, 10);
+  if (end == e || *end != '\0' || v < lo || v > hi) return def;
+  return static_cast<int>(v);
+}
 
 #ifdef __CUDACC__
 template <typename... KArgs, typename... Args>

@@ -14,6 +14,7 @@
 //     stage s^1; tcgen05.commit -> mbarrier releases a stage;
 //   * epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32(w%4).. = rows),
 //     alpha/beta/bias, or a split-K partial for the in-order reduction.
+#include <mutex>
 #include <cuda_bf16.h>
 
 #include "gemm_simt.cuh"
@@ -344,11 +345,15 @@ __global__ void __launch_bounds__(TNT2, 1) gemm_tc_kernel(const __grid_constant_
 void splitk_reduce_launch(const GemmGroup& g, cudaStream_t s);
 
 void gemm_tc_prepare() {
-  static bool attr_set = false;
-  if (!attr_set) {
-    TGB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBytes));
-    attr_set = true;
+  // the attribute is per device: set it once on every device this process uses
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  TGB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!(done >> dev & 1ull)) {
+    TGB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    done |= 1ull << dev;
   }
 }
 

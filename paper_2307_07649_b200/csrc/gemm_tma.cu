@@ -593,10 +593,7 @@ struct KeyHash {
 
 // TGNN_TC_BULK (bit mask, default 7): 1 plain stores, 2 split-K partials, 4 reduce-add;
 // 0 forces the per-lane epilogue stores (A/B measurements)
-int g_tc_bulk_store = [] {
-  const char* e = std::getenv("TGNN_TC_BULK");
-  return e ? std::atoi(e) : 7;
-}();
+int g_tc_bulk_store = env_knob("TGNN_TC_BULK", 7, 0, 7);
 
 BfMat bf_alloc(int64_t rows, int64_t cols) {
   BfMat m;
@@ -612,7 +609,7 @@ BfMat bf_alloc(int64_t rows, int64_t cols) {
 
 void bf_from_f32(const BfMat& m, const float* src, int64_t rows, int64_t cols, int64_t ld_src, cudaStream_t s) {
   if (rows * cols == 0) return;
-  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(rows * cols, 256), 4 * kSMs));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(rows * cols, 256), 4 * num_sms()));
   launch_pdl(bf_from_f32_kernel, dim3(blocks), dim3(256), 0, s, m, src, rows, cols, ld_src);
   TGB_CUDA(cudaGetLastError());
 }
@@ -644,11 +641,33 @@ TmaOp tma_view(const BfMat& m, int64_t col0, int64_t cols, int64_t rows, bool km
 }
 
 void tc_gemm_prepare() {
-  static bool attr = false;
-  if (!attr) {
+  // the attribute is per device: set it once on every device this process uses
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  TGB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!(done >> dev & 1ull)) {
     TGB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-    attr = true;
+    done |= 1ull << dev;
   }
+}
+
+namespace {
+thread_local std::vector<TcTraceEntry>* g_trace = nullptr;
+}
+
+void tc_trace_begin() {
+  delete g_trace;
+  g_trace = new std::vector<TcTraceEntry>();
+}
+
+std::vector<TcTraceEntry> tc_trace_end() {
+  std::vector<TcTraceEntry> out;
+  if (g_trace) out.swap(*g_trace);
+  delete g_trace;
+  g_trace = nullptr;
+  return out;
 }
 
 void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_stream, cudaEvent_t ev) {
@@ -698,15 +717,33 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_strea
   const int fixed = 1024 + 256;
   int budget = kSmemMax - fixed;
   const int half = 113 * 1024 - kEpiStageB - fixed;  // two CTAs per SM
-  if (total_tiles > kSMs && half / gp.stage_bytes >= 2 && cols <= 256) budget = half;
+  if (total_tiles > num_sms() && half / gp.stage_bytes >= 2 && cols <= 256) budget = half;
   gp.stages = std::max(2, std::min(kStMax, budget / gp.stage_bytes));
   const int smem = gp.stages * gp.stage_bytes + fixed;
   int ctas_per_sm = (228 * 1024) / (smem + kEpiStageB + 1024);
   if (ctas_per_sm < 1) ctas_per_sm = 1;
   if (ctas_per_sm * cols > 512) ctas_per_sm = 512 / cols;
-  const int grid = std::min(gp.tile_base[g.count], kSMs * ctas_per_sm);
+  const int grid = std::min(gp.tile_base[g.count], num_sms() * ctas_per_sm);
+  TcTraceEntry* tr = nullptr;
+  if (g_trace) {
+    g_trace->emplace_back();
+    tr = &g_trace->back();
+    TGB_CUDA(cudaEventCreate(&tr->e0));
+    TGB_CUDA(cudaEventCreate(&tr->e1));
+    tr->count = g.count;
+    for (int i = 0; i < g.count; ++i) {
+      tr->M[i] = g.p[i].M;
+      tr->N[i] = g.p[i].N;
+      tr->K[i] = g.p[i].K;
+      tr->splits[i] = g.p[i].splits;
+      tr->M_dev[i] = g.p[i].M_dev;
+      tr->K_dev[i] = g.p[i].K_dev;
+    }
+    TGB_CUDA(cudaEventRecord(tr->e0, s));
+  }
   launch_pdl(tc_gemm_kernel, dim3(grid), dim3(kThreads), smem, s, gp);
   TGB_CUDA(cudaGetLastError());
+  if (tr) TGB_CUDA(cudaEventRecord(tr->e1, s));
   if (any_split) {
     cudaStream_t rs = s;
     if (reduce_stream && ev) {  // the split outputs are leaves: reduce them off the critical path
@@ -749,17 +786,17 @@ void tc_debug_bench(int M, int N, int K, int ntile, int iters, double* us, unsig
   TGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   *us = 1e3 * ms / iters;
   const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, T.ntile));
-  *grid_out = std::min(tiles, kSMs * 2);
+  *grid_out = std::min(tiles, num_sms() * 2);
   if (trace_out) {
     unsigned long long* d = nullptr;
-    TGB_CUDA(cudaMalloc(&d, sizeof(unsigned long long) * 16 * 2 * kSMs));
-    TGB_CUDA(cudaMemset(d, 0, sizeof(unsigned long long) * 16 * 2 * kSMs));
+    TGB_CUDA(cudaMalloc(&d, sizeof(unsigned long long) * 16 * 2 * num_sms()));
+    TGB_CUDA(cudaMemset(d, 0, sizeof(unsigned long long) * 16 * 2 * num_sms()));
     TGB_CUDA(cudaMemcpyToSymbol(g_tc_trace, &d, sizeof(d)));
     tc_group_launch(tg, nullptr);
     TGB_CUDA(cudaDeviceSynchronize());
     unsigned long long* z = nullptr;
     TGB_CUDA(cudaMemcpyToSymbol(g_tc_trace, &z, sizeof(z)));
-    TGB_CUDA(cudaMemcpy(trace_out, d, sizeof(unsigned long long) * 16 * 2 * kSMs, cudaMemcpyDeviceToHost));
+    TGB_CUDA(cudaMemcpy(trace_out, d, sizeof(unsigned long long) * 16 * 2 * num_sms(), cudaMemcpyDeviceToHost));
     cudaFree(d);
   }
   cudaEventDestroy(e0);

@@ -10,6 +10,8 @@
 // The kernel computes D = A_hi B_hi + A_hi B_lo + A_lo B_hi (fp32 in TMEM).
 #pragma once
 
+#include <vector>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -83,6 +85,20 @@ inline int tc_ntile(int N, int cap = 256) {
   const int w = (N + tiles - 1) / tiles;
   return static_cast<int>(std::min<int64_t>(cap, (w + 15) / 16 * 16));
 }
+
+// GEMM launch trace (bench.py's kernel roofline): while a trace is active on
+// the calling thread, every tc_group_launch brackets its tcgen05 kernel with
+// CUDA events and records the group's problem shapes (capacities plus the
+// device pointers of the runtime row counts).
+struct TcTraceEntry {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int count = 0;
+  int M[kMaxTc] = {}, N[kMaxTc] = {}, K[kMaxTc] = {}, splits[kMaxTc] = {};
+  const int* M_dev[kMaxTc] = {};
+  const int* K_dev[kMaxTc] = {};
+};
+void tc_trace_begin();
+std::vector<TcTraceEntry> tc_trace_end();  // caller destroys the events
 
 extern int g_tc_bulk_store;  // 0: per-lane epilogue stores only (A/B switch)
 

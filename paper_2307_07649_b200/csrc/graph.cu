@@ -29,7 +29,7 @@ T* dmalloc(size_t n) {
 }
 
 inline int grid_for(int64_t n, int threads = 256) {
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), 16 * kSMs)));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), 16 * num_sms())));
 }
 
 __global__ void unsorted_kernel(const double* __restrict__ t, int64_t E, int* flag) {

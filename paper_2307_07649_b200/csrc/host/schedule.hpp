@@ -72,6 +72,13 @@ class Schedule {
   std::vector<std::pair<int64_t, int64_t>> batches;
   std::vector<std::vector<Stint>> groups;          // per memory copy
   std::vector<int64_t> active_trainers, traversed_after, eval_barriers;
+  std::vector<std::pair<int64_t, int64_t>> segments;  // k chronological batch ranges
+
+  // DaemonOp::Snapshot placement (ref parallel.hpp:288-290): after the write
+  // bracket of a pair whose batch closes its segment.
+  bool snapshot_after(const Stint& st) const {
+    return st.batch == segments[static_cast<size_t>(st.segment)].second - 1;
+  }
 
   int group_of(int r) const { return r / (cfg.i * cfg.j); }
   int team_of(int r) const { return (r % (cfg.i * cfg.j)) / cfg.i; }
@@ -150,6 +157,7 @@ class Schedule {
     const int64_t seg_len = (a.nb + cfg.k - 1) / cfg.k;
     for (int64_t s = 0; s < a.nb; s += seg_len) seg.emplace_back(s, std::min(a.nb, s + seg_len));
     while (static_cast<int>(seg.size()) < cfg.k) seg.emplace_back(a.nb, a.nb);
+    a.segments = seg;
     // team-iteration budget spread over the k memory copies
     const int64_t iters = static_cast<int64_t>(cfg.epochs) * a.nb;
     a.groups.resize(static_cast<size_t>(cfg.k));

@@ -350,7 +350,7 @@ void sample_queries_launch(const DGraph& g, const int32_t* nodes, const double* 
                            int32_t* nbr_count, cudaStream_t s) {
   if (count <= 0) return;
   int blocks = static_cast<int>(ceil_div(count, 8));
-  if (blocks > 8 * kSMs) blocks = 8 * kSMs;
+  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
   launch_pdl(sample_queries_kernel, dim3(blocks), dim3(256), 0, s, g, nodes, times, count, n, nbr_node, nbr_event,
                                                nbr_dt, nbr_count);
   TGB_CUDA(cudaGetLastError());
@@ -379,14 +379,14 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) 
                                                                         pl.negs);
   } else if (pl.eval_negs && pl.rpe > 2) {
     const int64_t total = static_cast<int64_t>(B) * (pl.rpe - 2);
-    launch_pdl(eval_negatives_kernel, dim3(static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * kSMs))), dim3(256), 0, s, 
+    launch_pdl(eval_negatives_kernel, dim3(static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 8 * num_sms()))), dim3(256), 0, s, 
         pl.args, g, pl.rpe - 2, pl.negs);
   }
   TGB_CUDA(cudaGetLastError());
   const int R = pl.cap_R;
   const int warps_per_block = 8;
   int blocks = static_cast<int>(ceil_div(R, warps_per_block));
-  if (blocks > 4 * kSMs * 8) blocks = 4 * kSMs * 8;
+  if (blocks > 4 * num_sms() * 8) blocks = 4 * num_sms() * 8;
   launch_pdl(sample_kernel, dim3(blocks), dim3(32 * warps_per_block), 0, s, pl.args, g, pl, bitmap);
   TGB_CUDA(cudaGetLastError());
   launch_pdl(plan_finalize_kernel, dim3(1), dim3(1024), 0, s, pl.args, g.N, pl, bitmap);
@@ -413,7 +413,7 @@ void plan_launch(const DGraph& g, DPlan& pl, cudaStream_t s, cudaStream_t side) 
 
 void gather_view_launch(const DPlan& pl, const DMem& st, DView& vw, cudaStream_t s) {
   int blocks = static_cast<int>(ceil_div(pl.cap_U, 8));
-  if (blocks > 8 * kSMs) blocks = 8 * kSMs;
+  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
   launch_pdl(gather_view_kernel, dim3(blocks), dim3(256), 0, s, pl, st, vw);
   TGB_CUDA(cudaGetLastError());
 }

@@ -44,13 +44,13 @@ ParamLayout ParamLayout::make(const ModelDims& m) {
 
 namespace {
 
-static const int kWarps = [] { const char* e = std::getenv("TGNN_KW"); return e ? std::atoi(e) : 4; }();  // warps per block for row kernels (TGNN_KW; A/B: 4 > 8 > 2)
+static const int kWarps = env_knob("TGNN_KW", 4, 1, 8);  // warps per block for row kernels (TGNN_KW; A/B: 4 > 8 > 2)
 constexpr int kChunk = 32; // routing chunk (items)
 constexpr int kOmegaRows = 256;
 
 inline int row_blocks(int64_t rows) {
   int64_t b = ceil_div(rows, kWarps);
-  if (b > 16 * kSMs) b = 16 * kSMs;
+  if (b > 16 * num_sms()) b = 16 * num_sms();
   return static_cast<int>(b < 1 ? 1 : b);
 }
 
@@ -1350,11 +1350,11 @@ int choose_splits_engine(int engine, int M, int N, int64_t Kcap) {
     // tensor tiles are 128 x 256; keep >= ~1024 reduction rows per CTA so the
     // split-K partial traffic stays small next to the MMA work
     const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
-    int s = static_cast<int>(std::min<int64_t>(ceil_div(Kcap, 1024), ceil_div(2 * kSMs, tiles)));
+    int s = static_cast<int>(std::min<int64_t>(ceil_div(Kcap, 1024), ceil_div(2 * num_sms(), tiles)));
     return std::max(1, std::min(s, 64));
   }
   const int tiles = static_cast<int>(ceil_div(M, 64) * ceil_div(N, 64));
-  int s = static_cast<int>(ceil_div(2 * kSMs, tiles));
+  int s = static_cast<int>(ceil_div(2 * num_sms(), tiles));
   (void)engine;
   const int max_by_k = static_cast<int>(ceil_div(Kcap, 128));
   if (s > max_by_k) s = max_by_k;
@@ -1414,18 +1414,18 @@ Operand ones_op(const float* ones, int K) { return op_dense(ones, 0, 0, K); }
 // the fp32 partial traffic, bounds these latency-bound groups (A/B sweep on
 // B200 at C2: 32 / 512 -> 48 / 128 is +3.6 %). TGNN_SK_T / _R / _C override.
 int choose_splits_tma(int M, int N, int64_t Kcap) {
-  static const int target = [] { const char* e = std::getenv("TGNN_SK_T"); return e ? std::atoi(e) : 48; }();
-  static const int rows = [] { const char* e = std::getenv("TGNN_SK_R"); return e ? std::atoi(e) : 128; }();
+  static const int target = env_knob("TGNN_SK_T", 48, 1, 4096);
+  static const int rows = env_knob("TGNN_SK_R", 128, 64, 1 << 20);
   const int tiles = static_cast<int>(ceil_div(M, 128) * ceil_div(N, 256));
   int64_t s = std::min<int64_t>(ceil_div(target, tiles), ceil_div(Kcap, rows));
-  static const int cap = [] { const char* e = std::getenv("TGNN_SK_C"); return e ? std::atoi(e) : 32; }();
+  static const int cap = env_knob("TGNN_SK_C", 32, 1, 256);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, cap)));
 }
 
 // Forward-style problem: A K-major [M x K] (runtime rows M_dev), B K-major [N x K].
 // Narrow N tiles for the short (supports / roots) problems so the grid fills
 // the 148 SMs; full-width tiles for the pair-level projections.
-int g_wide = 0;  // set around the pair-level projections
+thread_local int g_wide = 0;  // set around the pair-level projections
 int nn_ntile(int Mcap, int N) {
   (void)Mcap;
   return tc_ntile(N, g_wide ? 256 : 64);
@@ -1770,7 +1770,7 @@ void adam_pack_launch(const StepCtx& c, float* m, float* v, cudaStream_t s, cons
   int64_t lo = 0, hi = 0, slo = 0, shi = 0;
   const PackMap pm = gemm_impl() == kGemmTma ? make_pack_map(c, lo, hi, slo, shi) : PackMap{};
   const int64_t n = r_hi < 0 ? c.L.total : r_hi;
-  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n - r_lo, 256), 8 * kSMs)));
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n - r_lo, 256), 8 * num_sms())));
   launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, c.params, c.grads, m, v, n, 0.f, 1.f, 1.f, 1.f, desc, ctr, pm, lo, hi,
              slo, shi, r_lo);
   TGB_CUDA(cudaGetLastError());
@@ -1795,7 +1795,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   c.mark(phGruFwd, s);
   if (tma && !c.packed) pack_weights_launch(c, s);
   if (tma && c.xg_pre) {
-    launch_pdl(assemble_gru_time_kernel, dim3(4 * kSMs), dim3(256), 0, s, D, pl, vw, P + L.off[tOmega], bfx, U);
+    launch_pdl(assemble_gru_time_kernel, dim3(4 * num_sms()), dim3(256), 0, s, D, pl, vw, P + L.off[tOmega], bfx, U);
   } else {
     const int stage = (D.gin + 1 + D.dt + 7) / 8 * 8;
     launch_pdl(assemble_gru_kernel, dim3(row_blocks(U)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, 
@@ -1814,7 +1814,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
            3 * d, P + L.off[tBh]);
     gemm_group_launch(gg, s);
   }
-  static const int eblocks = [] { const char* e = std::getenv("TGNN_EB"); return e ? std::atoi(e) : 4; }() * kSMs;  // elementwise grid (TGNN_EB x SMs)
+  const int eblocks = env_knob("TGNN_EB", 4, 1, 64) * num_sms();  // elementwise grid (TGNN_EB x SMs)
   launch_pdl(gru_mid_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, tma ? nullptr : w.RS, bfx, U);
   if (tma) {
     TcGroup tg;  // Gh += [r*s | 1] [Wh_s | bh]^T  (the bias rides the ones column)
@@ -1941,7 +1941,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   const StepBf& B = w.bf;
 
   if (!c.br) TGB_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * L.total, s));  // else zeroed on the branch
-  static const int eblocks = [] { const char* e = std::getenv("TGNN_EB"); return e ? std::atoi(e) : 4; }() * kSMs;  // elementwise grid (TGNN_EB x SMs)
+  const int eblocks = env_knob("TGNN_EB", 4, 1, 64) * num_sms();  // elementwise grid (TGNN_EB x SMs)
 
   attn_forward_launch(c, pl, s);
 
@@ -2019,7 +2019,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     launch_pdl(chunk, dim3(row_blocks(3 * nchunks)), dim3(32 * kWarps), 0, s, D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
                                                       part_first, part_last, bfx);
     const int fix_threads = std::min(1024, (3 * da + 31) / 32 * 32);
-    launch_pdl(routing_fixup_kernel, dim3(std::min(U, 8 * kSMs)), dim3(fix_threads), 0, s, D, pl, tma ? nullptr : w.dNodeAcc,
+    launch_pdl(routing_fixup_kernel, dim3(std::min(U, 8 * num_sms())), dim3(fix_threads), 0, s, D, pl, tma ? nullptr : w.dNodeAcc,
                                                                        part_first, part_last, bfx);
   }
   c.mark(phAttnBwdGemm, s);
@@ -2212,7 +2212,7 @@ void reset_state_launch(DMem& st, cudaStream_t s) {
   TGB_CUDA(cudaMemsetAsync(st.last_update, 0, sizeof(double) * st.N, s));
   TGB_CUDA(cudaMemsetAsync(st.mail_t, 0, sizeof(double) * st.N, s));
   TGB_CUDA(cudaMemsetAsync(st.mail_dt, 0, sizeof(double) * st.N, s));
-  launch_pdl(fill_kernel, dim3(static_cast<int>(std::min<int64_t>(ceil_div(st.N, 256), 4 * kSMs))), dim3(256), 0, s, 
+  launch_pdl(fill_kernel, dim3(static_cast<int>(std::min<int64_t>(ceil_div(st.N, 256), 4 * num_sms()))), dim3(256), 0, s, 
       st.mail_ev, st.N, -1);
   TGB_CUDA(cudaGetLastError());
 }
@@ -2220,7 +2220,7 @@ void reset_state_launch(DMem& st, cudaStream_t s) {
 void adam_launch(float* params, const float* grads, float* m, float* v, int64_t n, float lr,
                  float c1, float c2, float grad_scale, cudaStream_t s, const BarrierDesc* desc,
                  const int* ctr) {
-  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * kSMs));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 8 * num_sms()));
   launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, s, params, grads, m, v, n, lr, c1, c2, grad_scale, desc, ctr, PackMap{}, 0, 0, 0, 0,
              static_cast<int64_t>(0));
   TGB_CUDA(cudaGetLastError());
@@ -2247,7 +2247,7 @@ __global__ void stamp_kernel(unsigned long long* dst) {
 
 void params_hash_launch(const float* p, int64_t n, unsigned long long* out, cudaStream_t s) {
   TGB_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
-  params_hash_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 4 * kSMs)), 256, 0, s>>>(p, n, out);
+  params_hash_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 4 * num_sms())), 256, 0, s>>>(p, n, out);
   TGB_CUDA(cudaGetLastError());
 }
 
@@ -2257,7 +2257,7 @@ void stamp_launch(unsigned long long* dst, cudaStream_t s) {
 }
 
 void reset_cond_launch(DMem& st, const BarrierDesc* desc, const int* ctr, cudaStream_t s, int offset) {
-  launch_pdl(reset_cond_kernel, dim3(4 * kSMs), dim3(256), 0, s, st, desc, ctr, offset);
+  launch_pdl(reset_cond_kernel, dim3(4 * num_sms()), dim3(256), 0, s, st, desc, ctr, offset);
   TGB_CUDA(cudaGetLastError());
 }
 

@@ -131,3 +131,39 @@ def test_ingest_is_ordered_before_later_work(ctx):
     assert np.array_equal(g1.edge_feats(), ef2.astype(np.float32))
     assert np.array_equal(res[0][0], res[1][0])
     assert np.array_equal(res[0][1], res[1][1])
+
+
+def test_ingest_rejects_events_that_differ_from_the_index(ctx):
+    """Ingested src / dst / t are verified bitwise against the finalized
+    T-CSR events (never rewritten): a differing event fails the next
+    synchronising call with ProtocolError and leaves the graph unchanged."""
+    g = T.TemporalGraph.synthetic(ctx, T.SynthParams(nodes=50, events=400, d_e=2, seed=4))
+    src, dst, t = g.events()
+    a, n = 100, 20
+    p_src = T.pinned_empty((n,), np.int32)
+    p_dst = T.pinned_empty((n,), np.int32)
+    p_t = T.pinned_empty((n,), np.float64)
+    p_f = T.pinned_empty((n, 2), np.float32)
+    p_src[:], p_dst[:], p_t[:] = src[a:a + n], dst[a:a + n], t[a:a + n]
+    p_f[:] = g.edge_feats(a, n)
+    g.ingest(a, p_src, p_dst, p_t, p_f)
+    ctx.synchronize()
+    for field in ("src", "t"):
+        q_src, q_t = p_src.copy(), p_t.copy()
+        if field == "src":
+            q_src[3] = (q_src[3] + 1) % 50
+        else:
+            q_t[7] = np.nextafter(q_t[7], np.inf)
+        b_src = T.pinned_empty((n,), np.int32)
+        b_t = T.pinned_empty((n,), np.float64)
+        b_src[:], b_t[:] = q_src, q_t
+        g.ingest(a, b_src, p_dst, b_t, p_f)
+        mc = T.ModelConfig(d_mem=4, d_time=2, d_static=0, d_attn=4, d_hidden=4, d_e=2, n_neighbors=3,
+                           num_nodes=50, max_t=float(t[-1]))
+        run = T.Run(ctx, g, mc, T.TrainConfig(local_batch=50, epochs=1), 0, 200)
+        run.step(1)
+        with pytest.raises(T.ProtocolError):
+            run.losses()
+        run.close()
+    s2, d2, t2 = g.events()
+    assert np.array_equal(s2, src) and np.array_equal(d2, dst) and np.array_equal(t2, t)
