@@ -20,6 +20,18 @@
 extern "C" {
 #endif
 
+/* Status codes (ref common.hpp:16-34, tensor.hpp:16). */
+enum {
+  TGNN_OK = 0,
+  TGNN_CONFIG_ERROR = 1,   /* config_error */
+  TGNN_PARSE_ERROR = 2,    /* parse_error (a config_error) */
+  TGNN_NUMERIC_ERROR = 3,  /* numeric_error */
+  TGNN_PROTOCOL_ERROR = 4, /* protocol_error */
+  TGNN_SHAPE_ERROR = 5,    /* shape_error */
+  TGNN_CUDA_ERROR = 6,
+  TGNN_NCCL_ERROR = 7
+};
+
 typedef struct tgnn_ctx tgnn_ctx;
 typedef struct tgnn_graph tgnn_graph;
 typedef struct tgnn_memstore tgnn_memstore;
@@ -232,13 +244,17 @@ int tgnn_run_oplog(tgnn_run* r, int64_t* count, int64_t* rows);
  * output may be NULL; count receives the number of snapshots taken so far. */
 int tgnn_run_snapshots(tgnn_run* r, int64_t* count, int64_t* meta, double* memory, double* last_update);
 /* Replica invariant (ref SPEC.md:397): collective over all ranks; fails with
- * TGNN_PROTOCOL if any rank's parameters differ bitwise; hash_out receives the
+ * TGNN_PROTOCOL_ERROR if any rank's parameters differ bitwise; hash_out receives the
  * order-independent 64-bit parameter fingerprint. Also checked automatically at
  * every eval point of a multi-rank run. */
 int tgnn_run_check_replicas(tgnn_run* r, uint64_t* hash_out);
 /* evaluate_mrr of the run's current weights (rank-local, no collective). */
 int tgnn_run_evaluate_mrr(tgnn_run* r, int64_t eval_begin, int64_t eval_end, int64_t batch_size,
                           int32_t n_negatives, uint64_t seed, double* mrr, int64_t* queries);
+/* Assignment::eval_barriers (ref parallel.hpp:316-329): the barriers after
+ * which run_training records a metrics row (one per epoch-equivalent of
+ * traversed events, plus the last barrier). out may be NULL (count only). */
+int tgnn_run_eval_barriers(tgnn_run* r, int64_t* count, int64_t* out);
 /* Events traversed by ALL ranks in barriers [first, first+count) (ref parallel.hpp:302-314). */
 int tgnn_run_traversed(tgnn_run* r, int64_t first, int64_t count, int64_t* out);
 /* Kernel launches issued per barrier by this rank (counted by capturing the
@@ -281,7 +297,7 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
  * edge features (float32 [count x d_e]) overwrite the device rows; src / dst /
  * t are uploaded and verified bitwise against the finalized (T-CSR indexed)
  * events -- they are never rewritten, and a mismatch fails the next
- * synchronising call with TGNN_PROTOCOL. Used to stream feature windows and
+ * synchronising call with TGNN_PROTOCOL_ERROR. Used to stream feature windows and
  * by the end-to-end measurement. Pinned buffers make the copies asynchronous:
  * they run on the context's copy stream, overlap work enqueued before the call
  * and are ordered before any work enqueued after it. Ordering contract: in
@@ -324,7 +340,7 @@ int tgnn_eval_candidates(tgnn_evaluator* ev, int64_t begin, int64_t end, uint64_
 
 /* ---- artifacts: model.ckpt (ref model.hpp:168-222), byte-compatible with
  * save_checkpoint / load_checkpoint; flat = f64 weights in canonical order.
- * Load refuses a manifest that does not match the config (TGNN_CONFIG). */
+ * Load refuses a manifest that does not match the config (TGNN_CONFIG_ERROR). */
 int tgnn_checkpoint_save(const tgnn_model_config* m, const double* flat, const char* path);
 int tgnn_checkpoint_load(const tgnn_model_config* m, const char* path, double* flat);
 
@@ -337,7 +353,7 @@ int tgnn_checkpoint_load(const tgnn_model_config* m, const char* path, double* f
 int tgnn_graph_synthetic(tgnn_ctx* ctx, const tgnn_synth_params* p, int32_t threads, tgnn_graph** out);
 /* load_dataset (ref temporal_graph.hpp:136-258): the event CSV plus its
  * ".meta" sidecar, parsed by `threads` workers; the reference's grammar and
- * errors (TGNN_PARSE for malformed input, TGNN_CONFIG for missing files). */
+ * errors (TGNN_PARSE_ERROR for malformed input, TGNN_CONFIG_ERROR for missing files). */
 int tgnn_graph_load_dataset(tgnn_ctx* ctx, const char* csv_path, int32_t threads, tgnn_graph** out);
 /* write_dataset (ref temporal_graph.hpp:237-262): CSV + sidecar, %.17g numbers. */
 int tgnn_write_dataset(const char* csv_path, int64_t num_nodes, int64_t bipartite_boundary, int64_t num_events,

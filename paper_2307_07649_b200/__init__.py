@@ -670,6 +670,15 @@ class Run:
         check(lib().tgnn_run_traversed(self.h, first, count, C.byref(out)))
         return out.value
 
+    def eval_barriers(self):
+        """Assignment::eval_barriers (parallel.hpp:316-329)."""
+        n = C.c_int64()
+        check(lib().tgnn_run_eval_barriers(self.h, C.byref(n), None))
+        out = np.zeros(n.value, np.int64)
+        if n.value:
+            check(lib().tgnn_run_eval_barriers(self.h, C.byref(n), _p(out, i64p)))
+        return out
+
     def metrics(self):
         """MetricsRow list (trainer.hpp:562-570) for the eval barriers run so far:
         [rows x 5] = iter, traversed, loss, val_mrr, elapsed_s. Collective at nranks > 1."""

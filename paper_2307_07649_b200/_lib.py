@@ -137,6 +137,7 @@ SIGNATURES = {
     "tgnn_run_params": [vp, f64p],
     "tgnn_run_loss_async": [vp, i64, f64p],
     "tgnn_run_traversed": [vp, i64, i64, i64p],
+    "tgnn_run_eval_barriers": [vp, i64p, i64p],
     "tgnn_run_metrics": [vp, i64p, f64p],
     "tgnn_run_oplog": [vp, i64p, i64p],
     "tgnn_run_snapshots": [vp, i64p, i64p, f64p, f64p],

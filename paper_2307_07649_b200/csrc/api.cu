@@ -2405,6 +2405,15 @@ int tgnn_run_evaluate_mrr(tgnn_run* r, int64_t eval_begin, int64_t eval_end, int
   API_END
 }
 
+int tgnn_run_eval_barriers(tgnn_run* r, int64_t* count, int64_t* out) {
+  API_BEGIN
+  const auto& e = r->sched.eval_barriers;
+  *count = static_cast<int64_t>(e.size());
+  if (out)
+    for (size_t x = 0; x < e.size(); ++x) out[x] = e[x];
+  API_END
+}
+
 int tgnn_run_traversed(tgnn_run* r, int64_t first, int64_t count, int64_t* out) {
   API_BEGIN
   const auto& ta = r->sched.traversed_after;
