@@ -54,13 +54,21 @@ CONFIGS = {
     "c4": dict(workload="synthetic MOOC-shape CTDG (C4): 7,144 nodes, 411,749 events, no edge feats, "
                         "TGN + static memory, 10 recent nbrs, mem 100, local batch 600, epoch parallelism j=N",
                nodes=7144, events=411_749, d_e=0, d_static=100, axis="j"),
+    # SURVEY 8(d) C5 variant: the paper's global batch of 3200 events per trainer
+    "c5p3200": dict(workload="synthetic GDELT-shape CTDG (C5, 5M-event prefix), local batch 3200 "
+                             "(the paper's batch, SURVEY 8(d)): 16,682 nodes, 186-d edge feats, TGN + static memory",
+                    nodes=16682, events=5_000_000, d_e=186, d_static=100, batch=3200),
     # BASELINE.json configs[4] at full size: 191M events x 186 fp32 features
     # (143 GB) streamed into HBM by the chunked generator
     "c5": dict(workload="synthetic GDELT-shape CTDG (C5): 16,682 nodes, 191,290,882 events, "
                         "186-d edge feats, TGN + static memory, batch 600",
                nodes=16682, events=191_290_882, d_e=186, d_static=100),
 }
-LOCAL_BATCH = 600
+LOCAL_BATCH = 600  # default local batch (BASELINE configs); a config may set "batch"
+
+
+def batch_of(cfg):
+    return cfg.get("batch", LOCAL_BATCH)
 TRAIN_FRAC = 0.70
 REF_MAX_EVENTS = 5_000_000  # f64 host copy of a GDELT-shape prefix: ~7.5 GB
 
@@ -231,8 +239,8 @@ def reference_time(cfg, ijk, barriers, warmup, log=print):
         if nbar <= 0:
             continue
         lo = mid
-        hi = lo + nbar * LOCAL_BATCH * i * k
-        tc = ref.train_cfg(i=i, j=j, k=k, local_batch=LOCAL_BATCH, seed=1, epochs=j, lr_base=1e-3)
+        hi = lo + nbar * batch_of(cfg) * i * k
+        tc = ref.train_cfg(i=i, j=j, k=k, local_batch=batch_of(cfg), seed=1, epochs=j, lr_base=1e-3)
         r = g.run(mc, tc, lo, hi, want_params=False)
         if phase == "timed":
             ev = int(ref.assignment(tc, lo, hi)["traversed_after"][-1])
@@ -260,7 +268,7 @@ def reference_arm(args, world, rank, emit):
         # group (trainer + daemon thread) per two cores, at least one per GPU of
         # the B200 arm, and no more than the mid-stream event window holds
         n_ev = min(cfg["events"], REF_MAX_EVENTS)
-        room = (n_ev - int(n_ev * TRAIN_FRAC) // 2) // ((warm + steps) * LOCAL_BATCH)
+        room = (n_ev - int(n_ev * TRAIN_FRAC) // 2) // ((warm + steps) * batch_of(cfg))
         groups = args.ref_groups or max(world, min(16, (os.cpu_count() or 2) // 2, room))
         shape = (1, 1, groups)
     else:  # i- and j-parallel configs: the reference at the B200 arm's own (i, j, k)
@@ -275,10 +283,10 @@ def reference_arm(args, world, rank, emit):
                    "parallelism": f"(i,j,k)={shape} host threads (the B200 arm: (i,j,k)={ours}, "
                                   f"one trainer per GPU)",
                    "same_parallelism_as_b200_arm": shape == ours,
-                   "global_batch": LOCAL_BATCH * shape[0] * shape[2], "host_cpus": os.cpu_count(),
+                   "global_batch": batch_of(cfg) * shape[0] * shape[2], "host_cpus": os.cpu_count(),
                    "window": {"first_event": window[0], "last_event": window[1]}},
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
-                         "sample": f"{steps} barriers at (i,j,k)={shape} x 600 events, mid-stream window "
+                         "sample": f"{steps} barriers at (i,j,k)={shape} x {batch_of(cfg)} events, mid-stream window "
                                    f"[{window[0]}, {window[1]}), run_{'training' if threads > 1 else 'sequential'} "
                                    f"(oracle/_ref)"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -363,7 +371,7 @@ def main():
     ijk = ijk_of(cfg, world)
     # weak scaling: every memory copy / team sweeps the training range once per
     # rank along the parallel axis, so the barrier count stays ~ constant in N
-    tc = T.TrainConfig(i=ijk[0], j=ijk[1], k=ijk[2], local_batch=LOCAL_BATCH, lr_base=1e-3, seed=1, epochs=world)
+    tc = T.TrainConfig(i=ijk[0], j=ijk[1], k=ijk[2], local_batch=batch_of(cfg), lr_base=1e-3, seed=1, epochs=world)
     run = T.Run(ctx, g, mc, tc, 0, train_end, rank=rank, nranks=world)
     need = args.warmup + args.steps + 3 * args.profile_steps + args.e2e_steps + 1
     if run.barriers < need:
@@ -540,7 +548,7 @@ def main():
         if ref.available():
             v, secs, ev, thr, cw = reference_time(cfg, (1, 1, 1), args.cpu_baseline_steps, 0, log=log)
             cpu = {"value": v, "unit": "events/s", "cores": thr, "kind": "reference",
-                   "sample": f"{args.cpu_baseline_steps} barriers x 600 events, mid-stream window "
+                   "sample": f"{args.cpu_baseline_steps} barriers x {batch_of(cfg)} events, mid-stream window "
                              f"[{cw[0]}, {cw[1]}), run_sequential of the unmodified reference "
                              f"(oracle/_ref), {secs:.1f}s",
                    "window": {"first_event": cw[0], "last_event": cw[1]}}
@@ -553,7 +561,7 @@ def main():
             "data": "synthetic (bit-identical gen_synthetic, seed 1)",
             "config": {"workload": cfg["workload"],
                        "parallelism": f"(i,j,k)={ijk}, one trainer per GPU",
-                       "global_batch": LOCAL_BATCH * ijk[0], "local_batch": LOCAL_BATCH,
+                       "global_batch": batch_of(cfg) * ijk[0], "local_batch": batch_of(cfg),
                        "window": window,
                        "l2": "inputs larger than L2 (edge features "
                              f"{cfg['events'] * cfg['d_e'] * 4 / 1e6:.0f} MB; each step reads a new "

@@ -312,6 +312,12 @@ int tgnn_graph_ingest(tgnn_graph* g, int64_t first, int64_t count, const int32_t
  * epilogue start, epilogue end, exit, first TMA issued. */
 int tgnn_debug_gemm_bench(int64_t M, int64_t N, int64_t K, int32_t ntile, int32_t iters, double* us,
                           uint64_t* trace, int32_t* grid);
+/* Debug: per-CTA globaltimer timeline of the fused GRU kernel. out == NULL
+ * arms it for up to cap_ctas CTAs; otherwise synchronises, copies [cap x 16]
+ * stamps (entry, after the dependency wait, producer done, MMA done, GEMM2
+ * operands ready, epilogue start, epilogue mid, GEMM2 seen, epilogue end,
+ * CTA sync, exit) and disarms. */
+int tgnn_debug_gru_trace(uint64_t* out, int32_t cap_ctas, int32_t* n_ctas);
 int tgnn_pinned_alloc(int64_t bytes, void** out);
 int tgnn_pinned_free(void* p);
 

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", CSRC, "-I", os.path.join(HERE, "..", "include")]
-SOURCES = ["plan.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_tma.cu", "step.cu", "graph.cu", "api.cu",
+SOURCES = ["plan.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_tma.cu", "gru_fused.cu", "step.cu", "graph.cu", "api.cu",
            "host/dataset.cpp"]
 CXX = os.environ.get("TGNN_HOST_CXX", "g++")
 CXXFLAGS = ["-O2", "-std=c++20", "-fPIC", "-pthread", "-g", "-I", CSRC, "-I", "/usr/local/cuda/include"]

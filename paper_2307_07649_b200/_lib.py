@@ -165,6 +165,7 @@ SIGNATURES = {
     "tgnn_get_gemm_impl": [C.POINTER(C.c_int)],
     "tgnn_debug_gemm": [C.c_int, i64, i64, i64, f32p, C.c_int, f32p, C.c_int, f32p, C.c_int],
     "tgnn_pinned_free": [vp],
+    "tgnn_debug_gru_trace": [C.POINTER(C.c_uint64), i32, C.POINTER(i32)],
 }
 
 

@@ -31,6 +31,7 @@
 #include "plan.cuh"
 #include "step.cuh"
 #include "gemm_tma.cuh"
+#include "gru_fused.cuh"
 
 using namespace tgb;
 
@@ -2723,6 +2724,12 @@ int tgnn_debug_gemm(int impl, int64_t M, int64_t N, int64_t K, const float* A, i
   cudaFree(dB);
   cudaFree(dC);
   if (ws) cudaFree(ws);
+  API_END
+}
+
+int tgnn_debug_gru_trace(uint64_t* out, int32_t cap_ctas, int32_t* n_ctas) {
+  API_BEGIN
+  gru_debug_trace(reinterpret_cast<unsigned long long*>(out), cap_ctas, n_ctas);
   API_END
 }
 

@@ -20,6 +20,7 @@
 #include <unordered_map>
 
 #include "gemm_tma.cuh"
+#include "tc_ptx.cuh"
 
 namespace tgb {
 
@@ -44,73 +45,6 @@ struct TcParams {
   int tmem_cols;     // power of two >= max(32, max ntile)
   int stages;        // shared-memory ring depth (2..kStMax), as deep as the CTA budget allows
 };
-
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra W_%=;\n\t}\n" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
-      : "memory");
-}
-
-// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100).
-//  K-major : LBO 16 B (unused), SBO 1024 B (8-row group stride);
-//  MN-major: LBO 8192 B (64-element MN block stride = one 64 x 64 TMA box),
-//            SBO 1024 B (8-k-row group stride).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, bool kmajor) {
-  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
-  d |= static_cast<uint64_t>(kmajor ? 1 : (8192 >> 4)) << 16;
-  d |= static_cast<uint64_t>(1024 >> 4) << 32;
-  d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(2) << 61;
-  return d;
-}
-
-__device__ __forceinline__ uint32_t idesc(int n, bool a_k, bool b_k) {
-  uint32_t d = (1u << 4) | (1u << 7) | (1u << 10);
-  d |= (a_k ? 0u : 1u) << 15;
-  d |= (b_k ? 0u : 1u) << 16;
-  d |= static_cast<uint32_t>(n >> 3) << 17;
-  d |= static_cast<uint32_t>(kBM >> 4) << 24;
-  return d;
-}
-
-__device__ __forceinline__ void umma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
-               : "memory");
-}
 
 // Optional per-CTA timeline (debug benchmark only): 8 globaltimer stamps per CTA.
 __device__ unsigned long long* g_tc_trace = nullptr;
@@ -482,12 +416,22 @@ __global__ void tc_splitk_reduce_kernel(const __grid_constant__ TcParams gp) {
   pdl_trigger();
   const TcProblem& P = gp.p[blockIdx.y];
   if (P.splits <= 1) return;
-  const int64_t total = static_cast<int64_t>(P.M) * P.N;
-  const int64_t ldw = P.ldw > 0 ? P.ldw : P.N, pstride = static_cast<int64_t>(P.M) * ldw;
+  const int N = P.N, S = P.splits;
+  const int64_t total = static_cast<int64_t>(P.M) * N;
+  const int64_t ldw = P.ldw > 0 ? P.ldw : N, pstride = static_cast<int64_t>(P.M) * ldw;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t m = x / P.N, n = x % P.N;
+    const int m = static_cast<int>(x / N), n = static_cast<int>(x - static_cast<int64_t>(m) * N);
+    const float* src = P.ws + static_cast<int64_t>(m) * ldw + n;
+    // the partials in split order (fixed summation order), 8 loads in flight
     float s = 0.0f;
-    for (int sp = 0; sp < P.splits; ++sp) s += P.ws[sp * pstride + m * ldw + n];
+    for (int sp = 0; sp < S; sp += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = sp + k < S ? src[(sp + k) * pstride] : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (sp + k < S) s += v[k];
+    }
     const float v = P.alpha * s;
     if (P.C2 && n == P.N - 1) {
       P.C2[m] = P.beta != 0.0f ? v + P.beta * P.C2[m] : v;
@@ -751,7 +695,11 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_strea
       TGB_CUDA(cudaStreamWaitEvent(reduce_stream, ev, 0));
       rs = reduce_stream;
     }
-    launch_pdl(tc_splitk_reduce_kernel, dim3(dim3(64, g.count)), dim3(256), 0, rs, gp);
+    int64_t most = 0;
+    for (int i = 0; i < g.count; ++i)
+      if (g.p[i].splits > 1) most = std::max<int64_t>(most, static_cast<int64_t>(g.p[i].M) * g.p[i].N);
+    const int bx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((most + 255) / 256, 8 * num_sms() / g.count)));
+    launch_pdl(tc_splitk_reduce_kernel, dim3(dim3(bx, g.count)), dim3(256), 0, rs, gp);
     TGB_CUDA(cudaGetLastError());
   }
 }

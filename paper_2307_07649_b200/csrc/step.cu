@@ -20,6 +20,7 @@
 #include <cmath>
 
 #include "step.cuh"
+#include "gru_fused.cuh"
 
 namespace tgb {
 
@@ -1800,6 +1801,32 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
     const int stage = (D.gin + 1 + D.dt + 7) / 8 * 8;
     launch_pdl(assemble_gru_kernel, dim3(row_blocks(U)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, 
         D, pl, vw, g, P + L.off[tOmega], tma ? nullptr : w.Xg, w.ldx, w.GU, bfx, U, stage);
+  }
+  // one fused tcgen05 kernel for GEMM -> sigmoid -> GEMM -> tanh / blend
+  // (gru_fused.cu), opt-in with TGNN_GRU_FUSED=1. A/B on B200 at C2: the
+  // GRU phase of the critical path drops from 57 to 40 us, but the step does
+  // not (259.7 vs 261.8 us): the kernel holds 96 SMs exclusively (224 KB of
+  // shared memory each), so the per-pair edge projection running beside it
+  // on the edge stream becomes the critical path (attn_assemble 0.8 -> 12 us).
+  static const int fused_knob = env_knob("TGNN_GRU_FUSED", 0, 0, 1);
+  if (tma && fused_knob && gru_fused_supported(d)) {
+    GruFusedParams fp;
+    fp.U_dev = szU;
+    fp.cap_U = U;
+    fp.d = d;
+    fp.ds = D.ds;
+    fp.gin = gin;
+    fp.supports = pl.supports;
+    fp.mem = vw.mem;
+    fp.mail_ev = vw.mail_ev;
+    fp.stat = P + L.off[tStatic];
+    fp.gates = w.Gates;
+    fp.s_hat = w.s_hat;
+    fp.rs = w.bf.RS;
+    fp.nf = w.bf.NF;
+    fp.flag = c.d_numeric_flag;
+    gru_fused_launch(fp, w.bf.Xg, w.bf.Wzr, w.bf.Whm, w.bf.Whs, md, s);
+    return;
   }
   if (tma) {
     TcGroup tg;
