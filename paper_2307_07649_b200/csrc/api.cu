@@ -169,6 +169,8 @@ struct tgnn_ctx {
   cudaStream_t edge = nullptr;  // per-pair edge projection, overlapped with the GRU
   cudaStream_t h2d = nullptr;   // event ingestion (copy engine), overlapped with earlier work
   cudaEvent_t ev_h2d = nullptr;
+  cudaStream_t xch = nullptr;   // i-axis write exchange (broadcast + apply), off the critical path
+  cudaStream_t hd = nullptr;    // the head gradient bucket's all-reduce + Adam (its own communicator)
   cudaStream_t d2h = nullptr;   // asynchronous result reads, off the compute stream
   cudaEvent_t ev_d2h = nullptr;
   int* d_flag = nullptr;
@@ -572,6 +574,11 @@ struct tgnn_run {
   int rank = 0, nranks = 1;
   int group = 0, team = 0, member = 0, group_size = 1;
   ncclComm_t comm = nullptr, gcomm = nullptr;
+  ncclComm_t hcomm = nullptr;  // duplicate of comm for the head bucket (its own stream, no FIFO behind the tail)
+  // graph capture of consecutive barriers: the tail range's update (all-reduce
+  // + Adam of attention / static / decoder, 88 % of the parameters) may finish
+  // under the NEXT barrier's GRU forward; its first reader waits for it
+  bool defer_tail = false, tail_pending = false;
   bool comm_ready = false;
   // in-process exchange (tgnn_run_local_init) instead of NCCL
   tgnn_local_hub* hub = nullptr;
@@ -589,6 +596,10 @@ struct tgnn_run {
   bool use_graphs = false;
   BarrierDesc* d_desc = nullptr;
   int* d_ctr = nullptr;
+  // the tail-range Adam's own barrier counter: deferred inside a multi-barrier
+  // graph it may run after the main stream advanced d_ctr, so it keeps its own
+  // (advanced on the tail chain's stream right after the update)
+  int* d_ctr_tail = nullptr;
   cudaGraph_t graph[2] = {nullptr, nullptr};
   cudaGraphExec_t exec[2] = {nullptr, nullptr};  // barrier b runs exec[b % 2]
   // kMultiBarrier consecutive barriers (from an even b) captured as one graph:
@@ -658,9 +669,11 @@ struct tgnn_run {
       if (e) cudaEventDestroy(e);
     if (d_desc) cudaFree(d_desc);
     if (d_ctr) cudaFree(d_ctr);
+    if (d_ctr_tail) cudaFree(d_ctr_tail);
     if (ev_lready) cudaEventDestroy(ev_lready);
     if (ev_ldone) cudaEventDestroy(ev_ldone);
     if (lscratch) cudaFree(lscratch);
+    if (hcomm) nccl::api().CommDestroy(hcomm);
     if (gcomm) nccl::api().CommDestroy(gcomm);
     if (comm) nccl::api().CommDestroy(comm);
     if (d_losses) cudaFree(d_losses);
@@ -999,26 +1012,32 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
   if (r->nranks > 1) {
     NCCL_CHECK(nccl::api().AllReduce(tr->grads + split, tr->grads + split, static_cast<size_t>(tr->L.total - split),
                                           ncclFloat, ncclSum, r->comm, c));
-    // the tail Adam on the (idle by now) branch stream, so the head bucket's
-    // all-reduce does not queue behind it on the comm stream
+    // the tail Adam on the (idle by now) branch stream
     TGB_CUDA(cudaEventRecord(r->ev_artail, c));
     TGB_CUDA(cudaStreamWaitEvent(r->ctx->br, r->ev_artail, 0));
     u = r->ctx->br;
   }
-  adam_pack_launch(sc, tr->am, tr->av, u, r->d_desc, r->d_ctr, split, tr->L.total);
+  adam_pack_launch(sc, tr->am, tr->av, u, r->d_desc, r->d_ctr_tail, split, tr->L.total);
+  incr_launch(r->d_ctr_tail, u);
+  TGB_CUDA(cudaEventRecord(r->ev_upd, u));
   if (r->nranks > 1) {
-    TGB_CUDA(cudaEventRecord(r->ev_upd, u));
+    // the head bucket (omega + GRU, the next barrier's first readers) on its
+    // own stream and communicator: not queued behind the tail all-reduce
+    cudaStream_t h = r->ctx->hd;
     TGB_CUDA(cudaEventRecord(r->ev_head, s));
-    TGB_CUDA(cudaStreamWaitEvent(c, r->ev_head, 0));
-    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(split), ncclFloat, ncclSum, r->comm, c));
-    adam_pack_launch(sc, tr->am, tr->av, c, r->d_desc, r->d_ctr, 0, split);
-    TGB_CUDA(cudaEventRecord(r->ev_comm, c));
+    TGB_CUDA(cudaStreamWaitEvent(h, r->ev_head, 0));
+    NCCL_CHECK(nccl::api().AllReduce(tr->grads, tr->grads, static_cast<size_t>(split), ncclFloat, ncclSum, r->hcomm, h));
+    adam_pack_launch(sc, tr->am, tr->av, h, r->d_desc, r->d_ctr, 0, split);
+    TGB_CUDA(cudaEventRecord(r->ev_comm, h));
     TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
-    TGB_CUDA(cudaStreamWaitEvent(s, r->ev_upd, 0));
   } else {
     adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr, 0, split);
-    TGB_CUDA(cudaEventRecord(r->ev_comm, c));
-    TGB_CUDA(cudaStreamWaitEvent(s, r->ev_comm, 0));
+  }
+  if (r->defer_tail) {
+    r->tail_pending = true;  // the next barrier of this capture waits before its first tail read
+  } else {
+    TGB_CUDA(cudaStreamWaitEvent(s, r->ev_upd, 0));
+    r->tail_pending = false;
   }
 }
 
@@ -1077,8 +1096,14 @@ void barrier_body_slot(tgnn_run* r, int p, bool xg_split) {
   sc.ev_red = r->ev_red;
   // edge branch: the plan-only half of the attention projection runs beside the GRU
   static const bool no_edge = std::getenv("TGNN_NOEDGE") != nullptr;  // A/B: edge part inline
+  // the previous barrier's tail update (deferred inside this capture): the
+  // edge branch reads Wq / Wk / Wv edge columns, gru_out the static table
+  const bool tail_wait = r->tail_pending;
+  r->tail_pending = false;
+  if (tail_wait) sc.ev_params_tail = r->ev_upd;
   if (gemm_impl() == kGemmTma && !no_edge) {
     TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_fork, 0));
+    if (tail_wait) TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_upd, 0));
     StepCtx se = sc;
     se.marks = nullptr;  // phase markers live on the main stream
     attn_edge_launch(se, pl, ctx->edge);
@@ -1105,8 +1130,14 @@ void barrier_body_slot(tgnn_run* r, int p, bool xg_split) {
       oplog_record_launch(sc, op, r->d_oplog, 0, ws);
     }
     if (r->group_size > 1) {
-      comm_bcast_packs(r, 0, s);
-      apply_gathered(r, s);
+      // the i-axis write exchange only feeds the NEXT barrier's read: it runs
+      // on its own stream beside this barrier's attention / backward (the
+      // group communicator is distinct from the gradient all-reduce's)
+      TGB_CUDA(cudaEventRecord(r->ev_gru, s));
+      TGB_CUDA(cudaStreamWaitEvent(ctx->xch, r->ev_gru, 0));
+      comm_bcast_packs(r, 0, ctx->xch);
+      apply_gathered(r, ctx->xch);
+      ws = ctx->xch;
     }
     // join: the next barrier reads the memory copy once this barrier's writes landed
     TGB_CUDA(cudaEventRecord(r->ev_written, ws));
@@ -1245,6 +1276,10 @@ void build_stint_graphs(tgnn_run* r) {
     TGB_CUDA(cudaStreamEndCapture(s, &r->sgraph[static_cast<size_t>(x)]));
     TGB_CUDA(cudaGraphInstantiate(&r->sexec[static_cast<size_t>(x)], r->sgraph[static_cast<size_t>(x)], 0));
   }
+  // the plans' routing-sort events were only recorded inside the captures:
+  // record them once eagerly so a direct barrier (profiling) may wait on them
+  for (auto& pl : r->tr->plans)
+    if (pl.ev_sorted) TGB_CUDA(cudaEventRecord(pl.ev_sorted, r->ctx->side));
   size_t n = 0;
   TGB_CUDA(cudaGraphGetNodes(r->sgraph[0], nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
@@ -1290,8 +1325,14 @@ void build_graph(tgnn_run* r) {
   }
   TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   try {
-    for (int x = 0; x < kMultiBarrier; ++x) barrier_body_dev(r, x & 1);
+    for (int x = 0; x < kMultiBarrier; ++x) {
+      r->defer_tail = x + 1 < kMultiBarrier;  // joined by the capture's last barrier
+      barrier_body_dev(r, x & 1);
+    }
+    r->defer_tail = false;
   } catch (...) {
+    r->defer_tail = false;
+    r->tail_pending = false;
     cudaGraph_t g = nullptr;
     cudaStreamEndCapture(s, &g);
     if (g) cudaGraphDestroy(g);
@@ -1320,6 +1361,7 @@ void prepare_barrier(tgnn_run* r, int64_t b) {
   cudaStream_t s = ctx->stream;
   DPlan& pl = tr->plans[static_cast<size_t>(b & 1)];
   set_int_kernel<<<1, 1, 0, s>>>(r->d_ctr, static_cast<int>(b));
+  set_int_kernel<<<1, 1, 0, s>>>(r->d_ctr_tail, static_cast<int>(b));
   TGB_CUDA(cudaGetLastError());
   reset_cond_launch(r->mem->d, r->d_desc, r->d_ctr, s, 0);
   select_plan_args_launch(pl.args, r->d_desc, r->d_ctr, s, 0);
@@ -1441,6 +1483,8 @@ int tgnn_ctx_create(int device, tgnn_ctx** out) {
   TGB_CUDA(cudaStreamCreateWithPriority(&c->br, cudaStreamNonBlocking, lo_prio));
   TGB_CUDA(cudaStreamCreateWithPriority(&c->edge, cudaStreamNonBlocking, lo_prio));
   TGB_CUDA(cudaStreamCreateWithPriority(&c->h2d, cudaStreamNonBlocking, hi_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->xch, cudaStreamNonBlocking, hi_prio));
+  TGB_CUDA(cudaStreamCreateWithPriority(&c->hd, cudaStreamNonBlocking, hi_prio));
   TGB_CUDA(cudaEventCreateWithFlags(&c->ev_h2d, cudaEventDisableTiming));
   TGB_CUDA(cudaStreamCreateWithPriority(&c->d2h, cudaStreamNonBlocking, lo_prio));
   TGB_CUDA(cudaEventCreateWithFlags(&c->ev_d2h, cudaEventDisableTiming));
@@ -1462,10 +1506,14 @@ int tgnn_ctx_destroy(tgnn_ctx* ctx) {
   cudaStreamSynchronize(ctx->edge);
   cudaStreamSynchronize(ctx->h2d);
   cudaStreamSynchronize(ctx->d2h);
+  cudaStreamSynchronize(ctx->xch);
+  cudaStreamSynchronize(ctx->hd);
   cudaEventDestroy(ctx->ev_h2d);
   cudaEventDestroy(ctx->ev_d2h);
   cudaStreamDestroy(ctx->h2d);
   cudaStreamDestroy(ctx->d2h);
+  cudaStreamDestroy(ctx->xch);
+  cudaStreamDestroy(ctx->hd);
   cudaStreamDestroy(ctx->aux);
   cudaStreamDestroy(ctx->br);
   cudaStreamDestroy(ctx->edge);
@@ -2193,6 +2241,8 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
     TGB_CUDA(cudaMemcpy(r->d_desc, desc.data(), sizeof(BarrierDesc) * desc.size(), cudaMemcpyHostToDevice));
     r->d_ctr = dalloc<int>(1);
     TGB_CUDA(cudaMemset(r->d_ctr, 0, sizeof(int)));
+    r->d_ctr_tail = dalloc<int>(1);
+    TGB_CUDA(cudaMemset(r->d_ctr_tail, 0, sizeof(int)));
   }
   *out = r.release();
   API_END
@@ -2209,6 +2259,7 @@ int tgnn_run_comm_init(tgnn_run* r, const char* unique_id128) {
   if (r->group_size > 1) {
     NCCL_CHECK(nccl::api().CommSplit(r->comm, r->group, r->rank, &r->gcomm, nullptr));
   }
+  NCCL_CHECK(nccl::api().CommSplit(r->comm, 0, r->rank, &r->hcomm, nullptr));
   TGB_CUDA(cudaEventCreateWithFlags(&r->ev_tail, cudaEventDisableTiming));
   TGB_CUDA(cudaEventCreateWithFlags(&r->ev_head, cudaEventDisableTiming));
   TGB_CUDA(cudaEventCreateWithFlags(&r->ev_comm, cudaEventDisableTiming));

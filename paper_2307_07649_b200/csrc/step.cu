@@ -1825,6 +1825,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
     fp.rs = w.bf.RS;
     fp.nf = w.bf.NF;
     fp.flag = c.d_numeric_flag;
+    if (c.ev_params_tail) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_params_tail, 0));  // static table updated
     gru_fused_launch(fp, w.bf.Xg, w.bf.Wzr, w.bf.Whm, w.bf.Whs, md, s);
     return;
   }
@@ -1853,6 +1854,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
            3 * d, nullptr, 1.0f);
     gemm_group_launch(gg, s);
   }
+  if (c.ev_params_tail) TGB_CUDA(cudaStreamWaitEvent(s, c.ev_params_tail, 0));  // static table updated
   launch_pdl(gru_out_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, w.s_hat, c.d_numeric_flag,
              P + L.off[tStatic], bfx, U);
   TGB_CUDA(cudaGetLastError());

@@ -142,6 +142,10 @@ struct StepCtx {
   cudaEvent_t ev_edge = nullptr;
   cudaEvent_t ev_g_zero = nullptr, ev_br_dec = nullptr, ev_br_join = nullptr;
   cudaEvent_t ev_red = nullptr;  // split-K reductions of the weight gradients on the branch
+  // graph pipeline: the previous barrier's tail-range update (static table,
+  // attention, decoder) was deferred; wait for it before the first reader on
+  // the main stream (gru_out's static columns of NF)
+  cudaEvent_t ev_params_tail = nullptr;
   void mark(int slot, cudaStream_t s) const {
     if (marks) marks->mark(slot, s);
   }

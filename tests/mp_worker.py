@@ -19,11 +19,17 @@ sys.path.insert(0, ROOT)
 
 def rank_body(a, rank, world, device, join):
     import paper_2307_07649_b200 as T
-    s = T.gen_synthetic(T.SynthParams(nodes=20, events=120, d_e=2, seed=21))
     ctx = T.Context(device)
-    g = T.TemporalGraph.from_stream(ctx, s)
-    mc = T.ModelConfig(d_mem=3, d_time=2, d_static=2, d_attn=3, d_hidden=2, d_e=2, n_neighbors=2,
-                       num_nodes=20, max_t=float(s.t[-1]))
+    if a.shape == "reddit":  # C2 dimensions: the production graph pipeline at realistic timings
+        g = T.TemporalGraph.synthetic(ctx, T.SynthParams(nodes=10984, events=60000, d_e=172, seed=4))
+        _, _, t = g.events()
+        mc = T.ModelConfig(d_mem=100, d_time=100, d_static=100, d_attn=100, d_hidden=100, d_e=172,
+                           n_neighbors=10, num_nodes=10984, max_t=float(t[-1]))
+    else:
+        s = T.gen_synthetic(T.SynthParams(nodes=20, events=120, d_e=2, seed=21))
+        g = T.TemporalGraph.from_stream(ctx, s)
+        mc = T.ModelConfig(d_mem=3, d_time=2, d_static=2, d_attn=3, d_hidden=2, d_e=2, n_neighbors=2,
+                           num_nodes=20, max_t=float(s.t[-1]))
     tc = T.TrainConfig(i=a.i, j=a.j, k=a.k, local_batch=a.local_batch, epochs=a.epochs, seed=3,
                        lr_base=a.lr)
     run = T.Run(ctx, g, mc, tc, 0, a.train_end, rank=rank, nranks=world, oplog=True,
@@ -68,6 +74,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "local"])
     ap.add_argument("--snapshots", action="store_true")
+    ap.add_argument("--shape", default="tiny", choices=["tiny", "reddit"])
     ap.add_argument("--direct", action="store_true", help="single-stream path instead of CUDA graphs")
     a = ap.parse_args()
     import paper_2307_07649_b200 as T

@@ -113,6 +113,27 @@ if _STINT:  # the captured stint graphs exist on the NCCL backend only (>= 2 GPU
             assert np.array_equal(res["graph"][key], res["direct"][key]), key
 
 
+if _NGPUS >= 2:  # the NCCL graph pipeline at C2 dimensions (one process per GPU)
+    @pytest.mark.parametrize("i,j,k", [(1, 1, 2), (2, 1, 1)])
+    def test_graph_pipeline_bitwise_equal_direct_at_c2_dims(i, j, k, tmp_path):
+        """k = 2 / i = 2 at Reddit dimensions over 40 barriers: the production
+        multi-barrier graphs (deferred tail update, head bucket on its own
+        communicator, i-axis exchange on its own stream) reproduce the direct
+        path bitwise and every replica stays identical."""
+        T_ = i * j * k
+        res = {}
+        for mode in ("graph", "direct"):
+            out = tmp_path / f"{mode}.npz"
+            launch("mp_worker.py", T_, "nccl", ["--i", str(i), "--j", str(j), "--k", str(k), "--epochs", str(T_),
+                                                "--shape", "reddit", "--local-batch", "600", "--train-end", "24000",
+                                                "--out", str(out)] + (["--direct"] if mode == "direct" else []),
+                   29800 + 7 * i + k + (mode == "direct"))
+            res[mode] = np.load(out)
+            assert bool(res[mode]["replicas_identical"])
+        for key in ("losses", "params"):
+            assert np.array_equal(res["graph"][key], res["direct"][key]), key
+
+
 # acceptance criterion 8 (ref/tests/acceptance.cpp:435-458, SURVEY 8c): final val
 # MRR at 525,000 traversed events; reference anchors and tolerances
 ANCHORS = {(1, 1, 1): (0.8767, 0.02), (1, 1, 4): (0.8824, 0.02), (1, 4, 1): (0.8368, 0.05)}
