@@ -141,13 +141,14 @@ def step_roofline(sz, cfg, nparam, events_s_per_gpu, peaks):
 
 
 def roofline_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum of the roofline kernel from
-    the committed ncu --set full capture (profiles/), per launch."""
+    """dram__bytes_read.sum + dram__bytes_write.sum of the roofline kernel (the
+    tc_gemm_kernel group) from the committed ncu --set full capture of one
+    barrier's GEMM launches (profiles/r02_roofline_traffic.json), per launch."""
     p = os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
-    return d["dram_read_bytes"] + d["dram_write_bytes"]
+    return d["dram_bytes_per_launch"]
 
 
 # ----------------------------------------------------------------- clocks

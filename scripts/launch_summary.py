@@ -26,7 +26,7 @@ def main() -> None:
             continue
         v = float(r[col["Metric Value"]].replace(",", ""))
         unit = r[col["Metric Unit"]]
-        us = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+        us = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
         name = r[col["Kernel Name"]].split("(")[0].replace("tgb::<unnamed>::", "").replace("(anonymous namespace)::", "")
         rows.append((int(r[col["ID"]]), name, r[col["Grid Size"]], us))
     starts = [i for i, r in enumerate(rows) if r[1].startswith("select_args_kernel")]
