@@ -608,9 +608,14 @@ struct tgnn_run {
   cudaGraphExec_t mexec = nullptr;
   // j > 1: one graph per sub-iteration position s = b % j (a whole stint is
   // j consecutive launches); per-stint plan args and team resets in d_stint
+  // (j > 1: 2 j of them -- [plan set][position]; a stint's j plans live in
+  // set (stint start / j) % 2, and the previous stint's last position plans
+  // the next stint into the other set on the aux stream)
   std::vector<cudaGraph_t> sgraph;
   std::vector<cudaGraphExec_t> sexec;
   StintDesc* d_stint = nullptr;
+  std::vector<StintDesc> h_stint;  // host copy (eager planning of a stint)
+  int64_t stint_planned = -1;      // stint start whose plans the graphs prepared ahead
   int64_t prepared = -1;  // barrier whose plan + read view are ready in plans/views[b % 2]
   cudaEvent_t ev_fork = nullptr, ev_written = nullptr, ev_next = nullptr;
   cudaEvent_t ev_gru = nullptr, ev_gzero = nullptr, ev_dec = nullptr, ev_brjoin = nullptr, ev_edge = nullptr;
@@ -740,7 +745,8 @@ void local_wait_all(tgnn_run* r, bool done, cudaStream_t s) {
     if (q != r->rank) TGB_CUDA(cudaStreamWaitEvent(s, done ? h->runs[q]->ev_ldone : h->runs[q]->ev_lready, 0));
 }
 
-void comm_allreduce(tgnn_run* r, void* buf, size_t count, RedTy ty, RedOp op, cudaStream_t s) {
+void comm_allreduce(tgnn_run* r, void* buf, size_t count, RedTy ty, RedOp op, cudaStream_t s,
+                    ncclComm_t nc = nullptr) {
   if (r->nranks == 1 || count == 0) return;
   if (r->hub) {
     tgnn_local_hub* h = r->hub;
@@ -771,7 +777,20 @@ void comm_allreduce(tgnn_run* r, void* buf, size_t count, RedTy ty, RedOp op, cu
   }
   const ncclDataType_t dt = ty == RedTy::F32 ? ncclFloat : ty == RedTy::F64 ? ncclDouble : ncclUint64;
   const ncclRedOp_t o = op == RedOp::Sum ? ncclSum : op == RedOp::Min ? ncclMin : ncclMax;
-  NCCL_CHECK(nccl::api().AllReduce(buf, buf, count, dt, o, r->comm, s));
+  NCCL_CHECK(nccl::api().AllReduce(buf, buf, count, dt, o, nc ? nc : r->comm, s));
+}
+
+// The flat gradient in the two buckets of the graph pipeline's split-phase
+// update (update_split): tail [split, end) on the global communicator, head
+// [0, split) on its duplicate -- the same NCCL calls, so the direct path
+// reproduces the graph path's sums bitwise at any rank count.
+int64_t grad_split(const tgnn_trainer* tr) { return (tr->L.off[tWq] + 3) / 4 * 4; }
+
+void comm_allreduce_grads(tgnn_run* r, cudaStream_t s) {
+  tgnn_trainer* tr = r->tr.get();
+  const int64_t split = grad_split(tr);
+  comm_allreduce(r, tr->grads + split, static_cast<size_t>(tr->L.total - split), RedTy::F32, RedOp::Sum, s);
+  comm_allreduce(r, tr->grads, static_cast<size_t>(split), RedTy::F32, RedOp::Sum, s, r->hcomm);
 }
 
 // The write packs of team `team`'s i members into r->gathered[member]
@@ -920,6 +939,11 @@ void run_barrier(tgnn_run* r, int64_t b) {
   sc.mark(phPlan, s);
   double* loss_slot = r->d_losses + b;
   const int i = c.i, j = c.j;
+  // j > 1: the stint's plan set (shared with the stint graphs, so the two
+  // paths can alternate mid-stint)
+  const size_t base = j > 1 ? static_cast<size_t>(((b / j) % 2) * j) : 0;
+  std::vector<DPlan>& plans = tr->plans;
+  std::vector<DView>& views = tr->views;
   if (b % j == 0) {
     // Stint start: the group's teams read and write in pair order (the
     // daemon plan's R/W brackets, parallel.hpp:278-291). A team publishes its
@@ -941,20 +965,20 @@ void run_barrier(tgnn_run* r, int64_t b) {
           a.seed = c.seed;
           a.neg_mode = 1;
           a.valid = 1;
-          DPlan& pl = tr->plans[static_cast<size_t>(sub)];
+          DPlan& pl = plans[base + static_cast<size_t>(sub)];
           set_plan_args_launch(pl.args, a, s);
           plan_launch(r->g->d, pl, s, ctx->side);
-          gather_view_launch(pl, r->mem->d, tr->views[static_cast<size_t>(sub)], s);
+          gather_view_launch(pl, r->mem->d, views[base + static_cast<size_t>(sub)], s);
         }
-        substep_gru_launch(sc, tr->plans[0], tr->views[0], s);
+        substep_gru_launch(sc, plans[base], views[base], s);
         sc.mark(phWrites, s);
-        root_writes_launch(sc, tr->plans[0], tr->views[0], s, r->group_size > 1 ? nullptr : &r->mem->d);
+        root_writes_launch(sc, plans[base], views[base], s, r->group_size > 1 ? nullptr : &r->mem->d);
         if (r->oplog) {
           OplogPlans op;
           op.n = std::min(t.subs, 8);
           for (int x = 0; x < op.n; ++x) {
-            op.sizes[x] = tr->plans[static_cast<size_t>(x)].sizes;
-            op.supports[x] = tr->plans[static_cast<size_t>(x)].supports;
+            op.sizes[x] = plans[base + static_cast<size_t>(x)].sizes;
+            op.supports[x] = plans[base + static_cast<size_t>(x)].supports;
           }
           oplog_record_launch(sc, op, r->d_oplog, b, s);
         }
@@ -966,14 +990,14 @@ void run_barrier(tgnn_run* r, int64_t b) {
       if (r->snaps) take_snapshot(r, (b / j) * j + tt, s);
     }
     if (t.active) {
-      substep_rest_launch(sc, tr->plans[0], tr->views[0], loss_slot, s);
+      substep_rest_launch(sc, plans[base], views[base], loss_slot, s);
     } else {
       TGB_CUDA(cudaMemsetAsync(tr->grads, 0, sizeof(float) * tr->L.total, s));
       TGB_CUDA(cudaMemsetAsync(loss_slot, 0, sizeof(double), s));
     }
   } else {
     if (t.active) {
-      substep_launch(sc, tr->plans[static_cast<size_t>(t.sub)], tr->views[static_cast<size_t>(t.sub)],
+      substep_launch(sc, plans[base + static_cast<size_t>(t.sub)], views[base + static_cast<size_t>(t.sub)],
                      loss_slot, s);
     } else {
       TGB_CUDA(cudaMemsetAsync(tr->grads, 0, sizeof(float) * tr->L.total, s));
@@ -982,7 +1006,7 @@ void run_barrier(tgnn_run* r, int64_t b) {
   }
   // average_active_grads (trainer.hpp:473-483): idle ranks contribute zeros.
   sc.mark(phAllreduce, s);
-  comm_allreduce(r, tr->grads, static_cast<size_t>(tr->L.total), RedTy::F32, RedOp::Sum, s);
+  comm_allreduce_grads(r, s);
   const int64_t active = r->sched.active_trainers[static_cast<size_t>(b)];
   sc.mark(phAdam, s);
   tr->adam_t = b;  // Adam's step counter advances on every rank at every barrier
@@ -1005,7 +1029,7 @@ void update_split(tgnn_run* r, const StepCtx& sc, cudaStream_t s) {
   tgnn_trainer* tr = r->tr.get();
   cudaStream_t c = r->nranks > 1 ? r->ctx->comm : r->ctx->br;
   // 16-byte aligned split: the few Wq entries below it join the head bucket
-  const int64_t split = (tr->L.off[tWq] + 3) / 4 * 4;
+  const int64_t split = grad_split(tr);
   TGB_CUDA(cudaStreamWaitEvent(c, r->ev_tail, 0));
   if (c != r->ctx->br) TGB_CUDA(cudaStreamWaitEvent(c, r->ev_brjoin, 0));  // the branch's tail gradients
   cudaStream_t u = c;  // the tail update
@@ -1173,9 +1197,9 @@ void barrier_body_slot(tgnn_run* r, int p, bool xg_split) {
   pl.ev_sorted = sorted;
 }
 
-__global__ void select_stint_args_kernel(const StintDesc* __restrict__ sd, const int* __restrict__ ctr, int sub,
-                                         PlanArgs* dst) {
-  *dst = sd[*ctr].args[sub];
+__global__ void select_stint_args_kernel(const StintDesc* __restrict__ sd, const int* __restrict__ ctr, int offset,
+                                         int sub, PlanArgs* dst) {
+  *dst = sd[*ctr + offset].args[sub];
 }
 
 __global__ void reset_stint_kernel(DMem st, const StintDesc* __restrict__ sd, const int* __restrict__ ctr, int team) {
@@ -1198,39 +1222,83 @@ __global__ void reset_stint_kernel(DMem st, const StintDesc* __restrict__ sd, co
 // stint start the group's teams run the daemon's R/W chain in pair order (an
 // idle team contributes an empty plan and an empty write pack, so every rank
 // issues the same collectives); later positions run their pre-planned sub.
-void barrier_body_stint(tgnn_run* r, int sidx) {
+// Graph body for j > 1 at stint position sidx with the stint's plans in plan
+// set `set` (slots set*j .. set*j + j - 1): the direct path's launch sequence
+// with every per-barrier value taken from the device tables. The plans were
+// made one stint ahead (by the previous stint's last position, on the aux
+// stream), so the stint-start team chain is only the daemon's R/W brackets:
+// the gathers, the GRU freshen, the root writes and their exchange per team in
+// pair order (an idle team contributes an empty plan and an empty write pack,
+// so every rank issues the same collectives). The rest of each position runs
+// the j = 1 pipeline's branches and split-phase update.
+void barrier_body_stint(tgnn_run* r, int sidx, int set) {
   tgnn_ctx* ctx = r->ctx;
   tgnn_trainer* tr = r->tr.get();
   cudaStream_t s = ctx->stream;
   StepCtx sc = tr->sc();
   sc.d_ctr = r->d_ctr;
-  const int i = r->tc.i, j = r->tc.j;
-  std::vector<cudaEvent_t> saved(static_cast<size_t>(j));
-  for (int x = 0; x < j; ++x) saved[static_cast<size_t>(x)] = tr->plans[static_cast<size_t>(x)].ev_sorted;
+  sc.packed = true;  // by the previous barrier's Adam (or the segment prologue)
+  const int j = r->tc.j;
+  const size_t base = static_cast<size_t>(set * j), nbase = static_cast<size_t>((1 - set) * j);
+  std::vector<cudaEvent_t> saved(tr->plans.size());
+  for (size_t x = 0; x < tr->plans.size(); ++x) saved[x] = tr->plans[x].ev_sorted;
   auto restore = [&]() {
-    for (int x = 0; x < j; ++x) tr->plans[static_cast<size_t>(x)].ev_sorted = saved[static_cast<size_t>(x)];
+    for (size_t x = 0; x < tr->plans.size(); ++x) tr->plans[x].ev_sorted = saved[x];
   };
+  TGB_CUDA(cudaEventRecord(r->ev_fork, s));
+  cudaStream_t br = ctx->br;
+  TGB_CUDA(cudaStreamWaitEvent(br, r->ev_fork, 0));
+  TGB_CUDA(cudaMemsetAsync(tr->grads, 0, sizeof(float) * tr->L.total, br));
+  TGB_CUDA(cudaEventRecord(r->ev_gzero, br));
+  sc.br = br;
+  sc.ev_g_zero = r->ev_gzero;
+  sc.ev_br_dec = r->ev_dec;
+  sc.ev_br_join = r->ev_brjoin;
+  sc.ev_red = r->ev_red;
+  sc.ev_tail_grads = r->ev_tail;
   try {
+    for (int sub = 0; sub < j; ++sub) tr->plans[base + static_cast<size_t>(sub)].ev_sorted = nullptr;  // sorted ahead
+    DPlan& pl = tr->plans[base + static_cast<size_t>(sidx)];
+    DView& vw = tr->views[base + static_cast<size_t>(sidx)];
+    if (gemm_impl() == kGemmTma) {  // the plan-only half of the attention projection, from the start
+      TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_fork, 0));
+      StepCtx se = sc;
+      attn_edge_launch(se, pl, ctx->edge);
+      TGB_CUDA(cudaEventRecord(r->ev_edge, ctx->edge));
+      sc.ev_edge = r->ev_edge;
+    }
+    const bool plan_next = sidx == j - 1;
+    if (plan_next) {  // the next stint's plans into the other set, beside this position
+      cudaStream_t aux = ctx->aux;
+      TGB_CUDA(cudaStreamWaitEvent(aux, r->ev_fork, 0));
+      for (int sub = 0; sub < j; ++sub) {
+        DPlan& nx = tr->plans[nbase + static_cast<size_t>(sub)];
+        select_stint_args_kernel<<<1, 1, 0, aux>>>(r->d_stint, r->d_ctr, 1, sub, nx.args);
+        TGB_CUDA(cudaGetLastError());
+        plan_launch(r->g->d, nx, aux, ctx->side);
+      }
+      for (int sub = 0; sub < j; ++sub) {
+        DPlan& nx = tr->plans[nbase + static_cast<size_t>(sub)];
+        if (nx.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(aux, nx.ev_sorted, 0));
+      }
+      TGB_CUDA(cudaEventRecord(r->ev_next, aux));
+    }
     if (sidx == 0) {
       for (int tt = 0; tt < j; ++tt) {
         reset_stint_kernel<<<4 * num_sms(), 256, 0, s>>>(r->mem->d, r->d_stint, r->d_ctr, tt);
         TGB_CUDA(cudaGetLastError());
         if (tt == r->team) {
-          for (int sub = 0; sub < j; ++sub) {
-            DPlan& pl = tr->plans[static_cast<size_t>(sub)];
-            select_stint_args_kernel<<<1, 1, 0, s>>>(r->d_stint, r->d_ctr, sub, pl.args);
-            TGB_CUDA(cudaGetLastError());
-            plan_launch(r->g->d, pl, s, ctx->side);
-            gather_view_launch(pl, r->mem->d, tr->views[static_cast<size_t>(sub)], s);
-          }
-          substep_gru_launch(sc, tr->plans[0], tr->views[0], s);
-          root_writes_launch(sc, tr->plans[0], tr->views[0], s, nullptr);
+          for (int sub = 0; sub < j; ++sub)
+            gather_view_launch(tr->plans[base + static_cast<size_t>(sub)], r->mem->d,
+                               tr->views[base + static_cast<size_t>(sub)], s);
+          substep_gru_launch(sc, pl, vw, s);
+          root_writes_launch(sc, pl, vw, s, nullptr);
           if (r->oplog) {
             OplogPlans op;
             op.n = j;
             for (int x = 0; x < j; ++x) {
-              op.sizes[x] = tr->plans[static_cast<size_t>(x)].sizes;
-              op.supports[x] = tr->plans[static_cast<size_t>(x)].supports;
+              op.sizes[x] = tr->plans[base + static_cast<size_t>(x)].sizes;
+              op.supports[x] = tr->plans[base + static_cast<size_t>(x)].supports;
             }
             oplog_record_launch(sc, op, r->d_oplog, 0, s);
           }
@@ -1238,16 +1306,15 @@ void barrier_body_stint(tgnn_run* r, int sidx) {
         comm_bcast_packs(r, tt, s);
         apply_gathered(r, s);
       }
-      substep_rest_launch(sc, tr->plans[0], tr->views[0], r->d_losses, s);
-      // the later subs' routing sorts ran on the side stream: join them here
-      for (int sub = 1; sub < j; ++sub) TGB_CUDA(cudaStreamWaitEvent(s, tr->plans[static_cast<size_t>(sub)].ev_sorted, 0));
     } else {
-      DPlan& pl = tr->plans[static_cast<size_t>(sidx)];
-      pl.ev_sorted = nullptr;  // sorted inside the stint-start graph
-      substep_launch(sc, pl, tr->views[static_cast<size_t>(sidx)], r->d_losses, s);
+      substep_gru_launch(sc, pl, vw, s);
     }
-    comm_allreduce(r, tr->grads, static_cast<size_t>(tr->L.total), RedTy::F32, RedOp::Sum, s);
-    adam_pack_launch(sc, tr->am, tr->av, s, r->d_desc, r->d_ctr);
+    substep_rest_launch(sc, pl, vw, r->d_losses, s);
+    const bool defer = r->defer_tail;
+    r->defer_tail = false;  // every position is its own graph: join the tail update
+    update_split(r, sc, s);
+    r->defer_tail = defer;
+    if (plan_next) TGB_CUDA(cudaStreamWaitEvent(s, r->ev_next, 0));
     incr_launch(r->d_ctr, s);
   } catch (...) {
     restore();
@@ -1256,17 +1323,51 @@ void barrier_body_stint(tgnn_run* r, int sidx) {
   restore();
 }
 
+// Eager planning of stint b0 (the first stint of a run, or after the direct
+// path ran the previous stint's last position) into its plan set.
+void plan_stint_now(tgnn_run* r, int64_t b0) {
+  tgnn_trainer* tr = r->tr.get();
+  cudaStream_t s = r->ctx->stream;
+  const int j = r->tc.j;
+  const size_t base = static_cast<size_t>(((b0 / j) % 2) * j);
+  const StintDesc& sd = r->h_stint[static_cast<size_t>(b0)];
+  for (int sub = 0; sub < j; ++sub) {
+    DPlan& pl = tr->plans[base + static_cast<size_t>(sub)];
+    set_plan_args_launch(pl.args, sd.args[sub], s);
+    plan_launch(r->g->d, pl, s, r->ctx->side);
+  }
+  for (int sub = 0; sub < j; ++sub) {
+    DPlan& pl = tr->plans[base + static_cast<size_t>(sub)];
+    if (pl.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));
+  }
+  r->stint_planned = b0;
+}
+
+void ensure_graph_events(tgnn_run* r) {
+  if (r->ev_fork) return;
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming));
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_written, cudaEventDisableTiming));
+  TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
+  cudaEvent_t* more[] = {&r->ev_gru,  &r->ev_gzero, &r->ev_dec,    &r->ev_brjoin,
+                         &r->ev_edge, &r->ev_red,   &r->ev_artail, &r->ev_upd, &r->ev_mid};
+  for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  cudaEvent_t* upd[] = {&r->ev_tail, &r->ev_head, &r->ev_comm};
+  for (cudaEvent_t* e : upd)
+    if (!*e) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
 void build_stint_graphs(tgnn_run* r) {
   cudaStream_t s = r->ctx->stream;
   gemm_kernels_prepare();
+  ensure_graph_events(r);
   TGB_CUDA(cudaStreamSynchronize(s));
   const int j = r->tc.j;
-  r->sgraph.assign(static_cast<size_t>(j), nullptr);
-  r->sexec.assign(static_cast<size_t>(j), nullptr);
-  for (int x = 0; x < j; ++x) {
+  r->sgraph.assign(static_cast<size_t>(2 * j), nullptr);
+  r->sexec.assign(static_cast<size_t>(2 * j), nullptr);
+  for (int x = 0; x < 2 * j; ++x) {
     TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     try {
-      barrier_body_stint(r, x);
+      barrier_body_stint(r, x % j, x / j);
     } catch (...) {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(s, &g);
@@ -1299,17 +1400,7 @@ void build_graph(tgnn_run* r) {
   cudaStream_t s = r->ctx->stream;
   gemm_kernels_prepare();
   TGB_CUDA(cudaStreamSynchronize(s));
-  if (!r->ev_fork) {
-    TGB_CUDA(cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming));
-    TGB_CUDA(cudaEventCreateWithFlags(&r->ev_written, cudaEventDisableTiming));
-    TGB_CUDA(cudaEventCreateWithFlags(&r->ev_next, cudaEventDisableTiming));
-    cudaEvent_t* more[] = {&r->ev_gru,  &r->ev_gzero, &r->ev_dec,    &r->ev_brjoin,
-                           &r->ev_edge, &r->ev_red,   &r->ev_artail, &r->ev_upd, &r->ev_mid};
-    for (cudaEvent_t* e : more) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    cudaEvent_t* upd[] = {&r->ev_tail, &r->ev_head, &r->ev_comm};
-    for (cudaEvent_t* e : upd)
-      if (!*e) TGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  }
+  ensure_graph_events(r);
   for (int p = 0; p < 2; ++p) {
     TGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     try {
@@ -2153,7 +2244,7 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
   r->group_size = r->tc.i * r->tc.j;
   ModelDims m = dims_of(&opt->model);
   r->tr = std::make_unique<tgnn_trainer>();
-  r->tr->init(ctx, g, m, r->tc.local_batch, r->tc.seed, r->tc.j);
+  r->tr->init(ctx, g, m, r->tc.local_batch, r->tc.seed, r->tc.j > 1 ? 2 * r->tc.j : 1);
   r->mem.reset(memstore_new(ctx, g->d.N, m.d_mem));
   r->d_losses = dalloc<double>(static_cast<size_t>(std::max<int64_t>(r->sched.barriers, 1)));
   TGB_CUDA(cudaMemset(r->d_losses, 0, sizeof(double) * std::max<int64_t>(r->sched.barriers, 1)));
@@ -2189,7 +2280,7 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
   TGB_CUDA(cudaEventCreate(&r->ev_t0));
   r->use_graphs = opt->use_graphs != 0 && r->tc.j <= kMaxStintJ && !r->snaps;
   if (r->use_graphs && r->tc.j > 1) {
-    std::vector<StintDesc> sd(static_cast<size_t>(r->sched.barriers + 1));
+    std::vector<StintDesc> sd(static_cast<size_t>(r->sched.barriers + r->tc.j + 1));
     for (int64_t b = 0; b < r->sched.barriers; b += r->tc.j) {
       StintDesc& e = sd[static_cast<size_t>(b)];
       const host::Task t = r->sched.task(r->rank, b);
@@ -2211,6 +2302,7 @@ int tgnn_run_create(tgnn_ctx* ctx, tgnn_graph* g, const tgnn_run_options* opt, t
     }
     r->d_stint = dalloc<StintDesc>(sd.size());
     TGB_CUDA(cudaMemcpy(r->d_stint, sd.data(), sizeof(StintDesc) * sd.size(), cudaMemcpyHostToDevice));
+    r->h_stint = sd;
   }
   if (r->use_graphs) {
     // one idle entry past the end: the last barrier prepares an empty plan
@@ -2353,9 +2445,18 @@ int tgnn_run_barriers(tgnn_run* r, int64_t first, int64_t count) {
     if (r->use_graphs && r->tc.j > 1) {
       if (r->sexec.empty()) build_stint_graphs(r);
       set_int_kernel<<<1, 1, 0, r->ctx->stream>>>(r->d_ctr, static_cast<int>(b));
+      set_int_kernel<<<1, 1, 0, r->ctx->stream>>>(r->d_ctr_tail, static_cast<int>(b));
       TGB_CUDA(cudaGetLastError());
-      for (int64_t x = b; x < seg_end; ++x)
-        TGB_CUDA(cudaGraphLaunch(r->sexec[static_cast<size_t>(x % r->tc.j)], r->ctx->stream));
+      pack_weights(r->tr->sc(), r->ctx->stream);  // the stint graphs read packed weights
+      const int j = r->tc.j;
+      for (int64_t x = b; x < seg_end; ++x) {
+        const int sidx = static_cast<int>(x % j);
+        const int64_t b0 = x - sidx;
+        const int set = static_cast<int>((b0 / j) % 2);
+        if (sidx == 0 && r->stint_planned != b0) plan_stint_now(r, b0);
+        TGB_CUDA(cudaGraphLaunch(r->sexec[static_cast<size_t>(set * j + sidx)], r->ctx->stream));
+        if (sidx == j - 1) r->stint_planned = b0 + j;  // planned ahead by this position
+      }
       r->tr->adam_t = seg_end;
     } else if (r->use_graphs) {
       if (!r->exec[0]) build_graph(r);
@@ -2593,8 +2694,10 @@ int tgnn_run_profile_barrier(tgnn_run* r, double* phase_ms, int32_t* sizes, int3
   for (size_t q = 0; q + 1 < at.size(); ++q)
     if (at[q].second < phCount) phase_ms[at[q].second] += at[q + 1].first - at[q].first;
   int32_t sz[kSzCount];
-  TGB_CUDA(cudaMemcpy(sz, r->tr->plans[r->use_graphs && r->tc.j == 1 && !direct ? static_cast<size_t>(b & 1) : 0].sizes, sizeof(sz),
-                      cudaMemcpyDeviceToHost));
+  const int jj = r->tc.j;
+  const size_t slot = jj > 1 ? static_cast<size_t>(((b / jj) % 2) * jj + b % jj)
+                             : (r->use_graphs && !direct ? static_cast<size_t>(b & 1) : 0);
+  TGB_CUDA(cudaMemcpy(sz, r->tr->plans[slot].sizes, sizeof(sz), cudaMemcpyDeviceToHost));
   TGB_CUDA(cudaMemcpy(&sz[7], r->tr->w.w_count, sizeof(int32_t), cudaMemcpyDeviceToHost));  // W root writes
   for (int x = 0; x < kSzCount; ++x) sizes[x] = sz[x];
   API_END
