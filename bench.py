@@ -326,7 +326,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--e2e-chunk", type=int, default=4, help="barriers per run.step call in the e2e loop")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--cpu-baseline-steps", type=int, default=3)

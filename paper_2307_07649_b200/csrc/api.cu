@@ -1288,11 +1288,18 @@ void barrier_body_stint(tgnn_run* r, int sidx, int set) {
         reset_stint_kernel<<<4 * num_sms(), 256, 0, s>>>(r->mem->d, r->d_stint, r->d_ctr, tt);
         TGB_CUDA(cudaGetLastError());
         if (tt == r->team) {
-          for (int sub = 0; sub < j; ++sub)
+          // the read bracket: sub 0's view on the chain, the later subs' views
+          // beside its GRU freshen (joined before this team's writes land)
+          gather_view_launch(pl, r->mem->d, vw, s);
+          TGB_CUDA(cudaEventRecord(r->ev_gru, s));
+          TGB_CUDA(cudaStreamWaitEvent(ctx->aux, r->ev_gru, 0));
+          for (int sub = 1; sub < j; ++sub)
             gather_view_launch(tr->plans[base + static_cast<size_t>(sub)], r->mem->d,
-                               tr->views[base + static_cast<size_t>(sub)], s);
+                               tr->views[base + static_cast<size_t>(sub)], ctx->aux);
+          TGB_CUDA(cudaEventRecord(r->ev_written, ctx->aux));
           substep_gru_launch(sc, pl, vw, s);
           root_writes_launch(sc, pl, vw, s, nullptr);
+          TGB_CUDA(cudaStreamWaitEvent(s, r->ev_written, 0));
           if (r->oplog) {
             OplogPlans op;
             op.n = j;
