@@ -9,6 +9,8 @@
 //   shim_driver gpu   -- the drop-in on cuda:0 against the reference
 // Prints one line per check ("ok ..." / "FAIL ..."); exit status = failures.
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <fstream>
 #include <sstream>
@@ -22,6 +24,8 @@ using namespace tgnn;
 namespace {
 
 int g_fail = 0;
+
+double g_ref_mean[2] = {0, 0};  // reference mean MRR over seeds 5..12 at (1,1,1), (1,1,4) (argv)
 
 void report(bool ok, const std::string& what) {
   std::printf("%s %s\n", ok ? "ok" : "FAIL", what.c_str());
@@ -314,8 +318,12 @@ void gpu_checks() {
     double harmonic = 0;
     for (int k = 1; k <= 50; ++k) harmonic += 1.0 / k;
     const double want7 = 3.0 * harmonic / 50.0;
-    // (i, j, k), reference final val MRR at 525,000 traversed events, tolerance
-    const struct { int i, j, k; double mrr, tol; } runs[] = {{1, 1, 1, 0.8767, 0.02}, {1, 1, 4, 0.8824, 0.02}};
+    // (i, j, k), the reference's mean final val MRR at 525,000 traversed events
+    // over training seeds 5..12 (tests/golden/convergence_ref.json, passed on
+    // the command line by tests/test_shim_cpp.py; seed 5 alone is the
+    // reference's anchor 0.8767 / 0.8824), tolerance 0.02 on the mean
+    const struct { int i, j, k; double mrr, tol; } runs[] = {{1, 1, 1, g_ref_mean[0], 0.02},
+                                                            {1, 1, 4, g_ref_mean[1], 0.02}};
     for (const auto& v : runs) {
       RunOptions x = o;
       x.train.i = v.i;
@@ -341,9 +349,30 @@ void gpu_checks() {
         report(best20 >= want7, tag + " criterion 7: best val MRR " + std::to_string(best20) +
                                     " within 20 epochs >= " + std::to_string(want7));
       const MetricsRow& last = r.metrics.back();
-      report(last.traversed == 525000 && std::fabs(last.val_mrr - v.mrr) <= v.tol,
-             tag + " criterion 8: final val MRR " + std::to_string(last.val_mrr) + " at " +
-                 std::to_string(last.traversed) + " traversed (reference " + std::to_string(v.mrr) + ")");
+      // criterion 8 over seeds 5..12: seed 5 is this run, the others train
+      // without per-epoch validation and score the final weights the same way
+      double sum = last.val_mrr;
+      std::string per = std::to_string(last.val_mrr);
+      bool traversed_ok = last.traversed == 525000;
+      for (std::uint64_t sd = 6; sd <= 12; ++sd) {
+        RunOptions y = x;
+        y.train.seed = sd;
+        y.val_begin = y.val_end = 0;
+        y.on_eval = nullptr;
+        y.metrics_out = nullptr;
+        const RunResult ry = b200::run_training(g, y);
+        b200::Context cx(0);
+        b200::Graph Gx(cx, g);
+        const double m = b200::evaluate_mrr(cx, Gx, ry.params, 3500, 4500, 175, 49, 5).mrr;
+        sum += m;
+        per += " " + std::to_string(m);
+        traversed_ok = traversed_ok && ry.barriers == r.barriers;
+      }
+      const double mean = sum / 8.0;
+      report(traversed_ok && v.mrr > 0 && std::fabs(mean - v.mrr) <= v.tol,
+             tag + " criterion 8: final val MRR at " + std::to_string(last.traversed) +
+                 " traversed, seeds 5..12: " + per + "; mean " + std::to_string(mean) + " (reference mean " +
+                 std::to_string(v.mrr) + ")");
       // checkpoint-on-best through on_eval (trainer.hpp:584-587): the best row's
       // weights score that row's MRR again
       b200::Context ctx(0);
@@ -363,9 +392,15 @@ int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   try {
     if (mode == "cpu") cpu_checks();
-    else if (mode == "gpu") gpu_checks();
+    else if (mode == "gpu") {
+      if (argc > 3) {
+        g_ref_mean[0] = std::atof(argv[2]);
+        g_ref_mean[1] = std::atof(argv[3]);
+      }
+      gpu_checks();
+    }
     else {
-      std::fprintf(stderr, "usage: shim_driver cpu|gpu\n");
+      std::fprintf(stderr, "usage: shim_driver cpu | gpu [ref_mean_111 ref_mean_114]\n");
       return 2;
     }
   } catch (const std::exception& e) {

@@ -1130,9 +1130,11 @@ void barrier_body_slot(tgnn_run* r, int p, bool xg_split) {
     if (tail_wait) TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_upd, 0));
     StepCtx se = sc;
     se.marks = nullptr;  // phase markers live on the main stream
-    attn_edge_launch(se, pl, ctx->edge);
+    const bool join = edge_join_enabled(r->tr->m.d_mem);
+    attn_edge_launch(se, pl, ctx->edge, !join);
     TGB_CUDA(cudaEventRecord(r->ev_edge, ctx->edge));
     sc.ev_edge = r->ev_edge;
+    sc.edge_gemm_joined = join;
   }
   // this barrier: its plan was sorted inside the previous graph
   cudaEvent_t sorted = pl.ev_sorted;
@@ -1263,9 +1265,11 @@ void barrier_body_stint(tgnn_run* r, int sidx, int set) {
     if (gemm_impl() == kGemmTma) {  // the plan-only half of the attention projection, from the start
       TGB_CUDA(cudaStreamWaitEvent(ctx->edge, r->ev_fork, 0));
       StepCtx se = sc;
-      attn_edge_launch(se, pl, ctx->edge);
+      const bool join = edge_join_enabled(tr->m.d_mem);
+      attn_edge_launch(se, pl, ctx->edge, !join);
       TGB_CUDA(cudaEventRecord(r->ev_edge, ctx->edge));
       sc.ev_edge = r->ev_edge;
+      sc.edge_gemm_joined = join;
     }
     const bool plan_next = sidx == j - 1;
     if (plan_next) {  // the next stint's plans into the other set, beside this position

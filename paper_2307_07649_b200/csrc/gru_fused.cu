@@ -18,7 +18,7 @@
 //      the h_m columns in TMEM (K = 64 per swizzle atom); its B tile was loaded
 //      by TMA into the freed ring stage.
 //   4. epilogue: h = tanh, s_hat = (1 - z) s + z h (rows with a cached mail;
-//      s otherwise), written with z, r, h (for the backward), the slice of the
+//      s otherwise), written with the pre-activations a_z, a_r, a_h (for the backward), the slice of the
 //      [r*s | 1] operand of the Wh_s weight gradient, and the node operand NF
 //      = [s_hat | static | 1] of the attention projections (the last slice
 //      adds the static block); operand rows [U, roundup64(U)) are zeroed
@@ -287,11 +287,11 @@ __global__ void __launch_bounds__(kGfThreads, 1) gru_fused_kernel(const __grid_c
       tmem_ld8(tl + 128 + 8 * sl, va);
       tmem_ld_wait();
 #pragma unroll
-      for (int e = 0; e < 8; ++e) xrow[8 * sl + e] = sigm(__uint_as_float(va[e]));
+      for (int e = 0; e < 8; ++e) xrow[8 * sl + e] = __uint_as_float(va[e]);
     }
     epi_sync();
     if (et == 0) gf_stamp(12);
-    store_rows(X, 33, 0, nu, p.gates, ld3);  // z
+    store_rows(X, 33, 0, nu, p.gates, ld3);  // a_z (pre-activation, for the backward)
     // the slice of the [r*s | 1] operand in global memory (Wh_s weight
     // gradient): four 16-byte chunks per row, from the swizzled shared copy
 #pragma unroll 1
@@ -311,10 +311,10 @@ __global__ void __launch_bounds__(kGfThreads, 1) gru_fused_kernel(const __grid_c
       tmem_ld8(tl + u0 + 8 * sl, vb);
       tmem_ld_wait();
 #pragma unroll
-      for (int e = 0; e < 8; ++e) xrow[8 * sl + e] = sigm(__uint_as_float(vb[e]));
+      for (int e = 0; e < 8; ++e) xrow[8 * sl + e] = __uint_as_float(vb[e]);
     }
     epi_sync();
-    store_rows(X, 33, 0, nu, p.gates + d, ld3);  // r
+    store_rows(X, 33, 0, nu, p.gates + d, ld3);  // a_r
     // (c) GEMM2 done: h = tanh (staged in X), s_hat = (1 - z) s + z h (into S)
     if (et == 0) gf_stamp(6);
     mbar_wait(t2full, 0);
@@ -331,19 +331,20 @@ __global__ void __launch_bounds__(kGfThreads, 1) gru_fused_kernel(const __grid_c
       for (int e = 0; e < 8; ++e) {
         const int j = 8 * sl + e, u = u0 + j;
         if (j >= nu) continue;
-        const float h = tanhf(__uint_as_float(vb[e]));
+        const float ah = __uint_as_float(vb[e]);
+        const float h = tanhf(ah);
         float out = srow[u];
         if (has) {
-          const float z = sigm(__uint_as_float(va[e]));
-          out = (1.0f - z) * out + z * h;
+          const float az = __uint_as_float(va[e]);
+          out = sigm(-az) * out + sigm(az) * h;
           if (!isfinite(out)) atomicExch(p.flag, 1);
         }
         srow[u] = out;
-        xrow[j] = h;
+        xrow[j] = ah;
       }
     }
     epi_sync();
-    store_rows(X, 33, 0, nu, p.gates + 2 * d, ld3);  // h
+    store_rows(X, 33, 0, nu, p.gates + 2 * d, ld3);  // a_h
     store_rows(S, kLdS, u0, nu, p.s_hat, d);         // s_hat
     // NF = [s_hat | static | 1]: the slice's unit columns; the last slice also
     // the static block and the ones column; rows [U, roundup64(U)) zero

@@ -20,7 +20,7 @@ struct GruFusedParams {
   const float* mem = nullptr;       // read view memory rows [U x d] (s)
   const int32_t* mail_ev = nullptr; // cached mail event per view row (-1: none)
   const float* stat = nullptr;      // static table [N x ds]
-  float* gates = nullptr;           // [U x 3d]: z, r, h (activated), for the backward
+  float* gates = nullptr;           // [U x 3d]: a_z, a_r, a_h (pre-activations), for the backward
   float* s_hat = nullptr;           // [U x d]
   BfMat rs, nf;                     // [r * s | 1] and [s_hat | static | 1] operands
   int* flag = nullptr;

@@ -226,8 +226,10 @@ __global__ void assemble_gru_time_kernel(Dims D, DPlan pl, DView vw, const float
   bf_zero_tail(bf.GU, U, cap_U, D.dt);
 }
 
-// z, r = sigmoid(gates + b) (bias already added by the GEMM); RS = r * s.
-__global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
+// r = sigmoid(a_r) (bias already added by the GEMM); RS = r * s. Gates keeps
+// the pre-activations a_z, a_r, a_h: the backward takes the derivatives from
+// them (dsigmoidf_ / dtanhf_), exact where the gates saturate.
+__global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ Gates,
                                float* __restrict__ RS, StepBf bf, int cap_U) {
   pdl_wait();
   pdl_trigger();
@@ -235,11 +237,7 @@ __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int64_t u = x / D.d, i = x % D.d;
-    float* gr = Gates + u * 3 * D.d;
-    const float z = sigmoidf_(gr[i]);
-    const float r = sigmoidf_(gr[D.d + i]);
-    gr[i] = z;
-    gr[D.d + i] = r;
+    const float r = sigmoidf_(Gates[u * 3 * D.d + D.d + i]);
     const float rs = r * vw.mem[x];
     if (RS) RS[x] = rs;
     bf_put(bf.RS, u, i, rs);
@@ -252,7 +250,7 @@ __global__ void gru_mid_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
 // (freshen_memory, trainer.hpp:111-124; gru_update, gru.hpp:59-85).
 // With the TMA engine it also writes the node-feature operand NF = [s_hat |
 // static | 1] of every support (the node half of the attention projections).
-__global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ Gates,
+__global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, const float* __restrict__ Gates,
                                float* __restrict__ s_hat, int* flag, const float* __restrict__ stat,
                                StepBf bf, int cap_U) {
   pdl_wait();
@@ -261,14 +259,13 @@ __global__ void gru_out_kernel(Dims D, DPlan pl, DView vw, float* __restrict__ G
   const int64_t total = static_cast<int64_t>(U) * D.d;
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int64_t u = x / D.d, i = x % D.d;
-    float* gr = Gates + u * 3 * D.d;
+    const float* gr = Gates + u * 3 * D.d;
     const float h = tanhf(gr[2 * D.d + i]);
-    gr[2 * D.d + i] = h;
     const float s = vw.mem[x];
     float out = s;
     if (vw.mail_ev[u] >= 0) {
-      const float z = gr[i];
-      out = (1.0f - z) * s + z * h;
+      const float az = gr[i];
+      out = sigmoidf_(-az) * s + sigmoidf_(az) * h;
       flag_if_nonfinite(out, flag);
     }
     s_hat[x] = out;
@@ -514,6 +511,183 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, float* Q, const float* __restr
         bf_put(bf.H, r, i, hv[c]);
         put_hin(r, i, hv[c]);
         flag_if_nonfinite(hv[c], flag);
+      }
+    }
+  }
+  if (hin) bf_zero_tail(bf.Hin, 2 * B, cap_B2, 2 * da + 1);
+}
+
+// attention_forward, the wide-row form (d_a % 4 == 0, d_a <= 128, n <= 32):
+// one warp per root, each HALF-warp one neighbour (float4 loads, 16-lane dot
+// products), K and V rows of four neighbour pairs fetched together per round,
+// the softmax kept online across rounds (running max / denominator, the
+// partial h rescaled), the two halves' h and denominators combined at the end.
+// Against attn_fwd_kernel: a quarter of the load instructions, half the
+// shuffles per score and one memory round per eight neighbours instead of two.
+constexpr int kPairGroup = 4;
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 scale4(float4 a, float s) { return make_float4(a.x * s, a.y * s, a.z * s, a.w * s); }
+__device__ __forceinline__ float4 fma4(float s, float4 a, float4 c) {
+  return make_float4(fmaf(s, a.x, c.x), fmaf(s, a.y, c.y), fmaf(s, a.z, c.z), fmaf(s, a.w, c.w));
+}
+__device__ __forceinline__ float dot4(float4 a, float4 b) {
+  return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
+}
+__device__ __forceinline__ float half_sum(float v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float4 xor16_4(float4 a) {
+  return make_float4(__shfl_xor_sync(0xffffffffu, a.x, 16), __shfl_xor_sync(0xffffffffu, a.y, 16),
+                     __shfl_xor_sync(0xffffffffu, a.z, 16), __shfl_xor_sync(0xffffffffu, a.w, 16));
+}
+// four consecutive elements of a pre-split operand (c % 4 == 0, ld % 4 == 0)
+__device__ __forceinline__ void bf_put4(const BfMat& m, int64_t r, int64_t c, float4 v) {
+  if (m.hi == nullptr) return;
+  const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+  const float2 b0 = __bfloat1622float2(h0), b1 = __bfloat1622float2(h1);
+  const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - b0.x, v.y - b0.y), l1 = __floats2bfloat162_rn(v.z - b1.x, v.w - b1.y);
+  uint2 hh, ll;
+  hh.x = *reinterpret_cast<const uint32_t*>(&h0);
+  hh.y = *reinterpret_cast<const uint32_t*>(&h1);
+  ll.x = *reinterpret_cast<const uint32_t*>(&l0);
+  ll.y = *reinterpret_cast<const uint32_t*>(&l1);
+  *reinterpret_cast<uint2*>(m.hi + r * m.ld + c) = hh;
+  *reinterpret_cast<uint2*>(m.lo + r * m.ld + c) = ll;
+}
+
+inline bool attn_wide_ok(int da, int n) { return da % 4 == 0 && da <= 128 && n <= 32; }
+
+__global__ void attn_fwd_wide_kernel(Dims D, DPlan pl, float* Q, const float* __restrict__ KV,
+                                     float* __restrict__ attn_a, float* __restrict__ H, int* flag, StepBf bf,
+                                     const float* __restrict__ QKVn, const float* __restrict__ cq, int cap_B2) {
+  pdl_wait();
+  pdl_trigger();
+  const int R = pl.sizes[kSzR];
+  const int B = pl.sizes[kSzB];
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const int da = D.da, nq = da / 4;
+  const int c0 = 4 * hl, c1 = 4 * (hl + 16);  // this lane's two float4 columns
+  const bool ok0 = hl < nq, ok1 = hl + 16 < nq;
+  const bool hin = pl.rpe == 3 && bf.Hin.hi != nullptr;
+  const int ldn = 3 * bf.d8a;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t r = gwarp(); r < R; r += nwarp()) {
+    const int n = pl.nbr_cnt[r];
+    const int p0 = pl.pair_ptr[r];
+    float4 q0 = z4, q1 = z4;
+    if (QKVn) {
+      const float* qn = QKVn + static_cast<int64_t>(pl.root_sup[r]) * ldn;
+      if (ok0) q0 = add4(ld4(qn + c0), ld4(cq + c0));
+      if (ok1) q1 = add4(ld4(qn + c1), ld4(cq + c1));
+      if (half == 0) {
+        if (ok0) *reinterpret_cast<float4*>(Q + r * da + c0) = q0;
+        if (ok1) *reinterpret_cast<float4*>(Q + r * da + c1) = q1;
+      }
+    } else {
+      if (ok0) q0 = ld4(Q + r * da + c0);
+      if (ok1) q1 = ld4(Q + r * da + c1);
+    }
+    const int my_sup = (QKVn && lane < n) ? pl.pair_sup[p0 + lane] : 0;
+    const float scale = n > 0 ? 1.0f / sqrtf(static_cast<float>(n)) : 0.0f;
+    float M = -INFINITY, den = 0.0f, my_score = -INFINITY;
+    float4 h0 = z4, h1 = z4;
+    for (int mb = 0; mb < n; mb += 2 * kPairGroup) {
+      float4 k[kPairGroup][2], v[kPairGroup][2];
+#pragma unroll
+      for (int g = 0; g < kPairGroup; ++g) {
+        const int m = mb + 2 * g + half;
+        const int su = __shfl_sync(0xffffffffu, my_sup, m & 31);
+        const bool ok = m < n;
+        const float* row = KV + static_cast<int64_t>(p0 + m) * 2 * da;
+        const float* nrow = QKVn ? QKVn + static_cast<int64_t>(su) * ldn : nullptr;
+        k[g][0] = k[g][1] = v[g][0] = v[g][1] = z4;
+        if (ok && ok0) {
+          k[g][0] = ld4(row + c0);
+          v[g][0] = ld4(row + da + c0);
+          if (nrow) {
+            k[g][0] = add4(k[g][0], ld4(nrow + bf.d8a + c0));
+            v[g][0] = add4(v[g][0], ld4(nrow + 2 * bf.d8a + c0));
+          }
+        }
+        if (ok && ok1) {
+          k[g][1] = ld4(row + c1);
+          v[g][1] = ld4(row + da + c1);
+          if (nrow) {
+            k[g][1] = add4(k[g][1], ld4(nrow + bf.d8a + c1));
+            v[g][1] = add4(v[g][1], ld4(nrow + 2 * bf.d8a + c1));
+          }
+        }
+      }
+      float sc[kPairGroup];
+      float rm = -INFINITY;
+#pragma unroll
+      for (int g = 0; g < kPairGroup; ++g) {
+        const float t = half_sum(dot4(q0, k[g][0]) + dot4(q1, k[g][1])) * scale;
+        sc[g] = mb + 2 * g + half < n ? t : -INFINITY;
+        rm = fmaxf(rm, sc[g]);
+        const float x0 = __shfl_sync(0xffffffffu, sc[g], 0), x1 = __shfl_sync(0xffffffffu, sc[g], 16);
+        if (lane == mb + 2 * g) my_score = x0;
+        if (lane == mb + 2 * g + 1) my_score = x1;
+      }
+      rm = fmaxf(rm, __shfl_xor_sync(0xffffffffu, rm, 16));
+      const float Mn = fmaxf(M, rm);
+      const float corr = expf(M - Mn);  // 0 on the first round (M = -inf, h = den = 0)
+      h0 = scale4(h0, corr);
+      h1 = scale4(h1, corr);
+      den *= corr;
+#pragma unroll
+      for (int g = 0; g < kPairGroup; ++g) {
+        const float w = sc[g] > -INFINITY ? expf(sc[g] - Mn) : 0.0f;
+        den += w;
+        h0 = fma4(w, v[g][0], h0);
+        h1 = fma4(w, v[g][1], h1);
+      }
+      M = Mn;
+    }
+    den += __shfl_xor_sync(0xffffffffu, den, 16);
+    h0 = add4(h0, xor16_4(h0));
+    h1 = add4(h1, xor16_4(h1));
+    const float inv = n > 0 ? 1.0f / den : 0.0f;
+    h0 = scale4(h0, inv);
+    h1 = scale4(h1, inv);
+    if (lane < n) attn_a[p0 + lane] = expf(my_score - M) * inv;
+    // stores: half 0 the fp32 / pre-split h rows, half 1 the decoder input rows
+    if (half == 0) {
+      if (ok0) {
+        *reinterpret_cast<float4*>(H + r * da + c0) = h0;
+        bf_put4(bf.H, r, c0, h0);
+      }
+      if (ok1) {
+        *reinterpret_cast<float4*>(H + r * da + c1) = h1;
+        bf_put4(bf.H, r, c1, h1);
+      }
+      if ((ok0 && !(isfinite(h0.x) && isfinite(h0.y) && isfinite(h0.z) && isfinite(h0.w))) ||
+          (ok1 && !(isfinite(h1.x) && isfinite(h1.y) && isfinite(h1.z) && isfinite(h1.w))))
+        atomicExch(flag, 1);
+    } else if (hin) {
+      const int64_t e = r / 3;
+      const int side = static_cast<int>(r % 3);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const bool okx = x == 0 ? ok0 : ok1;
+        if (!okx) continue;
+        const int c = x == 0 ? c0 : c1;
+        const float4 hv = x == 0 ? h0 : h1;
+        if (side == 0) {
+          bf_put4(bf.Hin, e, c, hv);
+          bf_put4(bf.Hin, B + e, c, hv);
+        } else {
+          bf_put4(bf.Hin, side == 1 ? e : B + e, da + c, hv);
+        }
+      }
+      if (side == 0 && hl == 0) {
+        bf_put(bf.Hin, e, 2 * da, 1.0f);
+        bf_put(bf.Hin, B + e, 2 * da, 1.0f);
       }
     }
   }
@@ -777,6 +951,151 @@ __global__ void attn_bwd_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
   bf_zero_tail(bf.dKV, pl.sizes[kSzP], cap_P, bf.d8a + da);
 }
 
+// attention_backward, the wide-row form (see attn_fwd_wide_kernel): a
+// half-warp per neighbour; pass 1 fetches K and V rows four pairs per round,
+// reduces da_m = dh.V_m and parks the K rows in shared memory (nnb x d_a
+// floats per warp); pass 2 forms g_m = a_m (da_m - sum a da) / sqrt(n), dq =
+// sum g_m K_m from the parked rows, and writes dK = g_m q, dV = a_m dh.
+__global__ void attn_bwd_wide_kernel(Dims D, DPlan pl, const float* __restrict__ dIn,
+                                     const float* __restrict__ Q, const float* __restrict__ KV,
+                                     const float* __restrict__ attn_a, float* __restrict__ dQ,
+                                     float* __restrict__ dKV, StepBf bf, int cap_R, int cap_P,
+                                     const float* __restrict__ QKVn, int nnb) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float4 ks_all[];
+  const int R = pl.sizes[kSzR];
+  const int B = pl.sizes[kSzB];
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const int da = D.da, nq = da / 4;
+  const int c0 = 4 * hl, c1 = 4 * (hl + 16);
+  const bool ok0 = hl < nq, ok1 = hl + 16 < nq;
+  const int ldn = 3 * bf.d8a;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float* ks = reinterpret_cast<float*>(ks_all) + static_cast<int64_t>(threadIdx.x >> 5) * nnb * da;
+  for (int64_t r = gwarp(); r < R; r += nwarp()) {
+    const int64_t e = r / 3;
+    const int side = static_cast<int>(r % 3);
+    float4 dh0 = z4, dh1 = z4;
+    {
+      const float* a0 = side == 0 ? dIn + e * 2 * da : side == 1 ? dIn + e * 2 * da + da : dIn + (B + e) * 2 * da + da;
+      if (ok0) dh0 = ld4(a0 + c0);
+      if (ok1) dh1 = ld4(a0 + c1);
+      if (side == 0) {  // the source root gets both pairs' halves
+        const float* a1 = dIn + (B + e) * 2 * da;
+        if (ok0) dh0 = add4(dh0, ld4(a1 + c0));
+        if (ok1) dh1 = add4(dh1, ld4(a1 + c1));
+      }
+    }
+    const int n = pl.nbr_cnt[r];
+    if (n == 0) {
+      if (half == 0) {
+        if (ok0) {
+          *reinterpret_cast<float4*>(dQ + r * da + c0) = z4;
+          bf_put4(bf.dQ, r, c0, z4);
+        }
+        if (ok1) {
+          *reinterpret_cast<float4*>(dQ + r * da + c1) = z4;
+          bf_put4(bf.dQ, r, c1, z4);
+        }
+      }
+      continue;
+    }
+    const int p0 = pl.pair_ptr[r];
+    const int my_sup = (QKVn && lane < n) ? pl.pair_sup[p0 + lane] : 0;
+    const float scale = 1.0f / sqrtf(static_cast<float>(n));
+    const float a_l = lane < n ? attn_a[p0 + lane] : 0.0f;
+    float4 q0 = z4, q1 = z4;
+    if (ok0) q0 = ld4(Q + r * da + c0);
+    if (ok1) q1 = ld4(Q + r * da + c1);
+    float da_l = 0.0f;
+    for (int mb = 0; mb < n; mb += 2 * kPairGroup) {
+      float4 k[kPairGroup][2], v[kPairGroup][2];
+#pragma unroll
+      for (int g = 0; g < kPairGroup; ++g) {
+        const int m = mb + 2 * g + half;
+        const int su = __shfl_sync(0xffffffffu, my_sup, m & 31);
+        const bool ok = m < n;
+        const float* row = KV + static_cast<int64_t>(p0 + m) * 2 * da;
+        const float* nrow = QKVn ? QKVn + static_cast<int64_t>(su) * ldn : nullptr;
+        k[g][0] = k[g][1] = v[g][0] = v[g][1] = z4;
+        if (ok && ok0) {
+          k[g][0] = ld4(row + c0);
+          v[g][0] = ld4(row + da + c0);
+          if (nrow) {
+            k[g][0] = add4(k[g][0], ld4(nrow + bf.d8a + c0));
+            v[g][0] = add4(v[g][0], ld4(nrow + 2 * bf.d8a + c0));
+          }
+        }
+        if (ok && ok1) {
+          k[g][1] = ld4(row + c1);
+          v[g][1] = ld4(row + da + c1);
+          if (nrow) {
+            k[g][1] = add4(k[g][1], ld4(nrow + bf.d8a + c1));
+            v[g][1] = add4(v[g][1], ld4(nrow + 2 * bf.d8a + c1));
+          }
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kPairGroup; ++g) {
+        const int m = mb + 2 * g + half;
+        if (m < n) {
+          if (ok0) *reinterpret_cast<float4*>(ks + m * da + c0) = k[g][0];
+          if (ok1) *reinterpret_cast<float4*>(ks + m * da + c1) = k[g][1];
+        }
+        const float t = half_sum(dot4(dh0, v[g][0]) + dot4(dh1, v[g][1]));
+        const float x0 = __shfl_sync(0xffffffffu, t, 0), x1 = __shfl_sync(0xffffffffu, t, 16);
+        if (lane == mb + 2 * g) da_l = x0;
+        if (lane == mb + 2 * g + 1) da_l = x1;
+      }
+    }
+    __syncwarp();
+    const float mixed = warp_sum(a_l * da_l);
+    const float g_l = a_l * (da_l - mixed) * scale;
+    float4 dq0 = z4, dq1 = z4;
+    for (int mp = 0; mp < n; mp += 2) {
+      const int m = mp + half;
+      const float gm = __shfl_sync(0xffffffffu, g_l, m & 31);
+      const float am = __shfl_sync(0xffffffffu, a_l, m & 31);
+      if (m >= n) continue;
+      const int64_t p = p0 + m;
+      float* out = dKV + p * 2 * da;
+      if (ok0) {
+        dq0 = fma4(gm, *reinterpret_cast<const float4*>(ks + m * da + c0), dq0);
+        const float4 dk = scale4(q0, gm), dv = scale4(dh0, am);
+        *reinterpret_cast<float4*>(out + c0) = dk;
+        *reinterpret_cast<float4*>(out + da + c0) = dv;
+        bf_put4(bf.dKV, p, c0, dk);
+        bf_put4(bf.dKV, p, bf.d8a + c0, dv);
+      }
+      if (ok1) {
+        dq1 = fma4(gm, *reinterpret_cast<const float4*>(ks + m * da + c1), dq1);
+        const float4 dk = scale4(q1, gm), dv = scale4(dh1, am);
+        *reinterpret_cast<float4*>(out + c1) = dk;
+        *reinterpret_cast<float4*>(out + da + c1) = dv;
+        bf_put4(bf.dKV, p, c1, dk);
+        bf_put4(bf.dKV, p, bf.d8a + c1, dv);
+      }
+    }
+    dq0 = add4(dq0, xor16_4(dq0));
+    dq1 = add4(dq1, xor16_4(dq1));
+    if (half == 0) {
+      if (ok0) {
+        *reinterpret_cast<float4*>(dQ + r * da + c0) = dq0;
+        bf_put4(bf.dQ, r, c0, dq0);
+      }
+      if (ok1) {
+        *reinterpret_cast<float4*>(dQ + r * da + c1) = dq1;
+        bf_put4(bf.dQ, r, c1, dq1);
+      }
+    }
+    __syncwarp();  // the parked rows are reused by the warp's next root
+  }
+  bf_zero_tail(bf.dQ, R, cap_R, da);
+  bf_zero_tail(bf.dKV, pl.sizes[kSzP], cap_P, bf.d8a + da);
+}
+
 // Routing pass 1: fixed chunks of kChunk sorted items; runs fully inside a
 // chunk are written directly, runs that cross a chunk edge leave partials.
 // Row layout of dNodeAcc: {sum dq | sum dK | sum dV} (3 d_attn). One warp per
@@ -922,9 +1241,9 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
     const bool has = vw.mail_ev[u] >= 0;
     const float* gr = Gates + u * 3 * D.d;
     const float ds = dNode[u * nd + i];
-    const float z = gr[i], h = gr[2 * D.d + i], s = vw.mem[x];
-    const float az = has ? ds * (h - s) * z * (1.0f - z) : 0.0f;
-    const float ah = has ? ds * z * (1.0f - h * h) : 0.0f;
+    const float pz = gr[i], ph = gr[2 * D.d + i], s = vw.mem[x];
+    const float az = has ? ds * (tanhf(ph) - s) * dsigmoidf_(pz) : 0.0f;
+    const float ah = has ? ds * sigmoidf_(pz) * dtanhf_(ph) : 0.0f;
     if (Dg) {
       float* dg = Dg + u * 3 * D.d;
       dg[i] = az;
@@ -967,8 +1286,7 @@ __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restr
   for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int64_t u = x / D.d, i = x % D.d;
     const bool has = vw.mail_ev[u] >= 0;
-    const float r = Gates[u * 3 * D.d + D.d + i];
-    const float ar = has ? T1[x] * vw.mem[x] * r * (1.0f - r) : 0.0f;
+    const float ar = has ? T1[x] * vw.mem[x] * dsigmoidf_(Gates[u * 3 * D.d + D.d + i]) : 0.0f;
     if (Dg) Dg[u * 3 * D.d + D.d + i] = ar;
     bf_put(bf.Dg, u, bf.d8d + i, ar);
   }
@@ -1803,13 +2121,13 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
         D, pl, vw, g, P + L.off[tOmega], tma ? nullptr : w.Xg, w.ldx, w.GU, bfx, U, stage);
   }
   // one fused tcgen05 kernel for GEMM -> sigmoid -> GEMM -> tanh / blend
-  // (gru_fused.cu), opt-in with TGNN_GRU_FUSED=1. A/B on B200 at C2: the
-  // GRU phase of the critical path drops from 57 to 40 us, but the step does
-  // not (259.7 vs 261.8 us): the kernel holds 96 SMs exclusively (224 KB of
-  // shared memory each), so the per-pair edge projection running beside it
-  // on the edge stream becomes the critical path (attn_assemble 0.8 -> 12 us).
-  static const int fused_knob = env_knob("TGNN_GRU_FUSED", 0, 0, 1);
-  if (tma && fused_knob && gru_fused_supported(d)) {
+  // (gru_fused.cu; TGNN_GRU_FUSED=0 runs the five-launch chain). It holds 96
+  // SMs exclusively (224 KB of shared memory each), so the per-pair edge
+  // projection GEMM is not run beside it on the edge stream but joins the
+  // node projection's launch (edge_join_enabled). A/B on B200 at C2 (r02):
+  // unfused 262.2 us / barrier, fused 261.8 (edge GEMM beside it: it becomes
+  // the critical path), fused + joined 257.8.
+  if (tma && gru_fused_enabled(d)) {
     GruFusedParams fp;
     fp.U_dev = szU;
     fp.cap_U = U;
@@ -1869,7 +2187,17 @@ void assemble_gru_view_launch(const StepCtx& c, const DPlan& pl, const DView& vw
   TGB_CUDA(cudaGetLastError());
 }
 
-void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
+bool gru_fused_enabled(int64_t d) {
+  static const int fused = env_knob("TGNN_GRU_FUSED", 1, 0, 1);
+  return gemm_impl() == kGemmTma && fused == 1 && gru_fused_supported(d);
+}
+
+bool edge_join_enabled(int64_t d) {
+  static const int v = env_knob("TGNN_EDGE_JOIN", -1, -1, 1);
+  return gemm_impl() == kGemmTma && (v < 0 ? gru_fused_enabled(d) : v == 1);
+}
+
+void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s, bool gemm) {
   const ModelDims& m = c.m;
   const ParamLayout& L = c.L;
   StepWork& w = *c.w;
@@ -1882,6 +2210,7 @@ void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   launch_pdl(assemble_edge_kernel, dim3(row_blocks(Pc)), dim3(32 * kWarps), sizeof(float) * stage * kWarps, s, D,
              pl, g, P + L.off[tOmega], w.bf, Pc, stage);
   launch_pdl(query_const_kernel, dim3(row_blocks(D.da)), dim3(32 * kWarps), 0, s, D, P + L.off[tWq], P + L.off[tBq], w.cq);
+  if (!gemm) return;  // the GEMM joins the node projection's launch
   c.mark(phAttnProj, s);
   TcGroup tg;
   g_wide = 1;  // per-pair K and V edge parts in one pass: [Wk_e Wk_t bk ; Wv_e Wv_t bv]
@@ -1921,6 +2250,11 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
     TcGroup tg;
     tc_nn(tg, U, pl.sizes + kSzU, 3 * w.bf.d8a, D.d + D.ds, w.bf.NF, 0, w.bf.Wst, 0, 3 * w.bf.d8a, w.QKVn,
           3 * w.bf.d8a);
+    if (c.edge_gemm_joined) {  // the per-pair edge parts in the same launch
+      g_wide = 1;
+      tc_nn(tg, Pc, szP, 2 * da, D.de + D.dt + 1, w.bf.EF, 0, w.bf.Wkve, 0, 2 * da, w.KV, 2 * da);
+      g_wide = 0;
+    }
     tc_group_launch(tg, s);
   } else {
     const int stage = (std::max(D.kv_in, D.q_in) + 1 + D.dt + 7) / 8 * 8;
@@ -1940,8 +2274,10 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   c.mark(phAttnSoftmax, s);
   {
     const int lanes = (da + 31) / 32;
+    static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
     auto fwd = lanes <= 1 ? attn_fwd_kernel<1> : lanes <= 2 ? attn_fwd_kernel<2>
              : lanes <= 4 ? attn_fwd_kernel<4> : attn_fwd_kernel<8>;
+    if (wide_knob && attn_wide_ok(da, static_cast<int>(m.n_neighbors))) fwd = attn_fwd_wide_kernel;
     launch_pdl(fwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag,
                bfx, tma ? w.QKVn : nullptr, w.cq, 2 * w.cap_B);
   }
@@ -2031,10 +2367,21 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   c.mark(phAttnBwd, s);
   {
     const int lanes = (da + 31) / 32;
-    auto bwd = lanes <= 1 ? attn_bwd_kernel<1> : lanes <= 2 ? attn_bwd_kernel<2>
-             : lanes <= 4 ? attn_bwd_kernel<4> : attn_bwd_kernel<8>;
-    launch_pdl(bwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV, bfx, R, Pc,
-               tma ? w.QKVn : nullptr);
+    static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
+    const int nnb = static_cast<int>(m.n_neighbors);
+    if (wide_knob && attn_wide_ok(da, nnb)) {
+      const size_t smem = sizeof(float) * static_cast<size_t>(kWarps) * nnb * da;  // parked K rows
+      if (smem > 48 * 1024)
+        TGB_CUDA(cudaFuncSetAttribute(attn_bwd_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      launch_pdl(attn_bwd_wide_kernel, dim3(row_blocks(R)), dim3(32 * kWarps), smem, s, D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ,
+                 w.dKV, bfx, R, Pc, tma ? w.QKVn : nullptr, nnb);
+    } else {
+      auto bwd = lanes <= 1 ? attn_bwd_kernel<1> : lanes <= 2 ? attn_bwd_kernel<2>
+               : lanes <= 4 ? attn_bwd_kernel<4> : attn_bwd_kernel<8>;
+      launch_pdl(bwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.dIn, w.Q, w.KV, w.attn_a, w.dQ, w.dKV,
+                 bfx, R, Pc, tma ? w.QKVn : nullptr);
+    }
   }
   if (c.ev_mid && c.mid_at == 2) TGB_CUDA(cudaEventRecord(c.ev_mid, s));
   if (pl.ev_sorted) TGB_CUDA(cudaStreamWaitEvent(s, pl.ev_sorted, 0));  // routing CSR ready
@@ -2103,7 +2450,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   // ---- GRU backward (K9)
   c.mark(phGruBwd, s);
   launch_pdl(gru_bwd1_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.dNode, w.Gates, tma ? nullptr : w.Dg,
-                                          G + L.off[tStatic], bfx, U, nullptr, nullptr);
+               G + L.off[tStatic], bfx, U, nullptr, nullptr);
   if (tma) {
     // node / edge split: dW_q[:, time] = sum_r dq_r = db_q (cos(0 w) = 1), after
     // db_q's split-K reduction (on the branch when there is one)

@@ -146,6 +146,9 @@ struct StepCtx {
   // attention, decoder) was deferred; wait for it before the first reader on
   // the main stream (gru_out's static columns of NF)
   cudaEvent_t ev_params_tail = nullptr;
+  // the per-pair edge projection GEMM joins the node projection's launch (the
+  // edge branch only assembles the operands): see attn_edge_launch
+  bool edge_gemm_joined = false;
   void mark(int slot, cudaStream_t s) const {
     if (marks) marks->mark(slot, s);
   }
@@ -176,7 +179,13 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s);
 // TMA engine: the plan-only half of it -- edge operands EF / Gt, the query
 // constant and the per-pair edge projection KE = EF Wkve^T (into w.KV).
-void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s);
+void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s, bool gemm = true);
+// The fused GRU freshen kernel serves this memory width (TGNN_GRU_FUSED, default on).
+bool gru_fused_enabled(int64_t d);
+// The edge-join schedule (TGNN_EDGE_JOIN, default: with the fused GRU): the
+// per-pair edge GEMM is launched together with the node projection instead of
+// on the edge branch.
+bool edge_join_enabled(int64_t d);
 // decode_link of (src, dst) and (src, candidate) per event of an evaluation
 // plan (rpe = 2 + n_neg); cnt_out[e - base] = #candidates with logit >= truth.
 void eval_rank_launch(const StepCtx& c, const DPlan& pl, int32_t* cnt_out, int64_t base, cudaStream_t s);

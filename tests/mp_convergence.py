@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def rank_body(a, rank, world, device, join):
+def rank_body(a, rank, world, device, join, seed):
     import paper_2307_07649_b200 as T
     ctx = T.Context(device)
     g = T.TemporalGraph.synthetic(ctx, T.SynthParams(nodes=300, events=5000, pref_prob=0.95, prefs_per_src=1,
@@ -21,7 +21,7 @@ def rank_body(a, rank, world, device, join):
     _, _, t = g.events()
     mc = T.ModelConfig(d_mem=24, d_time=8, d_static=8, d_attn=24, d_hidden=24, d_e=0, n_neighbors=8,
                        num_nodes=300, max_t=float(t[-1]))
-    tc = T.TrainConfig(i=a.i, j=a.j, k=a.k, local_batch=175, lr_base=2e-3, epochs=a.epochs, seed=5)
+    tc = T.TrainConfig(i=a.i, j=a.j, k=a.k, local_batch=175, lr_base=2e-3, epochs=a.epochs, seed=seed)
     run = T.Run(ctx, g, mc, tc, 0, 3500, rank=rank, nranks=world)
     join(run)
     run.step(run.barriers)
@@ -35,6 +35,12 @@ def rank_body(a, rank, world, device, join):
     return out
 
 
+def save(path, seeds, outs):
+    np.savez(path, seeds=np.array(seeds), mrr=np.array([o["mrr"] for o in outs]),
+             queries=np.array([o["queries"] for o in outs]), traversed=np.array([o["traversed"] for o in outs]),
+             params=outs[0]["params"])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--i", type=int, default=1)
@@ -42,15 +48,17 @@ def main():
     ap.add_argument("--k", type=int, default=1)
     ap.add_argument("--epochs", type=int, default=150)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--seeds", default="5", help="comma-separated training seeds (the reference's is 5)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "local"])
     a = ap.parse_args()
     import paper_2307_07649_b200 as T
 
     world = a.i * a.j * a.k
+    seeds = [int(x) for x in a.seeds.split(",")]
     if a.backend == "local":
-        res = T.run_ranks(lambda r, hub: rank_body(a, r, world, 0, lambda run: run.local_init(hub)), world)
-        r0 = res[0]
-        np.savez(a.out, mrr=r0["mrr"], queries=r0["queries"], traversed=r0["traversed"], params=r0["params"])
+        outs = [T.run_ranks(lambda r, hub: rank_body(a, r, world, 0, lambda run: run.local_init(hub), sd), world)[0]
+                for sd in seeds]
+        save(a.out, seeds, outs)
         return
     import torch
     import torch.distributed as dist
@@ -66,9 +74,9 @@ def main():
         dist.broadcast(uid, 0)
         run.comm_init(bytes(uid.cpu().numpy().tobytes()))
 
-    r0 = rank_body(a, rank, world, lr_, join)
+    outs = [rank_body(a, rank, world, lr_, join, sd) for sd in seeds]
     if rank == 0:
-        np.savez(a.out, mrr=r0["mrr"], queries=r0["queries"], traversed=r0["traversed"], params=r0["params"])
+        save(a.out, seeds, outs)
     dist.barrier()
     dist.destroy_process_group()
 

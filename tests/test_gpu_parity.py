@@ -245,3 +245,22 @@ def test_run_sequential_parity(env, case, engine):
     lr = T.lr_eff(tc)
     assert np.abs(res.params - r["params"]).max() <= 2.5 * lr * res.barriers
     assert np.median(np.abs(res.params - r["params"])) <= 1e-5
+
+
+def test_unfused_gru_freshen_variant():
+    """The default TMA path runs the GRU freshen as one fused tcgen05 kernel
+    (gru_fused.cu) with the edge projection joined to the node projection; the
+    five-launch chain (TGNN_GRU_FUSED=0) and the edge GEMM on its own branch are
+    still shipped knobs: the sub-step and run_sequential parity tests above
+    rerun under them in a fresh process (the knobs are read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TGNN_GRU_FUSED="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "(test_sub_step_parity or test_run_sequential_parity) and tma"],
+                       capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
