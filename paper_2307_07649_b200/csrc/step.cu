@@ -213,10 +213,9 @@ __global__ void assemble_gru_time_kernel(Dims D, DPlan pl, DView vw, const float
   pdl_wait();
   pdl_trigger();
   const int U = pl.sizes[kSzU];
-  const int64_t total = static_cast<int64_t>(U) * D.dt;
-  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t u = x / D.dt;
-    const int i = static_cast<int>(x % D.dt);
+  const int total = U * D.dt;  // 32-bit index arithmetic (U x dt < 2^31 here)
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int u = x / D.dt, i = x - u * D.dt;
     const double dt = vw.mail_dt[u];
     float sn, cs;
     time_sincos(dt, omega[i], &sn, &cs);
@@ -770,6 +769,55 @@ __global__ void decoder_kernel(Dims D, DPlan pl, const float* __restrict__ H,
   bf_zero_tail(bf.Dhid, 2 * B, cap_B2, dh);
 }
 
+// decoder_kernel, the wide form (d_hidden % 4 == 0, <= 128; the pre-split
+// engine: no fp32 Dhid / Hin copies): half 0 of the warp decodes the
+// positive pair, half 1 the negative one, float4 per lane.
+__global__ void decoder_wide_kernel(Dims D, DPlan pl, const float* __restrict__ AB, const float* __restrict__ b1,
+                                    const float* __restrict__ W2, const float* __restrict__ b2,
+                                    float* __restrict__ HID, float* __restrict__ dlogit,
+                                    float* __restrict__ logits, double* __restrict__ loss_terms, int* flag,
+                                    StepBf bf, int cap_B2) {
+  pdl_wait();
+  pdl_trigger();
+  const int B = pl.sizes[kSzB];
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const int dh = D.dh, nq = dh / 4;
+  const int c0 = 4 * hl, c1 = 4 * (hl + 16);
+  const bool ok0 = hl < nq, ok1 = hl + 16 < nq;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 bb0 = ok0 ? ld4(b1 + c0) : z4, bb1 = ok1 ? ld4(b1 + c1) : z4;
+  const float4 w0 = ok0 ? ld4(W2 + c0) : z4, w1 = ok1 ? ld4(W2 + c1) : z4;
+  const double invB = 1.0 / static_cast<double>(B);
+  auto relu4 = [](float4 a) { return make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f)); };
+  auto grad4 = [](float4 h, float4 w, float dl) {
+    return make_float4(h.x > 0.f ? dl * w.x : 0.f, h.y > 0.f ? dl * w.y : 0.f, h.z > 0.f ? dl * w.z : 0.f,
+                       h.w > 0.f ? dl * w.w : 0.f);
+  };
+  for (int64_t e = gwarp(); e < B; e += nwarp()) {
+    const float* As = AB + (3 * e) * 2 * dh;
+    const float* Bx = AB + (3 * e + 1 + half) * 2 * dh + dh;  // destination (pos) / negative
+    const int64_t row = half == 0 ? e : B + e;
+    float4 h0 = z4, h1 = z4;
+    if (ok0) h0 = relu4(add4(add4(ld4(As + c0), ld4(Bx + c0)), bb0));
+    if (ok1) h1 = relu4(add4(add4(ld4(As + c1), ld4(Bx + c1)), bb1));
+    if (ok0) *reinterpret_cast<float4*>(HID + row * dh + c0) = h0;
+    if (ok1) *reinterpret_cast<float4*>(HID + row * dh + c1) = h1;
+    const float logit = half_sum(dot4(w0, h0) + dot4(w1, h1)) + b2[0];
+    const float dl = half == 0 ? static_cast<float>(-(1.0 / (1.0 + exp(static_cast<double>(logit)))) * invB)
+                               : static_cast<float>((1.0 / (1.0 + exp(-static_cast<double>(logit)))) * invB);
+    if (ok0) bf_put4(bf.Dhid, row, c0, grad4(h0, w0, dl));
+    if (ok1) bf_put4(bf.Dhid, row, c1, grad4(h1, w1, dl));
+    if (hl == 0) {
+      dlogit[row] = dl;
+      logits[row] = logit;
+      loss_terms[2 * e + half] = softplus_d(half == 0 ? -static_cast<double>(logit) : static_cast<double>(logit));
+      flag_if_nonfinite(logit, flag);
+    }
+  }
+  bf_zero_tail(bf.Dhid, 2 * B, cap_B2, dh);
+}
+
 // bce_loss: mean softplus(-pos) + mean softplus(neg), fixed-order f64 reduction.
 __global__ void __launch_bounds__(1024) loss_kernel(DPlan pl, const double* __restrict__ terms,
                                                     double* loss_base, const int* ctr, int* flag) {
@@ -1188,6 +1236,101 @@ __global__ void routing_chunk_kernel(Dims D, DPlan pl, const float* __restrict__
   }
 }
 
+// Routing pass 1, the wide-row form (d_a % 4 == 0, d_a <= 128): as
+// routing_chunk_kernel, but a half-warp per item row with float4 loads (eight
+// rows in flight per warp): half 0 accumulates the even items of a run, half
+// 1 the odd ones, and a run's two partial sums are combined where it ends.
+__global__ void routing_chunk_wide_kernel(Dims D, DPlan pl, const float* __restrict__ dQ,
+                                          const float* __restrict__ dKV, float* __restrict__ dNodeAcc,
+                                          float* __restrict__ part_first, float* __restrict__ part_last,
+                                          StepBf bf) {
+  pdl_wait();
+  pdl_trigger();
+  const int items = pl.sizes[kSzItems];
+  const int R = pl.sizes[kSzR];
+  const int nchunks = (items + kChunk - 1) / kChunk;
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const int da = D.da, w3 = 3 * D.da, nq = da / 4;
+  const int c0 = 4 * hl, c1 = 4 * (hl + 16);
+  const bool ok0 = hl < nq, ok1 = hl + 16 < nq;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int kPairs = 4;  // item pairs fetched per round
+  for (int64_t gw = gwarp(); gw < 3ll * nchunks; gw += nwarp()) {
+    const int64_t c = gw / 3;
+    const int part = static_cast<int>(gw % 3);
+    const int i0 = static_cast<int>(c) * kChunk;
+    const int i1 = min(items, i0 + kChunk);
+    const int n = i1 - i0;
+    const int it = i0 + lane;
+    const int my_key = it < i1 ? pl.item_key_s[it] : -1;
+    const int my_val = it < i1 ? pl.item_val_s[it] : -1;
+    const int nxt_key = it + 1 < items ? pl.item_key_s[it + 1] : -2;
+    const unsigned ends = __ballot_sync(0xffffffffu, it < i1 && (it + 1 == i1 || nxt_key != my_key));
+    const int prev_key = (lane == 0 && i0 > 0) ? pl.item_key_s[i0 - 1] : -3;
+    const bool cont_in = __shfl_sync(0xffffffffu, prev_key == my_key, 0) && i0 > 0;
+    const bool cont_out =
+        i1 < items && __shfl_sync(0xffffffffu, nxt_key == my_key ? 1 : 0, n - 1) != 0;
+    const bool mine = my_val >= 0 && (part == 0 ? my_val < R : my_val >= R);
+    const float* my_row = !mine ? nullptr
+                        : part == 0 ? dQ + static_cast<int64_t>(my_val) * da
+                                    : dKV + static_cast<int64_t>(my_val - R) * 2 * da + (part - 1) * da;
+    const unsigned have = __ballot_sync(0xffffffffu, mine);
+    float4 a0 = z4, a1 = z4;
+    bool at_start = true;
+    auto emit = [&](int x) {  // the run ending at item x: both halves' sums
+      const float4 t0 = add4(a0, xor16_4(a0)), t1 = add4(a1, xor16_4(a1));
+      const int key = __shfl_sync(0xffffffffu, my_key, x & 31);
+      const bool first = at_start && cont_in;
+      const bool last = (x + 1 == n) && cont_out;
+      const bool direct = !first && !last;
+      float* dst = first ? part_first + c * w3 : last ? part_last + c * w3
+                 : dNodeAcc ? dNodeAcc + static_cast<int64_t>(key) * w3 : nullptr;
+      if (half == 0) {
+        if (ok0) {
+          if (dst) *reinterpret_cast<float4*>(dst + part * da + c0) = t0;
+          if (direct) bf_put4(bf.dNA, key, part * bf.d8a + c0, t0);
+        }
+        if (ok1) {
+          if (dst) *reinterpret_cast<float4*>(dst + part * da + c1) = t1;
+          if (direct) bf_put4(bf.dNA, key, part * bf.d8a + c1, t1);
+        }
+      }
+      a0 = a1 = z4;
+      at_start = false;
+    };
+    for (int ib = 0; ib < n; ib += 2 * kPairs) {
+      float4 ld[kPairs][2];
+#pragma unroll
+      for (int a = 0; a < kPairs; ++a) {
+        const int x = ib + 2 * a + half;
+        const float* row = reinterpret_cast<const float*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_row), x & 31));
+        const bool ok = x < n && ((have >> (x & 31)) & 1u);
+        ld[a][0] = (ok && ok0) ? ld4(row + c0) : z4;
+        ld[a][1] = (ok && ok1) ? ld4(row + c1) : z4;
+      }
+#pragma unroll
+      for (int a = 0; a < kPairs; ++a) {
+        const int x0 = ib + 2 * a;
+        if (x0 >= n) break;
+        if (half == 0) {
+          a0 = add4(a0, ld[a][0]);
+          a1 = add4(a1, ld[a][1]);
+        }
+        if ((ends >> x0) & 1u) emit(x0);
+        if (x0 + 1 < n) {
+          if (half == 1) {
+            a0 = add4(a0, ld[a][0]);
+            a1 = add4(a1, ld[a][1]);
+          }
+          if ((ends >> (x0 + 1)) & 1u) emit(x0 + 1);
+        }
+      }
+    }
+  }
+}
+
 // Routing pass 2: a support whose item run spans chunks (a hub) sums its
 // partials in chunk order. One block per support, one thread per feature.
 __global__ void routing_fixup_kernel(Dims D, DPlan pl, float* __restrict__ dNodeAcc,
@@ -1235,17 +1378,18 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
       gWq[r * D.q_in + nd + j] = gBq[r];
     }
   }
-  const int64_t total = static_cast<int64_t>(U) * D.d;
-  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
-    const int64_t u = x / D.d, i = x % D.d;
+  // flat element loops with 32-bit index arithmetic (U x d < 2^31 here)
+  const int total = U * D.d;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int u = x / D.d, i = x - u * D.d;
     const bool has = vw.mail_ev[u] >= 0;
-    const float* gr = Gates + u * 3 * D.d;
-    const float ds = dNode[u * nd + i];
+    const float* gr = Gates + static_cast<int64_t>(u) * 3 * D.d;
+    const float ds = dNode[static_cast<int64_t>(u) * nd + i];
     const float pz = gr[i], ph = gr[2 * D.d + i], s = vw.mem[x];
     const float az = has ? ds * (tanhf(ph) - s) * dsigmoidf_(pz) : 0.0f;
     const float ah = has ? ds * sigmoidf_(pz) * dtanhf_(ph) : 0.0f;
     if (Dg) {
-      float* dg = Dg + u * 3 * D.d;
+      float* dg = Dg + static_cast<int64_t>(u) * 3 * D.d;
       dg[i] = az;
       dg[D.d + i] = 0.0f;
       dg[2 * D.d + i] = ah;
@@ -1253,14 +1397,14 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
     bf_put(bf.Dg, u, i, az);
     bf_put(bf.Dg, u, 2 * bf.d8d + i, ah);
   }
-  bf_zero_tail(bf.Dg, U, cap_U, 2 * bf.d8d + D.d);
   if (D.ds > 0) {
-    const int64_t tot2 = static_cast<int64_t>(U) * D.ds;
-    for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < tot2; x += gridDim.x * blockDim.x) {
-      const int64_t u = x / D.ds, j = x % D.ds;
-      g_static[static_cast<int64_t>(pl.supports[u]) * D.ds + j] = dNode[u * nd + D.d + j];
+    const int tot2 = U * D.ds;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < tot2; x += gridDim.x * blockDim.x) {
+      const int u = x / D.ds, j = x - u * D.ds;
+      g_static[static_cast<int64_t>(pl.supports[u]) * D.ds + j] = dNode[static_cast<int64_t>(u) * nd + D.d + j];
     }
   }
+  bf_zero_tail(bf.Dg, U, cap_U, 2 * bf.d8d + D.d);
 }
 
 // Node / edge split: the query's time block is the constant cos(0 w) = 1, so
@@ -1282,12 +1426,12 @@ __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restr
   pdl_wait();
   pdl_trigger();
   const int U = pl.sizes[kSzU];
-  const int64_t total = static_cast<int64_t>(U) * D.d;
-  for (int64_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
-    const int64_t u = x / D.d, i = x % D.d;
+  const int total = U * D.d;  // 32-bit index arithmetic (U x d < 2^31 here)
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int u = x / D.d, i = x - u * D.d;
     const bool has = vw.mail_ev[u] >= 0;
-    const float ar = has ? T1[x] * vw.mem[x] * dsigmoidf_(Gates[u * 3 * D.d + D.d + i]) : 0.0f;
-    if (Dg) Dg[u * 3 * D.d + D.d + i] = ar;
+    const float ar = has ? T1[x] * vw.mem[x] * dsigmoidf_(Gates[static_cast<int64_t>(u) * 3 * D.d + D.d + i]) : 0.0f;
+    if (Dg) Dg[static_cast<int64_t>(u) * 3 * D.d + D.d + i] = ar;
     bf_put(bf.Dg, u, bf.d8d + i, ar);
   }
 }
@@ -1822,6 +1966,9 @@ void step_alloc(StepWork& w, const ModelDims& m, int cap_B, int cap_U, int64_t n
   w.ldq = r4(m.q_in());
   w.ldkv = r4(m.kv_in());
   const int64_t U = cap_U, R = w.cap_R, P = w.cap_P, B2 = 2 * cap_B;
+  // the elementwise GRU kernels index U x width with 32-bit arithmetic
+  TGB_REQUIRE(U * std::max(std::max(d, dt), static_cast<int64_t>(m.d_static)) < (int64_t{1} << 31), kConfig,
+              "support capacity x memory width exceeds 2^31 elements");
   // backward-only buffers are skipped by forward-only (evaluation) workspaces
   const int64_t bU = fwd_only ? 0 : U, bR = fwd_only ? 0 : R, bP = fwd_only ? 0 : P;
   w.Xg = dalloc<float>(U * w.ldx);
@@ -2324,9 +2471,14 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
            2 * dh);
     gemm_group_launch(gg, s);
   }
-  launch_pdl(decoder_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s, 
-      D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, tma ? nullptr : w.Dhid,
-      tma ? nullptr : w.Hin, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
+  static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
+  if (tma && wide_knob && dh % 4 == 0 && dh <= 128)
+    launch_pdl(decoder_wide_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s, D, pl, w.AB, P + L.off[tB1],
+               P + L.off[tW2], P + L.off[tB2], w.HID, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
+  else
+    launch_pdl(decoder_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s,
+        D, pl, w.H, w.AB, P + L.off[tB1], P + L.off[tW2], P + L.off[tB2], w.HID, tma ? nullptr : w.Dhid,
+        tma ? nullptr : w.Hin, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
   if (c.ev_mid && c.mid_at == 1) TGB_CUDA(cudaEventRecord(c.ev_mid, s));
   WsCarver wc{w.splitk_ws, 0, w.splitk_ws_floats};
   c.mark(phDecoderBwd, s);
@@ -2390,8 +2542,10 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   float* part_last = wc.take(static_cast<size_t>(nchunks) * 3 * da);
   {
     const int lanes = (da + 31) / 32;
+    static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
     auto chunk = lanes <= 1 ? routing_chunk_kernel<1> : lanes <= 2 ? routing_chunk_kernel<2>
                : lanes <= 4 ? routing_chunk_kernel<4> : routing_chunk_kernel<8>;
+    if (wide_knob && da % 4 == 0 && da <= 128) chunk = routing_chunk_wide_kernel;
     launch_pdl(chunk, dim3(row_blocks(3 * nchunks)), dim3(32 * kWarps), 0, s, D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
                                                       part_first, part_last, bfx);
     const int fix_threads = std::min(1024, (3 * da + 31) / 32 * 32);
