@@ -44,6 +44,7 @@ struct TcParams {
   int stage_bytes;
   int tmem_cols;     // power of two >= max(32, max ntile)
   int stages;        // shared-memory ring depth (2..kStMax), as deep as the CTA budget allows
+  int sizes_early;   // runtime sizes final before launch: read them before griddepcontrol.wait
 };
 
 // Optional per-CTA timeline (debug benchmark only): 8 globaltimer stamps per CTA.
@@ -63,7 +64,8 @@ struct TileInfo {
   int pi, m0, n0, split, kbeg, nk, M;
 };
 
-__device__ __forceinline__ bool tile_info(const TcParams& gp, int t, TileInfo& ti) {
+// rt_m / rt_k: each problem's runtime M / K (shared memory, read once per CTA)
+__device__ __forceinline__ bool tile_info(const TcParams& gp, const int* rt_m, const int* rt_k, int t, TileInfo& ti) {
   int pi = 0;
   while (pi + 1 < gp.count && t >= gp.tile_base[pi + 1]) ++pi;
   const TcProblem& P = gp.p[pi];
@@ -74,10 +76,10 @@ __device__ __forceinline__ bool tile_info(const TcParams& gp, int t, TileInfo& t
   const int t2 = local % (tm * tn);
   ti.m0 = (t2 / tn) * kBM;
   ti.n0 = (t2 % tn) * P.ntile;
-  ti.M = P.M_dev ? min(P.M, *P.M_dev) : P.M;
+  ti.M = rt_m[pi];
   if (ti.m0 >= ti.M && P.splits == 1) return false;  // beyond the runtime rows: no work, no output
   const int Kcap = P.K;
-  const int K = P.K_dev ? min(Kcap, *P.K_dev) : Kcap;
+  const int K = rt_k[pi];
   // split-K partition of the RUNTIME reduction length (64-row chunks): the
   // splits stay balanced however loose the capacity is; still a fixed
   // function of the data, so the reduction order is deterministic.
@@ -101,8 +103,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint64_t* tempty = tfull + 2;    // [2] accumulator drained by the epilogue
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ __align__(1024) float epi_stage[kEpiWarps * 32 * 32];  // epilogue staging (128 B swizzle)
+  __shared__ int rt_m[kMaxTc], rt_k[kMaxTc];  // runtime M / K per problem
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = gp.tile_base[gp.count];
+  auto load_sizes = [&]() {
+    if (threadIdx.x < gp.count) {
+      const TcProblem& Q = gp.p[threadIdx.x];
+      rt_m[threadIdx.x] = Q.M_dev ? min(Q.M, *Q.M_dev) : Q.M;
+      rt_k[threadIdx.x] = Q.K_dev ? min(Q.K, *Q.K_dev) : Q.K;
+    }
+  };
+  // sizes produced well before this launch (the plan's counts) are read
+  // before griddepcontrol.wait: their load latency overlaps the predecessor
+  if (gp.sizes_early) load_sizes();
 
   // Prologue independent of the predecessor's output (it overlaps its tail
   // under programmatic dependent launch): descriptor prefetch, barriers, TMEM.
@@ -134,8 +147,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
   const int acc_cols = gp.tmem_cols / 2;
-  pdl_wait();  // operands and runtime sizes come from the predecessor
+  pdl_wait();  // operands (and, unless sizes_early, runtime sizes) come from the predecessor
   pdl_trigger();
+  if (!gp.sizes_early) {
+    load_sizes();
+    __syncthreads();
+  }
   if (threadIdx.x == 0) trace(1);
 
   if (warp == 0) {
@@ -143,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       uint32_t it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         TileInfo ti;
-        if (!tile_info(gp, t, ti)) continue;
+        if (!tile_info(gp, rt_m, rt_k, t, ti)) continue;
         const TcProblem& P = gp.p[ti.pi];
         const bool a_k = P.a.kmajor != 0, b_k = P.b.kmajor != 0;
         const int b_boxes = b_k ? 1 : (P.ntile + 63) / 64;
@@ -182,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       uint32_t it = 0, lt = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         TileInfo ti;
-        if (!tile_info(gp, t, ti)) continue;
+        if (!tile_info(gp, rt_m, rt_k, t, ti)) continue;
         const TcProblem& P = gp.p[ti.pi];
         const bool a_k = P.a.kmajor != 0, b_k = P.b.kmajor != 0;
         const uint32_t acc = lt & 1;
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       TileInfo ti;
-      if (!tile_info(gp, t, ti)) continue;
+      if (!tile_info(gp, rt_m, rt_k, t, ti)) continue;
       const TcProblem& P = gp.p[ti.pi];
       const uint32_t acc = lt & 1;
       mbar_wait(tfull + acc, (lt >> 1) & 1);
@@ -400,8 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       if (warp == 2 && lane == 0) trace(5);
       ++lt;
     }
-    // bulk stores must finish reading shared memory before the CTA exits
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // bulk stores must have READ shared memory before the CTA exits; their
+    // global writes complete with the grid (as CUTLASS's epilogue tail)
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -620,6 +638,7 @@ void tc_group_launch(const TcGroup& g, cudaStream_t s, cudaStream_t reduce_strea
   TcParams gp;
   std::memset(&gp, 0, sizeof(gp));
   gp.count = g.count;
+  gp.sizes_early = g.sizes_ready ? 1 : 0;
   int max_tiles = 0, max_ntile = 16;
   bool any_split = false;
   for (int i = 0; i < g.count; ++i) {

@@ -71,6 +71,10 @@ constexpr int kMaxTc = 8;
 struct TcGroup {
   TcProblem p[kMaxTc];
   int count = 0;
+  // every M_dev / K_dev is final before the launch (written by a kernel at
+  // least two launches back in stream order, or across a full dependency):
+  // the GEMM reads them before griddepcontrol.wait
+  bool sizes_ready = false;
 };
 
 // Operand views. A K-major: matrix [M rows x K cols]; MN-major: stored

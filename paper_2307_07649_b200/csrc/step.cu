@@ -1894,6 +1894,15 @@ int nn_ntile(int Mcap, int N) {
   return tc_ntile(N, g_wide ? 256 : 64);
 }
 
+// A GEMM group of the step: its runtime sizes are the plan's counts, written
+// by the planner long before (a barrier ahead, or many launches back in
+// stream order), so the GEMM may read them before griddepcontrol.wait.
+TcGroup plan_group() {
+  TcGroup g;
+  g.sizes_ready = true;
+  return g;
+}
+
 void tc_nn(TcGroup& g, int Mcap, const int* M_dev, int N, int K, const BfMat& A, int a_col0,
            const BfMat& B, int b_col0, int b_rows_cap, float* C, int64_t ldc, float beta = 0.0f) {
   TcProblem& P = g.p[g.count++];
@@ -2295,7 +2304,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
     return;
   }
   if (tma) {
-    TcGroup tg;
+    TcGroup tg = plan_group();
     tc_nn(tg, U, szU, 2 * d, gin + 1, w.bf.Xg, 0, w.bf.Wzr, 0, 2 * d, w.Gates, 3 * d);
     tc_nn(tg, U, szU, d, md, w.bf.Xg, 0, w.bf.Whm, 0, d, w.Gates + 2 * d, 3 * d);
     tc_group_launch(tg, s);
@@ -2310,7 +2319,7 @@ void substep_gru_launch(const StepCtx& c, const DPlan& pl, const DView& vw, cuda
   const int eblocks = env_knob("TGNN_EB", 4, 1, 64) * num_sms();  // elementwise grid (TGNN_EB x SMs)
   launch_pdl(gru_mid_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.Gates, tma ? nullptr : w.RS, bfx, U);
   if (tma) {
-    TcGroup tg;  // Gh += [r*s | 1] [Wh_s | bh]^T  (the bias rides the ones column)
+    TcGroup tg = plan_group();  // Gh += [r*s | 1] [Wh_s | bh]^T  (the bias rides the ones column)
     tc_nn(tg, U, szU, d, d + 1, w.bf.RS, 0, w.bf.Whs, 0, d, w.Gates + 2 * d, 3 * d, 1.0f);
     tc_group_launch(tg, s);
   } else {
@@ -2359,7 +2368,7 @@ void attn_edge_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s, bool ge
   launch_pdl(query_const_kernel, dim3(row_blocks(D.da)), dim3(32 * kWarps), 0, s, D, P + L.off[tWq], P + L.off[tBq], w.cq);
   if (!gemm) return;  // the GEMM joins the node projection's launch
   c.mark(phAttnProj, s);
-  TcGroup tg;
+  TcGroup tg = plan_group();
   g_wide = 1;  // per-pair K and V edge parts in one pass: [Wk_e Wk_t bk ; Wv_e Wv_t bv]
   tc_nn(tg, Pc, pl.sizes + kSzP, 2 * da, ke, w.bf.EF, 0, w.bf.Wkve, 0, 2 * da, w.KV, 2 * da);
   g_wide = 0;
@@ -2394,7 +2403,7 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
     } else {
       attn_edge_launch(c, pl, s);  // marks phAttnProj before its GEMM
     }
-    TcGroup tg;
+    TcGroup tg = plan_group();
     tc_nn(tg, U, pl.sizes + kSzU, 3 * w.bf.d8a, D.d + D.ds, w.bf.NF, 0, w.bf.Wst, 0, 3 * w.bf.d8a, w.QKVn,
           3 * w.bf.d8a);
     if (c.edge_gemm_joined) {  // the per-pair edge parts in the same launch
@@ -2460,7 +2469,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   // ---- decoder + loss (K7)
   c.mark(phDecoder, s);
   if (tma) {
-    TcGroup tg;
+    TcGroup tg = plan_group();
     tc_nn(tg, R, szR, dh, da, B.H, 0, B.W1a, 0, dh, w.AB, 2 * dh);
     tc_nn(tg, R, szR, dh, da, B.H, 0, B.W1b, 0, dh, w.AB + dh, 2 * dh);
     tc_group_launch(tg, s);
@@ -2509,7 +2518,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     gemm_group_launch(gg, s);
   }
   if (tma) {
-    TcGroup tg;
+    TcGroup tg = plan_group();
     tc_tn(tg, wc, dh, 2 * da + 1, B2, sz2B, B.Dhid, 0, B.Hin, 0, G + L.off[tW1], 2 * da, G + L.off[tB1]);
     tc_nmn(tg, B2, sz2B, 2 * da, dh, B.Dhid, 0, B.W1, 0, w.dIn, 2 * da);
     tc_group_launch(tg, s, c.br, c.ev_red);
@@ -2554,7 +2563,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   }
   c.mark(phAttnBwdGemm, s);
   if (tma) {
-    TcGroup tg;
+    TcGroup tg = plan_group();
     const int nd = d + D.ds, et = D.de + dt;
     // dX of the node features (once per support) ...
     tc_nmn(tg, U, szU, nd, 3 * B.d8a, B.dNA, 0, B.Wst, 0, w.dNode, nd);
@@ -2617,7 +2626,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   if (c.br) TGB_CUDA(cudaEventRecord(c.ev_br_join, c.br));
   if (c.ev_tail_grads) TGB_CUDA(cudaEventRecord(c.ev_tail_grads, s));
   if (tma) {
-    TcGroup tg;
+    TcGroup tg = plan_group();
     tc_nmn(tg, U, szU, d, d, B.Dg, 2 * B.d8d, B.Whs, 0, w.T1, d);
     tc_group_launch(tg, s);
   } else {
@@ -2627,7 +2636,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   }
   launch_pdl(gru_bwd2_kernel, dim3(eblocks), dim3(256), 0, s, D, pl, vw, w.T1, w.Gates, tma ? nullptr : w.Dg, bfx);
   if (tma) {
-    TcGroup tg;
+    TcGroup tg = plan_group();
     tc_tn(tg, wc, d, gin + 1, U, szU, B.Dg, 0, B.Xg, 0, G + L.off[tWz], gin, G + L.off[tBz]);
     tc_tn(tg, wc, d, gin + 1, U, szU, B.Dg, B.d8d, B.Xg, 0, G + L.off[tWr], gin, G + L.off[tBr]);
     tc_tn(tg, wc, d, md, U, szU, B.Dg, 2 * B.d8d, B.Xg, 0, G + L.off[tWh], gin);
@@ -2663,7 +2672,7 @@ void eval_rank_launch(const StepCtx& c, const DPlan& pl, int32_t* cnt_out, int64
   const int* szR = pl.sizes + kSzR;
   c.mark(phDecoder, s);
   if (gemm_impl() == kGemmTma) {
-    TcGroup tg;
+    TcGroup tg = plan_group();
     tc_nn(tg, R, szR, dh, da, w.bf.H, 0, w.bf.W1a, 0, dh, w.AB, 2 * dh);
     tc_nn(tg, R, szR, dh, da, w.bf.H, 0, w.bf.W1b, 0, dh, w.AB + dh, 2 * dh);
     tc_group_launch(tg, s);
