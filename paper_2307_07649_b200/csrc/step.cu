@@ -786,8 +786,10 @@ __global__ void decoder_wide_kernel(Dims D, DPlan pl, const float* __restrict__ 
   const int c0 = 4 * hl, c1 = 4 * (hl + 16);
   const bool ok0 = hl < nq, ok1 = hl + 16 < nq;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4 bb0 = ok0 ? ld4(b1 + c0) : z4, bb1 = ok1 ? ld4(b1 + c1) : z4;
-  const float4 w0 = ok0 ? ld4(W2 + c0) : z4, w1 = ok1 ? ld4(W2 + c1) : z4;
+  // b1 / W2 live at arbitrary offsets of the flat parameter vector: scalar loads
+  auto ld4u = [](const float* p) { return make_float4(p[0], p[1], p[2], p[3]); };
+  const float4 bb0 = ok0 ? ld4u(b1 + c0) : z4, bb1 = ok1 ? ld4u(b1 + c1) : z4;
+  const float4 w0 = ok0 ? ld4u(W2 + c0) : z4, w1 = ok1 ? ld4u(W2 + c1) : z4;
   const double invB = 1.0 / static_cast<double>(B);
   auto relu4 = [](float4 a) { return make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f)); };
   auto grad4 = [](float4 h, float4 w, float dl) {
