@@ -2520,10 +2520,21 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
     gemm_group_launch(gg, s);
   }
   if (tma) {
+    // W1 / b1 gradients on the branch (only the tail update reads them); the
+    // main stream forms the attention's input gradient alone
+    cudaStream_t wst = c.br ? c.br : s;
+    if (c.br) {
+      TGB_CUDA(cudaEventRecord(c.ev_red, s));
+      TGB_CUDA(cudaStreamWaitEvent(c.br, c.ev_red, 0));
+    }
+    {
+      TcGroup tg = plan_group();
+      tc_tn(tg, wc, dh, 2 * da + 1, B2, sz2B, B.Dhid, 0, B.Hin, 0, G + L.off[tW1], 2 * da, G + L.off[tB1]);
+      tc_group_launch(tg, wst);
+    }
     TcGroup tg = plan_group();
-    tc_tn(tg, wc, dh, 2 * da + 1, B2, sz2B, B.Dhid, 0, B.Hin, 0, G + L.off[tW1], 2 * da, G + L.off[tB1]);
     tc_nmn(tg, B2, sz2B, 2 * da, dh, B.Dhid, 0, B.W1, 0, w.dIn, 2 * da);
-    tc_group_launch(tg, s, c.br, c.ev_red);
+    tc_group_launch(tg, s);
   }
 
   // ---- attention backward (K8)
@@ -2565,21 +2576,33 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   }
   c.mark(phAttnBwdGemm, s);
   if (tma) {
-    TcGroup tg = plan_group();
     const int nd = d + D.ds, et = D.de + dt;
-    // dX of the node features (once per support) ...
-    tc_nmn(tg, U, szU, nd, 3 * B.d8a, B.dNA, 0, B.Wst, 0, w.dNode, nd);
-    // ... node-column weight gradients and the biases from the per-support sums ...
-    tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, 0, B.NF, 0, G + L.off[tWq], D.q_in, G + L.off[tBq]);
-    tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, B.d8a, B.NF, 0, G + L.off[tWk], D.kv_in, G + L.off[tBk]);
-    tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, 2 * B.d8a, B.NF, 0, G + L.off[tWv], D.kv_in, G + L.off[tBv]);
-    // ... edge / time-column weight gradients and the omega moments per pair
-    if (et > 0) {
-      tc_tn(tg, wc, da, et, Pc, szP, B.dKV, 0, B.EF, 0, G + L.off[tWk] + nd, D.kv_in);
-      tc_tn(tg, wc, da, et, Pc, szP, B.dKV, B.d8a, B.EF, 0, G + L.off[tWv] + nd, D.kv_in);
+    // the attention weight gradients feed only the tail-range update and the
+    // omega gradient: they run on the branch (GEMM and split-K reduction),
+    // off the critical path, while the main stream forms dX of the node
+    // features alone and goes on into the GRU backward
+    cudaStream_t wst = c.br ? c.br : s;
+    if (c.br) {
+      TGB_CUDA(cudaEventRecord(c.ev_red, s));
+      TGB_CUDA(cudaStreamWaitEvent(c.br, c.ev_red, 0));
     }
-    if (dt > 0) tc_tn(tg, wc, B.d8a + da, dt, Pc, szP, B.dKV, 0, B.Gt, 0, w.Mom, dt);
-    tc_group_launch(tg, s, c.br, c.ev_red);
+    {
+      TcGroup tg = plan_group();
+      // node-column weight gradients and the biases from the per-support sums ...
+      tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, 0, B.NF, 0, G + L.off[tWq], D.q_in, G + L.off[tBq]);
+      tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, B.d8a, B.NF, 0, G + L.off[tWk], D.kv_in, G + L.off[tBk]);
+      tc_tn(tg, wc, da, nd + 1, U, szU, B.dNA, 2 * B.d8a, B.NF, 0, G + L.off[tWv], D.kv_in, G + L.off[tBv]);
+      // ... edge / time-column weight gradients and the omega moments per pair
+      if (et > 0) {
+        tc_tn(tg, wc, da, et, Pc, szP, B.dKV, 0, B.EF, 0, G + L.off[tWk] + nd, D.kv_in);
+        tc_tn(tg, wc, da, et, Pc, szP, B.dKV, B.d8a, B.EF, 0, G + L.off[tWv] + nd, D.kv_in);
+      }
+      if (dt > 0) tc_tn(tg, wc, B.d8a + da, dt, Pc, szP, B.dKV, 0, B.Gt, 0, w.Mom, dt);
+      tc_group_launch(tg, wst);
+    }
+    TcGroup tg = plan_group();  // dX of the node features (once per support)
+    tc_nmn(tg, U, szU, nd, 3 * B.d8a, B.dNA, 0, B.Wst, 0, w.dNode, nd);
+    tc_group_launch(tg, s);
     if (c.ev_mid && c.mid_at == 3) TGB_CUDA(cudaEventRecord(c.ev_mid, s));
   } else {
     GemmGroup gg;
@@ -2604,7 +2627,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
 
   // omega gradient, attention part (Wk / Wv time rows x Mom): read before the
   // split-phase Adam may update those rows (on the branch with Mom's reduction)
-  if (dt > 0 && c.br) {  // Mom is final once the group (and its branch reduction) is done
+  if (dt > 0 && c.br && !tma) {  // Mom is final once the group is done (TMA: formed on the branch)
     TGB_CUDA(cudaEventRecord(c.ev_red, s));
     TGB_CUDA(cudaStreamWaitEvent(c.br, c.ev_red, 0));
   }
