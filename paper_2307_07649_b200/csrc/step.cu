@@ -1380,7 +1380,26 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
       gWq[r * D.q_in + nd + j] = gBq[r];
     }
   }
-  // flat element loops with 32-bit index arithmetic (U x d < 2^31 here)
+  // flat element loops with 32-bit index arithmetic (U x d < 2^31 here);
+  // pre-split engine with d, d + ds % 4 == 0: four columns per thread
+  if (Dg == nullptr && D.d % 4 == 0 && nd % 4 == 0) {
+    const int q = D.d / 4, total4 = U * q;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total4; x += gridDim.x * blockDim.x) {
+      const int u = x / q, i = 4 * (x - u * q);
+      const bool has = vw.mail_ev[u] >= 0;
+      const float* gr = Gates + static_cast<int64_t>(u) * 3 * D.d;
+      const float4 ds = ld4(dNode + static_cast<int64_t>(u) * nd + i);
+      const float4 pz = ld4(gr + i), ph = ld4(gr + 2 * D.d + i);
+      const float4 sm = ld4(vw.mem + static_cast<int64_t>(u) * D.d + i);
+      auto az = [&](float g, float z, float h, float s) { return has ? g * (tanhf(h) - s) * dsigmoidf_(z) : 0.0f; };
+      auto ah = [&](float g, float z, float h) { return has ? g * sigmoidf_(z) * dtanhf_(h) : 0.0f; };
+      bf_put4(bf.Dg, u, i,
+              make_float4(az(ds.x, pz.x, ph.x, sm.x), az(ds.y, pz.y, ph.y, sm.y), az(ds.z, pz.z, ph.z, sm.z),
+                          az(ds.w, pz.w, ph.w, sm.w)));
+      bf_put4(bf.Dg, u, 2 * bf.d8d + i,
+              make_float4(ah(ds.x, pz.x, ph.x), ah(ds.y, pz.y, ph.y), ah(ds.z, pz.z, ph.z), ah(ds.w, pz.w, ph.w)));
+    }
+  } else {
   const int total = U * D.d;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int u = x / D.d, i = x - u * D.d;
@@ -1398,6 +1417,7 @@ __global__ void gru_bwd1_kernel(Dims D, DPlan pl, DView vw, const float* __restr
     }
     bf_put(bf.Dg, u, i, az);
     bf_put(bf.Dg, u, 2 * bf.d8d + i, ah);
+  }
   }
   if (D.ds > 0) {
     const int tot2 = U * D.ds;
@@ -1428,6 +1448,20 @@ __global__ void gru_bwd2_kernel(Dims D, DPlan pl, DView vw, const float* __restr
   pdl_wait();
   pdl_trigger();
   const int U = pl.sizes[kSzU];
+  if (Dg == nullptr && D.d % 4 == 0) {  // pre-split engine: four columns per thread
+    const int q = D.d / 4, total4 = U * q;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total4; x += gridDim.x * blockDim.x) {
+      const int u = x / q, i = 4 * (x - u * q);
+      const bool has = vw.mail_ev[u] >= 0;
+      const int64_t e = static_cast<int64_t>(u) * D.d + i;
+      const float4 t = ld4(T1 + e), sm = ld4(vw.mem + e);
+      const float4 pr = ld4(Gates + static_cast<int64_t>(u) * 3 * D.d + D.d + i);
+      auto ar = [&](float a, float b, float c) { return has ? a * b * dsigmoidf_(c) : 0.0f; };
+      bf_put4(bf.Dg, u, bf.d8d + i, make_float4(ar(t.x, sm.x, pr.x), ar(t.y, sm.y, pr.y), ar(t.z, sm.z, pr.z),
+                                               ar(t.w, sm.w, pr.w)));
+    }
+    return;
+  }
   const int total = U * D.d;  // 32-bit index arithmetic (U x d < 2^31 here)
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int u = x / D.d, i = x - u * D.d;
