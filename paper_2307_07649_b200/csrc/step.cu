@@ -80,6 +80,40 @@ __device__ __forceinline__ void bf_zero_tail(const BfMat& m, int count, int cap,
   }
 }
 
+// float4 helpers of the wide-row kernels
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 scale4(float4 a, float s) { return make_float4(a.x * s, a.y * s, a.z * s, a.w * s); }
+__device__ __forceinline__ float4 fma4(float s, float4 a, float4 c) {
+  return make_float4(fmaf(s, a.x, c.x), fmaf(s, a.y, c.y), fmaf(s, a.z, c.z), fmaf(s, a.w, c.w));
+}
+__device__ __forceinline__ float dot4(float4 a, float4 b) {
+  return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
+}
+__device__ __forceinline__ float half_sum(float v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float4 xor16_4(float4 a) {
+  return make_float4(__shfl_xor_sync(0xffffffffu, a.x, 16), __shfl_xor_sync(0xffffffffu, a.y, 16),
+                     __shfl_xor_sync(0xffffffffu, a.z, 16), __shfl_xor_sync(0xffffffffu, a.w, 16));
+}
+// four consecutive elements of a pre-split operand (c % 4 == 0, ld % 4 == 0)
+__device__ __forceinline__ void bf_put4(const BfMat& m, int64_t r, int64_t c, float4 v) {
+  if (m.hi == nullptr) return;
+  const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+  const float2 b0 = __bfloat1622float2(h0), b1 = __bfloat1622float2(h1);
+  const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - b0.x, v.y - b0.y), l1 = __floats2bfloat162_rn(v.z - b1.x, v.w - b1.y);
+  uint2 hh, ll;
+  hh.x = *reinterpret_cast<const uint32_t*>(&h0);
+  hh.y = *reinterpret_cast<const uint32_t*>(&h1);
+  ll.x = *reinterpret_cast<const uint32_t*>(&l0);
+  ll.y = *reinterpret_cast<const uint32_t*>(&l1);
+  *reinterpret_cast<uint2*>(m.hi + r * m.ld + c) = hh;
+  *reinterpret_cast<uint2*>(m.lo + r * m.ld + c) = ll;
+}
+
 // Writes one staged row (cols floats in shared memory) of a pre-split operand
 // with 16-byte stores: each lane converts 8 consecutive values to bf16 hi/lo.
 // Columns [cols, roundup8(cols)) receive zeros. f32row (nullable) gets the
@@ -213,14 +247,29 @@ __global__ void assemble_gru_time_kernel(Dims D, DPlan pl, DView vw, const float
   pdl_wait();
   pdl_trigger();
   const int U = pl.sizes[kSzU];
-  const int total = U * D.dt;  // 32-bit index arithmetic (U x dt < 2^31 here)
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
-    const int u = x / D.dt, i = x - u * D.dt;
-    const double dt = vw.mail_dt[u];
-    float sn, cs;
-    time_sincos(dt, omega[i], &sn, &cs);
-    bf_put(bf.Xg, u, 2 * D.d + i, cs);
-    bf_put(bf.GU, u, i, vw.mail_ev[u] >= 0 ? static_cast<float>(-dt) * sn : 0.0f);
+  if (D.dt % 4 == 0 && D.d % 2 == 0) {  // four columns per thread (8-byte bf16 stores)
+    const int q = D.dt / 4, total4 = U * q;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total4; x += gridDim.x * blockDim.x) {
+      const int u = x / q, i = 4 * (x - u * q);
+      const double dt = vw.mail_dt[u];
+      const bool has = vw.mail_ev[u] >= 0;
+      float sn[4], cs[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) time_sincos(dt, omega[i + e], &sn[e], &cs[e]);
+      const float m = static_cast<float>(-dt);
+      bf_put4(bf.Xg, u, 2 * D.d + i, make_float4(cs[0], cs[1], cs[2], cs[3]));
+      bf_put4(bf.GU, u, i, has ? make_float4(m * sn[0], m * sn[1], m * sn[2], m * sn[3]) : make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+  } else {
+    const int total = U * D.dt;  // 32-bit index arithmetic (U x dt < 2^31 here)
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+      const int u = x / D.dt, i = x - u * D.dt;
+      const double dt = vw.mail_dt[u];
+      float sn, cs;
+      time_sincos(dt, omega[i], &sn, &cs);
+      bf_put(bf.Xg, u, 2 * D.d + i, cs);
+      bf_put(bf.GU, u, i, vw.mail_ev[u] >= 0 ? static_cast<float>(-dt) * sn : 0.0f);
+    }
   }
   bf_zero_tail(bf.GU, U, cap_U, D.dt);
 }
@@ -524,39 +573,6 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, float* Q, const float* __restr
 // Against attn_fwd_kernel: a quarter of the load instructions, half the
 // shuffles per score and one memory round per eight neighbours instead of two.
 constexpr int kPairGroup = 4;
-
-__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
-__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-__device__ __forceinline__ float4 scale4(float4 a, float s) { return make_float4(a.x * s, a.y * s, a.z * s, a.w * s); }
-__device__ __forceinline__ float4 fma4(float s, float4 a, float4 c) {
-  return make_float4(fmaf(s, a.x, c.x), fmaf(s, a.y, c.y), fmaf(s, a.z, c.z), fmaf(s, a.w, c.w));
-}
-__device__ __forceinline__ float dot4(float4 a, float4 b) {
-  return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
-}
-__device__ __forceinline__ float half_sum(float v) {
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ float4 xor16_4(float4 a) {
-  return make_float4(__shfl_xor_sync(0xffffffffu, a.x, 16), __shfl_xor_sync(0xffffffffu, a.y, 16),
-                     __shfl_xor_sync(0xffffffffu, a.z, 16), __shfl_xor_sync(0xffffffffu, a.w, 16));
-}
-// four consecutive elements of a pre-split operand (c % 4 == 0, ld % 4 == 0)
-__device__ __forceinline__ void bf_put4(const BfMat& m, int64_t r, int64_t c, float4 v) {
-  if (m.hi == nullptr) return;
-  const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
-  const float2 b0 = __bfloat1622float2(h0), b1 = __bfloat1622float2(h1);
-  const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - b0.x, v.y - b0.y), l1 = __floats2bfloat162_rn(v.z - b1.x, v.w - b1.y);
-  uint2 hh, ll;
-  hh.x = *reinterpret_cast<const uint32_t*>(&h0);
-  hh.y = *reinterpret_cast<const uint32_t*>(&h1);
-  ll.x = *reinterpret_cast<const uint32_t*>(&l0);
-  ll.y = *reinterpret_cast<const uint32_t*>(&l1);
-  *reinterpret_cast<uint2*>(m.hi + r * m.ld + c) = hh;
-  *reinterpret_cast<uint2*>(m.lo + r * m.ld + c) = ll;
-}
 
 inline bool attn_wide_ok(int da, int n) { return da % 4 == 0 && da <= 128 && n <= 32; }
 
