@@ -143,8 +143,11 @@ def step_roofline(sz, cfg, nparam, events_s_per_gpu, peaks):
 def roofline_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of the roofline kernel (the
     tc_gemm_kernel group) from the committed ncu --set full capture of one
-    barrier's GEMM launches (profiles/r02_roofline_traffic.json), per launch."""
-    p = os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")
+    barrier's GEMM launches (profiles/r02b_roofline_traffic.json, else the
+    round-2 capture), per launch."""
+    p = os.path.join(ROOT, "profiles", "r02b_roofline_traffic.json")
+    if not os.path.exists(p):
+        p = os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
