@@ -264,3 +264,33 @@ def test_unfused_gru_freshen_variant():
                        capture_output=True, text=True, timeout=900, cwd=root, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout
+
+
+# Shapes for the wide-row kernels' edge cases (d_attn, d_hidden % 4 == 0):
+# n_neighbours above one 8-neighbour round and odd, the maximum 32 (one
+# neighbour per lane), d_attn 128 (every float4 column pair in use), d_mem
+# % 4 == 0 (the four-column GRU backward) and not, hub-heavy plans (SMALL has
+# 60 nodes, so supports repeat across many pairs: cross-chunk routing runs).
+WIDE_MODELS = {
+    "n13_da8": dict(d_mem=8, d_time=4, d_static=4, d_attn=8, d_hidden=12, n_neighbors=13),
+    "n32_da12": dict(d_mem=6, d_time=4, d_static=3, d_attn=12, d_hidden=4, n_neighbors=32),
+    "n5_da128": dict(d_mem=12, d_time=8, d_static=0, d_attn=128, d_hidden=128, n_neighbors=5),
+}
+
+
+@pytest.mark.parametrize("name", sorted(WIDE_MODELS))
+def test_wide_kernel_shapes_parity(env, name):
+    begin, B = 300, 50
+    s, rg, g, mc, params, negs, plan, vm, vl = _substep_case(env, SMALL, WIDE_MODELS[name], begin, B, seed=2)
+    loss_r, grads_r, shat_r = rg.sub_step(mc, params, begin, begin + B, negs, vm, vl)
+    tr = T.TrainerCore(env, g, mc, B, 1)
+    tr.set_params(params)
+    loss, shat = tr.sub_step(begin, begin + B, negs, vm, vl)
+    grads = tr.grads()
+    assert abs(loss - loss_r) <= REL_TOL * abs(loss_r), (loss, loss_r)
+    ok, err, sc = rel_close(shat, shat_r)
+    assert ok, ("s_hat", err, sc)
+    for tname, sl in tensor_slices(mc).items():
+        ok, err, sc = rel_close(grads[sl], grads_r[sl], floor=1e-7)
+        assert ok, (tname, err, sc)
+    tr.close()
