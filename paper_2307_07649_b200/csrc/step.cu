@@ -575,6 +575,12 @@ __global__ void attn_fwd_kernel(Dims D, DPlan pl, float* Q, const float* __restr
 constexpr int kPairGroup = 4;
 
 inline bool attn_wide_ok(int da, int n) { return da % 4 == 0 && da <= 128 && n <= 32; }
+// The wide-row attention / routing / decoder kernels (TGNN_ATTN_WIDE=0: the
+// scalar forms, A/B).
+inline bool wide_rows_enabled() {
+  static const int v = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
+  return v == 1;
+}
 
 __global__ void attn_fwd_wide_kernel(Dims D, DPlan pl, float* Q, const float* __restrict__ KV,
                                      float* __restrict__ attn_a, float* __restrict__ H, int* flag, StepBf bf,
@@ -2482,10 +2488,9 @@ void attn_forward_launch(const StepCtx& c, const DPlan& pl, cudaStream_t s) {
   c.mark(phAttnSoftmax, s);
   {
     const int lanes = (da + 31) / 32;
-    static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
     auto fwd = lanes <= 1 ? attn_fwd_kernel<1> : lanes <= 2 ? attn_fwd_kernel<2>
              : lanes <= 4 ? attn_fwd_kernel<4> : attn_fwd_kernel<8>;
-    if (wide_knob && attn_wide_ok(da, static_cast<int>(m.n_neighbors))) fwd = attn_fwd_wide_kernel;
+    if (wide_rows_enabled() && attn_wide_ok(da, static_cast<int>(m.n_neighbors))) fwd = attn_fwd_wide_kernel;
     launch_pdl(fwd, dim3(row_blocks(R)), dim3(32 * kWarps), 0, s, D, pl, w.Q, w.KV, w.attn_a, w.H, c.d_numeric_flag,
                bfx, tma ? w.QKVn : nullptr, w.cq, 2 * w.cap_B);
   }
@@ -2532,8 +2537,7 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
            2 * dh);
     gemm_group_launch(gg, s);
   }
-  static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
-  if (tma && wide_knob && dh % 4 == 0 && dh <= 128)
+  if (tma && wide_rows_enabled() && dh % 4 == 0 && dh <= 128)
     launch_pdl(decoder_wide_kernel, dim3(row_blocks(w.cap_B)), dim3(32 * kWarps), 0, s, D, pl, w.AB, P + L.off[tB1],
                P + L.off[tW2], P + L.off[tB2], w.HID, w.dlogit, w.logits, w.loss_terms, c.d_numeric_flag, bfx, B2);
   else
@@ -2591,9 +2595,8 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   c.mark(phAttnBwd, s);
   {
     const int lanes = (da + 31) / 32;
-    static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
     const int nnb = static_cast<int>(m.n_neighbors);
-    if (wide_knob && attn_wide_ok(da, nnb)) {
+    if (wide_rows_enabled() && attn_wide_ok(da, nnb)) {
       const size_t smem = sizeof(float) * static_cast<size_t>(kWarps) * nnb * da;  // parked K rows
       if (smem > 48 * 1024)
         TGB_CUDA(cudaFuncSetAttribute(attn_bwd_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2614,10 +2617,9 @@ void substep_rest_launch(const StepCtx& c, const DPlan& pl, const DView& vw, dou
   float* part_last = wc.take(static_cast<size_t>(nchunks) * 3 * da);
   {
     const int lanes = (da + 31) / 32;
-    static const int wide_knob = env_knob("TGNN_ATTN_WIDE", 1, 0, 1);
     auto chunk = lanes <= 1 ? routing_chunk_kernel<1> : lanes <= 2 ? routing_chunk_kernel<2>
                : lanes <= 4 ? routing_chunk_kernel<4> : routing_chunk_kernel<8>;
-    if (wide_knob && da % 4 == 0 && da <= 128) chunk = routing_chunk_wide_kernel;
+    if (wide_rows_enabled() && da % 4 == 0 && da <= 128) chunk = routing_chunk_wide_kernel;
     launch_pdl(chunk, dim3(row_blocks(3 * nchunks)), dim3(32 * kWarps), 0, s, D, pl, w.dQ, w.dKV, tma ? nullptr : w.dNodeAcc,
                                                       part_first, part_last, bfx);
     const int fix_threads = std::min(1024, (3 * da + 31) / 32 * 32);

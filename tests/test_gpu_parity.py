@@ -249,15 +249,17 @@ def test_run_sequential_parity(env, case, engine):
 
 def test_unfused_gru_freshen_variant():
     """The default TMA path runs the GRU freshen as one fused tcgen05 kernel
-    (gru_fused.cu) with the edge projection joined to the node projection; the
-    five-launch chain (TGNN_GRU_FUSED=0) and the edge GEMM on its own branch are
-    still shipped knobs: the sub-step and run_sequential parity tests above
-    rerun under them in a fresh process (the knobs are read once)."""
+    (gru_fused.cu) with the edge projection joined to the node projection, and
+    the wide-row attention / routing / decoder kernels; the five-launch chain
+    (TGNN_GRU_FUSED=0), the edge GEMM on its own branch and the scalar
+    attention kernels (TGNN_ATTN_WIDE=0) are still shipped knobs: the sub-step
+    and run_sequential parity tests above rerun under them in a fresh process
+    (the knobs are read once)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TGNN_GRU_FUSED="0")
+    env = dict(os.environ, TGNN_GRU_FUSED="0", TGNN_ATTN_WIDE="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_gpu_parity.py"),
                         "-k", "(test_sub_step_parity or test_run_sequential_parity) and tma"],
