@@ -150,3 +150,19 @@ def test_evaluate_mrr_golden(og, mc):
         mrr, q = O.evaluate_mrr(mc, params, og, 600, 800, 50, 9, 5)
         assert q == int(GOLD[key][1])
         assert abs(mrr - GOLD[key][0]) < 1e-12, (key, mrr, GOLD[key][0])
+
+
+def test_convergence_golden_pins_the_reference_anchors():
+    """tests/golden/convergence_ref.json (the unmodified reference's final val
+    MRR over training seeds 5..12, made by make_convergence_ref.py) reproduces
+    the reference's own acceptance anchors at seed 5
+    (ref/tests/acceptance.cpp:435-458: 0.8767, 0.8824, 0.8368), so the
+    eight-seed means the GPU tests compare against come from the same runs."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "convergence_ref.json")) as f:
+        conv = json.load(f)
+    for shape, anchor in (("1x1x1", 0.8767), ("1x1x4", 0.8824), ("1x4x1", 0.8368)):
+        row = conv[shape]
+        assert sorted(int(k) for k in row) == list(range(5, 13))
+        assert abs(row["5"] - anchor) <= 5e-5, (shape, row["5"], anchor)
